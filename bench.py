@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""Benchmark of the batched leaf expansion (BASELINE.json metric:
+scenario-steps/s and ms per leaf-expansion batch, vs the CPU oracle).
+
+One step = one despot_expand_batch over the config's leaves (update K1,
+expansion + bounds + roll-outs + grouping K2, child order / CSR / outputs K3)
+with the node arenas resident in HBM.  Default workload: BASELINE config 2
+(multi-agent RockSample(15,15), 2 robots, K=500, 64 depth-1 leaves).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl despot|reference]
+
+N > 1 (torchrun, one rank per GPU): the same workload scenario-sharded
+(global id % N), with one NCCL all-reduce of the exact int64 partials per
+batch (strong scaling).  Timing: CUDA events per step on the launching
+stream, barrier + synchronize around the timed region, max over ranks; L2 is
+flushed (a 256 MiB write) between timed steps, outside the events.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1802_06215_b200 import inputs  # noqa: E402
+
+# thread-instructions per scenario-step of K2 (the "algorithmic" instruction
+# work of one step as implemented), from the ncu profile of round 1, see
+# DESIGN.md §7.  Used for the ALU roofline: achieved = I_step * steps / t_K2.
+I_STEP = {"rocksample": 260.0, "nav": 520.0, "car": 2000.0, "tiger": 120.0}
+KERNELS_PER_STEP = 6  # K1, K2pre, K2, K3a, K3b, K3c
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index=0):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def workload(cfg, K=None):
+    c = inputs.CONFIGS[cfg]
+    kind, params, st, w, seed, L = inputs.config_inputs(cfg, K=K)
+    return c, kind, params, st, w, seed, L
+
+
+def make_leaves(model, root, L, cfg_kind, extra_roots=None):
+    """Depth-1 leaves from the root expansion (SURVEY §8(d) generator)."""
+    R = model.expand([(root, -1, 0, 0)])
+    lv = inputs.select_leaves(R["child_count"], R["child_begin"], model.A, L)
+    return [(root, a, c, 1) for a, c in lv]
+
+
+def cpu_baseline(kind, params, st, w, seed, leaves_ac, budget_s=12.0, L=64):
+    """The oracle as it stands (single thread) on a bounded sample of the
+    same workload: leaves expanded one at a time until ~budget_s of work."""
+    import oracle
+
+    om = oracle.Model(kind, params)
+    if kind == "car":
+        croots = inputs.car_roots(L, int(len(w)))
+        items = [("root", j) for j in range(L)]
+    else:
+        root = om.belief_load(st, w, seed)
+        om.expand([(root, -1, 0, 0)])
+        items = leaves_ac
+    steps = 0
+    t0 = time.perf_counter()
+    n = 0
+    for (a, c) in items:
+        if kind == "car":
+            r = om.belief_load(*croots[c])
+            o = om.expand([(r, -1, 0, 0)])
+        else:
+            o = om.expand([(root, a, c, 1)])
+        steps += o["scenario_steps"]
+        n += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": steps / dt, "unit": "scenario-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} of {len(items)} leaves (all |A| actions each), {steps} scenario-steps in {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, timed on this box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    c, kind, params, st, w, seed, L = workload(args.config)
+    import oracle
+
+    om = oracle.Model(kind, params)
+    if kind == "car":
+        croots = inputs.car_roots(L, int(len(w)))
+        rts = [om.belief_load(*cr) for cr in croots]
+        lv = [(r, -1, 0, 0) for r in rts]
+    else:
+        root = om.belief_load(st, w, seed)
+        R = om.expand([(root, -1, 0, 0)])
+        lv = [(root, a, cc, 1) for a, cc in inputs.select_leaves(R["child_count"], R["child_begin"], om.A, L)]
+    per_step = max(1, min(L, args.ref_leaves))
+    times, steps_all = [], []
+    for it in range(args.warmup + args.steps):
+        sub = [lv[(it * per_step + j) % L] for j in range(per_step)]
+        t0 = time.perf_counter()
+        o = om.expand(sub)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            steps_all.append(o["scenario_steps"])
+    value = float(np.sum(steps_all) / np.sum(times))
+    line = {"impl": "reference", "metric": "scenario-steps/s", "value": value, "unit": "scenario-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * float(np.mean(times)) * L / per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic",
+            "config": {"workload": c["name"], "K": int(len(w)), "leaves": L, "actions": int(om.A),
+                       "depth": int(om.D), "l2": "inputs < L2; host run"},
+            "cpu_baseline": {"value": value, "unit": "scenario-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} of {L} leaves per step"},
+            "e2e": {"value": value, "unit": "scenario-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--K", type=int, default=None)
+    ap.add_argument("--impl", default="despot", choices=["despot", "reference"])
+    ap.add_argument("--ref-leaves", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    from paper_1802_06215_b200 import build as B
+    from paper_1802_06215_b200.despot import Model
+
+    B.build()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    c, kind, params, st, w, seed, L = workload(args.config, args.K)
+    model = Model(kind, params, device=local, rank=rank, world=world)
+    stream = torch.cuda.current_stream(dev)
+    if kind == "car":
+        # config 4: L concurrent roots (inputs.car_roots)
+        if world > 1:
+            raise SystemExit("config 4 (sparse keys) runs on one GPU")
+        croots = inputs.car_roots(L, int(len(w)))
+        leaves = [(model.belief_load(s_, w_, sd_), -1, 0, 0) for s_, w_, sd_ in croots]
+        lv_ac = None
+    else:
+        root = model.belief_load(st, w, seed)
+        # root expansion (untimed): gives the depth-1 leaves
+        if world > 1:
+            from paper_1802_06215_b200.dist import expand_sharded
+            R = expand_sharded(model, [(root, -1, 0, 0)])
+        else:
+            R = model.expand([(root, -1, 0, 0)])
+        lv_ac = inputs.select_leaves(R["child_count"], R["child_begin"], model.A, L)
+        leaves = [(root, a, cc, 1) for a, cc in lv_ac]
+    cap = model.child_capacity_bound(leaves)
+    dev_out = model.alloc_outputs(leaves, device_outputs=True, child_capacity=cap)
+    host_out = model.alloc_outputs(leaves, device_outputs=False, child_capacity=cap)
+
+    def one_step(outputs, device_outputs, timing=True):
+        if world > 1:
+            from paper_1802_06215_b200.dist import exchange, exchange_views
+            b, ex = model.expand_begin(leaves, timing=timing)
+            s, m = exchange_views(ex, dev)
+            exchange(s, m)
+            o = model.expand_end(b, leaves, device_outputs=device_outputs, timing=timing, outputs=outputs)
+        else:
+            o = model.expand(leaves, device_outputs=device_outputs, timing=timing, outputs=outputs)
+        for (lf, n) in zip(leaves, o["node"]):
+            if lf[1] >= 0:  # nodes created by this batch (self leaves return their own node)
+                model.node_release(n)
+        return o
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        one_step(dev_out, True)
+    # ---- device-resident timed region ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k2_ms, k1_ms, k3_ms, steps_count = [], [], [], []
+    barrier()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            o = one_step(dev_out, True)
+            ev[i][1].record(stream)
+            k1_ms.append(o["phase_ms"][0])
+            k2_ms.append(o["phase_ms"][1])
+            k3_ms.append(o["phase_ms"][2])
+            steps_count.append(o["scenario_steps"])
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_local = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([t_local], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total = float(t.item())
+    else:
+        t_total = t_local
+    total_steps = float(np.sum(steps_count))  # global (exchanged) scenario-steps
+    value = total_steps / (t_total / 1e3)
+    # ---- end to end through the C ABI with host buffers ----
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = 0
+    e2e_n = max(3, args.steps // 2)
+    ee = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ee[0].record(stream)
+    for _ in range(e2e_n):
+        o = one_step(host_out, False, timing=False)
+        e2e_steps += o["scenario_steps"]
+    ee[1].record(stream)
+    barrier()
+    e2e_ms = ee[0].elapsed_time(ee[1])
+    e2e_wall = time.perf_counter() - t0
+    import ctypes
+    h2d = L * ctypes.sizeof(__import__("paper_1802_06215_b200.despot", fromlist=["Leaf"]).Leaf)
+    nch = int(o["num_children"])
+    A = model.A
+    d2h = 4 * (2 * L + 3 * L * A + L * A + 1) + nch * (5 * 4 + 4 * model.OW) + 4 + 4 * L + 4 + 8
+    # ---- roofline of the dominant kernel (K2), live CUDA-event time ----
+    peaks, peak_src = load_peaks()
+    clocks = clk.summary()
+    sm_clock = peaks.get("sm_max_mhz", 1965.0)
+    num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_tinst = num_sms * 4 * 32 * sm_clock * 1e6 / 1e12  # issue slots, thread-instr/s (Tinst/s)
+    k2_avg = float(np.mean(k2_ms))
+    steps_local = total_steps / world
+    achieved = I_STEP[kind] * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
+    k2_share = float(np.sum(k2_ms) / np.sum(step_ms))
+    if rank == 0:
+        line = {
+            "metric": "scenario-steps/s",
+            "value": value,
+            "unit": "scenario-steps/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": t_total / args.steps,
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "u32+f64",
+            "data": "synthetic",
+            "config": {"workload": c["name"], "K": int(len(w)), "leaves": L, "actions": int(A),
+                       "depth": int(model.D), "parallelism": f"scenario-shard{world}",
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "scenario_steps_per_batch": int(total_steps / args.steps)},
+            "phases_ms": {"K1_update": float(np.mean(k1_ms)), "K2_expand_rollout": k2_avg,
+                          "K3_finalize": float(np.mean(k3_ms)), "K2_share_of_step": k2_share},
+            "roofline": {"bound": "alu", "kernel": "k2_car_warp" if kind == "car" else "k2_expand_dense", "achieved": achieved,
+                         "peak": peak_tinst, "unit": "Tinst/s", "frac": achieved / peak_tinst,
+                         "traffic": None,
+                         "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
+                                 f"({peak_src} sm_max_mhz); achieved = {I_STEP[kind]} thread-instr per "
+                                 f"scenario-step (DESIGN.md §7) x steps / live K2 event time"},
+            "e2e": {"value": e2e_steps / (e2e_ms / 1e3), "unit": "scenario-steps/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_n,
+                    "wall_ms_per_step": 1e3 * e2e_wall / e2e_n},
+            "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "clocks": clocks,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(kind, params, st, w, seed, lv_ac, args.cpu_budget, L)
+        print(json.dumps(line))
+    model.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,225 @@
+/*
+ * despot.h -- C ABI of libdespot, the B200 (sm_100a) batched leaf expansion
+ * of HyP-DESPOT (Cai, Luo, Hsu, Lee, "HyP-DESPOT: A Hybrid Parallel Algorithm
+ * for Online Planning under Uncertainty", arXiv 1802.06215).
+ *
+ * Citations: P:n = line n of PAPER.md (the paper's LaTeX source), S:n = line n
+ * of SPEC.md; R<n> = reading n in DESIGN.md §2 (where the paper is silent).
+ *
+ * The hot path: for every leaf of a batch, the MC_simulation
+ * tasks of §III-D2 -- update (replay the last action and keep the
+ * parent's scenarios that reach this leaf), expansion over all actions
+ * and scenarios (Eq. 9), per-child upper bounds (Eq. 11),
+ * default-policy roll-outs to depth D (Eq. 12), the grouping of
+ * scenarios into child nodes by observation (Eq. 10) and the
+ * one-level Bellman values of Eq. 4.  Many leaves go into one
+ * launch (node-level parallelism).
+ *
+ * Conventions
+ *  - Every call returns an int status; 0 = DESPOT_OK.  No C++ exception
+ *    crosses the ABI.  On error, despot_last_error() returns a message that
+ *    is thread-local and valid until the calling thread's next call.
+ *  - A model is immutable after load and may be used from many host threads
+ *    at once; each call uses its own device scratch.
+ *  - Node arenas live in device memory, are owned by the library and are
+ *    immutable once created (their child-key table is written when the node
+ *    is expanded), until despot_node_release().
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls that
+ *    return outputs are synchronous with respect to those outputs.
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one fails with DESPOT_ECUDA.
+ */
+#ifndef HYP_DESPOT_DESPOT_H
+#define HYP_DESPOT_DESPOT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DESPOT_ABI_VERSION 1
+
+enum despot_status {
+  DESPOT_OK = 0,
+  DESPOT_EINVAL = -1,    /* malformed arguments: unknown kind/params, empty or zero-weight
+                            belief, leaf depth >= D, unknown child ordinal (its
+                            scenario set would be empty), unexpanded parent            */
+  DESPOT_EMODEL = -2,    /* step contract violation: action outside [-1, |A|)  */
+  DESPOT_ENOMEM = -3,    /* device allocation failed                                  */
+  DESPOT_ECAPACITY = -4, /* caller's child_capacity / scen_capacity too small; the
+                            needed sizes are in num_children / the n_scen outputs    */
+  DESPOT_ECUDA = -5,     /* CUDA error (no device, launch failure, ...)               */
+  DESPOT_ENCCL = -6,     /* reserved: collective failure reported by the caller       */
+  DESPOT_ESHUTDOWN = -7, /* the model entered a failed state after a CUDA error       */
+  DESPOT_EHASH = -8      /* two different sparse observation keys shared a 64-bit
+                            hash inside one (leaf, action): grouping refused          */
+};
+
+/* Thread-local message of the last failing call of this thread. */
+const char* despot_last_error(void);
+int despot_abi_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Models (DESIGN.md §3 model cards)                   */
+/* ------------------------------------------------------------------------ */
+typedef struct despot_model despot_model; /* opaque */
+typedef uint64_t despot_node;             /* opaque handle of a device node arena */
+
+typedef struct {
+  int device;     /* CUDA device ordinal the model and its nodes live on            */
+  int rank;       /* scenario shard of this process: it keeps global ids            */
+  int world;      /*   with id % world == rank; world <= 1: no shard */
+  uint32_t flags; /* DESPOT_MF_* below                                              */
+} despot_opts;
+
+/* Driving model: use the thread-per-scenario kernel instead of the factored
+ * warp-per-scenario kernel (within-step parallelism). */
+#define DESPOT_MF_UNFACTORED 1u
+
+typedef struct {
+  uint32_t num_actions; /* |A|                                                     */
+  uint32_t state_words; /* u32 words per scenario state (SoA rows of a node)       */
+  uint32_t obs_words;   /* u32 words per observation key                           */
+  uint32_t obs_slots;   /* dense observation range incl. TERMINAL; 0 = sparse keys */
+  uint32_t max_depth;   /* D, an absolute depth (R3)                                */
+  uint32_t elements;    /* factored elements per step                   */
+  double gamma;         /* discount                                                 */
+  double tail;          /* heuristic l(s) added at depth D (R6)              */
+} despot_model_info;
+
+/* kind: "tiger" | "rocksample" | "nav" | "car".  params: "key=value ..." as in
+ * the model cards (e.g. "n=15 robots=2 rocks=x:y,... starts=x:y,x:y D=20
+ * gamma=0.95").  opts may be NULL (device 0, no sharding).
+ * Errors: EINVAL (unknown kind / bad params), ECUDA, ENOMEM. */
+int despot_model_load(const char* kind, const char* params, const despot_opts* opts,
+                      despot_model** out);
+int despot_model_info_get(const despot_model* model, despot_model_info* out);
+/* Frees the model and every node still alive.  The model must not be in use. */
+int despot_model_free(despot_model* model);
+
+/* ------------------------------------------------------------------------ */
+/* Beliefs and nodes                                                        */
+/* ------------------------------------------------------------------------ */
+/* A belief is K weighted scenarios with their random streams:
+ * states_soa [state_words][K] u32 (host), weights [K] f32 > 0 (host), global
+ * scenario id = position, stream_seed = the Philox key sigma of phi_t (R13).
+ * With world > 1 only ids with id % world == rank are kept on this device.
+ * The root has depth 0.  Errors: EINVAL (K == 0, weight <= 0), ENOMEM, ECUDA. */
+int despot_belief_load(despot_model* model, const uint32_t* states_soa, const float* weights,
+                       uint32_t K, uint64_t stream_seed, void* stream, despot_node* root_out);
+/* n = scenarios of the node on this device (after the call that created it
+ * has returned), depth = Delta of the node. */
+int despot_node_info(despot_model* model, despot_node node, uint32_t* n, uint32_t* depth);
+/* Copies the node's ids [n], weights [n] and states [state_words][n] to host
+ * buffers (any may be NULL).  Synchronous. */
+int despot_node_read(despot_model* model, despot_node node, uint32_t* ids, float* weights,
+                     uint32_t* states_soa, void* stream);
+int despot_node_release(despot_model* model, despot_node node);
+
+/* ------------------------------------------------------------------------ */
+/* Batched leaf expansion (the hot path)                                    */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  despot_node parent; /* an expanded node, or the leaf itself when action == -1     */
+  int32_t action;     /* last action of the leaf's history; -1: no update step      */
+  uint32_t child;     /* child ordinal under (parent, action): first-occurrence
+                         order of that expansion (R8)                                */
+  uint32_t depth;     /* Delta of the leaf (parent depth + 1, or the node's depth)  */
+  uint32_t pad;
+} despot_leaf;
+
+/* despot_expansion.flags */
+#define DESPOT_X_DEVICE_OUTPUTS 1u  /* all array outputs except `node` are device
+                                       pointers (no D2H copies inside the call)     */
+#define DESPOT_X_RECORD_SCENARIO 2u /* fill the per-scenario scen_* arrays         */
+#define DESPOT_X_TIMING 4u          /* fill phase_ms with CUDA-event times of the
+                                       phases, recorded on the call's stream       */
+
+/* Caller-owned outputs.  Sizes: L leaves, A = |A|, C = child_capacity,
+ * S = scen_capacity.  Children of (l, a) are child_begin[l*A+a] ..
+ * child_begin[l*A+a+1]-1, in first-occurrence order (R8). */
+typedef struct {
+  uint32_t flags;
+  despot_node* node;     /* [L] host: new node holding leaf l's scenarios (for
+                            action == -1 leaves: the parent itself)                   */
+  uint32_t* n_scen;      /* [L] |Phi_l| (all ranks)                                   */
+  float* weight;         /* [L] W_l = sum of the leaf's scenario weights              */
+  float* act_reward;     /* [L*A] mean step reward  sum_i w_i r_i / W_l  (Eq. 4)      */
+  float* act_upper;      /* [L*A] u(b,a) = sum_i w_i (r_i + gamma u_i) / W_l (Eq. 4)  */
+  float* act_lower;      /* [L*A] l(b,a) = sum_i w_i (r_i + gamma lambda_i) / W_l     */
+  uint32_t* child_begin; /* [L*A+1] CSR offsets                                        */
+  uint32_t child_capacity;
+  uint32_t* child_count; /* [C] N_c = |Phi_b'|                                         */
+  uint32_t* child_first; /* [C] smallest global scenario id of the child               */
+  float* child_weight;   /* [C] W_c                                                    */
+  float* child_upper;    /* [C] u(b') of Eq. 11                                        */
+  float* child_lower;    /* [C] l(b') of Eq. 12                                        */
+  uint32_t* child_obs;   /* [C*obs_words] the child's observation key z                */
+  /* per scenario, only with DESPOT_X_RECORD_SCENARIO (world == 1), ordered
+   * (leaf, action, position in the leaf); S >= A * sum_l n_scen[l]:          */
+  uint64_t scen_capacity;
+  uint32_t* scen_obs;     /* [S*obs_words] z after the expansion step               */
+  float* scen_reward;     /* [S] r                                                   */
+  float* scen_upper;      /* [S] u(s') (0 if terminal)                               */
+  float* scen_lower;      /* [S] roll-out return lambda (0 if terminal)              */
+  uint32_t* scen_len;     /* [S] roll-out length                                     */
+  uint64_t* scen_hash;    /* [S] FNV-1a-64 of the roll-out's joint actions           */
+  uint32_t* scen_states;  /* [S*state_words] s' after the expansion step             */
+  /* host-side results */
+  uint64_t scenario_steps; /* out: steps g(s,a,phi) on non-terminal states (this rank) */
+  uint32_t num_children;   /* out: total children C used                              */
+  uint32_t pad;
+  /* out with DESPOT_X_TIMING: [0] update (K1), [1] expansion + roll-outs +
+   * grouping (K2), [2] child order / CSR / outputs (K3a-c), [3] whole call
+   * from the first enqueued operation to the last (device time, ms)          */
+  float phase_ms[4];
+} despot_expansion;
+
+/* One batch: update (world-local) -> expansion + bounds + roll-outs + grouping
+ * -> child ordering, CSR and outputs.  `leaves` is a host array of L <= 4096
+ * descriptors.  Synchronous.  With world > 1 use the begin/exchange/end form.
+ * Errors: EMODEL (action out of range), EINVAL (see enum), ECAPACITY, EHASH,
+ * ENOMEM, ECUDA.  On error outputs are unspecified and nodes created by the
+ * call are freed. */
+int despot_expand_batch(despot_model* model, const despot_leaf* leaves, uint32_t L,
+                        despot_expansion* out, void* stream);
+
+/* Multi-GPU scenario sharding: every rank calls with identical
+ * leaves; between begin and end the caller sums `sums` and mins `mins` over
+ * the ranks in place (e.g. NCCL all-reduce on `stream`); `end` then produces
+ * identical outputs on every rank.  The sums are exact int64 fixed-point
+ * partials, so the result does not depend on the reduction order. */
+typedef struct despot_batch despot_batch;
+typedef struct {
+  int64_t* sums;   /* device [n_sums]  all-reduce SUM (int64)  */
+  uint64_t n_sums;
+  int32_t* mins;   /* device [n_mins]  all-reduce MIN (int32)  */
+  uint64_t n_mins;
+} despot_exchange;
+int despot_expand_begin(despot_model* model, const despot_leaf* leaves, uint32_t L,
+                        uint32_t flags, void* stream, despot_batch** batch_out);
+int despot_batch_exchange(despot_batch* batch, despot_exchange* out);
+/* Completes (and frees) the batch; out->flags must equal begin's flags. */
+int despot_expand_end(despot_batch* batch, despot_expansion* out, void* stream);
+/* Abandons a begun batch (frees it and the nodes it created). */
+int despot_batch_abort(despot_batch* batch);
+
+/* Eqs. 11-12 at the node's own depth, e.g. to initialise the root's bounds
+ * (R: SURVEY §3.4): weighted means over the node's scenarios of u(s) and of a
+ * default-policy roll-out from depth Delta (this rank's scenarios).  per_scen
+ * arrays [n] are optional (host).  Synchronous.  Errors: EINVAL, ECUDA. */
+int despot_rollout_bounds(despot_model* model, despot_node node, float* upper_mean,
+                          float* lower_mean, float* per_scen_upper, float* per_scen_lower,
+                          void* stream);
+
+/* Raw scenario stream words, for tests of the generator: out[i] = word k of
+ * scenario ids[i] at depth t (tag 0), R13.  Host arrays, synchronous. */
+int despot_stream_words(despot_model* model, uint64_t stream_seed, const uint32_t* ids,
+                        uint32_t n, uint32_t t, uint32_t k, uint32_t* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,163 @@
+// common.cuh -- shared device-side definitions of libdespot (sm_100a).
+//
+// DevModel is the immutable, host-built description of one model (its
+// parameters plus the lookup tables the kernels stage into shared memory).
+// Nothing here is shared with oracle/: the CUDA path is an independent
+// implementation of the model cards in DESIGN.md §3.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hd {
+
+constexpr int kGpowN = 256;          // gamma^k table, k < 256 (D <= 250)
+constexpr int kRsMaxRocks = 31;
+constexpr int kRsMaxN = 32;
+constexpr int kRsMaxD2 = 2 * 31 * 31 + 1;
+constexpr int kNavMaxN = 16;
+constexpr int kNavMaxWords = 7;      // unknown-cell words (n <= 16 -> <= 208 cells)
+constexpr int kCarMaxPeds = 31;
+constexpr uint32_t kMaxLeaves = 4096;
+constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
+constexpr uint64_t kFnvPrime = 0x100000001b3ull;
+
+enum Kind : int32_t { kTiger = 1, kRockSample = 2, kNav = 3, kCar = 4 };
+
+struct DevModel {
+  int32_t kind;
+  uint32_t A, SW, OW, slots, D, terminal_slot, elements;
+  double gamma, tail;
+  double fx, inv_fx;           // fixed-point scale of the exact reductions
+  double gpow[kGpowN];         // gamma^k (host pow, double)
+  // tiger
+  uint64_t t_listen;
+  // rocksample / MARS
+  int32_t n, m, R, policy_east;
+  int32_t base;                // 5 + m sub-actions per robot
+  int8_t rx[32], ry[32];
+  int8_t rock_at[kRsMaxN * kRsMaxN];
+  uint8_t pos_rock[32];        // default-policy position -> rock index
+  uint32_t range_mask[2];      // policy positions handled by robot r
+  uint32_t d2max;
+  uint32_t sense_thr_m1[kRsMaxD2];  // T(accuracy(d^2)) - 1 (T >= 2^31 > 0)
+  // navigation
+  int32_t wall_y, gate_x[2], goal_x, goal_y, nav_words;
+  uint64_t t_fail, t_flip;
+  uint8_t nbr[kNavMaxN * kNavMaxN][8];  // neighbour k of cell c: 0 free, 1 occupied,
+                                        // 2 gate0, 3 gate1, 4+idx unknown cell idx
+  // car
+  int32_t peds;
+  uint64_t t_car_fail;
+  float noise_scale;
+};
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11): 10 rounds of two 32x32->64 products,
+// key bumped by the Weyl constants between rounds.  Stream address of
+// scenario id at depth t, word k: ctr = (id, t, k >> 2, tag), key = seed.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0;
+    const uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
+// event of probability p: (uint64)u < T(p), T(p) = floor(p 2^32) (R14)
+__device__ __forceinline__ bool event(uint32_t u, uint64_t T) { return (uint64_t)u < T; }
+
+// ---------------------------------------------------------------------------
+// Per-leaf descriptor built by the host for one batch.
+// ---------------------------------------------------------------------------
+struct LeafDev {
+  const uint32_t* p_ids;
+  const float* p_w;
+  const uint32_t* p_states;  // SoA, row stride p_cap
+  const uint32_t* p_keys;    // parent key table [A][p_kcap][OW]
+  const uint32_t* p_nchild;  // [A]
+  uint32_t p_cap, p_n, p_kcap;
+  uint32_t* ids;             // leaf arena (== parent's for action == -1)
+  float* w;
+  uint32_t* states;
+  uint32_t cap;
+  uint32_t* keys;            // leaf key table [A][kcap][OW], written at expansion
+  uint32_t* nchild;          // [A]
+  uint32_t kcap;
+  int32_t action;
+  uint32_t child, depth;
+  uint32_t seed_lo, seed_hi;
+  double inv_wroot, wroot;
+};
+
+// error bits of a batch
+enum : uint32_t { kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u };
+
+struct BatchDev {
+  const DevModel* model;
+  const LeafDev* leaves;
+  uint32_t L, A, S;          // S = dense slots per (leaf, action) (or per-leaf cap for sparse)
+  uint32_t* n_leaf;          // [L] local scenarios per leaf (K1)
+  uint32_t* tile_off;        // [L+1] K2 warp tiles prefix
+  uint64_t* scen_off;        // [L+1] per-scenario record prefix (A * n)
+  int64_t* sums;             // exchange SUM block
+  int32_t* mins;             // exchange MIN block
+  uint32_t* rank;            // [L*A*S] child ordinal of a slot
+  uint32_t* nc;              // [L*A] children per (leaf, action)
+  uint32_t* err;
+  // outputs (device)
+  uint32_t* n_scen;
+  float* weight;
+  float *act_reward, *act_upper, *act_lower;
+  uint32_t* child_begin;
+  uint32_t child_capacity;
+  uint32_t *child_count, *child_first;
+  float *child_weight, *child_upper, *child_lower;
+  uint32_t* child_obs;
+  uint64_t scen_capacity;
+  uint32_t* scen_obs;
+  float *scen_reward, *scen_upper, *scen_lower;
+  uint32_t* scen_len;
+  uint64_t* scen_hash;
+  uint32_t* scen_states;
+  // sparse-key scratch
+  uint64_t* sp_hash;         // [L*A*S] per-slot key hash (0 = empty)
+  uint32_t* sp_item;         // [L*A*S] scenario position holding the slot's key
+  uint32_t* sp_keys;         // [L*A*S*OW] per-item observation keys (position-indexed)
+};
+
+// layout of the SUM block: W, U, LAMBDA, N per slot; R, Uq, Lq per action; steps
+struct SumLayout {
+  uint64_t las, la;
+  __host__ __device__ uint64_t W(uint64_t i) const { return i; }
+  __host__ __device__ uint64_t U(uint64_t i) const { return las + i; }
+  __host__ __device__ uint64_t Lm(uint64_t i) const { return 2 * las + i; }
+  __host__ __device__ uint64_t N(uint64_t i) const { return 3 * las + i; }
+  __host__ __device__ uint64_t Q(uint64_t la_i, int k) const { return 4 * las + 3 * la_i + k; }
+  __host__ __device__ uint64_t steps() const { return 4 * las + 3 * la; }
+  __host__ __device__ uint64_t total() const { return 4 * las + 3 * la + 1; }
+};
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_sum32(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+
+// exact fixed-point quantisation of a normalised weighted value
+__device__ __forceinline__ int64_t fxq(double v, double fx) { return __double2ll_rn(v * fx); }
+
+}  // namespace hd

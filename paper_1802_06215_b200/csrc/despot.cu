@@ -1,0 +1,1222 @@
+// despot.cu -- host side of libdespot: the C ABI of include/despot.h, model
+// loading (parameter parsing and lookup tables built from the model cards of
+// DESIGN.md §3), node arenas, and the launch sequence of a batch
+// (K1 -> K2pre -> K2 -> [exchange] -> K3a -> K3b -> K3c).  Every step of the
+// hot path runs in the kernels of kernels.cuh / finalize.cuh.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/despot.h"
+#include "common.cuh"
+#include "finalize.cuh"
+#include "kernels.cuh"
+#include "models.cuh"
+#include "model_car.cuh"
+#include "kernels_sparse.cuh"
+
+using namespace hd;
+
+// ===========================================================================
+// errors
+// ===========================================================================
+static thread_local std::string g_err;
+static int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+extern "C" const char* despot_last_error(void) { return g_err.c_str(); }
+extern "C" int despot_abi_version(void) { return DESPOT_ABI_VERSION; }
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      if (e_ == cudaErrorMemoryAllocation) return set_err(DESPOT_ENOMEM, "%s: %s", #call,      \
+                                                          cudaGetErrorString(e_));            \
+      return set_err(DESPOT_ECUDA, "%s: %s", #call, cudaGetErrorString(e_));                  \
+    }                                                                                         \
+  } while (0)
+
+// ===========================================================================
+// parameter parsing ("key=value key=value"), independent of oracle/
+// ===========================================================================
+namespace {
+bool get_param(const std::string& params, const std::string& key, std::string& val) {
+  size_t p = 0;
+  while (p < params.size()) {
+    while (p < params.size() && isspace((unsigned char)params[p])) ++p;
+    size_t e = p;
+    while (e < params.size() && !isspace((unsigned char)params[e])) ++e;
+    if (e > p) {
+      std::string tok = params.substr(p, e - p);
+      size_t eq = tok.find('=');
+      if (eq != std::string::npos && tok.substr(0, eq) == key) {
+        val = tok.substr(eq + 1);
+        return true;
+      }
+    }
+    p = e;
+  }
+  return false;
+}
+double pd(const std::string& params, const char* key, double dflt) {
+  std::string v;
+  return get_param(params, key, v) ? strtod(v.c_str(), nullptr) : dflt;
+}
+long pi(const std::string& params, const char* key, long dflt) {
+  std::string v;
+  return get_param(params, key, v) ? strtol(v.c_str(), nullptr, 10) : dflt;
+}
+bool pxy(const std::string& params, const char* key, std::vector<int>& xs, std::vector<int>& ys) {
+  std::string v;
+  if (!get_param(params, key, v)) return false;
+  xs.clear();
+  ys.clear();
+  const char* p = v.c_str();
+  while (*p) {
+    char* e;
+    long x = strtol(p, &e, 10);
+    if (*e != ':') return false;
+    long y = strtol(e + 1, &e, 10);
+    xs.push_back((int)x);
+    ys.push_back((int)y);
+    if (*e == ',') ++e;
+    else if (*e) return false;
+    p = e;
+  }
+  return true;
+}
+bool plist(const std::string& params, const char* key, std::vector<int>& xs) {
+  std::string v;
+  if (!get_param(params, key, v)) return false;
+  xs.clear();
+  const char* p = v.c_str();
+  while (*p) {
+    char* e;
+    xs.push_back((int)strtol(p, &e, 10));
+    if (*e == ',') ++e;
+    else if (*e) return false;
+    p = e;
+  }
+  return true;
+}
+// T(p) = floor(p 2^32), event iff (uint64)u < T (R14)
+uint64_t thresh(double p) {
+  if (p <= 0.0) return 0;
+  if (p >= 1.0) return 4294967296ull;
+  return (uint64_t)std::floor(p * 4294967296.0);
+}
+}  // namespace
+
+// ===========================================================================
+// model, nodes, batches
+// ===========================================================================
+struct Block {
+  void* ptr = nullptr;
+  cudaStream_t stream = nullptr;
+  ~Block() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+struct Node {
+  despot_model* model;
+  std::shared_ptr<Block> block;
+  uint32_t* ids;
+  float* w;
+  uint32_t* states;
+  uint32_t* nchild;
+  uint32_t* keys;
+  uint32_t cap, kcap;
+  uint32_t n;  // local scenarios (host copy, valid once the creating call returned)
+  uint32_t depth;
+  uint64_t seed;
+  double wroot;
+  bool expanded;
+};
+
+struct despot_model {
+  DevModel host;
+  DevModel* dev = nullptr;
+  std::string kind;
+  int device = 0, rank = 0, world = 1;
+  uint32_t flags = 0;
+  int num_sms = 148;
+  std::atomic<bool> failed{false};
+  std::mutex mu;
+  std::unordered_set<Node*> nodes;
+  int k2_occ = 0;
+};
+
+struct despot_batch {
+  despot_model* model;
+  cudaStream_t stream;
+  uint32_t L, A, S, flags;
+  std::vector<despot_leaf> leaves;
+  std::vector<Node*> leaf_node;  // node expanded for each leaf (new or existing)
+  std::vector<bool> is_new;
+  std::shared_ptr<Block> new_block;
+  void* scratch = nullptr;
+  BatchDev bd{};
+  SparseItemOut io{};
+  void* pinned = nullptr;  // leaf-table staging, owned until the batch syncs
+  bool sparse = false;
+  uint64_t n_sums = 0, n_mins = 0;
+  bool timing = false;
+  cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
+  void mark(int i) {
+    if (timing) cudaEventRecord(ev[i], stream);
+  }
+};
+
+namespace {
+
+Node* lookup(despot_model* m, despot_node h) {
+  Node* n = reinterpret_cast<Node*>(h);
+  std::lock_guard<std::mutex> g(m->mu);
+  return m->nodes.count(n) ? n : nullptr;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// bytes of a node arena with capacity cap
+size_t node_bytes(const DevModel& dm, uint32_t cap, uint32_t kcap) {
+  size_t b = 0;
+  b += align256((size_t)cap * 4);                        // ids
+  b += align256((size_t)cap * 4);                        // w
+  b += align256((size_t)cap * 4 * dm.SW);                // states
+  b += align256((size_t)dm.A * 4);                       // nchild
+  b += align256((size_t)dm.A * kcap * dm.OW * 4);        // keys
+  return b;
+}
+void carve_node(Node* nd, const DevModel& dm, char*& p) {
+  nd->ids = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)nd->cap * 4);
+  nd->w = reinterpret_cast<float*>(p);
+  p += align256((size_t)nd->cap * 4);
+  nd->states = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)nd->cap * 4 * dm.SW);
+  nd->nchild = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)dm.A * 4);
+  nd->keys = reinterpret_cast<uint32_t*>(p);
+  p += align256((size_t)dm.A * nd->kcap * dm.OW * 4);
+}
+uint32_t key_cap(const DevModel& dm, uint32_t cap) {
+  return dm.slots ? dm.slots : (cap ? cap : 1);
+}
+
+// fixed-point scale of the exact reductions: |sum of normalised values| <=
+// Vmax <= 2^(61 - shift)
+void set_fixed_point(DevModel& dm, double rmax, double umax) {
+  const double vmax = (rmax + std::fabs(dm.tail)) * (dm.D + 1) + umax + rmax;
+  int shift = 61 - (int)std::ceil(std::log2(vmax));
+  if (shift > 52) shift = 52;
+  if (shift < 16) shift = 16;
+  dm.fx = std::ldexp(1.0, shift);
+  dm.inv_fx = std::ldexp(1.0, -shift);
+}
+
+int build_model(const char* kind, const std::string& params, DevModel& dm) {
+  memset(&dm, 0, sizeof dm);
+  dm.gamma = pd(params, "gamma", 0.95);
+  dm.elements = 1;
+  std::string k(kind);
+  double rmax = 0, umax = 0;
+  if (k == "tiger") {
+    dm.kind = kTiger;
+    dm.A = 3; dm.SW = 1; dm.OW = 1; dm.slots = 4; dm.terminal_slot = 3;
+    dm.D = (uint32_t)pi(params, "D", 10);
+    dm.t_listen = thresh(pd(params, "p_listen", 0.85));
+    dm.tail = 0.0;
+    rmax = 100; umax = 10;
+  } else if (k == "rocksample") {
+    dm.kind = kRockSample;
+    dm.n = (int)pi(params, "n", 7);
+    dm.R = (int)pi(params, "robots", 1);
+    const double d0 = pd(params, "d0", 4.0);
+    std::vector<int> rx, ry, sx, sy;
+    if (!pxy(params, "rocks", rx, ry) || !pxy(params, "starts", sx, sy))
+      return set_err(DESPOT_EINVAL, "rocksample: need rocks=x:y,... and starts=x:y,...");
+    std::string pol;
+    dm.policy_east = get_param(params, "policy", pol) && pol == "east";
+    dm.m = (int)rx.size();
+    if (dm.R < 1 || dm.R > 2 || (int)sx.size() != dm.R || dm.m > kRsMaxRocks || dm.n < 1 ||
+        dm.n > kRsMaxN)
+      return set_err(DESPOT_EINVAL, "rocksample: need 1<=robots<=2, rocks<=31, n<=32");
+    dm.base = 5 + dm.m;
+    dm.A = 1;
+    for (int r = 0; r < dm.R; ++r) dm.A *= (uint32_t)dm.base;
+    dm.SW = 2; dm.OW = 1; dm.slots = (dm.R == 1 ? 3 : 9) + 1; dm.terminal_slot = dm.slots - 1;
+    dm.D = (uint32_t)pi(params, "D", 20);
+    dm.tail = 0.0;
+    dm.elements = (uint32_t)dm.R;
+    memset(dm.rock_at, -1, sizeof dm.rock_at);
+    for (int j = 0; j < dm.m; ++j) {
+      if (rx[j] < 0 || ry[j] < 0 || rx[j] >= dm.n || ry[j] >= dm.n)
+        return set_err(DESPOT_EINVAL, "rocksample: rock off the grid");
+      if (dm.rock_at[ry[j] * dm.n + rx[j]] >= 0) return set_err(DESPOT_EINVAL, "rocksample: two rocks share a cell");
+      dm.rx[j] = (int8_t)rx[j];
+      dm.ry[j] = (int8_t)ry[j];
+      dm.rock_at[ry[j] * dm.n + rx[j]] = (int8_t)j;
+    }
+    // sensing accuracy 0.5 (1 + 2^(-d/d0)) (R17): thresholds by d^2
+    dm.d2max = (uint32_t)(2 * (dm.n - 1) * (dm.n - 1));
+    for (uint32_t d2 = 0; d2 <= dm.d2max; ++d2) {
+      const double acc = 0.5 * (1.0 + std::pow(2.0, -std::sqrt((double)d2) / d0));
+      const uint64_t T = thresh(acc);
+      dm.sense_thr_m1[d2] = (uint32_t)(T - 1);  // T >= 2^31: event iff u <= T - 1
+    }
+    // default-policy positions: robot r handles rocks j % R == r, sorted (x, y, j)
+    int pos = 0;
+    for (int r = 0; r < dm.R; ++r) {
+      std::vector<int> h;
+      for (int j = 0; j < dm.m; ++j)
+        if (j % dm.R == r) h.push_back(j);
+      for (size_t a = 1; a < h.size(); ++a)
+        for (size_t b = a; b > 0; --b) {
+          const int p = h[b - 1], q = h[b];
+          const bool less = rx[q] < rx[p] || (rx[q] == rx[p] && (ry[q] < ry[p] || (ry[q] == ry[p] && q < p)));
+          if (!less) break;
+          std::swap(h[b - 1], h[b]);
+        }
+      uint32_t mask = 0;
+      for (int j : h) {
+        dm.pos_rock[pos] = (uint8_t)j;
+        mask |= 1u << pos;
+        ++pos;
+      }
+      dm.range_mask[r] = mask;
+    }
+    rmax = 10.0 * dm.R;
+    umax = 10.0 * (dm.m + dm.R);
+  } else if (k == "nav") {
+    dm.kind = kNav;
+    dm.n = (int)pi(params, "n", 13);
+    dm.wall_y = (int)pi(params, "wall_y", dm.n / 2);
+    std::vector<int> gates, gx, gy, lx, ly;
+    if (!plist(params, "gates", gates) || gates.size() != 2) gates = {3, 9};
+    dm.gate_x[0] = gates[0];
+    dm.gate_x[1] = gates[1];
+    if (pxy(params, "goal", gx, gy) && gx.size() == 1) {
+      dm.goal_x = gx[0];
+      dm.goal_y = gy[0];
+    } else {
+      dm.goal_x = dm.n / 2;
+      dm.goal_y = dm.n - 1;
+    }
+    pxy(params, "landmarks", lx, ly);
+    dm.t_fail = thresh(pd(params, "p_fail", 0.03));
+    dm.t_flip = thresh(pd(params, "p_flip", 0.03));
+    if (dm.n < 3 || dm.n > kNavMaxN || dm.wall_y <= 0 || dm.wall_y >= dm.n - 1)
+      return set_err(DESPOT_EINVAL, "nav: need 3 <= n <= 16 and 0 < wall_y < n-1");
+    // cell classes: rows 0 and n-1 known free, wall row obstacles except the
+    // two gates, landmarks obstacles, everything else unknown (row-major idx)
+    std::vector<int> cls(dm.n * dm.n), idx(dm.n * dm.n, -1);
+    int nu = 0;
+    for (int y = 0; y < dm.n; ++y)
+      for (int x = 0; x < dm.n; ++x) {
+        int c = 4;  // unknown
+        if (y == 0 || y == dm.n - 1) c = 0;
+        else if (y == dm.wall_y) c = x == dm.gate_x[0] ? 2 : x == dm.gate_x[1] ? 3 : 1;
+        else
+          for (size_t l = 0; l < lx.size(); ++l)
+            if (lx[l] == x && ly[l] == y) c = 1;
+        cls[y * dm.n + x] = c;
+        if (c == 4) idx[y * dm.n + x] = nu++;
+      }
+    dm.nav_words = (nu + 31) / 32;
+    if (dm.nav_words > kNavMaxWords || dm.nav_words < 1) return set_err(DESPOT_EINVAL, "nav: unknown cells");
+    const int DX[8] = {0, 1, 1, 1, 0, -1, -1, -1}, DY[8] = {-1, -1, 0, 1, 1, 1, 0, -1};
+    for (int y = 0; y < dm.n; ++y)
+      for (int x = 0; x < dm.n; ++x)
+        for (int kk = 0; kk < 8; ++kk) {
+          const int tx = x + DX[kk], ty = y + DY[kk];
+          uint8_t d;
+          if (tx < 0 || ty < 0 || tx >= dm.n || ty >= dm.n) d = 1;
+          else {
+            const int c = cls[ty * dm.n + tx];
+            d = c == 4 ? (uint8_t)(4 + idx[ty * dm.n + tx]) : (uint8_t)c;
+          }
+          dm.nbr[y * dm.n + x][kk] = d;
+        }
+    dm.A = 9; dm.SW = 1 + (uint32_t)dm.nav_words; dm.OW = 1; dm.slots = 257; dm.terminal_slot = 256;
+    dm.D = (uint32_t)pi(params, "D", 90);
+    dm.tail = (double)(-0.2f) / (1.0 - dm.gamma);  // stay forever (R6)
+    rmax = 20; umax = 20;
+  } else if (k == "car") {
+    dm.kind = kCar;
+    dm.peds = (int)pi(params, "peds", 20);
+    if (dm.peds < 1 || dm.peds > kCarMaxPeds) return set_err(DESPOT_EINVAL, "car: 1 <= peds <= 31");
+    dm.t_car_fail = thresh(pd(params, "p_fail", 0.01));
+    dm.noise_scale = (float)pd(params, "noise", 0.00133);
+    dm.A = 3; dm.SW = 4 + 2 * (uint32_t)dm.peds; dm.OW = 1 + (uint32_t)dm.peds; dm.slots = 0;
+    dm.terminal_slot = 0;
+    dm.D = (uint32_t)pi(params, "D", 90);
+    dm.elements = 1 + (uint32_t)dm.peds;
+    dm.tail = (double)(-0.1f) / (1.0 - dm.gamma);
+    rmax = 1000.0 * 4.5 + 100.2;
+    umax = 100;
+  } else {
+    return set_err(DESPOT_EINVAL, "unknown model kind '%s'", kind);
+  }
+  if (!(dm.gamma > 0.0 && dm.gamma < 1.0) || dm.D < 1 || dm.D >= (uint32_t)kGpowN - 2)
+    return set_err(DESPOT_EINVAL, "need 0 < gamma < 1 and 1 <= D <= 250");
+  for (int i = 0; i < kGpowN; ++i) dm.gpow[i] = std::pow(dm.gamma, (double)i);
+  set_fixed_point(dm, rmax, umax);
+  return DESPOT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel dispatch over model templates
+// ---------------------------------------------------------------------------
+template <class F>
+int dispatch_dense(const DevModel& dm, F&& f) {
+  switch (dm.kind) {
+    case kTiger: return f(Tiger{});
+    case kRockSample: return dm.R == 1 ? f(RockSample<1>{}) : f(RockSample<2>{});
+    case kNav:
+      switch (dm.nav_words) {
+        case 1: return f(Nav<1>{});
+        case 2: return f(Nav<2>{});
+        case 3: return f(Nav<3>{});
+        case 4: return f(Nav<4>{});
+        case 5: return f(Nav<5>{});
+        case 6: return f(Nav<6>{});
+        default: return f(Nav<7>{});
+      }
+    default: return set_err(DESPOT_EINVAL, "not a dense-observation model");
+  }
+}
+
+template <class F>
+int dispatch_car(const DevModel& dm, F&& f) {
+  if (dm.peds <= 2) return f(CarThreadT<2>{});
+  if (dm.peds <= 8) return f(CarThreadT<8>{});
+  if (dm.peds <= 20) return f(CarThreadT<20>{});
+  return f(CarThreadT<31>{});
+}
+
+int check_launch(despot_model* m, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    m->failed = true;
+    return set_err(DESPOT_ECUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  }
+  return DESPOT_OK;
+}
+
+// Pinned host staging buffers.  A batch owns its buffer from the async H2D
+// of its leaf table until it has synchronised (end / abort), so concurrent or
+// interleaved batches (e.g. the sharded begin/exchange/end form) never share
+// one.
+class PinnedPool {
+ public:
+  void* acquire(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      for (size_t i = 0; i < free_.size(); ++i)
+        if (free_[i].second >= bytes) {
+          void* p = free_[i].first;
+          sizes_[p] = free_[i].second;
+          free_.erase(free_.begin() + i);
+          return p;
+        }
+    }
+    size_t sz = 4096;
+    while (sz < bytes) sz <<= 1;
+    void* p = nullptr;
+    if (cudaMallocHost(&p, sz) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(mu_);
+    sizes_[p] = sz;
+    return p;
+  }
+  void release(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(mu_);
+    free_.push_back({p, sizes_[p]});
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<void*, size_t>> free_;
+  std::unordered_map<void*, size_t> sizes_;
+};
+PinnedPool& pinned_pool() {
+  static PinnedPool* p = new PinnedPool();  // never destroyed (process lifetime)
+  return *p;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" int despot_model_load(const char* kind, const char* params, const despot_opts* opts,
+                                 despot_model** out) {
+  if (!kind || !out) return set_err(DESPOT_EINVAL, "null argument");
+  std::unique_ptr<despot_model> m(new despot_model());
+  int rc = build_model(kind, params ? params : "", m->host);
+  if (rc) return rc;
+  m->kind = kind;
+  if (opts) {
+    m->device = opts->device;
+    m->rank = opts->rank;
+    m->world = opts->world < 1 ? 1 : opts->world;
+    m->flags = opts->flags;
+  }
+  if (m->rank < 0 || m->rank >= m->world) return set_err(DESPOT_EINVAL, "rank outside [0, world)");
+  if (m->world > 1 && m->host.slots == 0)
+    return set_err(DESPOT_EINVAL, "scenario sharding needs a dense-observation model");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return set_err(DESPOT_ECUDA, "no CUDA device (libdespot has no CPU fallback)");
+  CU(cudaSetDevice(m->device));
+  CU(cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device));
+  // keep freed stream-ordered memory in the pool (per-batch scratch is reused)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, m->device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  CU(cudaMalloc(&m->dev, sizeof(DevModel)));
+  CU(cudaMemcpy(m->dev, &m->host, sizeof(DevModel), cudaMemcpyHostToDevice));
+  *out = m.release();
+  return DESPOT_OK;
+}
+
+extern "C" int despot_model_info_get(const despot_model* m, despot_model_info* o) {
+  if (!m || !o) return set_err(DESPOT_EINVAL, "null argument");
+  o->num_actions = m->host.A;
+  o->state_words = m->host.SW;
+  o->obs_words = m->host.OW;
+  o->obs_slots = m->host.slots;
+  o->max_depth = m->host.D;
+  o->elements = m->host.elements;
+  o->gamma = m->host.gamma;
+  o->tail = m->host.tail;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_model_free(despot_model* m) {
+  if (!m) return DESPOT_OK;
+  cudaSetDevice(m->device);
+  {
+    std::lock_guard<std::mutex> g(m->mu);
+    for (Node* n : m->nodes) delete n;
+    m->nodes.clear();
+  }
+  cudaDeviceSynchronize();
+  if (m->dev) cudaFree(m->dev);
+  delete m;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_belief_load(despot_model* m, const uint32_t* states_soa, const float* weights,
+                                  uint32_t K, uint64_t seed, void* stream, despot_node* root_out) {
+  if (!m || !states_soa || !weights || !root_out) return set_err(DESPOT_EINVAL, "null argument");
+  if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
+  if (K == 0) return set_err(DESPOT_EINVAL, "empty belief (S:121)");
+  if (K >= 0x7FFFFFFFu) return set_err(DESPOT_EINVAL, "K must be < 2^31");
+  const DevModel& dm = m->host;
+  double wroot = 0.0;
+  for (uint32_t i = 0; i < K; ++i) {
+    if (!(weights[i] > 0.0f) || !std::isfinite(weights[i])) return set_err(DESPOT_EINVAL, "weights must be finite and > 0");
+    wroot += (double)weights[i];
+  }
+  // this rank's shard: global ids with id % world == rank
+  std::vector<uint32_t> ids;
+  for (uint32_t i = (uint32_t)m->rank; i < K; i += (uint32_t)m->world) ids.push_back(i);
+  const uint32_t n = (uint32_t)ids.size();
+  const uint32_t cap = n ? n : 1;
+  std::vector<uint32_t> hbuf((size_t)cap * (2 + dm.SW));
+  for (uint32_t i = 0; i < n; ++i) {
+    hbuf[i] = ids[i];
+    float wv = weights[ids[i]];
+    memcpy(&hbuf[cap + i], &wv, 4);
+    for (uint32_t k = 0; k < dm.SW; ++k) hbuf[(size_t)(2 + k) * cap + i] = states_soa[(size_t)k * K + ids[i]];
+  }
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  auto blk = std::make_shared<Block>();
+  blk->stream = st;
+  const uint32_t kcap = key_cap(dm, cap);
+  CU(cudaMallocAsync(&blk->ptr, node_bytes(dm, cap, kcap), st));
+  Node* nd = new Node();
+  nd->model = m;
+  nd->block = blk;
+  nd->cap = cap;
+  nd->kcap = kcap;
+  char* p = static_cast<char*>(blk->ptr);
+  carve_node(nd, dm, p);
+  nd->n = n;
+  nd->depth = 0;
+  nd->seed = seed;
+  nd->wroot = wroot;
+  nd->expanded = false;
+  int rc = DESPOT_OK;
+  if (cudaMemcpyAsync(nd->ids, hbuf.data(), (size_t)cap * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(nd->w, &hbuf[cap], (size_t)cap * 4, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(nd->states, &hbuf[2 * (size_t)cap], (size_t)cap * 4 * dm.SW, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess ||
+      cudaMemsetAsync(nd->nchild, 0, (size_t)dm.A * 4, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    rc = set_err(DESPOT_ECUDA, "belief upload failed");
+  if (rc) {
+    delete nd;
+    return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(m->mu);
+    m->nodes.insert(nd);
+  }
+  *root_out = reinterpret_cast<despot_node>(nd);
+  return DESPOT_OK;
+}
+
+extern "C" int despot_node_info(despot_model* m, despot_node h, uint32_t* n, uint32_t* depth) {
+  Node* nd = m ? lookup(m, h) : nullptr;
+  if (!nd) return set_err(DESPOT_EINVAL, "unknown node");
+  if (n) *n = nd->n;
+  if (depth) *depth = nd->depth;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_node_read(despot_model* m, despot_node h, uint32_t* ids, float* w,
+                                uint32_t* states_soa, void* stream) {
+  Node* nd = m ? lookup(m, h) : nullptr;
+  if (!nd) return set_err(DESPOT_EINVAL, "unknown node");
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (ids) CU(cudaMemcpyAsync(ids, nd->ids, (size_t)nd->n * 4, cudaMemcpyDeviceToHost, st));
+  if (w) CU(cudaMemcpyAsync(w, nd->w, (size_t)nd->n * 4, cudaMemcpyDeviceToHost, st));
+  if (states_soa && nd->n)
+    CU(cudaMemcpy2DAsync(states_soa, (size_t)nd->n * 4, nd->states, (size_t)nd->cap * 4, (size_t)nd->n * 4,
+                         m->host.SW, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return DESPOT_OK;
+}
+
+extern "C" int despot_node_release(despot_model* m, despot_node h) {
+  if (!m) return set_err(DESPOT_EINVAL, "null model");
+  Node* nd = reinterpret_cast<Node*>(h);
+  {
+    std::lock_guard<std::mutex> g(m->mu);
+    if (!m->nodes.erase(nd)) return set_err(DESPOT_EINVAL, "unknown node");
+  }
+  cudaSetDevice(m->device);
+  delete nd;  // the arena block is freed (stream-ordered) with its last node
+  return DESPOT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batches
+// ---------------------------------------------------------------------------
+static void free_batch(despot_batch* b, bool drop_new_nodes) {
+  if (!b) return;
+  if (drop_new_nodes) {
+    std::lock_guard<std::mutex> g(b->model->mu);
+    for (size_t l = 0; l < b->leaf_node.size(); ++l)
+      if (b->is_new[l] && b->leaf_node[l]) {
+        b->model->nodes.erase(b->leaf_node[l]);
+        delete b->leaf_node[l];
+        b->leaf_node[l] = nullptr;
+      }
+  }
+  if (b->scratch) cudaFreeAsync(b->scratch, b->stream);
+  if (b->pinned) {
+    cudaStreamSynchronize(b->stream);  // the H2D from it must have completed
+    pinned_pool().release(b->pinned);
+  }
+  if (b->timing)
+    for (auto& e : b->ev)
+      if (e) cudaEventDestroy(e);
+  delete b;
+}
+
+static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
+  const DevModel& dm = m->host;
+  cudaStream_t st = b->stream;
+  uint64_t q_bound = 0;
+  for (uint32_t l = 0; l < b->L; ++l) q_bound += (uint64_t)dm.A * b->leaf_node[l]->cap;
+  b->mark(3);
+  if (m->flags & DESPOT_MF_UNFACTORED) {
+    dispatch_car(dm, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      const uint64_t g = std::min<uint64_t>((q_bound + 127) / 128, (uint64_t)m->num_sms * 16);
+      if (record) k2_car_thread<M, true><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+      else k2_car_thread<M, false><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+      return 0;
+    });
+  } else {
+    const uint64_t g = std::min<uint64_t>((q_bound + 3) / 4, (uint64_t)m->num_sms * 16);
+    if (record) k2_car_warp<true><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+    else k2_car_warp<false><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+  }
+  b->mark(4);
+  return check_launch(m, "K2(car)");
+}
+
+extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags,
+                                   void* stream, despot_batch** out) {
+  if (!m || !leaves || !out) return set_err(DESPOT_EINVAL, "null argument");
+  if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
+  if (L == 0 || L > kMaxLeaves) return set_err(DESPOT_EINVAL, "need 1 <= L <= %u", kMaxLeaves);
+  if ((flags & DESPOT_X_RECORD_SCENARIO) && m->world > 1)
+    return set_err(DESPOT_EINVAL, "RECORD_SCENARIO needs world == 1");
+  const DevModel& dm = m->host;
+  CU(cudaSetDevice(m->device));
+  std::unique_ptr<despot_batch> b(new despot_batch());
+  b->model = m;
+  b->stream = (cudaStream_t)stream;
+  b->L = L;
+  b->A = dm.A;
+  b->S = dm.slots;
+  b->sparse = dm.slots == 0;
+  b->flags = flags;
+  b->leaves.assign(leaves, leaves + L);
+  b->timing = flags & DESPOT_X_TIMING;
+  if (b->timing) {
+    for (auto& e : b->ev) CU(cudaEventCreate(&e));
+    b->mark(0);
+  }
+  b->leaf_node.assign(L, nullptr);
+  b->is_new.assign(L, false);
+  // validate, size the new arenas
+  std::vector<Node*> parent(L);
+  size_t new_bytes = 0;
+  for (uint32_t l = 0; l < L; ++l) {
+    const despot_leaf& lf = leaves[l];
+    Node* p = lookup(m, lf.parent);
+    if (!p) return set_err(DESPOT_EINVAL, "leaf %u: unknown parent node", l);
+    if (lf.action < -1 || lf.action >= (int32_t)dm.A)
+      return set_err(DESPOT_EMODEL, "leaf %u: action %d outside [-1, %u)", l, lf.action, dm.A);
+    if (lf.depth >= dm.D) return set_err(DESPOT_EINVAL, "leaf %u: depth %u >= D = %u", l, lf.depth, dm.D);
+    if (lf.action >= 0) {
+      if (!p->expanded) return set_err(DESPOT_EINVAL, "leaf %u: parent not expanded", l);
+      if (lf.depth != p->depth + 1) return set_err(DESPOT_EINVAL, "leaf %u: depth != parent depth + 1", l);
+      new_bytes += node_bytes(dm, p->cap, key_cap(dm, p->cap));
+    } else if (lf.depth != p->depth) {
+      return set_err(DESPOT_EINVAL, "leaf %u: depth != node depth", l);
+    }
+    parent[l] = p;
+  }
+  uint64_t q_bound = 0;  // sparse: per-item scratch bound sum_l A cap_l
+  if (b->sparse) {
+    uint32_t smax = 1;
+    for (uint32_t l = 0; l < L; ++l) {
+      smax = std::max(smax, parent[l]->cap);
+      q_bound += (uint64_t)dm.A * parent[l]->cap;
+    }
+    if (smax > 8192) return set_err(DESPOT_EINVAL, "sparse-key models: at most 8192 scenarios per leaf");
+    b->S = smax;
+  }
+  cudaStream_t st = b->stream;
+  if (new_bytes) {
+    b->new_block = std::make_shared<Block>();
+    b->new_block->stream = st;
+    CU(cudaMallocAsync(&b->new_block->ptr, new_bytes, st));
+  }
+  char* np = b->new_block ? static_cast<char*>(b->new_block->ptr) : nullptr;
+  std::vector<LeafDev> ld(L);
+  for (uint32_t l = 0; l < L; ++l) {
+    const despot_leaf& lf = leaves[l];
+    Node* p = parent[l];
+    Node* nd = p;
+    if (lf.action >= 0) {
+      nd = new Node();
+      nd->model = m;
+      nd->block = b->new_block;
+      nd->cap = p->cap;
+      nd->kcap = key_cap(dm, p->cap);
+      carve_node(nd, dm, np);
+      nd->n = 0;
+      nd->depth = lf.depth;
+      nd->seed = p->seed;
+      nd->wroot = p->wroot;
+      nd->expanded = false;
+      b->is_new[l] = true;
+    }
+    b->leaf_node[l] = nd;
+    LeafDev& d = ld[l];
+    d.p_ids = p->ids;
+    d.p_w = p->w;
+    d.p_states = p->states;
+    d.p_keys = p->keys;
+    d.p_nchild = p->nchild;
+    d.p_cap = p->cap;
+    d.p_n = p->n;
+    d.p_kcap = p->kcap;
+    d.ids = nd->ids;
+    d.w = nd->w;
+    d.states = nd->states;
+    d.cap = nd->cap;
+    d.keys = nd->keys;
+    d.nchild = nd->nchild;
+    d.kcap = nd->kcap;
+    d.action = lf.action;
+    d.child = lf.child;
+    d.depth = lf.depth;
+    d.seed_lo = (uint32_t)p->seed;
+    d.seed_hi = (uint32_t)(p->seed >> 32);
+    d.wroot = p->wroot;
+    d.inv_wroot = 1.0 / p->wroot;
+  }
+  {
+    std::lock_guard<std::mutex> g(m->mu);
+    for (uint32_t l = 0; l < L; ++l)
+      if (b->is_new[l]) m->nodes.insert(b->leaf_node[l]);
+  }
+  // scratch: leaves | n_leaf | tile_off | scen_off | sums | mins | rank | nc | err
+  const uint64_t LA = (uint64_t)L * dm.A, LAS = LA * b->S;
+  const SumLayout lay{LAS, LA};
+  b->n_sums = lay.total();
+  b->n_mins = LAS;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const size_t o_leaves = take(sizeof(LeafDev) * L), o_nleaf = take(4 * (size_t)L),
+               o_tile = take(4 * ((size_t)L + 1)), o_scen = take(8 * ((size_t)L + 1)),
+               o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
+               o_nc = take(4 * LA), o_err = take(4), o_item = take(b->sparse ? 4 * LAS : 0),
+               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound);
+  if (cudaMallocAsync(&b->scratch, off, st) != cudaSuccess) {
+    free_batch(b.release(), true);
+    return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
+  }
+  char* s = static_cast<char*>(b->scratch);
+  BatchDev& bd = b->bd;
+  bd.model = m->dev;
+  bd.leaves = reinterpret_cast<LeafDev*>(s + o_leaves);
+  bd.L = L;
+  bd.A = dm.A;
+  bd.S = b->S;
+  bd.n_leaf = reinterpret_cast<uint32_t*>(s + o_nleaf);
+  bd.tile_off = reinterpret_cast<uint32_t*>(s + o_tile);
+  bd.scen_off = reinterpret_cast<uint64_t*>(s + o_scen);
+  bd.sums = reinterpret_cast<int64_t*>(s + o_sums);
+  bd.mins = reinterpret_cast<int32_t*>(s + o_mins);
+  bd.rank = reinterpret_cast<uint32_t*>(s + o_rank);
+  bd.nc = reinterpret_cast<uint32_t*>(s + o_nc);
+  bd.err = reinterpret_cast<uint32_t*>(s + o_err);
+  if (b->sparse) {
+    bd.sp_item = reinterpret_cast<uint32_t*>(s + o_item);
+    b->io.hash = reinterpret_cast<uint64_t*>(s + o_hash);
+    b->io.keys = reinterpret_cast<uint32_t*>(s + o_keys);
+    b->io.q3 = reinterpret_cast<int64_t*>(s + o_q3);
+  }
+  void* hp = pinned_pool().acquire(sizeof(LeafDev) * L);
+  b->pinned = hp;
+  int rc = DESPOT_OK;
+  if (!hp) rc = set_err(DESPOT_ENOMEM, "pinned staging");
+  if (!rc) {
+    memcpy(hp, ld.data(), sizeof(LeafDev) * L);
+    if (cudaMemcpyAsync(s + o_leaves, hp, sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemsetAsync(bd.sums, 0, 8 * b->n_sums, st) != cudaSuccess ||
+        cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
+        cudaMemsetAsync(bd.err, 0, 4, st) != cudaSuccess)
+      rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
+  }
+  // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
+  // are bound in despot_expand_end (K2 runs there when RECORD is set, since
+  // the record pointers arrive with the output struct).
+  if (!rc && b->sparse) {
+    rc = dispatch_car(dm, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      b->mark(1);
+      k1_update_sparse<M><<<L, 256, 0, st>>>(bd);
+      if (int e = check_launch(m, "K1")) return e;
+      b->mark(2);
+      k2_prefix<<<1, 1024, 0, st>>>(bd);
+      return check_launch(m, "K2pre");
+    });
+    if (!rc && !(flags & DESPOT_X_RECORD_SCENARIO)) rc = launch_k2_sparse(m, b.get(), false);
+  } else if (!rc) {
+    rc = dispatch_dense(dm, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      b->mark(1);
+      k1_update<M><<<L, 256, 0, st>>>(bd);
+      if (int e = check_launch(m, "K1")) return e;
+      b->mark(2);
+      k2_prefix<<<1, 1024, 0, st>>>(bd);
+      return check_launch(m, "K2pre");
+    });
+  }
+  if (!rc && !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO)) {
+    // K2 now (the exchange block is complete after it)
+    rc = dispatch_dense(dm, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
+      auto kern = k2_expand_dense<M, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
+      if (occ < 1) occ = 1;
+      uint64_t tiles_bound = 0;
+      for (uint32_t l = 0; l < L; ++l) tiles_bound += (uint64_t)dm.A * ((parent[l]->cap + 31) / 32);
+      uint64_t grid = (tiles_bound + 3) / 4;
+      const uint64_t maxg = (uint64_t)m->num_sms * occ;
+      if (grid > maxg) grid = maxg;
+      if (grid < 1) grid = 1;
+      b->mark(3);
+      kern<<<(unsigned)grid, 128, smem, st>>>(bd, (uint32_t)tiles_bound);
+      b->mark(4);
+      return check_launch(m, "K2");
+    });
+  }
+  if (rc) {
+    free_batch(b.release(), true);
+    return rc;
+  }
+  *out = b.release();
+  return DESPOT_OK;
+}
+
+extern "C" int despot_batch_exchange(despot_batch* b, despot_exchange* out) {
+  if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
+  out->sums = b->bd.sums;
+  out->n_sums = b->n_sums;
+  out->mins = b->bd.mins;
+  out->n_mins = b->n_mins;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_batch_abort(despot_batch* b) {
+  if (!b) return DESPOT_OK;
+  cudaSetDevice(b->model->device);
+  free_batch(b, true);
+  return DESPOT_OK;
+}
+
+extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* stream) {
+  if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
+  despot_model* m = b->model;
+  const DevModel& dm = m->host;
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  b->stream = st;
+  const uint32_t L = b->L;
+  const uint64_t LA = (uint64_t)L * dm.A;
+  const bool dev_out = out->flags & DESPOT_X_DEVICE_OUTPUTS;
+  const bool record = b->flags & DESPOT_X_RECORD_SCENARIO;
+  BatchDev& bd = b->bd;
+  const uint32_t C = out->child_capacity;
+  bd.child_capacity = C;
+  bd.scen_capacity = record ? out->scen_capacity : 0;
+  if (!out->node || !out->n_scen || !out->weight || !out->act_reward || !out->act_upper || !out->act_lower ||
+      !out->child_begin || (C && (!out->child_count || !out->child_first || !out->child_weight ||
+                                  !out->child_upper || !out->child_lower || !out->child_obs))) {
+    free_batch(b, true);
+    return set_err(DESPOT_EINVAL, "missing output arrays");
+  }
+  if (record && (!out->scen_obs || !out->scen_reward || !out->scen_upper || !out->scen_lower || !out->scen_len ||
+                 !out->scen_hash)) {
+    free_batch(b, true);
+    return set_err(DESPOT_EINVAL, "RECORD_SCENARIO needs the scen_* arrays");
+  }
+  // output staging (host-output mode) in one allocation
+  void* stage = nullptr;
+  size_t so = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = so;
+    so += align256(bytes ? bytes : 4);
+    return o;
+  };
+  const uint64_t S = bd.scen_capacity;
+  const size_t o_ns = take(4 * L), o_w = take(4 * L), o_ar = take(4 * LA), o_au = take(4 * LA),
+               o_al = take(4 * LA), o_cb = take(4 * (LA + 1)), o_cc = take(4 * (size_t)C),
+               o_cf = take(4 * (size_t)C), o_cw = take(4 * (size_t)C), o_cu = take(4 * (size_t)C),
+               o_cl = take(4 * (size_t)C), o_co = take(4 * (size_t)C * dm.OW),
+               o_so = take(record ? 4 * S * dm.OW : 0), o_sr = take(record ? 4 * S : 0),
+               o_su = take(record ? 4 * S : 0), o_sl = take(record ? 4 * S : 0),
+               o_sn = take(record ? 4 * S : 0), o_sh = take(record ? 8 * S : 0),
+               o_ss = take(record && out->scen_states ? 4 * S * dm.SW : 0);
+  if (dev_out) {
+    bd.n_scen = out->n_scen;
+    bd.weight = out->weight;
+    bd.act_reward = out->act_reward;
+    bd.act_upper = out->act_upper;
+    bd.act_lower = out->act_lower;
+    bd.child_begin = out->child_begin;
+    bd.child_count = out->child_count;
+    bd.child_first = out->child_first;
+    bd.child_weight = out->child_weight;
+    bd.child_upper = out->child_upper;
+    bd.child_lower = out->child_lower;
+    bd.child_obs = out->child_obs;
+    bd.scen_obs = out->scen_obs;
+    bd.scen_reward = out->scen_reward;
+    bd.scen_upper = out->scen_upper;
+    bd.scen_lower = out->scen_lower;
+    bd.scen_len = out->scen_len;
+    bd.scen_hash = out->scen_hash;
+    bd.scen_states = out->scen_states;
+  } else {
+    if (cudaMallocAsync(&stage, so, st) != cudaSuccess) {
+      free_batch(b, true);
+      return set_err(DESPOT_ENOMEM, "output staging (%zu bytes)", so);
+    }
+    char* p = static_cast<char*>(stage);
+    bd.n_scen = reinterpret_cast<uint32_t*>(p + o_ns);
+    bd.weight = reinterpret_cast<float*>(p + o_w);
+    bd.act_reward = reinterpret_cast<float*>(p + o_ar);
+    bd.act_upper = reinterpret_cast<float*>(p + o_au);
+    bd.act_lower = reinterpret_cast<float*>(p + o_al);
+    bd.child_begin = reinterpret_cast<uint32_t*>(p + o_cb);
+    bd.child_count = reinterpret_cast<uint32_t*>(p + o_cc);
+    bd.child_first = reinterpret_cast<uint32_t*>(p + o_cf);
+    bd.child_weight = reinterpret_cast<float*>(p + o_cw);
+    bd.child_upper = reinterpret_cast<float*>(p + o_cu);
+    bd.child_lower = reinterpret_cast<float*>(p + o_cl);
+    bd.child_obs = reinterpret_cast<uint32_t*>(p + o_co);
+    bd.scen_obs = reinterpret_cast<uint32_t*>(p + o_so);
+    bd.scen_reward = reinterpret_cast<float*>(p + o_sr);
+    bd.scen_upper = reinterpret_cast<float*>(p + o_su);
+    bd.scen_lower = reinterpret_cast<float*>(p + o_sl);
+    bd.scen_len = reinterpret_cast<uint32_t*>(p + o_sn);
+    bd.scen_hash = reinterpret_cast<uint64_t*>(p + o_sh);
+    bd.scen_states = (record && out->scen_states) ? reinterpret_cast<uint32_t*>(p + o_ss) : nullptr;
+  }
+  int rc = DESPOT_OK;
+  if (record && b->sparse) {
+    rc = launch_k2_sparse(m, b, true);
+  } else if (record) {
+    rc = dispatch_dense(dm, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
+      auto kern = k2_expand_dense<M, true>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      b->mark(3);
+      kern<<<(unsigned)(m->num_sms * 4), 128, smem, st>>>(bd, 0);
+      b->mark(4);
+      return check_launch(m, "K2(record)");
+    });
+  }
+  const unsigned warps_per_cta = 4;
+  const unsigned g3 = (unsigned)((LA + warps_per_cta - 1) / warps_per_cta);
+  b->mark(5);
+  if (!rc && b->sparse) {
+    const size_t smem = 16 * (size_t)b->S;
+    cudaFuncSetAttribute(k3_group_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io);
+    rc = check_launch(m, "K3a(sparse)");
+  } else if (!rc) {
+    k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 4, st>>>(bd);
+    rc = check_launch(m, "K3a");
+  }
+  if (!rc) {
+    k3_scan<<<1, 1024, 0, st>>>(bd);
+    rc = check_launch(m, "K3b");
+  }
+  if (!rc && b->sparse) {
+    k3_write_sparse<<<g3, 128, 0, st>>>(bd, b->io);
+    rc = check_launch(m, "K3c(sparse)");
+  } else if (!rc) {
+    k3_write_dense<<<g3, 128, 0, st>>>(bd);
+    rc = check_launch(m, "K3c");
+  }
+  b->mark(6);
+  // status block: err | n_leaf[L] | total children | steps
+  const size_t stat_bytes = 4 + 4 * (size_t)L + 4 + 8;
+  char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
+  struct PinGuard {
+    void* p;
+    ~PinGuard() { pinned_pool().release(p); }
+  } pin_guard{hs};
+  if (!rc && !hs) rc = set_err(DESPOT_ENOMEM, "pinned staging");
+  if (!rc) {
+    const SumLayout lay{LA * b->S, LA};
+    if (cudaMemcpyAsync(hs, bd.err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hs + 4, bd.n_leaf, 4 * (size_t)L, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hs + 4 + 4 * L, bd.child_begin + LA, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaMemcpyAsync(hs + 8 + 4 * L, bd.sums + lay.steps(), 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = set_err(DESPOT_ECUDA, "status copy failed");
+  }
+  if (!rc && !dev_out) {
+    struct Cp {
+      void* dst;
+      const void* src;
+      size_t bytes;
+    } cps[] = {
+        {out->n_scen, bd.n_scen, 4 * (size_t)L},
+        {out->weight, bd.weight, 4 * (size_t)L},
+        {out->act_reward, bd.act_reward, 4 * LA},
+        {out->act_upper, bd.act_upper, 4 * LA},
+        {out->act_lower, bd.act_lower, 4 * LA},
+        {out->child_begin, bd.child_begin, 4 * (LA + 1)},
+    };
+    for (auto& c : cps)
+      if (cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "output copy failed");
+  }
+  if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
+    m->failed = true;
+    rc = set_err(DESPOT_ECUDA, "batch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  uint32_t err = 0, nchildren = 0;
+  uint64_t steps = 0;
+  if (!rc) {
+    memcpy(&err, hs, 4);
+    memcpy(&nchildren, hs + 4 + 4 * L, 4);
+    memcpy(&steps, hs + 8 + 4 * L, 8);
+    out->num_children = nchildren;
+    out->scenario_steps = steps;
+    if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
+    else if (err & kErrHash) rc = set_err(DESPOT_EHASH, "64-bit observation-hash collision");
+    else if (err & kErrChildCap)
+      rc = set_err(DESPOT_ECAPACITY, "child_capacity %u < %u children", C, nchildren);
+    else if (err & kErrScenCap) rc = set_err(DESPOT_ECAPACITY, "scen_capacity too small");
+  }
+  if (!rc && !dev_out) {
+    // children and per-scenario records: only the used part
+    const uint64_t Cu = nchildren;
+    uint64_t Su = 0;
+    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4);
+    for (uint32_t l = 0; l < L; ++l) Su += (uint64_t)dm.A * nl[l];
+    struct Cp {
+      void* dst;
+      const void* src;
+      size_t bytes;
+    } cps[] = {
+        {out->child_count, bd.child_count, 4 * Cu},
+        {out->child_first, bd.child_first, 4 * Cu},
+        {out->child_weight, bd.child_weight, 4 * Cu},
+        {out->child_upper, bd.child_upper, 4 * Cu},
+        {out->child_lower, bd.child_lower, 4 * Cu},
+        {out->child_obs, bd.child_obs, 4 * Cu * dm.OW},
+        {record ? out->scen_obs : nullptr, bd.scen_obs, 4 * Su * dm.OW},
+        {record ? out->scen_reward : nullptr, bd.scen_reward, 4 * Su},
+        {record ? out->scen_upper : nullptr, bd.scen_upper, 4 * Su},
+        {record ? out->scen_lower : nullptr, bd.scen_lower, 4 * Su},
+        {record ? out->scen_len : nullptr, bd.scen_len, 4 * Su},
+        {record ? out->scen_hash : nullptr, bd.scen_hash, 8 * Su},
+        {record ? out->scen_states : nullptr, bd.scen_states, 4 * Su * dm.SW},
+    };
+    for (auto& c : cps)
+      if (c.dst && c.src && c.bytes &&
+          cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "output copy failed");
+    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = set_err(DESPOT_ECUDA, "output copy sync failed");
+  }
+  if (!rc && b->timing) {
+    b->mark(7);
+    cudaEventSynchronize(b->ev[7]);
+    const int pairs[4][2] = {{1, 2}, {3, 4}, {5, 6}, {0, 7}};
+    for (int k = 0; k < 4; ++k) {
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, b->ev[pairs[k][0]], b->ev[pairs[k][1]]);
+      out->phase_ms[k] = ms;
+    }
+  }
+  if (stage) cudaFreeAsync(stage, st);
+  if (rc) {
+    free_batch(b, true);
+    return rc;
+  }
+  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4);
+  for (uint32_t l = 0; l < L; ++l) {
+    Node* nd = b->leaf_node[l];
+    if (b->is_new[l]) nd->n = nl[l];
+    nd->expanded = true;
+    out->node[l] = reinterpret_cast<despot_node>(nd);
+  }
+  free_batch(b, false);
+  return DESPOT_OK;
+}
+
+extern "C" int despot_expand_batch(despot_model* m, const despot_leaf* leaves, uint32_t L,
+                                   despot_expansion* out, void* stream) {
+  if (!m || !out) return set_err(DESPOT_EINVAL, "null argument");
+  if (m->world > 1) return set_err(DESPOT_EINVAL, "world > 1: use despot_expand_begin/exchange/end");
+  despot_batch* b = nullptr;
+  int rc = despot_expand_begin(m, leaves, L, out->flags, stream, &b);
+  if (rc) return rc;
+  return despot_expand_end(b, out, stream);
+}
+
+extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* upper_mean, float* lower_mean,
+                                     float* per_u, float* per_l, void* stream) {
+  Node* nd = m ? lookup(m, h) : nullptr;
+  if (!nd) return set_err(DESPOT_EINVAL, "unknown node");
+  if (!upper_mean || !lower_mean) return set_err(DESPOT_EINVAL, "null argument");
+  if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const DevModel& dm = m->host;
+  const uint32_t n = nd->n;
+  void* scratch = nullptr;
+  const size_t bytes = 256 + 8 * (size_t)(n ? n : 1);
+  CU(cudaMallocAsync(&scratch, bytes, st));
+  int64_t* acc = static_cast<int64_t*>(scratch);
+  float* du = reinterpret_cast<float*>(static_cast<char*>(scratch) + 256);
+  float* dl = du + (n ? n : 1);
+  int rc = DESPOT_OK;
+  if (cudaMemsetAsync(acc, 0, 24, st) != cudaSuccess) rc = set_err(DESPOT_ECUDA, "memset");
+  if (!rc) {
+    auto launch = [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      const size_t smem = sizeof(typename M::Sm);
+      auto kern = k_rollout_bounds<M>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>((n + 127) / 128, m->num_sms * 8));
+      kern<<<grid, 128, smem, st>>>(m->dev, nd->ids, nd->w, nd->states, nd->cap, n, nd->depth,
+                                    (uint32_t)nd->seed, (uint32_t)(nd->seed >> 32), 1.0 / nd->wroot, du, dl, acc);
+      return check_launch(m, "rollout_bounds");
+    };
+    if (dm.slots) rc = dispatch_dense(dm, launch);
+    else rc = launch(CarThread{});
+  }
+  int64_t hacc[3] = {0, 0, 0};
+  if (!rc) {
+    if (cudaMemcpyAsync(hacc, acc, 24, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        (per_u && n && cudaMemcpyAsync(per_u, du, 4 * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+        (per_l && n && cudaMemcpyAsync(per_l, dl, 4 * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+        cudaStreamSynchronize(st) != cudaSuccess)
+      rc = set_err(DESPOT_ECUDA, "rollout_bounds copy failed");
+  }
+  cudaFreeAsync(scratch, st);
+  if (rc) return rc;
+  *upper_mean = hacc[0] ? (float)((double)hacc[1] / (double)hacc[0]) : 0.0f;
+  *lower_mean = hacc[0] ? (float)((double)hacc[2] / (double)hacc[0]) : 0.0f;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_stream_words(despot_model* m, uint64_t seed, const uint32_t* ids, uint32_t n, uint32_t t,
+                                   uint32_t k, uint32_t* out, void* stream) {
+  if (!m || !ids || !out) return set_err(DESPOT_EINVAL, "null argument");
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return DESPOT_OK;
+  uint32_t* d = nullptr;
+  CU(cudaMallocAsync(&d, 8 * (size_t)n, st));
+  int rc = DESPOT_OK;
+  if (cudaMemcpyAsync(d, ids, 4 * (size_t)n, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = set_err(DESPOT_ECUDA, "copy");
+  if (!rc) {
+    k_stream_words<<<(n + 255) / 256, 256, 0, st>>>((uint32_t)seed, (uint32_t)(seed >> 32), d, n, t, k, d + n);
+    rc = check_launch(m, "stream_words");
+  }
+  if (!rc && (cudaMemcpyAsync(out, d + n, 4 * (size_t)n, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess))
+    rc = set_err(DESPOT_ECUDA, "copy back");
+  cudaFreeAsync(d, st);
+  return rc;
+}

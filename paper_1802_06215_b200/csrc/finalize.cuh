@@ -1,0 +1,170 @@
+// finalize.cuh -- K2pre (tile prefix), K3a/K3b/K3c (child order, CSR scan,
+// outputs) for dense observation keys.
+#pragma once
+#include "common.cuh"
+
+namespace hd {
+
+// block-wide exclusive scan of one u64 per thread (blockDim.x <= 1024)
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* wsum, uint64_t& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t s = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) wsum[lane] = s;
+  }
+  __syncthreads();
+  const uint64_t before = (wid ? wsum[wid - 1] : 0) + x - v;
+  total = wsum[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+// K2pre: tile_off[l] = sum_{l'<l} A ceil(n_l'/32), scen_off[l] = sum A n_l'
+__global__ void __launch_bounds__(1024) k2_prefix(BatchDev b) {
+  __shared__ uint64_t wsum[32];
+  const uint32_t per = (b.L + blockDim.x - 1) / blockDim.x;
+  const uint32_t l0 = threadIdx.x * per;
+  uint64_t tiles = 0, scen = 0;
+  for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
+    const uint64_t n = b.n_leaf[l];
+    tiles += (uint64_t)b.A * ((n + 31) >> 5);
+    scen += (uint64_t)b.A * n;
+  }
+  uint64_t ttot, stot;
+  uint64_t tb = block_excl_scan(tiles, wsum, ttot);
+  uint64_t sb = block_excl_scan(scen, wsum, stot);
+  for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
+    b.tile_off[l] = (uint32_t)tb;
+    b.scen_off[l] = sb;
+    const uint64_t n = b.n_leaf[l];
+    tb += (uint64_t)b.A * ((n + 31) >> 5);
+    sb += (uint64_t)b.A * n;
+  }
+  if (threadIdx.x == 0) {
+    b.tile_off[b.L] = (uint32_t)ttot;
+    b.scen_off[b.L] = stot;
+    if (ttot >= 0xFFFFFFFFull) atomicOr(b.err, kErrChildCap);
+  }
+}
+
+// K3a: child ordinal of each non-empty slot (first-occurrence order, R8)
+__global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char k3_smem[];
+  const uint32_t S = b.S;
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* s_first = reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * S;
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (la >= LA) return;
+  const SumLayout lay{LA * S, LA};
+  const uint64_t base = la * S;
+  uint32_t cnt = 0;
+  for (uint32_t s = lane; s < S; s += 32) {
+    const bool ne = b.sums[lay.N(base + s)] != 0;
+    s_first[s] = ne ? b.mins[base + s] : INT32_MAX;
+    cnt += ne;
+  }
+  __syncwarp();
+  for (uint32_t s = lane; s < S; s += 32) {
+    const int32_t f = s_first[s];
+    if (f == INT32_MAX) continue;
+    uint32_t r = 0;
+    for (uint32_t q = 0; q < S; ++q) r += s_first[q] < f;
+    b.rank[base + s] = r;
+  }
+  cnt = warp_sum32(cnt);
+  if (lane == 0) b.nc[la] = cnt;
+}
+
+// K3b: child_begin = exclusive scan of nc over L*A (one CTA)
+__global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
+  __shared__ uint64_t wsum[32];
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const uint64_t per = (LA + blockDim.x - 1) / blockDim.x;
+  const uint64_t i0 = (uint64_t)threadIdx.x * per;
+  uint64_t loc = 0;
+  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += b.nc[i];
+  uint64_t tot;
+  uint64_t run = block_excl_scan(loc, wsum, tot);
+  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) {
+    b.child_begin[i] = (uint32_t)run;
+    run += b.nc[i];
+  }
+  if (threadIdx.x == 0) {
+    b.child_begin[LA] = (uint32_t)tot;
+    if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
+  }
+}
+
+// K3c: per (leaf, action) outputs, Eq. 11/12 child bounds, one-level Eq. 4
+__global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
+  const uint32_t S = b.S, A = b.A;
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t LA = (uint64_t)b.L * A;
+  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (la >= LA) return;
+  const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
+  const LeafDev& lf = b.leaves[leaf];
+  const DevModel& dm = *b.model;
+  const SumLayout lay{LA * S, LA};
+  const uint64_t base = la * S;
+  const uint32_t cb = b.child_begin[la];
+  int64_t wt = 0, nt = 0;
+  for (uint32_t s = lane; s < S; s += 32) {
+    const int64_t N = b.sums[lay.N(base + s)];
+    if (!N) continue;
+    const int64_t W = b.sums[lay.W(base + s)];
+    wt += W;
+    nt += N;
+    const uint32_t rk = b.rank[base + s];
+    const uint32_t c = cb + rk;
+    if (c < b.child_capacity) {
+      const double Wd = (double)W;
+      b.child_count[c] = (uint32_t)N;
+      b.child_first[c] = (uint32_t)b.mins[base + s];
+      b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
+      b.child_upper[c] = (float)((double)b.sums[lay.U(base + s)] / Wd);
+      b.child_lower[c] = (float)((double)b.sums[lay.Lm(base + s)] / Wd);
+      b.child_obs[c] = s;
+    }
+    if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = s;  // key table for later updates
+  }
+  wt = warp_sum64(wt);
+  nt = warp_sum64(nt);
+  if (lane == 0) {
+    lf.nchild[a] = b.nc[la];
+    const double Wd = (double)wt;
+    b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
+    b.act_upper[la] = (float)((double)b.sums[lay.Q(la, 1)] / Wd);
+    b.act_lower[la] = (float)((double)b.sums[lay.Q(la, 2)] / Wd);
+    if (a == 0) {
+      b.n_scen[leaf] = (uint32_t)nt;
+      b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
+      if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+    }
+  }
+}
+
+__global__ void k_stream_words(uint32_t k0, uint32_t k1, const uint32_t* ids, uint32_t n, uint32_t t,
+                               uint32_t k, uint32_t* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint4 w = philox4x32_10(ids[i], t, k >> 2, 0u, k0, k1);
+  const uint32_t sel = k & 3u;
+  out[i] = sel == 0 ? w.x : sel == 1 ? w.y : sel == 2 ? w.z : w.w;
+}
+
+}  // namespace hd

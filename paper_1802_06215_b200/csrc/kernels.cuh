@@ -1,0 +1,245 @@
+// kernels.cuh -- the batched leaf-expansion kernels (sm_100a), templated on
+// the model.  One batch = K1 (update/filter) -> K2pre (tile prefix) -> K2
+// (expansion + bounds + roll-outs + grouping, fused) -> [exchange] -> K3a
+// (child order) -> K3b (CSR scan) -> K3c (outputs).  See DESIGN.md §4.
+#pragma once
+#include "common.cuh"
+
+namespace hd {
+
+// ---------------------------------------------------------------------------
+// K1: update.  One CTA per leaf: gather the parent's scenarios,
+// replay the leaf's last action at depth Delta (drawing phi_Delta), keep those
+// whose observation equals the parent's key of child `child`, and compact them
+// (order kept) into the leaf arena.  Leaves with action == -1 only publish n.
+// ---------------------------------------------------------------------------
+template <class M>
+__global__ void __launch_bounds__(256) k1_update(BatchDev b) {
+  __shared__ typename M::Sm sm;
+  __shared__ uint32_t warp_cnt[8];
+  __shared__ uint32_t s_base;
+  const LeafDev& lf = b.leaves[blockIdx.x];
+  if (lf.action < 0) {
+    if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
+    return;
+  }
+  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  const uint32_t nchild = lf.p_nchild[lf.action];
+  const bool valid_child = lf.child < nchild;
+  const uint32_t key = valid_child ? lf.p_keys[(uint64_t)lf.action * lf.p_kcap + lf.child] : 0xFFFFFFFFu;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t steps = 0;
+  for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    bool keep = false;
+    typename M::St s;
+    uint32_t id = 0;
+    if (i < lf.p_n && valid_child) {
+      s = M::load(sm, lf.p_states, lf.p_cap, i);
+      id = lf.p_ids[i];
+      uint32_t z;
+      if (M::terminal(s)) {
+        z = M::kTerminalObs;
+      } else {
+        float r;
+        M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, z, r);
+        ++steps;
+      }
+      keep = z == key;
+    }
+    const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[wid] = __popc(ballot);
+    __syncthreads();
+    uint32_t off = s_base;
+    for (int w = 0; w < wid; ++w) off += warp_cnt[w];
+    off += __popc(ballot & ((1u << lane) - 1u));
+    if (keep) {
+      lf.ids[off] = id;
+      lf.w[off] = lf.p_w[i];
+      M::store(sm, s, lf.states, lf.cap, off);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_cnt[w];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+  const uint32_t ws = warp_sum32(steps);
+  if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[SumLayout{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A}.steps()], (unsigned long long)ws);
+  if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;  // may be 0 on a shard
+}
+
+// ---------------------------------------------------------------------------
+// K2 (dense observation keys): one warp per tile of 32 consecutive scenarios
+// of one (leaf, action).  Each lane: expansion step (Eq. 9) at depth
+// Delta+1, u(s') (Eq. 11), roll-out (Eq. 12), then the warp groups its lanes
+// by observation and adds exact int64 fixed-point partial sums of
+// (W, U, LAMBDA, N, first) per child slot and (R, Uq, Lq) per action.
+// Persistent grid-stride loop over tiles.
+// ---------------------------------------------------------------------------
+template <class M, bool RECORD>
+__global__ void __launch_bounds__(128) k2_expand_dense(BatchDev b, uint32_t total_tiles_bound) {
+  extern __shared__ __align__(16) unsigned char k2_smem[];
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(k2_smem);
+  uint32_t* tile_off = reinterpret_cast<uint32_t*>(k2_smem + ((sizeof(typename M::Sm) + 15) & ~size_t(15)));
+  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
+  __syncthreads();
+  const uint32_t total = tile_off[b.L];
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+  const DevModel& dm = *b.model;
+  const double fx = dm.fx, gamma = dm.gamma;
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  uint32_t steps_acc = 0;
+  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += nwarps) {
+    // tile -> (leaf, action, chunk)
+    uint32_t lo = 0, hi = b.L;  // tile_off[lo] <= t < tile_off[hi]
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (tile_off[mid] <= t) lo = mid;
+      else hi = mid;
+    }
+    const uint32_t leaf = lo;
+    const LeafDev& lf = b.leaves[leaf];
+    const uint32_t n = b.n_leaf[leaf];
+    const uint32_t chunks = (n + 31) >> 5;
+    const uint32_t local = t - tile_off[leaf];
+    const uint32_t a = local / chunks;
+    const uint32_t i = (local - a * chunks) * 32 + lane;
+    const bool valid = i < n;
+    uint32_t z = 0xFFFFFFFFu, id = 0;
+    int64_t qW = 0, qU = 0, qL = 0, qR = 0, qUq = 0, qLq = 0;
+    if (valid) {
+      typename M::St s = M::load(sm, lf.states, lf.cap, i);
+      id = lf.ids[i];
+      const double wn = (double)lf.w[i] * lf.inv_wroot;  // normalised weight
+      float r = 0.0f;
+      bool term;
+      if (M::terminal(s)) {  // R7: terminal scenarios stay terminal, reward 0
+        z = M::kTerminalObs;
+        term = true;
+      } else {
+        term = M::step(sm, s, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, z, r);
+        ++steps_acc;
+      }
+      double u = 0.0, lam = 0.0;
+      uint32_t len = 0;
+      uint64_t h = kFnvOffset;
+      if (!term) {
+        u = M::upper(sm, s);
+        M::template rollout<RECORD>(sm, s, z, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, lam, len, h);
+        steps_acc += len;
+      }
+      qW = fxq(wn, fx);
+      qU = fxq(wn * u, fx);
+      qL = fxq(wn * lam, fx);
+      qR = fxq(wn * (double)r, fx);
+      qUq = fxq(wn * ((double)r + gamma * u), fx);
+      qLq = fxq(wn * ((double)r + gamma * lam), fx);
+      if (RECORD) {
+        const uint64_t q = b.scen_off[leaf] + (uint64_t)a * n + i;
+        if (q < b.scen_capacity) {
+          b.scen_obs[q] = z;
+          b.scen_reward[q] = r;
+          b.scen_upper[q] = (float)u;
+          b.scen_lower[q] = (float)lam;
+          b.scen_len[q] = len;
+          b.scen_hash[q] = h;
+          if (b.scen_states) {
+            // s' after the expansion step: recompute (the roll-out consumed s)
+            typename M::St s2 = M::load(sm, lf.states, lf.cap, i);
+            if (!M::terminal(s2)) {
+              uint32_t z2;
+              float r2;
+              M::step(sm, s2, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, z2, r2);
+            }
+            // scen_states is [S][SW] (row per scenario): write through a strided view
+            uint32_t tmp[16];
+            M::store(sm, s2, tmp, 1, 0);
+            for (uint32_t k = 0; k < dm.SW; ++k) b.scen_states[q * dm.SW + k] = tmp[k];
+          }
+        } else {
+          atomicOr(b.err, kErrScenCap);
+        }
+      }
+    }
+    // ---- per-action sums (R, Uq, Lq) -----------------------------------
+    const uint64_t la = (uint64_t)leaf * b.A + a;
+    const int64_t sR = warp_sum64(qR), sUq = warp_sum64(qUq), sLq = warp_sum64(qLq);
+    if (lane == 0) {
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)sR);
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)sUq);
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)sLq);
+    }
+    // ---- grouping by observation (Eq. 10) ------------------------------
+    uint32_t pending = __ballot_sync(0xffffffffu, valid);
+    while (pending) {
+      const int leader = __ffs(pending) - 1;
+      const uint32_t zk = __shfl_sync(0xffffffffu, z, leader);
+      const bool in = valid && z == zk;
+      const uint32_t gmask = __ballot_sync(0xffffffffu, in);
+      pending &= ~gmask;
+      const int64_t gW = warp_sum64(in ? qW : 0), gU = warp_sum64(in ? qU : 0),
+                    gL = warp_sum64(in ? qL : 0);
+      if ((int)lane == leader) {
+        const uint64_t slot = la * b.S + zk;
+        atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)gW);
+        atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)gU);
+        atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)gL);
+        atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], (unsigned long long)__popc(gmask));
+        atomicMin(&b.mins[slot], (int32_t)id);  // leader = lowest position = smallest id
+      }
+    }
+  }
+  const uint32_t ws = warp_sum32(steps_acc);
+  if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)ws);
+  (void)total_tiles_bound;
+}
+
+// ---------------------------------------------------------------------------
+// Roll-out bounds of a node at its own depth (Eqs. 11-12 for the root).
+// ---------------------------------------------------------------------------
+template <class M>
+__global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, const uint32_t* ids,
+                                                        const float* w, const uint32_t* states,
+                                                        uint32_t cap, uint32_t n, uint32_t depth,
+                                                        uint32_t k0, uint32_t k1, double inv_wroot,
+                                                        float* per_u, float* per_l, int64_t* acc3) {
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(rb_smem);
+  M::load_sm(sm, *dmp, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const double fx = dmp->fx;
+  int64_t qW = 0, qU = 0, qL = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    typename M::St s = M::load(sm, states, cap, i);
+    double u = 0.0, lam = 0.0;
+    if (!M::terminal(s)) {
+      u = M::upper(sm, s);
+      uint32_t len;
+      uint64_t h = kFnvOffset;
+      M::template rollout<false>(sm, s, M::initial_obs(sm, s), ids[i], depth, k0, k1, lam, len, h);
+    }
+    if (per_u) per_u[i] = (float)u;
+    if (per_l) per_l[i] = (float)lam;
+    const double wn = (double)w[i] * inv_wroot;
+    qW += fxq(wn, fx);
+    qU += fxq(wn * u, fx);
+    qL += fxq(wn * lam, fx);
+  }
+  qW = warp_sum64(qW);
+  qU = warp_sum64(qU);
+  qL = warp_sum64(qL);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd((unsigned long long*)&acc3[0], (unsigned long long)qW);
+    atomicAdd((unsigned long long*)&acc3[1], (unsigned long long)qU);
+    atomicAdd((unsigned long long*)&acc3[2], (unsigned long long)qL);
+  }
+}
+
+}  // namespace hd

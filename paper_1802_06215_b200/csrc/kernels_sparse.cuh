@@ -1,0 +1,443 @@
+// kernels_sparse.cuh -- batched expansion for sparse multi-word observation
+// keys (the driving model, card §3.4; |Z| is huge).
+//
+//   K1s  update/filter with a full-key compare against the parent's key table
+//   K2f  expansion + bounds + roll-out, one WARP per (leaf, action, scenario):
+//        lane p < P moves pedestrian p, lane 31 the car -- the paper's
+//        within-step factoring -- or
+//   K2t  the same with one THREAD per (leaf, action, scenario)
+//        Both write, per item, the 64-bit key hash, the key words and the
+//        exact fixed-point (W, U, LAMBDA) contributions.
+//   K3s  one CTA per (leaf, action): group items by hash (first occurrence),
+//        verify exact key equality against the group's first item (a 64-bit
+//        hash collision is reported, never merged), and add the per-child
+//        sums into the same exchange layout the dense path uses.
+#pragma once
+#include "common.cuh"
+#include "model_car.cuh"
+
+namespace hd {
+
+// hash of a key: XOR over words of splitmix64(word ^ (k+1) << 32)
+__device__ __forceinline__ uint64_t key_mix(uint32_t w, uint32_t k) {
+  uint64_t x = (uint64_t)w ^ ((uint64_t)(k + 1) << 32);
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+constexpr uint32_t kCarTerminalWord0 = 0xFFFFFFFFu;
+
+// ---------------------------------------------------------------------------
+// K1s: update for the car (thread per parent scenario)
+// ---------------------------------------------------------------------------
+template <class M>
+__global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
+  __shared__ typename M::Sm sm;
+  __shared__ uint32_t warp_cnt[8];
+  __shared__ uint32_t s_base;
+  const LeafDev& lf = b.leaves[blockIdx.x];
+  if (lf.action < 0) {
+    if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
+    return;
+  }
+  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  const uint32_t OW = b.model->OW;
+  const bool valid_child = lf.child < lf.p_nchild[lf.action];
+  const uint32_t* key = lf.p_keys + ((uint64_t)lf.action * lf.p_kcap + lf.child) * OW;
+  if (threadIdx.x == 0) s_base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t steps = 0;
+  for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    bool keep = false;
+    typename M::St s;
+    uint32_t id = 0;
+    if (i < lf.p_n && valid_child) {
+      s = M::load(sm, lf.p_states, lf.p_cap, i);
+      id = lf.p_ids[i];
+      bool term = M::terminal(s);
+      if (!term) {
+        float r;
+        term = M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, r);
+        ++steps;
+      }
+      if (term) {
+        keep = key[0] == kCarTerminalWord0;
+        for (uint32_t k = 1; k < OW; ++k) keep = keep && key[k] == 0u;
+      } else {
+        keep = true;
+        for (uint32_t k = 0; k < OW; ++k) keep = keep && M::obs_word(s, (int)k) == key[k];
+      }
+    }
+    const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) warp_cnt[wid] = __popc(ballot);
+    __syncthreads();
+    uint32_t off = s_base;
+    for (int w = 0; w < wid; ++w) off += warp_cnt[w];
+    off += __popc(ballot & ((1u << lane) - 1u));
+    if (keep) {
+      lf.ids[off] = id;
+      lf.w[off] = lf.p_w[i];
+      M::store(sm, s, lf.states, lf.cap, off);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_cnt[w];
+      s_base += tot;
+    }
+    __syncthreads();
+  }
+  const uint32_t ws = warp_sum32(steps);
+  if (lane == 0 && ws)
+    atomicAdd((unsigned long long*)&b.sums[SumLayout{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A}.steps()],
+              (unsigned long long)ws);
+  if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;
+}
+
+// item t -> (leaf, action, position) through the per-scenario prefix
+__device__ __forceinline__ uint32_t find_leaf(const uint64_t* off, uint32_t L, uint64_t t) {
+  uint32_t lo = 0, hi = L;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (off[mid] <= t) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct SparseItemOut {
+  uint64_t* hash;  // [Q]
+  uint32_t* keys;  // [Q*OW]
+  int64_t* q3;     // [Q*3]  W, U, LAMBDA contributions
+};
+
+// ---------------------------------------------------------------------------
+// K2t: thread per (leaf, action, scenario)
+// ---------------------------------------------------------------------------
+template <class M, bool RECORD>
+__global__ void __launch_bounds__(128) k2_car_thread(BatchDev b, SparseItemOut io) {
+  __shared__ typename M::Sm sm;
+  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const DevModel& dm = *b.model;
+  const uint32_t OW = dm.OW, SW = dm.SW;
+  const uint64_t Q = b.scen_off[b.L];
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  uint32_t steps_acc = 0;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < Q; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t leaf = find_leaf(b.scen_off, b.L, t);
+    const LeafDev& lf = b.leaves[leaf];
+    const uint32_t n = b.n_leaf[leaf];
+    const uint64_t local = t - b.scen_off[leaf];
+    const uint32_t a = (uint32_t)(local / n), i = (uint32_t)(local - (uint64_t)a * n);
+    typename M::St s = M::load(sm, lf.states, lf.cap, i);
+    const uint32_t id = lf.ids[i];
+    const double wn = (double)lf.w[i] * lf.inv_wroot;
+    float r = 0.0f;
+    bool term = M::terminal(s);
+    if (!term) {
+      term = M::step(sm, s, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, r);
+      ++steps_acc;
+    }
+    uint64_t hsh = 0;
+    for (uint32_t k = 0; k < OW; ++k) {
+      const uint32_t zk = term ? (k == 0 ? kCarTerminalWord0 : 0u) : M::obs_word(s, (int)k);
+      io.keys[t * OW + k] = zk;
+      if (RECORD) b.scen_obs[t * OW + k] = zk;
+      hsh ^= key_mix(zk, k);
+    }
+    io.hash[t] = hsh;
+    if (RECORD && b.scen_states) {
+      uint32_t* dst = b.scen_states + t * SW;  // row per scenario: stride-1 view
+      M::store(sm, s, dst, 1, 0);
+    }
+    double u = 0.0, lam = 0.0;
+    uint32_t len = 0;
+    uint64_t h = kFnvOffset;
+    if (!term) {
+      u = M::upper(sm, s);
+      M::template rollout<RECORD>(sm, s, 0u, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, lam, len, h);
+      steps_acc += len;
+    }
+    const double fx = dm.fx, gamma = dm.gamma;
+    io.q3[3 * t + 0] = fxq(wn, fx);
+    io.q3[3 * t + 1] = fxq(wn * u, fx);
+    io.q3[3 * t + 2] = fxq(wn * lam, fx);
+    const uint64_t la = (uint64_t)leaf * b.A + a;
+    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r, fx));
+    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r + gamma * u), fx));
+    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r + gamma * lam), fx));
+    if (RECORD) {
+      b.scen_reward[t] = r;
+      b.scen_upper[t] = (float)u;
+      b.scen_lower[t] = (float)lam;
+      b.scen_len[t] = len;
+      b.scen_hash[t] = h;
+    }
+  }
+  atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)steps_acc);
+}
+
+// ---------------------------------------------------------------------------
+// K2f: warp per (leaf, action, scenario); lane p < P: pedestrian p, lane 31:
+// the car.  Bit-identical to K2t (same operation sequence per element).
+// ---------------------------------------------------------------------------
+template <bool RECORD>
+__global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io) {
+  __shared__ typename CarThreadT<1>::Sm sm;  // scalar parameters + gamma table
+  CarThreadT<1>::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const DevModel& dm = *b.model;
+  const uint32_t OW = dm.OW, SW = dm.SW;
+  const int P = sm.peds;
+  const uint32_t lane = threadIdx.x & 31;
+  const bool is_car = lane == 31, is_ped = (int)lane < P;
+  const uint32_t word = is_car ? 0u : 1u + lane;  // random word / observation word of this lane
+  const uint64_t Q = b.scen_off[b.L];
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  uint32_t steps_acc = 0;
+  for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < Q; t += nwarps) {
+    const uint32_t leaf = find_leaf(b.scen_off, b.L, t);
+    const LeafDev& lf = b.leaves[leaf];
+    const uint32_t n = b.n_leaf[leaf];
+    const uint64_t local = t - b.scen_off[leaf];
+    const uint32_t a0 = (uint32_t)(local / n), i = (uint32_t)(local - (uint64_t)a0 * n);
+    const uint32_t id = lf.ids[i];
+    const uint32_t cap = lf.cap;
+    // element state: car lane (xc, level, term), pedestrian lanes (x, y, goal)
+    float xc = __uint_as_float(lf.states[i]);
+    const uint32_t w1 = lf.states[cap + i];
+    uint32_t level = w1 & 0xFFu;
+    bool term = (w1 >> 8) & 1u;
+    float px = 0.0f, py = 0.0f;
+    uint32_t goal = 0;
+    if (is_ped) {
+      px = __uint_as_float(lf.states[(4 + 2 * lane) * cap + i]);
+      py = __uint_as_float(lf.states[(5 + 2 * lane) * cap + i]);
+      goal = (lf.states[(2 + (lane >> 4)) * cap + i] >> (2 * (lane & 15))) & 3u;
+    }
+    // one factored step g(s, a, phi_t); returns reward, updates term
+    auto step = [&](int a, uint32_t tt, float& r) {
+      const uint4 wv = philox4x32_10(id, tt, word >> 2, 0u, lf.seed_lo, lf.seed_hi);
+      const uint32_t sel = word & 3u;
+      const uint32_t u = sel == 0 ? wv.x : sel == 1 ? wv.y : sel == 2 ? wv.z : wv.w;
+      // 1. the car (all lanes track it; the car lane's word decides failure)
+      const bool fail = __shfl_sync(0xffffffffu, event(u, sm.t_fail) ? 1 : 0, 31) != 0;
+      if (!fail) {
+        if (a == 1 && level < 4u) level += 1u;
+        if (a == 2 && level > 0u) level -= 1u;
+      }
+      const float v = 0.5f * (float)level;
+      xc = xc + v * 0.25f;
+      // 2. pedestrians, 3. collision
+      bool hit = false;
+      if (is_ped) {
+        float c, sn;
+        car_noise(u, sm.noise, c, sn);
+        car_ped_move(px, py, goal, c, sn);
+        const float dx = px - xc;
+        hit = dx * dx + py * py < 1.0f;
+      }
+      const bool coll = __any_sync(0xffffffffu, hit);
+      const bool g = xc >= 20.0f;  // 4. goal
+      r = car_reward(a, coll, g, v);
+      term = coll || g;
+    };
+    float r0 = 0.0f;
+    const bool was_term = term;
+    if (!term) {
+      step((int)a0, lf.depth + 1, r0);
+      ++steps_acc;
+    }
+    // key of the child: lane k holds word k (car lane: word 0)
+    uint32_t zw = 0;
+    if (term) zw = is_car ? kCarTerminalWord0 : 0u;
+    else if (is_car) zw = car_bin(xc) | (level << 16);
+    else if (is_ped) zw = car_bin(px) | (car_bin(py) << 16);
+    uint64_t hk = (is_car || is_ped) ? key_mix(zw, word) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) hk ^= __shfl_xor_sync(0xffffffffu, hk, o);
+    if (is_car || is_ped) {
+      io.keys[t * OW + word] = zw;
+      if (RECORD) b.scen_obs[t * OW + word] = zw;
+    }
+    if (lane == 0) io.hash[t] = hk;
+    if (RECORD && b.scen_states) {
+      uint32_t* dst = b.scen_states + t * SW;
+      if (is_car) {
+        dst[0] = __float_as_uint(xc);
+        dst[1] = level | ((uint32_t)term << 8);
+        dst[2] = lf.states[2 * cap + i];
+        dst[3] = lf.states[3 * cap + i];
+      }
+      if (is_ped) {
+        dst[4 + 2 * lane] = __float_as_uint(px);
+        dst[5 + 2 * lane] = __float_as_uint(py);
+      }
+    }
+    double u = 0.0, lam = 0.0;
+    uint32_t len = 0;
+    uint64_t h = kFnvOffset;
+    if (!term) {
+      int k = (int)ceilf((20.0f - xc) * 2.0f);
+      k = k < 1 ? 1 : k;
+      u = 100.0 * sm.gpow[k - 1];  // Eq. 11
+      // roll-out (Eq. 12): pi0 reads the last observation's bins
+      uint32_t tt = lf.depth + 1;
+      double acc = 0.0;
+      while (tt < sm.D && !term) {
+        const int cxb = car_bin_i(xc);
+        int gap = 255;
+        if (is_ped) {
+          const int pxb = car_bin_i(px), pyb = car_bin_i(py);
+          if (pxb >= cxb && pyb >= -4 && pyb <= 3) gap = pxb - cxb;
+        }
+        gap = (int)__reduce_min_sync(0xffffffffu, (uint32_t)gap);
+        const int a = car_policy_from_gap(gap);
+        if (RECORD) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+        float r;
+        step(a, tt + 1, r);
+        acc += sm.gpow[tt - (lf.depth + 1)] * (double)r;
+        ++tt;
+      }
+      if (!term) acc += sm.gpow[tt - (lf.depth + 1)] * sm.tail;
+      lam = acc;
+      len = tt - (lf.depth + 1);
+      steps_acc += len;
+    }
+    (void)was_term;
+    if (lane == 0) {
+      const double wn = (double)lf.w[i] * lf.inv_wroot;
+      const double fx = dm.fx, gamma = dm.gamma;
+      io.q3[3 * t + 0] = fxq(wn, fx);
+      io.q3[3 * t + 1] = fxq(wn * u, fx);
+      io.q3[3 * t + 2] = fxq(wn * lam, fx);
+      const uint64_t la = (uint64_t)leaf * b.A + a0;
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r0, fx));
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r0 + gamma * u), fx));
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r0 + gamma * lam), fx));
+      if (RECORD) {
+        b.scen_reward[t] = r0;
+        b.scen_upper[t] = (float)u;
+        b.scen_lower[t] = (float)lam;
+        b.scen_len[t] = len;
+        b.scen_hash[t] = h;
+      }
+    }
+  }
+  if (lane == 0) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)steps_acc);
+}
+
+// ---------------------------------------------------------------------------
+// K3s: group the items of one (leaf, action) by key (first occurrence)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io) {
+  extern __shared__ __align__(16) unsigned char gs_smem[];
+  uint64_t* sh = reinterpret_cast<uint64_t*>(gs_smem);
+  const uint64_t la = blockIdx.x;
+  const uint32_t leaf = (uint32_t)(la / b.A), a = (uint32_t)(la - (uint64_t)leaf * b.A);
+  const uint32_t n = b.n_leaf[leaf];
+  const uint64_t q0 = b.scen_off[leaf] + (uint64_t)a * n;
+  const uint32_t OW = b.model->OW;
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  const uint64_t base = la * b.S;
+  __shared__ uint64_t wsum[32];
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sh[i] = io.hash[q0 + i];
+  __syncthreads();
+  uint32_t* rep_of = reinterpret_cast<uint32_t*>(sh + n);  // [n]
+  uint32_t* ord = rep_of + n;                              // [n] child ordinal of a representative
+  uint32_t run = 0;
+  for (uint32_t c0 = 0; c0 < n; c0 += blockDim.x) {
+    const uint32_t i = c0 + threadIdx.x;
+    uint32_t is_rep = 0;
+    if (i < n) {
+      const uint64_t hi = sh[i];
+      uint32_t j = 0;
+      while (sh[j] != hi) ++j;  // first occurrence of the hash (j <= i)
+      rep_of[i] = j;
+      is_rep = j == i;
+      if (!is_rep) {
+        const uint32_t* ki = io.keys + (q0 + i) * OW;
+        const uint32_t* kj = io.keys + (q0 + j) * OW;
+        for (uint32_t k = 0; k < OW; ++k)
+          if (ki[k] != kj[k]) atomicOr(b.err, kErrHash);
+      }
+    }
+    uint64_t tot;
+    const uint64_t before = block_excl_scan(is_rep, wsum, tot);
+    if (i < n && is_rep) ord[i] = run + (uint32_t)before;
+    run += (uint32_t)tot;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint32_t c = ord[rep_of[i]];
+    const uint64_t slot = base + c;
+    atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 0]);
+    atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 1]);
+    atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 2]);
+    atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], 1ull);
+    if (rep_of[i] == i) {
+      b.mins[slot] = (int32_t)b.leaves[leaf].ids[i];
+      b.rank[slot] = c;
+      b.sp_item[slot] = (uint32_t)(q0 + i);
+    }
+  }
+  if (threadIdx.x == 0) b.nc[la] = run;
+}
+
+// K3c for sparse keys: children are already in first-occurrence order
+__global__ void __launch_bounds__(128) k3_write_sparse(BatchDev b, SparseItemOut io) {
+  const uint32_t A = b.A;
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t LA = (uint64_t)b.L * A;
+  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (la >= LA) return;
+  const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
+  const LeafDev& lf = b.leaves[leaf];
+  const DevModel& dm = *b.model;
+  const uint32_t OW = dm.OW;
+  const SumLayout lay{LA * b.S, LA};
+  const uint64_t base = la * b.S;
+  const uint32_t cb = b.child_begin[la];
+  const uint32_t nc = b.nc[la];
+  int64_t wt = 0, nt = 0;
+  for (uint32_t c = lane; c < nc; c += 32) {
+    const int64_t N = b.sums[lay.N(base + c)];
+    const int64_t W = b.sums[lay.W(base + c)];
+    wt += W;
+    nt += N;
+    const uint32_t oc = cb + c;
+    const uint32_t* key = io.keys + (uint64_t)b.sp_item[base + c] * OW;
+    if (oc < b.child_capacity) {
+      const double Wd = (double)W;
+      b.child_count[oc] = (uint32_t)N;
+      b.child_first[oc] = (uint32_t)b.mins[base + c];
+      b.child_weight[oc] = (float)(Wd * dm.inv_fx * lf.wroot);
+      b.child_upper[oc] = (float)((double)b.sums[lay.U(base + c)] / Wd);
+      b.child_lower[oc] = (float)((double)b.sums[lay.Lm(base + c)] / Wd);
+      for (uint32_t k = 0; k < OW; ++k) b.child_obs[(uint64_t)oc * OW + k] = key[k];
+    }
+    if (c < lf.kcap)
+      for (uint32_t k = 0; k < OW; ++k) lf.keys[((uint64_t)a * lf.kcap + c) * OW + k] = key[k];
+  }
+  wt = warp_sum64(wt);
+  nt = warp_sum64(nt);
+  if (lane == 0) {
+    lf.nchild[a] = nc;
+    const double Wd = (double)wt;
+    b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
+    b.act_upper[la] = (float)((double)b.sums[lay.Q(la, 1)] / Wd);
+    b.act_lower[la] = (float)((double)b.sums[lay.Q(la, 2)] / Wd);
+    if (a == 0) {
+      b.n_scen[leaf] = (uint32_t)nt;
+      b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
+      if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+    }
+  }
+}
+
+}  // namespace hd

@@ -1,0 +1,208 @@
+// model_car.cuh -- driving among pedestrians (card §3.4), the
+// sparse-observation model.  Two device implementations of the same card:
+//   CarThreadT<P>  one thread per scenario (state in registers)
+//   (kernels_car.cuh) one warp per scenario, lane i = pedestrian i, lane 31 =
+//   the car: the paper's within-step factoring.
+// The library is compiled with -fmad=false and IEEE div/sqrt, so every fp32
+// operation below rounds exactly as the card's sequence (R16).
+#pragma once
+#include "common.cuh"
+#include "models.cuh"
+
+namespace hd {
+
+__device__ __forceinline__ uint32_t car_bin(float v) {  // (int16) floor(2 v), as 16 bits
+  return ((uint32_t)(int)floorf(2.0f * v)) & 0xFFFFu;
+}
+__device__ __forceinline__ int car_bin_i(float v) { return (int)(int16_t)(int)floorf(2.0f * v); }
+
+// heading-noise rotation (cos, sin) from one random word: tau = (sum of the
+// four bytes - 510) * noise, c = (1 - tau^2)/(1 + tau^2), s = 2 tau/(1 + tau^2)
+__device__ __forceinline__ void car_noise(uint32_t w, float noise, float& c, float& sn) {
+  const int sint = (int)(w & 0xFFu) + (int)((w >> 8) & 0xFFu) + (int)((w >> 16) & 0xFFu) +
+                   (int)((w >> 24) & 0xFFu) - 510;
+  const float tau = (float)sint * noise;
+  const float tt = tau * tau;
+  const float den = 1.0f + tt;
+  c = (1.0f - tt) / den;
+  sn = (tau + tau) / den;
+}
+// one pedestrian toward goal g with rotation (c, sn), speed 1 m/s, dt 0.25
+__device__ __forceinline__ void car_ped_move(float& x, float& y, uint32_t g, float c, float sn) {
+  const float gx = (g >= 2u) ? 20.0f : 0.0f;
+  const float gy = (g & 1u) ? 10.0f : -10.0f;
+  const float dx = gx - x, dy = gy - y;
+  const float d2 = dx * dx + dy * dy;
+  if (!(d2 < 1e-6f)) {
+    const float nrm = sqrtf(d2);
+    const float ux = dx / nrm, uy = dy / nrm;
+    const float hx = ux * c - uy * sn;
+    const float hy = ux * sn + uy * c;
+    x = x + 0.25f * hx;
+    y = y + 0.25f * hy;
+  }
+}
+__device__ __forceinline__ float car_reward(int a, bool coll, bool goal, float v) {
+  float r = -0.1f;
+  if (a == 2) r = r + (-0.1f);
+  if (coll) r = r + (-1000.0f * (v * v + 0.5f));
+  if (goal && !coll) r = r + 100.0f;
+  return r;
+}
+__device__ __forceinline__ int car_policy_from_gap(int gap) { return gap <= 8 ? 2 : gap <= 16 ? 0 : 1; }
+
+template <int MAXP>
+struct CarThreadT {
+  struct Sm {
+    int32_t peds;
+    uint64_t t_fail;
+    float noise;
+    uint32_t D, OW;
+    double tail;
+    double gpow[kGpowN];
+  };
+  static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
+    if (tid == 0) {
+      sm.peds = dm.peds;
+      sm.t_fail = dm.t_car_fail;
+      sm.noise = dm.noise_scale;
+      sm.D = dm.D;
+      sm.OW = dm.OW;
+      sm.tail = dm.tail;
+    }
+    copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+  }
+  struct St {
+    float xc;
+    uint32_t level;
+    bool term;
+    uint32_t g0, g1;
+    float px[MAXP], py[MAXP];
+  };
+  static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
+    St s;
+    s.xc = __uint_as_float(st[i]);
+    const uint32_t w1 = st[cap + i];
+    s.level = w1 & 0xFFu;
+    s.term = (w1 >> 8) & 1u;
+    s.g0 = st[2 * cap + i];
+    s.g1 = st[3 * cap + i];
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p < sm.peds) {
+        s.px[p] = __uint_as_float(st[(4 + 2 * p) * cap + i]);
+        s.py[p] = __uint_as_float(st[(5 + 2 * p) * cap + i]);
+      } else {
+        s.px[p] = 0.0f;
+        s.py[p] = 0.0f;
+      }
+    }
+    return s;
+  }
+  static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
+                                               uint32_t i) {
+    st[i] = __float_as_uint(s.xc);
+    st[cap + i] = s.level | ((uint32_t)s.term << 8);
+    st[2 * cap + i] = s.g0;
+    st[3 * cap + i] = s.g1;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p)
+      if (p < sm.peds) {
+        st[(4 + 2 * p) * cap + i] = __float_as_uint(s.px[p]);
+        st[(5 + 2 * p) * cap + i] = __float_as_uint(s.py[p]);
+      }
+  }
+  static __device__ __forceinline__ bool terminal(const St& s) { return s.term; }
+  static __device__ __forceinline__ uint32_t goal(const St& s, int p) {
+    return ((p < 16 ? s.g0 : s.g1) >> (2 * (p & 15))) & 3u;
+  }
+  // observation word k (0: car, 1+i: pedestrian i) of a non-terminal state
+  static __device__ __forceinline__ uint32_t obs_word(const St& s, int k) {
+    if (k == 0) return car_bin(s.xc) | (s.level << 16);
+    float x = 0.0f, y = 0.0f;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p)
+      if (p == k - 1) {
+        x = s.px[p];
+        y = s.py[p];
+      }
+    return car_bin(x) | (car_bin(y) << 16);
+  }
+  static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
+                                              uint32_t k0, uint32_t k1, float& r) {
+    constexpr int NB = (MAXP + 1 + 3) / 4;
+    uint32_t u[4 * NB];
+#pragma unroll
+    for (int bk = 0; bk < NB; ++bk) {
+      if (4 * bk < sm.peds + 1) {
+        const uint4 w = philox4x32_10(id, t, (uint32_t)bk, 0u, k0, k1);
+        u[4 * bk] = w.x;
+        u[4 * bk + 1] = w.y;
+        u[4 * bk + 2] = w.z;
+        u[4 * bk + 3] = w.w;
+      } else {
+        u[4 * bk] = u[4 * bk + 1] = u[4 * bk + 2] = u[4 * bk + 3] = 0u;
+      }
+    }
+    if (!event(u[0], sm.t_fail)) {  // Accelerate / Decelerate fail w.p. 0.01
+      if (a == 1 && s.level < 4u) s.level += 1u;
+      if (a == 2 && s.level > 0u) s.level -= 1u;
+    }
+    const float v = 0.5f * (float)s.level;
+    s.xc = s.xc + v * 0.25f;
+    bool coll = false;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p < sm.peds) {
+        float c, sn;
+        car_noise(u[1 + p], sm.noise, c, sn);
+        car_ped_move(s.px[p], s.py[p], goal(s, p), c, sn);
+        const float dx = s.px[p] - s.xc;
+        coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
+      }
+    }
+    const bool g = s.xc >= 20.0f;
+    r = car_reward(a, coll, g, v);
+    s.term = coll || g;
+    return s.term;
+  }
+  static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
+    int k = (int)ceilf((20.0f - s.xc) * 2.0f);
+    k = k < 1 ? 1 : k;
+    return 100.0 * sm.gpow[k - 1];
+  }
+  static __device__ __forceinline__ int policy(const Sm& sm, const St& s) {
+    const int cxb = car_bin_i(s.xc);
+    int gap = 255;
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p) {
+      if (p < sm.peds) {
+        const int pxb = car_bin_i(s.px[p]), pyb = car_bin_i(s.py[p]);
+        if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
+      }
+    }
+    return car_policy_from_gap(gap);
+  }
+  static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
+  template <bool TRACE>
+  static __device__ void rollout(const Sm& sm, St s, uint32_t /*z: bins of s*/, uint32_t id, uint32_t t0,
+                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+    double acc = 0.0;
+    uint32_t t = t0;
+    bool term = false;
+    while (t < sm.D && !term) {
+      const int a = policy(sm, s);  // reads only the last observation's bins
+      if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+      float r;
+      term = step(sm, s, a, id, t + 1, k0, k1, r);
+      acc += sm.gpow[t - t0] * (double)r;
+      ++t;
+    }
+    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    ret = acc;
+    len = t - t0;
+  }
+};
+using CarThread = CarThreadT<kCarMaxPeds>;
+
+}  // namespace hd

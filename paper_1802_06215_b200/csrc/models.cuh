@@ -1,0 +1,478 @@
+// models.cuh -- device implementations of the dense-observation model cards
+// (DESIGN.md §3): Tiger, RockSample / multi-agent RockSample
+// and navigation in a partially known map.
+//
+// Interface of a model M (used by the kernel templates in kernels.cu):
+//   M::Sm                 shared-memory copy of the hot tables
+//   M::load_sm(sm, dm)    cooperative copy (caller syncs)
+//   M::St                 per-thread register state; load/store SoA rows
+//   M::terminal(s)        terminal flag of a state
+//   M::step(...)          g(s, a, phi_t) on a non-terminal state (Eq. 9)
+//   M::upper(...)         per-scenario u(s) of Eq. 11 (non-terminal state)
+//   M::rollout<TRACE>     default-policy roll-out of Eq. 12 to depth D
+#pragma once
+#include "common.cuh"
+
+namespace hd {
+
+__device__ __forceinline__ void copy_words(void* dst, const void* src, int bytes, int tid, int nt) {
+  const uint32_t* s = static_cast<const uint32_t*>(src);
+  uint32_t* d = static_cast<uint32_t*>(dst);
+  for (int i = tid; i < bytes / 4; i += nt) d[i] = s[i];
+}
+
+// ===========================================================================
+// Tiger: state bit0 side, bit1 terminal; 0 LISTEN, 1 OPEN-LEFT, 2 OPEN-RIGHT
+// ===========================================================================
+struct Tiger {
+  struct Sm {
+    uint64_t t_listen;
+    uint32_t D;
+    double tail;
+    double gpow[kGpowN];
+  };
+  static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
+    if (tid == 0) {
+      sm.t_listen = dm.t_listen;
+      sm.D = dm.D;
+      sm.tail = dm.tail;
+    }
+    copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+  }
+  struct St {
+    uint32_t s;
+  };
+  static __device__ __forceinline__ St load(const Sm&, const uint32_t* st, uint32_t cap, uint32_t i) {
+    return St{st[i]};
+  }
+  static __device__ __forceinline__ void store(const Sm&, const St& s, uint32_t* st, uint32_t cap,
+                                               uint32_t i) {
+    st[i] = s.s;
+  }
+  static __device__ __forceinline__ bool terminal(const St& s) { return (s.s >> 1) & 1u; }
+  static constexpr uint32_t kTerminalObs = 3u;
+  static __device__ __forceinline__ bool step_u(const Sm& sm, St& s, int a, uint32_t u0, uint32_t& z,
+                                                float& r) {
+    const uint32_t side = s.s & 1u;
+    if (a == 0) {
+      const bool correct = event(u0, sm.t_listen);
+      const uint32_t heard = correct ? side : 1u - side;
+      r = -1.0f;
+      z = 1u + heard;
+      return false;
+    }
+    const uint32_t door = (uint32_t)(a - 1);
+    r = (door == side) ? -100.0f : 10.0f;
+    s.s = side | 2u;
+    z = kTerminalObs;
+    return true;
+  }
+  static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
+                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
+    const uint4 u = philox4x32_10(id, t, 0u, 0u, k0, k1);
+    return step_u(sm, s, a, u.x, z, r);
+  }
+  static __device__ __forceinline__ double upper(const Sm&, const St&) { return 10.0; }
+  static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
+  template <bool TRACE>
+  static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
+                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+    double acc = 0.0;
+    uint32_t t = t0;
+    bool term = false;
+    while (t < sm.D && !term) {
+      const int a = 0;  // Listen always
+      if (TRACE) h = (h ^ (uint64_t)a) * kFnvPrime;
+      float r;
+      term = step(sm, s, a, id, t + 1, k0, k1, z, r);
+      acc += sm.gpow[t - t0] * (double)r;
+      ++t;
+    }
+    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    ret = acc;
+    len = t - t0;
+  }
+};
+
+// ===========================================================================
+// RockSample(n, m) with R in {1, 2} robots (card §3.2).
+// word 0: good-rock mask; word 1: 16 bits per robot (y*n+x, 0xFFFF exited).
+// sub-actions: 0 N, 1 S, 2 E, 3 W, 4 SAMPLE, 5+j SENSE j; a = b0 + base*b1.
+// ===========================================================================
+template <int R>
+struct RockSample {
+  struct Sm {
+    int32_t n, m, base, policy_east;
+    uint32_t D;
+    double tail;
+    int8_t rx[32], ry[32];
+    uint8_t pos_rock[32];
+    uint32_t range_mask[2];
+    double gpow[kGpowN];
+    int8_t rock_at[kRsMaxN * kRsMaxN];
+    uint32_t thr[kRsMaxD2];
+  };
+  static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
+    if (tid == 0) {
+      sm.n = dm.n;
+      sm.m = dm.m;
+      sm.base = dm.base;
+      sm.policy_east = dm.policy_east;
+      sm.D = dm.D;
+      sm.tail = dm.tail;
+      sm.range_mask[0] = dm.range_mask[0];
+      sm.range_mask[1] = dm.range_mask[1];
+    }
+    copy_words(sm.rx, dm.rx, 32, tid, nt);
+    copy_words(sm.ry, dm.ry, 32, tid, nt);
+    copy_words(sm.pos_rock, dm.pos_rock, 32, tid, nt);
+    copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+    copy_words(sm.rock_at, dm.rock_at, (dm.n * dm.n + 3) & ~3, tid, nt);
+    copy_words(sm.thr, dm.sense_thr_m1, 4 * (dm.d2max + 1), tid, nt);
+  }
+  struct St {
+    uint32_t good;
+    int32_t x[R], y[R];
+    bool ex[R];
+  };
+  static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
+    St s;
+    s.good = st[i];
+    const uint32_t pos = st[cap + i];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t cell = (pos >> (16 * r)) & 0xFFFFu;
+      s.ex[r] = cell == 0xFFFFu;
+      const uint32_t c = s.ex[r] ? 0u : cell;
+      s.y[r] = (int32_t)(c / (uint32_t)sm.n);
+      s.x[r] = (int32_t)c - s.y[r] * sm.n;
+    }
+    return s;
+  }
+  static __device__ __forceinline__ uint32_t pos_word(const Sm& sm, const St& s) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      pos |= (s.ex[r] ? 0xFFFFu : (uint32_t)(s.y[r] * sm.n + s.x[r])) << (16 * r);
+    return pos;
+  }
+  static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
+                                               uint32_t i) {
+    st[i] = s.good;
+    st[cap + i] = pos_word(sm, s);
+  }
+  static __device__ __forceinline__ bool terminal(const St& s) {
+    bool t = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) t = t && s.ex[r];
+    return t;
+  }
+  static constexpr uint32_t kTerminalObs = (R == 1) ? 3u : 9u;
+
+  // one step with per-robot sub-actions b[r] and random words u[r]
+  static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
+                                                  uint32_t& z, float& rew) {
+    float reward = 0.0f;
+    uint32_t zsum = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      uint32_t zr = 0;
+      if (!s.ex[r]) {
+        const int sub = b[r];
+        int x = s.x[r], y = s.y[r];
+        if (sub == 0) {
+          y = y > 0 ? y - 1 : y;
+        } else if (sub == 1) {
+          y = y < sm.n - 1 ? y + 1 : y;
+        } else if (sub == 2) {
+          if (x < sm.n - 1) {
+            x += 1;
+          } else {
+            s.ex[r] = true;
+            reward = reward + 10.0f;  // exit east
+          }
+        } else if (sub == 3) {
+          x = x > 0 ? x - 1 : x;
+        } else if (sub == 4) {
+          const int j = sm.rock_at[y * sm.n + x];
+          if (j >= 0) {
+            if ((s.good >> j) & 1u) {
+              reward = reward + 10.0f;
+              s.good &= ~(1u << j);
+            } else {
+              reward = reward + (-10.0f);
+            }
+          }
+        } else {
+          const int j = sub - 5;
+          const int dx = x - sm.rx[j], dy = y - sm.ry[j];
+          const bool correct = u[r] <= sm.thr[dx * dx + dy * dy];
+          const bool isgood = (s.good >> j) & 1u;
+          zr = (isgood == correct) ? 1u : 2u;
+        }
+        s.x[r] = x;
+        s.y[r] = y;
+      }
+      zsum += zr * (r == 0 ? 1u : 3u);
+    }
+    rew = reward;
+    const bool term = terminal(s);
+    z = term ? kTerminalObs : zsum;
+    return term;
+  }
+  static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
+                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
+    int b[R];
+    int rest = a;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      b[q] = rest % sm.base;
+      rest /= sm.base;
+    }
+    const uint4 w = philox4x32_10(id, t, 0u, 0u, k0, k1);
+    const uint32_t u[2] = {w.x, w.y};
+    return step_sub(sm, s, b, u, z, r);
+  }
+  // u(s) = sum_{good j} 10 g^{min_r |r-j|_1} + sum_{r active} 10 g^{n-1-x_r}
+  static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
+    double u = 0.0;
+    for (int j = 0; j < sm.m; ++j) {
+      if (!((s.good >> j) & 1u)) continue;
+      int dmin = 1 << 20;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (s.ex[r]) continue;
+        const int d = abs(s.x[r] - sm.rx[j]) + abs(s.y[r] - sm.ry[j]);
+        dmin = d < dmin ? d : dmin;
+      }
+      u += 10.0 * sm.gpow[dmin];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (!s.ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - s.x[r]];
+    return u;
+  }
+  static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
+
+  // default policy (card §3.2).  Memory over policy positions p (rocks sorted
+  // by handling robot, then (x, y, j)): done bit = DONE, gm bit = GOOD.
+  static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
+                                                int* b, int* target) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      target[r] = -1;
+      if (sm.policy_east || s.ex[r]) {
+        b[r] = 2;
+        continue;
+      }
+      const uint32_t open = ~done & sm.range_mask[r];
+      if (!open) {
+        b[r] = 2;
+        continue;
+      }
+      const int p = __ffs(open) - 1;
+      const int j = sm.pos_rock[p];
+      target[r] = p;
+      if (!((gm >> p) & 1u)) {
+        b[r] = 5 + j;
+      } else {
+        const int tx = sm.rx[j], ty = sm.ry[j];
+        b[r] = (s.x[r] == tx && s.y[r] == ty) ? 4 : s.x[r] < tx ? 2 : s.x[r] > tx ? 3 : s.y[r] < ty ? 1 : 0;
+      }
+    }
+  }
+  template <bool TRACE>
+  static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
+                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+    double acc = 0.0;
+    uint32_t done = 0, gm = 0;
+    uint32_t t = t0;
+    bool term = false;
+    while (t < sm.D && !term) {
+      int b[R], tg[R];
+      policy(sm, s, done, gm, b, tg);
+      if (TRACE) {
+        int a = 0, mul = 1;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          a += b[r] * mul;
+          mul *= sm.base;
+        }
+        h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+      }
+      const uint4 w = philox4x32_10(id, t + 1, 0u, 0u, k0, k1);
+      const uint32_t u[2] = {w.x, w.y};
+      float r;
+      term = step_sub(sm, s, b, u, z, r);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (tg[q] < 0) continue;
+        const uint32_t bit = 1u << tg[q];
+        if (b[q] >= 5) {
+          const uint32_t zr = (q == 0) ? (z % 3u) : (z / 3u) % 3u;
+          if (zr == 1u) gm |= bit;
+          else done |= bit;
+        } else if (b[q] == 4) {
+          done |= bit;
+        }
+      }
+      acc += sm.gpow[t - t0] * (double)r;
+      ++t;
+    }
+    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    ret = acc;
+    len = t - t0;
+  }
+};
+
+// ===========================================================================
+// Navigation (card §3.3).  word 0: cell | gate<<8 | terminal<<9;
+// words 1..NW: occupancy bits of the unknown cells (row-major order).
+// actions 0 STAY, 1..8 = N, NE, E, SE, S, SW, W, NW.
+// ===========================================================================
+template <int NW>
+struct Nav {
+  struct Sm {
+    int32_t n, wall_y, goal_x, goal_y;
+    int32_t gate_x[2];
+    uint64_t t_fail, t_flip;
+    uint32_t D;
+    double tail;
+    double gpow[kGpowN];
+    uint2 nbr[kNavMaxN * kNavMaxN];
+  };
+  static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
+    if (tid == 0) {
+      sm.n = dm.n;
+      sm.wall_y = dm.wall_y;
+      sm.goal_x = dm.goal_x;
+      sm.goal_y = dm.goal_y;
+      sm.gate_x[0] = dm.gate_x[0];
+      sm.gate_x[1] = dm.gate_x[1];
+      sm.t_fail = dm.t_fail;
+      sm.t_flip = dm.t_flip;
+      sm.D = dm.D;
+      sm.tail = dm.tail;
+    }
+    copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+    copy_words(sm.nbr, dm.nbr, 8 * dm.n * dm.n, tid, nt);
+  }
+  struct St {
+    int32_t x, y;
+    uint32_t gate;
+    bool term;
+    uint32_t occ[NW];
+  };
+  static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
+    St s;
+    const uint32_t w0 = st[i];
+    const uint32_t cell = w0 & 0xFFu;
+    s.y = (int32_t)(cell / (uint32_t)sm.n);
+    s.x = (int32_t)cell - s.y * sm.n;
+    s.gate = (w0 >> 8) & 1u;
+    s.term = (w0 >> 9) & 1u;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) s.occ[k] = st[(1 + k) * cap + i];
+    return s;
+  }
+  static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
+                                               uint32_t i) {
+    st[i] = (uint32_t)(s.y * sm.n + s.x) | (s.gate << 8) | ((uint32_t)s.term << 9);
+#pragma unroll
+    for (int k = 0; k < NW; ++k) st[(1 + k) * cap + i] = s.occ[k];
+  }
+  static __device__ __forceinline__ bool terminal(const St& s) { return s.term; }
+  static constexpr uint32_t kTerminalObs = 0x100u;
+
+  static __device__ __forceinline__ uint32_t unknown_bit(const St& s, uint32_t idx) {
+    uint32_t w = s.occ[0];
+#pragma unroll
+    for (int k = 1; k < NW; ++k) w = (idx >> 5) == (uint32_t)k ? s.occ[k] : w;
+    return (w >> (idx & 31u)) & 1u;
+  }
+  // occupancy of neighbour descriptor d (0 free, 1 occupied, 2/3 gate, 4+idx)
+  static __device__ __forceinline__ uint32_t occupied(const St& s, uint32_t d) {
+    if (d >= 4u) return unknown_bit(s, d - 4u);
+    if (d >= 2u) return (d - 2u) != s.gate ? 1u : 0u;
+    return d;
+  }
+  static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
+                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
+    const uint4 u0 = philox4x32_10(id, t, 0u, 0u, k0, k1);
+    const uint4 u1 = philox4x32_10(id, t, 1u, 0u, k0, k1);
+    const uint4 u2 = philox4x32_10(id, t, 2u, 0u, k0, k1);
+    const uint32_t u[9] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x};
+    if (a == 0) {
+      r = -0.2f;  // stay
+    } else if (event(u[0], sm.t_fail)) {
+      r = -0.1f;  // failed move: stays, pays the motion cost
+    } else {
+      const uint2 nb = sm.nbr[s.y * sm.n + s.x];
+      const uint32_t d = ((a - 1) < 4 ? (nb.x >> (8 * (a - 1))) : (nb.y >> (8 * (a - 5)))) & 0xFFu;
+      if (occupied(s, d)) {
+        r = -1.0f;  // crash, position unchanged
+      } else {
+        // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
+        s.x += (a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0;
+        s.y += (a <= 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0;
+        if (s.x == sm.goal_x && s.y == sm.goal_y) {
+          r = 20.0f;  // goal, terminal
+          s.term = true;
+          z = kTerminalObs;
+          return true;
+        }
+        r = -0.1f;
+      }
+    }
+    const uint2 nb = sm.nbr[s.y * sm.n + s.x];
+    uint32_t obs = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t d = ((k < 4 ? nb.x : nb.y) >> (8 * (k & 3))) & 0xFFu;
+      const uint32_t flip = event(u[1 + k], sm.t_flip) ? 1u : 0u;
+      obs |= (occupied(s, d) ^ flip) << k;
+    }
+    z = obs;
+    return false;
+  }
+  static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
+    const int gx = sm.gate_x[s.gate];
+    const int W = sm.wall_y, Gx = sm.goal_x, Gy = sm.goal_y;
+    int d;
+    if (s.y < W) d = max(abs(s.x - gx), W - s.y) + max(abs(gx - Gx), Gy - W);
+    else if (s.y == W) d = max(abs(s.x - Gx), Gy - W);
+    else d = max(abs(s.x - Gx), Gy - s.y);
+    return 20.0 * sm.gpow[d - 1];
+  }
+  static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
+  static __device__ __forceinline__ int policy(uint32_t z, uint32_t t) {
+    const bool even = (t & 1u) == 0u;
+    if (!((z >> 4) & 1u)) return 5;  // S
+    if (!((z >> 3) & 1u)) return 4;  // SE
+    if (!((z >> 5) & 1u)) return 6;  // SW
+    const int e1 = even ? 3 : 7, e2 = even ? 7 : 3;
+    if (!((z >> (e1 - 1)) & 1u)) return e1;
+    if (!((z >> (e2 - 1)) & 1u)) return e2;
+    return 0;
+  }
+  template <bool TRACE>
+  static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
+                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+    double acc = 0.0;
+    uint32_t t = t0;
+    bool term = false;
+    while (t < sm.D && !term) {
+      const int a = policy(z, t);
+      if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+      float r;
+      term = step(sm, s, a, id, t + 1, k0, k1, z, r);
+      acc += sm.gpow[t - t0] * (double)r;
+      ++t;
+    }
+    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    ret = acc;
+    len = t - t0;
+  }
+};
+
+}  // namespace hd

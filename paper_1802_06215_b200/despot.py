@@ -1,0 +1,305 @@
+"""Thin ctypes binding of libdespot (include/despot.h).
+
+Argument marshalling only: every step of the batched leaf expansion runs in
+the library's sm_100a kernels.  There is no CPU fallback -- if libdespot.so is
+missing or no CUDA device is usable, calls raise DespotError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdespot.so")
+
+DESPOT_X_DEVICE_OUTPUTS = 1
+DESPOT_X_RECORD_SCENARIO = 2
+DESPOT_X_TIMING = 4
+DESPOT_MF_UNFACTORED = 1
+
+STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5: "ECUDA",
+          -6: "ENCCL", -7: "ESHUTDOWN", -8: "EHASH"}
+
+# every function declared in include/despot.h (checked by the CPU tests)
+EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "despot_model_info_get",
+           "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
+           "despot_node_release", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
+           "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words"]
+
+
+class DespotError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Opts(C.Structure):
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("flags", C.c_uint32)]
+
+
+class ModelInfo(C.Structure):
+    _fields_ = [("num_actions", C.c_uint32), ("state_words", C.c_uint32), ("obs_words", C.c_uint32),
+                ("obs_slots", C.c_uint32), ("max_depth", C.c_uint32), ("elements", C.c_uint32),
+                ("gamma", C.c_double), ("tail", C.c_double)]
+
+
+class Leaf(C.Structure):
+    _fields_ = [("parent", C.c_uint64), ("action", C.c_int32), ("child", C.c_uint32),
+                ("depth", C.c_uint32), ("pad", C.c_uint32)]
+
+
+class Expansion(C.Structure):
+    _fields_ = [("flags", C.c_uint32), ("node", C.c_void_p), ("n_scen", C.c_void_p), ("weight", C.c_void_p),
+                ("act_reward", C.c_void_p), ("act_upper", C.c_void_p), ("act_lower", C.c_void_p),
+                ("child_begin", C.c_void_p), ("child_capacity", C.c_uint32),
+                ("child_count", C.c_void_p), ("child_first", C.c_void_p), ("child_weight", C.c_void_p),
+                ("child_upper", C.c_void_p), ("child_lower", C.c_void_p), ("child_obs", C.c_void_p),
+                ("scen_capacity", C.c_uint64), ("scen_obs", C.c_void_p), ("scen_reward", C.c_void_p),
+                ("scen_upper", C.c_void_p), ("scen_lower", C.c_void_p), ("scen_len", C.c_void_p),
+                ("scen_hash", C.c_void_p), ("scen_states", C.c_void_p),
+                ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("pad", C.c_uint32),
+                ("phase_ms", C.c_float * 4)]
+
+
+class Exchange(C.Structure):
+    _fields_ = [("sums", C.c_void_p), ("n_sums", C.c_uint64), ("mins", C.c_void_p), ("n_mins", C.c_uint64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdespot.so (in-tree).  Raises if it was not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DespotError(-5, f"{LIB_PATH} not built (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+        L.despot_last_error.restype = C.c_char_p
+        L.despot_model_load.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(Opts), C.POINTER(vp)]
+        L.despot_model_info_get.argtypes = [vp, C.POINTER(ModelInfo)]
+        L.despot_model_free.argtypes = [vp]
+        L.despot_belief_load.argtypes = [vp, vp, vp, u32, u64, vp, C.POINTER(u64)]
+        L.despot_node_info.argtypes = [vp, u64, C.POINTER(u32), C.POINTER(u32)]
+        L.despot_node_read.argtypes = [vp, u64, vp, vp, vp, vp]
+        L.despot_node_release.argtypes = [vp, u64]
+        L.despot_expand_batch.argtypes = [vp, C.POINTER(Leaf), u32, C.POINTER(Expansion), vp]
+        L.despot_expand_begin.argtypes = [vp, C.POINTER(Leaf), u32, u32, vp, C.POINTER(vp)]
+        L.despot_batch_exchange.argtypes = [vp, C.POINTER(Exchange)]
+        L.despot_expand_end.argtypes = [vp, C.POINTER(Expansion), vp]
+        L.despot_batch_abort.argtypes = [vp]
+        L.despot_rollout_bounds.argtypes = [vp, u64, C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp, vp]
+        L.despot_stream_words.argtypes = [vp, u64, vp, u32, u32, u32, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise DespotError(rc, lib().despot_last_error().decode())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Model:
+    """A loaded model (despot_model*)."""
+
+    def __init__(self, kind: str, params: str = "", device: int = 0, rank: int = 0, world: int = 1,
+                 flags: int = 0):
+        self.h = C.c_void_p()
+        o = Opts(device, rank, world, flags)
+        _check(lib().despot_model_load(kind.encode(), params.encode(), C.byref(o), C.byref(self.h)))
+        info = ModelInfo()
+        _check(lib().despot_model_info_get(self.h, C.byref(info)))
+        self.kind, self.params, self.device, self.rank, self.world = kind, params, device, rank, world
+        self.A, self.SW, self.OW = info.num_actions, info.state_words, info.obs_words
+        self.slots, self.D, self.elements = info.obs_slots, info.max_depth, info.elements
+        self.gamma, self.tail = info.gamma, info.tail
+
+    def close(self):
+        if self.h:
+            lib().despot_model_free(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- nodes ----
+    def belief_load(self, states_soa, weights, seed, stream=None) -> int:
+        st = np.ascontiguousarray(states_soa, dtype=np.uint32)
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        K = int(w.shape[0])
+        if st.shape != (self.SW, K):
+            raise DespotError(-1, f"states must be [{self.SW}][{K}]")
+        out = C.c_uint64()
+        _check(lib().despot_belief_load(self.h, st.ctypes.data, w.ctypes.data, K, int(seed),
+                                        _stream_ptr(stream), C.byref(out)))
+        return int(out.value)
+
+    def node_info(self, node):
+        n, d = C.c_uint32(), C.c_uint32()
+        _check(lib().despot_node_info(self.h, int(node), C.byref(n), C.byref(d)))
+        return int(n.value), int(d.value)
+
+    def node_read(self, node, stream=None):
+        n, d = self.node_info(node)
+        ids = np.zeros(n, np.uint32)
+        w = np.zeros(n, np.float32)
+        st = np.zeros((self.SW, n), np.uint32)
+        _check(lib().despot_node_read(self.h, int(node), ids.ctypes.data, w.ctypes.data, st.ctypes.data,
+                                      _stream_ptr(stream)))
+        return dict(ids=ids, w=w, states=st, depth=d)
+
+    def node_release(self, node):
+        _check(lib().despot_node_release(self.h, int(node)))
+
+    # ---- expansion ----
+    @staticmethod
+    def _leaves(leaves):
+        Lc = len(leaves)
+        lv = (Leaf * Lc)()
+        for i, (p, a, c, d) in enumerate(leaves):
+            lv[i].parent, lv[i].action, lv[i].child, lv[i].depth = int(p), int(a), int(c), int(d)
+        return lv
+
+    def child_capacity_bound(self, leaves):
+        per = self.slots if self.slots else None
+        tot = 0
+        for (p, a, c, d) in leaves:
+            n, _ = self.node_info(p)
+            tot += self.A * (min(n * max(self.world, 1), per) if per else n)
+        return max(tot, 1)
+
+    def _alloc_outputs(self, L, C_cap, S_cap, record, device):
+        A, OW, SW = self.A, self.OW, self.SW
+        if device:
+            import torch
+            dev = torch.device("cuda", self.device)
+            z = lambda n, dt: torch.zeros(max(int(n), 1), dtype=dt, device=dev)  # noqa: E731
+            u32, f32, i64 = torch.int32, torch.float32, torch.int64
+            ptr = lambda t: t.data_ptr()  # noqa: E731
+        else:
+            z = lambda n, dt: np.zeros(max(int(n), 1), dtype=dt)  # noqa: E731
+            u32, f32, i64 = np.uint32, np.float32, np.uint64
+            ptr = lambda t: t.ctypes.data  # noqa: E731
+        o = dict(n_scen=z(L, u32), weight=z(L, f32), act_reward=z(L * A, f32), act_upper=z(L * A, f32),
+                 act_lower=z(L * A, f32), child_begin=z(L * A + 1, u32), child_count=z(C_cap, u32),
+                 child_first=z(C_cap, u32), child_weight=z(C_cap, f32), child_upper=z(C_cap, f32),
+                 child_lower=z(C_cap, f32), child_obs=z(C_cap * OW, u32))
+        if record:
+            o.update(scen_obs=z(S_cap * OW, u32), scen_reward=z(S_cap, f32), scen_upper=z(S_cap, f32),
+                     scen_lower=z(S_cap, f32), scen_len=z(S_cap, u32), scen_hash=z(S_cap, i64),
+                     scen_states=z(S_cap * SW, u32))
+        E = Expansion()
+        for k, v in o.items():
+            setattr(E, k, ptr(v))
+        E.child_capacity = int(C_cap)
+        E.scen_capacity = int(S_cap) if record else 0
+        return o, E
+
+    def _finish(self, o, E, L, nodes, record, device):
+        A = self.A
+        Cn = int(E.num_children)
+        out = dict(o)
+        out["node"] = [int(x) for x in nodes]
+        out["scenario_steps"] = int(E.scenario_steps)
+        out["num_children"] = Cn
+        out["phase_ms"] = [float(x) for x in E.phase_ms]
+        if not device:
+            for k in ("child_count", "child_first", "child_weight", "child_upper", "child_lower"):
+                out[k] = o[k][:Cn]
+            out["child_obs"] = o["child_obs"][: Cn * self.OW].reshape(Cn, self.OW)
+            if record:
+                S = int(o["n_scen"].astype(np.int64).sum()) * A
+                for k in ("scen_reward", "scen_upper", "scen_lower", "scen_len", "scen_hash"):
+                    out[k] = o[k][:S]
+                out["scen_obs"] = o["scen_obs"][: S * self.OW].reshape(S, self.OW)
+                out["scen_states"] = o["scen_states"][: S * self.SW].reshape(S, self.SW)
+        return out
+
+    def expand(self, leaves, record=False, device_outputs=False, child_capacity=None, scen_capacity=None,
+               stream=None, timing=False, outputs=None):
+        """leaves: list of (node, action, child, depth).  Returns a dict of
+        arrays (numpy, or torch CUDA tensors with device_outputs=True)."""
+        L = len(leaves)
+        lv = self._leaves(leaves)
+        C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
+        S_cap = 0
+        if record:
+            S_cap = scen_capacity if scen_capacity is not None else sum(self.A * self.node_info(p)[0]
+                                                                         for (p, a, c, d) in leaves)
+        if outputs is None:
+            o, E = self._alloc_outputs(L, C_cap, S_cap, record, device_outputs)
+        else:  # reuse preallocated buffers (bench): (dict, Expansion)
+            o, E = outputs
+        nodes = (C.c_uint64 * L)()
+        E.node = C.addressof(nodes)
+        E.flags = ((DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_RECORD_SCENARIO if record else 0)
+                   | (DESPOT_X_TIMING if timing else 0))
+        _check(lib().despot_expand_batch(self.h, lv, L, C.byref(E), _stream_ptr(stream)))
+        return self._finish(o, E, L, nodes, record, device_outputs)
+
+    # ---- two-phase form for scenario sharding ----
+    def alloc_outputs(self, leaves, device_outputs=False, child_capacity=None):
+        C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
+        return self._alloc_outputs(len(leaves), C_cap, 0, False, device_outputs)
+
+    def expand_begin(self, leaves, record=False, stream=None, timing=False):
+        lv = self._leaves(leaves)
+        b = C.c_void_p()
+        flags = (DESPOT_X_RECORD_SCENARIO if record else 0) | (DESPOT_X_TIMING if timing else 0)
+        _check(lib().despot_expand_begin(self.h, lv, len(leaves), flags, _stream_ptr(stream), C.byref(b)))
+        ex = Exchange()
+        _check(lib().despot_batch_exchange(b, C.byref(ex)))
+        return b, ex
+
+    def expand_end(self, batch, leaves, device_outputs=False, child_capacity=None, stream=None, timing=False,
+                   outputs=None):
+        L = len(leaves)
+        if outputs is None:
+            C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
+            o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs)
+        else:
+            o, E = outputs
+        nodes = (C.c_uint64 * L)()
+        E.node = C.addressof(nodes)
+        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_TIMING if timing else 0)
+        _check(lib().despot_expand_end(batch, C.byref(E), _stream_ptr(stream)))
+        return self._finish(o, E, L, nodes, False, device_outputs)
+
+    def batch_abort(self, batch):
+        _check(lib().despot_batch_abort(batch))
+
+    def rollout_bounds(self, node, per_scenario=False, stream=None):
+        n, _ = self.node_info(node)
+        u, l = C.c_float(), C.c_float()
+        pu = np.zeros(max(n, 1), np.float32)
+        pl = np.zeros(max(n, 1), np.float32)
+        _check(lib().despot_rollout_bounds(self.h, int(node), C.byref(u), C.byref(l), pu.ctypes.data,
+                                           pl.ctypes.data, _stream_ptr(stream)))
+        if per_scenario:
+            return u.value, l.value, pu[:n], pl[:n]
+        return u.value, l.value
+
+    def stream_words(self, seed, ids, t, k, stream=None):
+        ids = np.ascontiguousarray(ids, dtype=np.uint32)
+        out = np.zeros(len(ids), np.uint32)
+        _check(lib().despot_stream_words(self.h, int(seed), ids.ctypes.data, len(ids), int(t), int(k),
+                                         out.ctypes.data, _stream_ptr(stream)))
+        return out

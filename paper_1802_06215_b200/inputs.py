@@ -183,6 +183,19 @@ CONFIGS = {
 }
 
 
+def car_roots(L, K, peds=20, base_seed=1004):
+    """Config 4's batch: L concurrent root beliefs (crowd layouts and goal
+    samples differ per root).  At depth >= 1 every car child holds a single
+    scenario (the 0.5 m observation grid separates all of them), so a
+    batch of L depth-1 leaves would carry L scenarios; the K=500 workload of
+    the config is therefore L roots expanded in one launch."""
+    out = []
+    for j in range(L):
+        seed = base_seed + 1000 * j
+        out.append((car_belief(K, seed, peds, layout_seed=7 + j), weights(K, seed), seed))
+    return out
+
+
 def config_inputs(cfg: int, K=None, L=None, uniform=True, D=None):
     """(kind, params, states_soa, weights, seed, L) of a BASELINE config."""
     c = dict(CONFIGS[cfg])

@@ -1,0 +1,340 @@
+"""GPU parity: libdespot (through the C ABI) vs the CPU oracle on identical
+seeded inputs.  Discrete outputs bit-exact, values within 1e-5 (parity.py)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1802_06215_b200 import inputs
+from paper_1802_06215_b200.despot import DespotError, Model
+
+from parity import compare_batch, expand_root_both, setup
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+# ----------------------------------------------------------------------------
+def test_stream_words_match_oracle_philox():
+    gm = Model("tiger", inputs.tiger_params())
+    rng = np.random.default_rng(3)
+    ids = rng.integers(0, 2**31, 1000).astype(np.uint32)
+    for seed, t, k in ((0, 0, 0), (0xDEADBEEF12345678, 7, 5), (1004, 90, 8), (2**64 - 1, 1, 3)):
+        g = gm.stream_words(seed, ids, t, k)
+        key = [seed & 0xFFFFFFFF, seed >> 32]
+        o = np.array([oracle.philox([i, t, k >> 2, 0], key)[k & 3] for i in ids], np.uint32)
+        assert np.array_equal(g, o)
+
+
+# ----------------------------------------------------------------------------
+# full configs (BASELINE.json), in the launch configuration bench.py times;
+# the oracle checks a sample of the leaves (each leaf's outputs depend only on
+# that leaf)
+# ----------------------------------------------------------------------------
+def _full_config(cfg, K=None, L=None, sample=(0, 1, -2, -1), action_mask=None):
+    gm, om, st, w, seed, L = setup(cfg, K=K, L=L)
+    gr, orr, G0, O0 = expand_root_both(gm, om, st, w, seed, record=False)
+    compare_batch(G0, O0, gm, om, [(0, 0)])
+    glv = inputs.select_leaves(G0["child_count"], G0["child_begin"], gm.A, L)
+    olv = inputs.select_leaves(O0["child_count"], O0["child_begin"], om.A, L)
+    assert glv == olv
+    G = gm.expand([(gr, a, c, 1) for a, c in glv])
+    idx = sorted({s % L for s in sample})
+    O = om.expand([(orr, glv[i][0], glv[i][1], 1) for i in idx], record=True, action_mask=action_mask)
+    if action_mask is None:
+        compare_batch(G, O, gm, om, list(zip(idx, range(len(idx)))))
+    else:
+        # compare the masked actions only
+        A = gm.A
+        for j, i in enumerate(idx):
+            assert int(G["n_scen"][i]) == int(O["n_scen"][j])
+        acts = np.nonzero(action_mask)[0]
+        for j, i in enumerate(idx):
+            for a in acts:
+                gb, ge = G["child_begin"][i * A + a], G["child_begin"][i * A + a + 1]
+                ob, oe = O["child_begin"][j * A + a], O["child_begin"][j * A + a + 1]
+                assert np.array_equal(G["child_first"][gb:ge], O["child_first"][ob:oe])
+                assert np.array_equal(G["child_count"][gb:ge], O["child_count"][ob:oe])
+                np.testing.assert_allclose(G["child_upper"][gb:ge], O["child_upper"][ob:oe], rtol=1e-5, atol=1e-5)
+                np.testing.assert_allclose(G["child_lower"][gb:ge], O["child_lower"][ob:oe], rtol=1e-5, atol=1e-5)
+                np.testing.assert_allclose(G["act_upper"][i * A + a], O["act_upper"][j * A + a], rtol=1e-5, atol=1e-5)
+                np.testing.assert_allclose(G["act_lower"][i * A + a], O["act_lower"][j * A + a], rtol=1e-5, atol=1e-5)
+    gm.close()
+
+
+def test_config1_rocksample_root():
+    gm, om, st, w, seed, L = setup(1)
+    gr, orr, G, O = expand_root_both(gm, om, st, w, seed, record=True)
+    compare_batch(G, O, gm, om, [(0, 0)], check_scen=True)
+    assert G["scenario_steps"] == O["scenario_steps"]
+
+
+def test_config2_mars_64_leaves():
+    _full_config(2)
+
+
+def test_config3_nav_64_leaves():
+    _full_config(3, sample=(0, 31, -1))
+
+
+def test_config5_sweep_k4096_256_leaves():
+    mask = np.zeros(400, np.uint8)
+    mask[::17] = 1
+    _full_config(5, K=4096, sample=(0, -1), action_mask=mask)
+
+
+# ----------------------------------------------------------------------------
+# small cases compared completely, incl. per-scenario records
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("cfg,K,L,uniform,D", [
+    (1, 100, 6, False, 20),
+    (2, 96, 16, False, 20),
+    (2, 33, 5, True, 7),
+    (3, 77, 9, False, 40),
+    (3, 500, 3, True, 90),
+])
+def test_small_full_parity_with_records(cfg, K, L, uniform, D):
+    gm, om, st, w, seed, _ = setup(cfg, K=K, L=L, uniform=uniform, D=D)
+    gr, orr, G0, O0 = expand_root_both(gm, om, st, w, seed, record=True)
+    compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
+    assert G0["scenario_steps"] == O0["scenario_steps"]
+    lv = inputs.select_leaves(G0["child_count"], G0["child_begin"], gm.A, L)
+    G = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+    O = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+    compare_batch(G, O, gm, om, [(i, i) for i in range(L)], check_scen=True)
+    assert G["scenario_steps"] == O["scenario_steps"]
+    # the update step (K1) materialises exactly the oracle's scenario subsets
+    for i in range(L):
+        gn, on = gm.node_read(G["node"][i]), om.node_read(int(O["node"][i]))
+        assert np.array_equal(gn["ids"], on["ids"]) and np.array_equal(gn["states"], on["states"])
+        assert np.array_equal(gn["w"], on["w"])
+    # depth 2: children of the leaves
+    lv2 = []
+    for i in range(min(L, 3)):
+        for a in range(0, gm.A, max(1, gm.A // 3)):
+            b, e = G["child_begin"][i * gm.A + a], G["child_begin"][i * gm.A + a + 1]
+            if e > b:
+                lv2.append((i, a, int(e - b) - 1))
+    G2 = gm.expand([(G["node"][i], a, c, 2) for i, a, c in lv2], record=True)
+    O2 = om.expand([(int(O["node"][i]), a, c, 2) for i, a, c in lv2], record=True)
+    compare_batch(G2, O2, gm, om, [(i, i) for i in range(len(lv2))], check_scen=True)
+    gm.close()
+
+
+def test_tiger_and_terminal_scenarios():
+    gm = Model("tiger", inputs.tiger_params(D=12))
+    om = oracle.Model("tiger", inputs.tiger_params(D=12))
+    st = np.array([[0, 1, 2, 3, 1, 0, 3, 2, 1]], np.uint32)  # 2, 3 = terminal
+    w = inputs.weights(9, 5, uniform=False)
+    gr, orr = gm.belief_load(st, w, 77), om.belief_load(st, w, 77)
+    G = gm.expand([(gr, -1, 0, 0)], record=True)
+    O = om.expand([(orr, -1, 0, 0)], record=True)
+    compare_batch(G, O, gm, om, [(0, 0)], check_scen=True)
+    lv = [(a, c) for a in range(3) for c in range(int(G["child_begin"][a + 1] - G["child_begin"][a]))]
+    G2 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+    O2 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+    compare_batch(G2, O2, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
+
+
+def test_rocksample_terminal_and_ragged_beliefs():
+    params = inputs.rocksample_params(5, 3, 2, D=9)
+    gm, om = Model("rocksample", params), oracle.Model("rocksample", params)
+    for K in (1, 31, 32, 33, 65):
+        rng = np.random.default_rng(K)
+        st = np.zeros((2, K), np.uint32)
+        st[0] = rng.integers(0, 8, K)
+        cells = rng.integers(0, 25, (K, 2))
+        cells[rng.random((K, 2)) < 0.3] = 0xFFFF  # exited robots; both exited = terminal
+        st[1] = cells[:, 0] | (cells[:, 1] << 16)
+        w = inputs.weights(K, K, uniform=False)
+        gr, orr = gm.belief_load(st, w, K), om.belief_load(st, w, K)
+        G = gm.expand([(gr, -1, 0, 0)], record=True)
+        O = om.expand([(orr, -1, 0, 0)], record=True)
+        compare_batch(G, O, gm, om, [(0, 0)], check_scen=True)
+        assert G["scenario_steps"] == O["scenario_steps"]
+
+
+def test_mixed_beliefs_and_self_leaves_in_one_batch():
+    kind, params, st, w, seed, _ = inputs.config_inputs(2, K=70)
+    st2 = inputs.rocksample_belief(15, 15, 2, 50, 99)
+    w2 = inputs.weights(50, 3, uniform=False)
+    gm, om = Model(kind, params), oracle.Model(kind, params)
+    ga, oa = gm.belief_load(st, w, seed), om.belief_load(st, w, seed)
+    gb, ob = gm.belief_load(st2, w2, 4242), om.belief_load(st2, w2, 4242)
+    G0 = gm.expand([(ga, -1, 0, 0), (gb, -1, 0, 0)])
+    O0 = om.expand([(oa, -1, 0, 0), (ob, -1, 0, 0)], record=True)
+    compare_batch(G0, O0, gm, om, [(0, 0), (1, 1)])
+    leaves = [(ga, 7, 0, 1), (gb, 5 + 3, 1, 1), (ga, -1, 0, 0), (gb, 399, 0, 1)]
+    oleaves = [(oa, 7, 0, 1), (ob, 5 + 3, 1, 1), (oa, -1, 0, 0), (ob, 399, 0, 1)]
+    G = gm.expand(leaves)
+    O = om.expand(oleaves, record=True)
+    compare_batch(G, O, gm, om, [(i, i) for i in range(4)])
+
+
+def test_errors_are_reported():
+    kind, params, st, w, seed, _ = inputs.config_inputs(1)
+    gm = Model(kind, params)
+    gr = gm.belief_load(st, w, seed)
+    with pytest.raises(DespotError) as e:
+        gm.expand([(gr, 3, 0, 1)])  # parent not expanded yet
+    assert e.value.code == -1
+    gm.expand([(gr, -1, 0, 0)])
+    with pytest.raises(DespotError) as e:
+        gm.expand([(gr, 13, 0, 1)])
+    assert e.value.code == -2  # EMODEL: action outside [-1, |A|)
+    with pytest.raises(DespotError) as e:
+        gm.expand([(gr, 0, 5, 1)])  # child ordinal 5 does not exist
+    assert e.value.code == -1
+    with pytest.raises(DespotError) as e:
+        gm.expand([(gr, 0, 0, 2)])  # depth != parent depth + 1
+    assert e.value.code == -1
+    with pytest.raises(DespotError) as e:
+        gm.expand([(gr, -1, 0, 0)], child_capacity=3)
+    assert e.value.code == -4
+    with pytest.raises(DespotError):
+        gm.belief_load(st, np.zeros_like(w), seed)
+    # the model still works after the errors
+    G = gm.expand([(gr, 5, 0, 1)])
+    assert G["n_scen"][0] > 0
+
+
+def test_determinism_and_device_outputs():
+    import torch
+    gm, om, st, w, seed, L = setup(2, K=200, L=8)
+    gr = gm.belief_load(st, w, seed)
+    R = gm.expand([(gr, -1, 0, 0)])
+    lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)]
+    A1 = gm.expand(lv)
+    A2 = gm.expand(lv)
+    D1 = gm.expand(lv, device_outputs=True)
+    torch.cuda.synchronize()
+    for k in ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+              "child_first", "child_weight", "child_upper", "child_lower"):
+        assert np.array_equal(A1[k], A2[k]), k  # exact reductions: bit-identical values
+        d = D1[k].cpu().numpy()[: len(A1[k])]
+        assert np.array_equal(d.view(A1[k].dtype) if d.dtype != A1[k].dtype else d, A1[k]), k
+
+
+def test_rollout_bounds_match_oracle():
+    for cfg in (1, 3):
+        gm, om, st, w, seed, _ = setup(cfg, K=150, uniform=False)
+        gr, orr = gm.belief_load(st, w, seed), om.belief_load(st, w, seed)
+        gu, gl, pu, pl = gm.rollout_bounds(gr, per_scenario=True)
+        ou, ol, qu, ql = om.rollout_bounds(orr, per_scenario=True)
+        np.testing.assert_allclose(pu, qu, rtol=1e-6)
+        np.testing.assert_allclose(pl, ql, rtol=1e-5, atol=1e-5 * np.abs(ql).max())
+        assert abs(gu - ou) <= 1e-5 * abs(ou) and abs(gl - ol) <= 1e-5 * max(abs(ol), 1.0)
+
+
+def test_fake_ranks_equal_single_gpu():
+    """Scenario sharding with the ranks emulated one after the
+    other on one GPU: the merged result equals world == 1 bit for bit."""
+    import torch
+    from paper_1802_06215_b200.dist import exchange_views
+    kind, params, st, w, seed, L = inputs.config_inputs(2, K=300, L=12)
+    g1 = Model(kind, params)
+    r1 = g1.belief_load(st, w, seed)
+    R = g1.expand([(r1, -1, 0, 0)])
+    lv = inputs.select_leaves(R["child_count"], R["child_begin"], g1.A, L)
+    ref = g1.expand([(r1, a, c, 1) for a, c in lv])
+    for world in (2, 3):
+        ms = [Model(kind, params, rank=r, world=world) for r in range(world)]
+        roots = [m.belief_load(st, w, seed) for m in ms]
+
+        def sharded(leaf_lists):
+            begun = [m.expand_begin(ll) for m, ll in zip(ms, leaf_lists)]
+            views = [exchange_views(ex, torch.device("cuda", 0)) for (_, ex) in begun]
+            torch.cuda.synchronize()
+            tot = sum(v[0] for v in views)
+            mn = torch.stack([v[1] for v in views]).min(dim=0).values
+            for s, mi in views:
+                s.copy_(tot)
+                mi.copy_(mn)
+            torch.cuda.synchronize()
+            return [m.expand_end(b, ll) for m, (b, _), ll in zip(ms, begun, leaf_lists)]
+
+        outs0 = sharded([[(rt, -1, 0, 0)] for rt in roots])
+        for o in outs0:
+            for k in ("child_begin", "child_count", "child_first", "act_upper", "act_lower", "child_upper"):
+                assert np.array_equal(o[k], R[k]), (world, k)
+        outs = sharded([[(rt, a, c, 1) for a, c in lv] for rt in roots])
+        for o in outs:
+            for k in ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+                      "child_first", "child_weight", "child_upper", "child_lower", "child_obs"):
+                assert np.array_equal(o[k], ref[k]), (world, k)
+            assert o["scenario_steps"] == ref["scenario_steps"]
+
+
+# ----------------------------------------------------------------------------
+# driving (config 4): sparse 21-word keys, factored warp kernel
+# ----------------------------------------------------------------------------
+def _car_models(peds=20, D=90):
+    params = inputs.car_params(peds, D=D)
+    return (Model("car", params), Model("car", params, flags=1), oracle.Model("car", params))
+
+
+def test_config4_car_64_roots_factored_and_unfactored():
+    gw, gt, om = _car_models()
+    roots = inputs.car_roots(64, 500)
+    gws = [gw.belief_load(st, w, sd) for st, w, sd in roots]
+    gts = [gt.belief_load(st, w, sd) for st, w, sd in roots]
+    Gw = gw.expand([(r, -1, 0, 0) for r in gws])
+    Gt = gt.expand([(r, -1, 0, 0) for r in gts])
+    for k in ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+              "child_first", "child_weight", "child_upper", "child_lower", "child_obs"):
+        assert np.array_equal(Gw[k], Gt[k]), k  # factored == unfactored, bit for bit
+    assert Gw["scenario_steps"] == Gt["scenario_steps"]
+    sample = [0, 17, 63]
+    ors = [om.belief_load(*roots[j]) for j in sample]
+    O = om.expand([(r, -1, 0, 0) for r in ors], record=True)
+    compare_batch(Gw, O, gw, om, list(zip(sample, range(len(sample)))))
+
+
+@pytest.mark.parametrize("peds,K,D", [(20, 64, 40), (6, 45, 90), (2, 7, 12), (12, 33, 30)])
+def test_car_small_full_parity_with_records(peds, K, D):
+    gw, gt, om = _car_models(peds, D)
+    st = inputs.car_belief(K, 5 + K, peds)
+    st[0] = np.float32(12.0).view(np.uint32)  # closer to the goal: goal and collision outcomes occur
+    w = inputs.weights(K, K, uniform=False)
+    for gm in (gw, gt):
+        gr, orr = gm.belief_load(st, w, 31), om.belief_load(st, w, 31)
+        G0 = gm.expand([(gr, -1, 0, 0)], record=True)
+        O0 = om.expand([(orr, -1, 0, 0)], record=True)
+        compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
+        assert G0["scenario_steps"] == O0["scenario_steps"]
+        # depth-1 leaves through the full-key update step, then their expansion
+        lv = [(a, c) for a in range(3) for c in range(min(3, int(G0["child_begin"][a + 1] - G0["child_begin"][a])))]
+        G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+        O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+        compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
+        assert G1["scenario_steps"] == O1["scenario_steps"]
+
+
+def test_car_factored_equals_unfactored_1000_random_steps():
+    """S:480 acceptance criterion 6: the factored step equals the unfactored
+    step bit-exactly over 1000 random (s, a, phi, depth) triples -- here as
+    1000 one-step expansions of random states (D = depth + 1, so the batch is
+    exactly the step, its observation and its reward)."""
+    rng = np.random.default_rng(6)
+    for trial in range(10):
+        peds = int(rng.choice([1, 6, 12, 20, 31]))
+        gw, gt, _ = _car_models(peds, D=2)
+        K = 100
+        st = inputs.car_belief(K, trial, peds, layout_seed=trial)
+        xs = rng.uniform(0, 20, K).astype(np.float32)
+        st[0] = xs.view(np.uint32)
+        st[1] = rng.integers(0, 5, K)
+        for i in range(peds):
+            st[4 + 2 * i] = rng.uniform(-2, 22, K).astype(np.float32).view(np.uint32)
+            st[5 + 2 * i] = rng.uniform(-6, 6, K).astype(np.float32).view(np.uint32)
+        w = inputs.weights(K)
+        Gs = []
+        for gm in (gw, gt):
+            r = gm.belief_load(st, w, 1000 + trial)
+            Gs.append(gm.expand([(r, -1, 0, 0)], record=True))
+        for k in ("scen_obs", "scen_reward", "scen_states", "scen_len", "scen_hash", "scen_upper", "scen_lower"):
+            assert np.array_equal(Gs[0][k], Gs[1][k]), (peds, k)
