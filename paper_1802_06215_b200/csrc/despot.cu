@@ -794,10 +794,15 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     off += align256(bytes);
     return o;
   };
-  const size_t o_leaves = take(sizeof(LeafDev) * L), o_nleaf = take(4 * (size_t)L),
-               o_tile = take(4 * ((size_t)L + 1)), o_scen = take(8 * ((size_t)L + 1)),
-               o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
-               o_nc = take(4 * LA), o_err = take(4), o_item = take(b->sparse ? 4 * LAS : 0),
+  // status block [err u32 | total children u32 | steps u64 | n_leaf[L] u32]
+  // sits right before the SUM block: one memset zeroes both, one D2H reads it
+  const size_t stat_bytes = 16 + 4 * (size_t)L;
+  const size_t o_leaves = take(sizeof(LeafDev) * L), o_tile = take(4 * ((size_t)L + 1)),
+               o_scen = take(8 * ((size_t)L + 1));
+  const size_t o_stat = off;
+  off += (stat_bytes + 7) & ~size_t(7);
+  const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
+               o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
                o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound);
   if (cudaMallocAsync(&b->scratch, off, st) != cudaSuccess) {
     free_batch(b.release(), true);
@@ -810,14 +815,15 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   bd.L = L;
   bd.A = dm.A;
   bd.S = b->S;
-  bd.n_leaf = reinterpret_cast<uint32_t*>(s + o_nleaf);
+  bd.status = reinterpret_cast<uint32_t*>(s + o_stat);
+  bd.err = bd.status;
+  bd.n_leaf = bd.status + 4;
   bd.tile_off = reinterpret_cast<uint32_t*>(s + o_tile);
   bd.scen_off = reinterpret_cast<uint64_t*>(s + o_scen);
   bd.sums = reinterpret_cast<int64_t*>(s + o_sums);
   bd.mins = reinterpret_cast<int32_t*>(s + o_mins);
   bd.rank = reinterpret_cast<uint32_t*>(s + o_rank);
   bd.nc = reinterpret_cast<uint32_t*>(s + o_nc);
-  bd.err = reinterpret_cast<uint32_t*>(s + o_err);
   if (b->sparse) {
     bd.sp_item = reinterpret_cast<uint32_t*>(s + o_item);
     b->io.hash = reinterpret_cast<uint64_t*>(s + o_hash);
@@ -831,9 +837,8 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   if (!rc) {
     memcpy(hp, ld.data(), sizeof(LeafDev) * L);
     if (cudaMemcpyAsync(s + o_leaves, hp, sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(bd.sums, 0, 8 * b->n_sums, st) != cudaSuccess ||
-        cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
-        cudaMemsetAsync(bd.err, 0, 4, st) != cudaSuccess)
+        cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
+        cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
   }
   // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
@@ -867,10 +872,24 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       using M = decltype(mdl);
       const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
       auto kern = k2_expand_dense<M, false>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);
-      if (occ < 1) occ = 1;
+      // attribute + occupancy once per instantiation (host calls are not free)
+      static std::mutex mu;
+      static size_t smem_set = 0;
+      static int occ_cached = 0;
+      int occ;
+      {
+        std::lock_guard<std::mutex> g(mu);
+        if (smem > smem_set) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
+          smem_set = std::max<size_t>(smem, 48 << 10);
+          occ_cached = 0;
+        }
+        if (!occ_cached) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, kern, 128, smem_set);
+          if (occ_cached < 1) occ_cached = 1;
+        }
+        occ = occ_cached;
+      }
       uint64_t tiles_bound = 0;
       for (uint32_t l = 0; l < L; ++l) tiles_bound += (uint64_t)dm.A * ((parent[l]->cap + 31) / 32);
       uint64_t grid = (tiles_bound + 3) / 4;
@@ -1035,8 +1054,8 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     rc = check_launch(m, "K3c");
   }
   b->mark(6);
-  // status block: err | n_leaf[L] | total children | steps
-  const size_t stat_bytes = 4 + 4 * (size_t)L + 4 + 8;
+  // status block: err | total children | steps | n_leaf[L]
+  const size_t stat_bytes = 16 + 4 * (size_t)L;
   char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
   struct PinGuard {
     void* p;
@@ -1044,11 +1063,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   } pin_guard{hs};
   if (!rc && !hs) rc = set_err(DESPOT_ENOMEM, "pinned staging");
   if (!rc) {
-    const SumLayout lay{LA * b->S, LA};
-    if (cudaMemcpyAsync(hs, bd.err, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(hs + 4, bd.n_leaf, 4 * (size_t)L, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(hs + 4 + 4 * L, bd.child_begin + LA, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaMemcpyAsync(hs + 8 + 4 * L, bd.sums + lay.steps(), 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "status copy failed");
   }
   if (!rc && !dev_out) {
@@ -1076,8 +1091,8 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   uint64_t steps = 0;
   if (!rc) {
     memcpy(&err, hs, 4);
-    memcpy(&nchildren, hs + 4 + 4 * L, 4);
-    memcpy(&steps, hs + 8 + 4 * L, 8);
+    memcpy(&nchildren, hs + 4, 4);
+    memcpy(&steps, hs + 8, 8);
     out->num_children = nchildren;
     out->scenario_steps = steps;
     if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
@@ -1090,7 +1105,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     // children and per-scenario records: only the used part
     const uint64_t Cu = nchildren;
     uint64_t Su = 0;
-    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4);
+    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 16);
     for (uint32_t l = 0; l < L; ++l) Su += (uint64_t)dm.A * nl[l];
     struct Cp {
       void* dst;
@@ -1132,7 +1147,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     free_batch(b, true);
     return rc;
   }
-  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4);
+  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 16);
   for (uint32_t l = 0; l < L; ++l) {
     Node* nd = b->leaf_node[l];
     if (b->is_new[l]) nd->n = nl[l];

@@ -106,6 +106,11 @@ __global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
   if (threadIdx.x == 0) {
     b.child_begin[LA] = (uint32_t)tot;
     if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
+    // status block for the host: total children and the step counter
+    b.status[1] = (uint32_t)tot;
+    const uint64_t steps = (uint64_t)b.sums[SumLayout{LA * b.S, LA}.steps()];
+    b.status[2] = (uint32_t)steps;
+    b.status[3] = (uint32_t)(steps >> 32);
   }
 }
 

@@ -169,50 +169,41 @@ struct RockSample {
   }
   static constexpr uint32_t kTerminalObs = (R == 1) ? 3u : 9u;
 
-  // one step with per-robot sub-actions b[r] and random words u[r]
+  // one step with per-robot sub-actions b[r] and random words u[r].
+  // Branch-free: every lane evaluates the move, sample and sense effects and
+  // selects, so lanes of a warp taking different sub-actions in a roll-out do
+  // not diverge.  Same results as the card's case analysis.
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
                                                   uint32_t& z, float& rew) {
     float reward = 0.0f;
     uint32_t zsum = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      uint32_t zr = 0;
-      if (!s.ex[r]) {
-        const int sub = b[r];
-        int x = s.x[r], y = s.y[r];
-        if (sub == 0) {
-          y = y > 0 ? y - 1 : y;
-        } else if (sub == 1) {
-          y = y < sm.n - 1 ? y + 1 : y;
-        } else if (sub == 2) {
-          if (x < sm.n - 1) {
-            x += 1;
-          } else {
-            s.ex[r] = true;
-            reward = reward + 10.0f;  // exit east
-          }
-        } else if (sub == 3) {
-          x = x > 0 ? x - 1 : x;
-        } else if (sub == 4) {
-          const int j = sm.rock_at[y * sm.n + x];
-          if (j >= 0) {
-            if ((s.good >> j) & 1u) {
-              reward = reward + 10.0f;
-              s.good &= ~(1u << j);
-            } else {
-              reward = reward + (-10.0f);
-            }
-          }
-        } else {
-          const int j = sub - 5;
-          const int dx = x - sm.rx[j], dy = y - sm.ry[j];
-          const bool correct = u[r] <= sm.thr[dx * dx + dy * dy];
-          const bool isgood = (s.good >> j) & 1u;
-          zr = (isgood == correct) ? 1u : 2u;
-        }
-        s.x[r] = x;
-        s.y[r] = y;
-      }
+      const bool act = !s.ex[r];
+      const int sub = b[r];
+      const int x = s.x[r], y = s.y[r];
+      // moves: 0 N (y-1), 1 S (y+1), 2 E (x+1), 3 W (x-1); off-grid N/S/W stay
+      const int nx = x + (sub == 2) - (sub == 3);
+      const int ny = y + (sub == 1) - (sub == 0);
+      const bool exits = act && sub == 2 && x == sm.n - 1;  // exit east
+      const bool inside = nx >= 0 && ny >= 0 && nx < sm.n && ny < sm.n;
+      const bool moves = act && inside;
+      // SAMPLE on the current cell
+      const int jr = sm.rock_at[y * sm.n + x];
+      const bool samples = act && sub == 4 && jr >= 0;
+      const uint32_t gbit = samples ? ((s.good >> jr) & 1u) : 0u;
+      // SENSE j
+      const int js = sub >= 5 ? sub - 5 : 0;
+      const int dx = x - sm.rx[js], dy = y - sm.ry[js];
+      const bool correct = u[r] <= sm.thr[dx * dx + dy * dy];
+      const uint32_t isgood = (s.good >> js) & 1u;
+      const uint32_t zr = (act && sub >= 5) ? (((isgood != 0u) == correct) ? 1u : 2u) : 0u;
+      reward = reward + (exits ? 10.0f : 0.0f);
+      reward = reward + (samples ? (gbit ? 10.0f : -10.0f) : 0.0f);
+      s.good &= ~(gbit << (jr & 31));
+      s.x[r] = moves ? nx : x;
+      s.y[r] = moves ? ny : y;
+      s.ex[r] = s.ex[r] || exits;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
     rew = reward;
@@ -236,16 +227,14 @@ struct RockSample {
   // u(s) = sum_{good j} 10 g^{min_r |r-j|_1} + sum_{r active} 10 g^{n-1-x_r}
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
     double u = 0.0;
-    for (int j = 0; j < sm.m; ++j) {
-      if (!((s.good >> j) & 1u)) continue;
-      int dmin = 1 << 20;
+    for (int j = 0; j < sm.m; ++j) {  // uniform trip count; bad rocks add +0.0
+      int dmin = 255;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (s.ex[r]) continue;
         const int d = abs(s.x[r] - sm.rx[j]) + abs(s.y[r] - sm.ry[j]);
-        dmin = d < dmin ? d : dmin;
+        dmin = (!s.ex[r] && d < dmin) ? d : dmin;
       }
-      u += 10.0 * sm.gpow[dmin];
+      u += ((s.good >> j) & 1u) ? 10.0 * sm.gpow[dmin] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -257,28 +246,19 @@ struct RockSample {
   // default policy (card §3.2).  Memory over policy positions p (rocks sorted
   // by handling robot, then (x, y, j)): done bit = DONE, gm bit = GOOD.
   static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
-                                                int* b, int* target) {
+                                                int* b, uint32_t* tbit) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      target[r] = -1;
-      if (sm.policy_east || s.ex[r]) {
-        b[r] = 2;
-        continue;
-      }
       const uint32_t open = ~done & sm.range_mask[r];
-      if (!open) {
-        b[r] = 2;
-        continue;
-      }
-      const int p = __ffs(open) - 1;
+      const bool has = open != 0u && !sm.policy_east && !s.ex[r];
+      const int p = has ? __ffs(open) - 1 : 0;
       const int j = sm.pos_rock[p];
-      target[r] = p;
-      if (!((gm >> p) & 1u)) {
-        b[r] = 5 + j;
-      } else {
-        const int tx = sm.rx[j], ty = sm.ry[j];
-        b[r] = (s.x[r] == tx && s.y[r] == ty) ? 4 : s.x[r] < tx ? 2 : s.x[r] > tx ? 3 : s.y[r] < ty ? 1 : 0;
-      }
+      const int tx = sm.rx[j], ty = sm.ry[j];
+      const int x = s.x[r], y = s.y[r];
+      const int mv = (x == tx && y == ty) ? 4 : x < tx ? 2 : x > tx ? 3 : y < ty ? 1 : 0;
+      const bool known_good = (gm >> p) & 1u;
+      b[r] = !has ? 2 : known_good ? mv : 5 + j;
+      tbit[r] = has ? (1u << p) : 0u;
     }
   }
   template <bool TRACE>
@@ -289,8 +269,9 @@ struct RockSample {
     uint32_t t = t0;
     bool term = false;
     while (t < sm.D && !term) {
-      int b[R], tg[R];
-      policy(sm, s, done, gm, b, tg);
+      int b[R];
+      uint32_t tb[R];
+      policy(sm, s, done, gm, b, tb);
       if (TRACE) {
         int a = 0, mul = 1;
 #pragma unroll
@@ -304,17 +285,14 @@ struct RockSample {
       const uint32_t u[2] = {w.x, w.y};
       float r;
       term = step_sub(sm, s, b, u, z, r);
+      // policy memory: a GOOD reading marks the rock GOOD, a BAD one DONE; a
+      // sample marks it DONE
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        if (tg[q] < 0) continue;
-        const uint32_t bit = 1u << tg[q];
-        if (b[q] >= 5) {
-          const uint32_t zr = (q == 0) ? (z % 3u) : (z / 3u) % 3u;
-          if (zr == 1u) gm |= bit;
-          else done |= bit;
-        } else if (b[q] == 4) {
-          done |= bit;
-        }
+        const uint32_t zr = (q == 0) ? (z % 3u) : (z / 3u) % 3u;
+        const bool sensed = b[q] >= 5, sampled = b[q] == 4;
+        gm |= (sensed && zr == 1u) ? tb[q] : 0u;
+        done |= ((sensed && zr != 1u) || sampled) ? tb[q] : 0u;
       }
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
@@ -385,55 +363,53 @@ struct Nav {
   static constexpr uint32_t kTerminalObs = 0x100u;
 
   static __device__ __forceinline__ uint32_t unknown_bit(const St& s, uint32_t idx) {
-    uint32_t w = s.occ[0];
+    // masked OR over the words (a select chain here is turned into an indexed
+    // local-memory load by the compiler)
+    const uint32_t wi = idx >> 5, b = idx & 31u;
+    uint32_t acc = 0;
 #pragma unroll
-    for (int k = 1; k < NW; ++k) w = (idx >> 5) == (uint32_t)k ? s.occ[k] : w;
-    return (w >> (idx & 31u)) & 1u;
+    for (int k = 0; k < NW; ++k) acc |= (s.occ[k] >> b) & (0u - (uint32_t)(wi == (uint32_t)k));
+    return acc & 1u;
   }
   // occupancy of neighbour descriptor d (0 free, 1 occupied, 2/3 gate, 4+idx)
   static __device__ __forceinline__ uint32_t occupied(const St& s, uint32_t d) {
-    if (d >= 4u) return unknown_bit(s, d - 4u);
-    if (d >= 2u) return (d - 2u) != s.gate ? 1u : 0u;
-    return d;
+    const uint32_t ub = unknown_bit(s, d >= 4u ? d - 4u : 0u);
+    const uint32_t gb = (d - 2u) != s.gate ? 1u : 0u;
+    return d >= 4u ? ub : d >= 2u ? gb : d;
   }
+  static __device__ __forceinline__ uint32_t desc(uint2 nb, int k) {
+    return ((k < 4 ? nb.x : nb.y) >> (8 * (k & 3))) & 0xFFu;
+  }
+  // g(s, a, phi_t), branch-free so that roll-out lanes choosing different
+  // actions do not diverge
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
                                               uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
     const uint4 u0 = philox4x32_10(id, t, 0u, 0u, k0, k1);
     const uint4 u1 = philox4x32_10(id, t, 1u, 0u, k0, k1);
     const uint4 u2 = philox4x32_10(id, t, 2u, 0u, k0, k1);
     const uint32_t u[9] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x};
-    if (a == 0) {
-      r = -0.2f;  // stay
-    } else if (event(u[0], sm.t_fail)) {
-      r = -0.1f;  // failed move: stays, pays the motion cost
-    } else {
-      const uint2 nb = sm.nbr[s.y * sm.n + s.x];
-      const uint32_t d = ((a - 1) < 4 ? (nb.x >> (8 * (a - 1))) : (nb.y >> (8 * (a - 5)))) & 0xFFu;
-      if (occupied(s, d)) {
-        r = -1.0f;  // crash, position unchanged
-      } else {
-        // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
-        s.x += (a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0;
-        s.y += (a <= 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0;
-        if (s.x == sm.goal_x && s.y == sm.goal_y) {
-          r = 20.0f;  // goal, terminal
-          s.term = true;
-          z = kTerminalObs;
-          return true;
-        }
-        r = -0.1f;
-      }
-    }
+    const bool stay = a == 0;
+    const bool fail = !stay && event(u[0], sm.t_fail);
+    const int k = stay ? 0 : a - 1;  // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
+    const uint32_t occ = occupied(s, desc(sm.nbr[s.y * sm.n + s.x], k));
+    const bool moves = !stay && !fail && !occ;
+    const int nx = s.x + ((a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0);
+    const int ny = s.y + ((a == 1 || a == 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0);
+    s.x = moves ? nx : s.x;
+    s.y = moves ? ny : s.y;
+    const bool goal = moves && s.x == sm.goal_x && s.y == sm.goal_y;
+    // stay -0.2, failed move -0.1, crash -1 in place, move -0.1, goal +20
+    r = stay ? -0.2f : fail ? -0.1f : occ ? -1.0f : goal ? 20.0f : -0.1f;
+    s.term = goal;
     const uint2 nb = sm.nbr[s.y * sm.n + s.x];
     uint32_t obs = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t d = ((k < 4 ? nb.x : nb.y) >> (8 * (k & 3))) & 0xFFu;
-      const uint32_t flip = event(u[1 + k], sm.t_flip) ? 1u : 0u;
-      obs |= (occupied(s, d) ^ flip) << k;
+    for (int q = 0; q < 8; ++q) {
+      const uint32_t flip = event(u[1 + q], sm.t_flip) ? 1u : 0u;
+      obs |= (occupied(s, desc(nb, q)) ^ flip) << q;
     }
-    z = obs;
-    return false;
+    z = goal ? kTerminalObs : obs;
+    return goal;
   }
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
     const int gx = sm.gate_x[s.gate];
@@ -445,15 +421,13 @@ struct Nav {
     return 20.0 * sm.gpow[d - 1];
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
+  // pi0: first of [S, SE, SW, t even ? E : W, t even ? W : E] read FREE
   static __device__ __forceinline__ int policy(uint32_t z, uint32_t t) {
+    const uint32_t fr = ~z;
     const bool even = (t & 1u) == 0u;
-    if (!((z >> 4) & 1u)) return 5;  // S
-    if (!((z >> 3) & 1u)) return 4;  // SE
-    if (!((z >> 5) & 1u)) return 6;  // SW
     const int e1 = even ? 3 : 7, e2 = even ? 7 : 3;
-    if (!((z >> (e1 - 1)) & 1u)) return e1;
-    if (!((z >> (e2 - 1)) & 1u)) return e2;
-    return 0;
+    return ((fr >> 4) & 1u) ? 5 : ((fr >> 3) & 1u) ? 4 : ((fr >> 5) & 1u) ? 6
+         : ((fr >> (e1 - 1)) & 1u) ? e1 : ((fr >> (e2 - 1)) & 1u) ? e2 : 0;
   }
   template <bool TRACE>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,

@@ -239,7 +239,9 @@ class Model:
         arrays (numpy, or torch CUDA tensors with device_outputs=True)."""
         L = len(leaves)
         lv = self._leaves(leaves)
-        C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
+        C_cap = child_capacity
+        if C_cap is None and outputs is None:
+            C_cap = self.child_capacity_bound(leaves)
         S_cap = 0
         if record:
             S_cap = scen_capacity if scen_capacity is not None else sum(self.A * self.node_info(p)[0]

@@ -13,6 +13,12 @@ import torch
 import torch.distributed as dist
 
 
+def shard_ids(K: int, rank: int, world: int):
+    """Global scenario ids kept by `rank` (the rule despot_belief_load applies)."""
+    import numpy as np
+    return np.arange(rank, K, world, dtype=np.int64)
+
+
 class _CudaArray:
     """Zero-copy view of a device buffer owned by libdespot."""
 
