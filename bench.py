@@ -36,7 +36,6 @@ from paper_1802_06215_b200 import inputs  # noqa: E402
 # work of one step as implemented), from the ncu profile of round 1, see
 # DESIGN.md §7.  Used for the ALU roofline: achieved = I_step * steps / t_K2.
 I_STEP = {"rocksample": 260.0, "nav": 520.0, "car": 2000.0, "tiger": 120.0}
-KERNELS_PER_STEP = 6  # K1, K2pre, K2, K3a, K3b, K3c
 
 
 def load_peaks():
@@ -49,20 +48,21 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons, sampled every 20 ms from before
+    the warm-up; summary() keeps the samples of the timed window (+-100 ms)."""
 
     def __init__(self, gpu_index=0):
         self.gpu = gpu_index
         self.rows = []
         self.proc = None
 
-    def __enter__(self):
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -72,9 +72,9 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append((time.monotonic(), [x.strip() for x in line.split(",")]))
 
-    def __exit__(self, *a):
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -82,19 +82,21 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+    def summary(self, t0, t1):
+        rows = [r for (t, r) in self.rows if t0 - 0.1 <= t <= t1 + 0.1]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        num = lambda v: v.replace(".", "").isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in rows if num(r[0])]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and num(r[1])]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 4 + i and r[4 + i].lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 def workload(cfg, K=None):
@@ -257,23 +259,28 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
+    clk = ClockSampler(local).start()
+    time.sleep(0.3)  # let nvidia-smi start streaming
     for _ in range(max(args.warmup, 3)):
         one_step(dev_out, True)
     # ---- device-resident timed region ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    k2_ms, k1_ms, k3_ms, steps_count = [], [], [], []
+    k2_ms, k1_ms, k3_ms, steps_count, launches = [], [], [], [], 0
     barrier()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            o = one_step(dev_out, True)
-            ev[i][1].record(stream)
-            k1_ms.append(o["phase_ms"][0])
-            k2_ms.append(o["phase_ms"][1])
-            k3_ms.append(o["phase_ms"][2])
-            steps_count.append(o["scenario_steps"])
-        barrier()
+    tw0 = time.monotonic()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        o = one_step(dev_out, True)
+        ev[i][1].record(stream)
+        k1_ms.append(o["phase_ms"][0])
+        k2_ms.append(o["phase_ms"][1])
+        k3_ms.append(o["phase_ms"][2])
+        steps_count.append(o["scenario_steps"])
+        launches += o["launches"]
+    barrier()
+    tw1 = time.monotonic()
+    clk.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     t_local = float(np.sum(step_ms))
     if world > 1:
@@ -305,7 +312,7 @@ def main():
     d2h = 4 * (2 * L + 3 * L * A + L * A + 1) + nch * (5 * 4 + 4 * model.OW) + 4 + 4 * L + 4 + 8
     # ---- roofline of the dominant kernel (K2), live CUDA-event time ----
     peaks, peak_src = load_peaks()
-    clocks = clk.summary()
+    clocks = clk.summary(tw0, tw1)
     sm_clock = peaks.get("sm_max_mhz", 1965.0)
     num_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     peak_tinst = num_sms * 4 * 32 * sm_clock * 1e6 / 1e12  # issue slots, thread-instr/s (Tinst/s)
@@ -342,7 +349,7 @@ def main():
             "e2e": {"value": e2e_steps / (e2e_ms / 1e3), "unit": "scenario-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_n,
                     "wall_ms_per_step": 1e3 * e2e_wall / e2e_n},
-            "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "gpu_launches": int(launches),
             "clocks": clocks,
         }
         if not args.no_cpu_baseline and world == 1:

@@ -170,7 +170,7 @@ typedef struct {
   /* host-side results */
   uint64_t scenario_steps; /* out: steps g(s,a,phi) on non-terminal states (this rank) */
   uint32_t num_children;   /* out: total children C used                              */
-  uint32_t pad;
+  uint32_t launches;       /* out: kernels this call launched (begin + end)          */
   /* out with DESPOT_X_TIMING: [0] update (K1), [1] expansion + roll-outs +
    * grouping (K2), [2] child order / CSR / outputs (K3a-c), [3] whole call
    * from the first enqueued operation to the last (device time, ms)          */

@@ -180,6 +180,7 @@ struct despot_batch {
   bool sparse = false;
   uint64_t n_sums = 0, n_mins = 0;
   bool timing = false;
+  uint32_t launches = 0;  // kernels launched for this batch
   cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
   void mark(int i) {
     if (timing) cudaEventRecord(ev[i], stream);
@@ -670,6 +671,7 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
     else k2_car_warp<false><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
   }
   b->mark(4);
+  ++b->launches;
   return check_launch(m, "K2(car)");
 }
 
@@ -794,9 +796,10 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     off += align256(bytes);
     return o;
   };
-  // status block [err u32 | total children u32 | steps u64 | n_leaf[L] u32]
-  // sits right before the SUM block: one memset zeroes both, one D2H reads it
-  const size_t stat_bytes = 16 + 4 * (size_t)L;
+  // status block [err u32 | total children u32 | steps u64 | K1 ticket u32 |
+  // pad | n_leaf[L] u32] sits right before the SUM block: one memset zeroes
+  // both, one D2H reads it
+  const size_t stat_bytes = 24 + 4 * (size_t)L;
   const size_t o_leaves = take(sizeof(LeafDev) * L), o_tile = take(4 * ((size_t)L + 1)),
                o_scen = take(8 * ((size_t)L + 1));
   const size_t o_stat = off;
@@ -817,7 +820,7 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   bd.S = b->S;
   bd.status = reinterpret_cast<uint32_t*>(s + o_stat);
   bd.err = bd.status;
-  bd.n_leaf = bd.status + 4;
+  bd.n_leaf = bd.status + 6;
   bd.tile_off = reinterpret_cast<uint32_t*>(s + o_tile);
   bd.scen_off = reinterpret_cast<uint64_t*>(s + o_scen);
   bd.sums = reinterpret_cast<int64_t*>(s + o_sums);
@@ -830,15 +833,39 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     b->io.keys = reinterpret_cast<uint32_t*>(s + o_keys);
     b->io.q3 = reinterpret_cast<int64_t*>(s + o_q3);
   }
-  void* hp = pinned_pool().acquire(sizeof(LeafDev) * L);
+  // all leaves are nodes themselves (e.g. roots): their sizes are known on the
+  // host, so the update kernel and the prefix are skipped and the host ships
+  // n, tile and record prefixes with the leaf table in one copy
+  bool all_self = true;
+  for (uint32_t l = 0; l < L; ++l) all_self = all_self && leaves[l].action < 0;
+  const size_t h2d_bytes = all_self ? o_stat + stat_bytes : sizeof(LeafDev) * L;
+  void* hp = pinned_pool().acquire(h2d_bytes);
   b->pinned = hp;
   int rc = DESPOT_OK;
   if (!hp) rc = set_err(DESPOT_ENOMEM, "pinned staging");
   if (!rc) {
-    memcpy(hp, ld.data(), sizeof(LeafDev) * L);
-    if (cudaMemcpyAsync(s + o_leaves, hp, sizeof(LeafDev) * L, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
-        cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess)
+    char* h = static_cast<char*>(hp);
+    memcpy(h + o_leaves, ld.data(), sizeof(LeafDev) * L);
+    if (all_self) {
+      uint32_t* tile = reinterpret_cast<uint32_t*>(h + o_tile);
+      uint64_t* scen = reinterpret_cast<uint64_t*>(h + o_scen);
+      uint32_t* stat = reinterpret_cast<uint32_t*>(h + o_stat);
+      memset(stat, 0, stat_bytes);
+      uint64_t tacc = 0, sacc = 0;
+      for (uint32_t l = 0; l < L; ++l) {
+        const uint32_t n = parent[l]->n;
+        stat[6 + l] = n;
+        tile[l] = (uint32_t)tacc;
+        scen[l] = sacc;
+        tacc += (uint64_t)dm.A * ((n + 31) / 32);
+        sacc += (uint64_t)dm.A * n;
+      }
+      tile[L] = (uint32_t)tacc;
+      scen[L] = sacc;
+    }
+    if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
+        cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
+        cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
   }
   // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
@@ -848,22 +875,24 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     rc = dispatch_car(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       b->mark(1);
-      k1_update_sparse<M><<<L, 256, 0, st>>>(bd);
-      if (int e = check_launch(m, "K1")) return e;
+      if (!all_self) {
+        k1_update_sparse<M><<<L, 256, 0, st>>>(bd);  // + prefix in its last CTA
+        ++b->launches;
+      }
       b->mark(2);
-      k2_prefix<<<1, 1024, 0, st>>>(bd);
-      return check_launch(m, "K2pre");
+      return check_launch(m, "K1");
     });
     if (!rc && !(flags & DESPOT_X_RECORD_SCENARIO)) rc = launch_k2_sparse(m, b.get(), false);
   } else if (!rc) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       b->mark(1);
-      k1_update<M><<<L, 256, 0, st>>>(bd);
-      if (int e = check_launch(m, "K1")) return e;
+      if (!all_self) {
+        k1_update<M><<<L, 256, 0, st>>>(bd);  // + prefix in its last CTA
+        ++b->launches;
+      }
       b->mark(2);
-      k2_prefix<<<1, 1024, 0, st>>>(bd);
-      return check_launch(m, "K2pre");
+      return check_launch(m, "K1");
     });
   }
   if (!rc && !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO)) {
@@ -872,21 +901,23 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       using M = decltype(mdl);
       const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
       auto kern = k2_expand_dense<M, false>;
-      // attribute + occupancy once per instantiation (host calls are not free)
+      // attribute + occupancy once per (instantiation, smem size); host calls
+      // are not free, and the occupancy must use the launch's real smem
       static std::mutex mu;
-      static size_t smem_set = 0;
+      static size_t smem_set = 48 << 10;
+      static size_t occ_smem = ~size_t(0);
       static int occ_cached = 0;
       int occ;
       {
         std::lock_guard<std::mutex> g(mu);
         if (smem > smem_set) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 48 << 10));
-          smem_set = std::max<size_t>(smem, 48 << 10);
-          occ_cached = 0;
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          smem_set = smem;
         }
-        if (!occ_cached) {
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, kern, 128, smem_set);
+        if (occ_smem != smem) {
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, kern, 128, smem);
           if (occ_cached < 1) occ_cached = 1;
+          occ_smem = smem;
         }
         occ = occ_cached;
       }
@@ -898,6 +929,7 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       if (grid < 1) grid = 1;
       b->mark(3);
       kern<<<(unsigned)grid, 128, smem, st>>>(bd, (uint32_t)tiles_bound);
+      ++b->launches;
       b->mark(4);
       return check_launch(m, "K2");
     });
@@ -1026,6 +1058,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       b->mark(3);
       kern<<<(unsigned)(m->num_sms * 4), 128, smem, st>>>(bd, 0);
+      ++b->launches;
       b->mark(4);
       return check_launch(m, "K2(record)");
     });
@@ -1037,25 +1070,38 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     const size_t smem = 16 * (size_t)b->S;
     cudaFuncSetAttribute(k3_group_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io);
+    ++b->launches;
     rc = check_launch(m, "K3a(sparse)");
+  } else if (!rc && LA <= kSmallLA) {
+    // small batch: rank + scan + write in one CTA (one launch instead of three)
+    const size_t smem = 4 * LA + 32 * 4 * (size_t)b->S;
+    static std::once_flag once;
+    std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
+    k3_small_dense<<<1, 1024, smem, st>>>(bd);
+    ++b->launches;
+    rc = check_launch(m, "K3(small)");
   } else if (!rc) {
     k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 4, st>>>(bd);
+    ++b->launches;
     rc = check_launch(m, "K3a");
   }
-  if (!rc) {
+  if (!rc && (b->sparse || LA > kSmallLA)) {
     k3_scan<<<1, 1024, 0, st>>>(bd);
+    ++b->launches;
     rc = check_launch(m, "K3b");
   }
   if (!rc && b->sparse) {
     k3_write_sparse<<<g3, 128, 0, st>>>(bd, b->io);
+    ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
-  } else if (!rc) {
+  } else if (!rc && LA > kSmallLA) {
     k3_write_dense<<<g3, 128, 0, st>>>(bd);
+    ++b->launches;
     rc = check_launch(m, "K3c");
   }
   b->mark(6);
-  // status block: err | total children | steps | n_leaf[L]
-  const size_t stat_bytes = 16 + 4 * (size_t)L;
+  // status block: err | total children | steps | ticket | pad | n_leaf[L]
+  const size_t stat_bytes = 24 + 4 * (size_t)L;
   char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
   struct PinGuard {
     void* p;
@@ -1095,6 +1141,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     memcpy(&steps, hs + 8, 8);
     out->num_children = nchildren;
     out->scenario_steps = steps;
+    out->launches = b->launches;
     if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
     else if (err & kErrHash) rc = set_err(DESPOT_EHASH, "64-bit observation-hash collision");
     else if (err & kErrChildCap)
@@ -1105,7 +1152,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     // children and per-scenario records: only the used part
     const uint64_t Cu = nchildren;
     uint64_t Su = 0;
-    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 16);
+    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 24);
     for (uint32_t l = 0; l < L; ++l) Su += (uint64_t)dm.A * nl[l];
     struct Cp {
       void* dst;
@@ -1147,7 +1194,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     free_batch(b, true);
     return rc;
   }
-  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 16);
+  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 24);
   for (uint32_t l = 0; l < L; ++l) {
     Node* nd = b->leaf_node[l];
     if (b->is_new[l]) nd->n = nl[l];

@@ -32,14 +32,14 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* wsum, 
   return before;
 }
 
-// K2pre: tile_off[l] = sum_{l'<l} A ceil(n_l'/32), scen_off[l] = sum A n_l'
-__global__ void __launch_bounds__(1024) k2_prefix(BatchDev b) {
-  __shared__ uint64_t wsum[32];
+// per-leaf prefixes: tile_off[l] = sum_{l'<l} A ceil(n_l'/32) (K2 warp tiles),
+// scen_off[l] = sum_{l'<l} A n_l' (per-scenario records).  Whole CTA.
+__device__ __forceinline__ void leaf_prefix(const BatchDev& b, uint64_t* wsum) {
   const uint32_t per = (b.L + blockDim.x - 1) / blockDim.x;
   const uint32_t l0 = threadIdx.x * per;
   uint64_t tiles = 0, scen = 0;
   for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
-    const uint64_t n = b.n_leaf[l];
+    const uint64_t n = __ldcg(&b.n_leaf[l]);
     tiles += (uint64_t)b.A * ((n + 31) >> 5);
     scen += (uint64_t)b.A * n;
   }
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(1024) k2_prefix(BatchDev b) {
   for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
     b.tile_off[l] = (uint32_t)tb;
     b.scen_off[l] = sb;
-    const uint64_t n = b.n_leaf[l];
+    const uint64_t n = __ldcg(&b.n_leaf[l]);
     tb += (uint64_t)b.A * ((n + 31) >> 5);
     sb += (uint64_t)b.A * n;
   }
@@ -59,16 +59,32 @@ __global__ void __launch_bounds__(1024) k2_prefix(BatchDev b) {
     if (ttot >= 0xFFFFFFFFull) atomicOr(b.err, kErrChildCap);
   }
 }
+__global__ void __launch_bounds__(1024) k2_prefix(BatchDev b) {
+  __shared__ uint64_t wsum[32];
+  leaf_prefix(b, wsum);
+}
+// the last CTA of a grid to arrive runs `leaf_prefix` (threadfence reduction)
+__device__ __forceinline__ void last_cta_prefix(const BatchDev& b) {
+  __shared__ bool am_last;
+  __shared__ uint64_t wsum[32];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    am_last = atomicAdd(&b.status[4], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    leaf_prefix(b, wsum);
+  }
+}
 
-// K3a: child ordinal of each non-empty slot (first-occurrence order, R8)
-__global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
-  extern __shared__ __align__(16) unsigned char k3_smem[];
+// K3a body: child ordinal of each non-empty slot of (leaf, action) la =
+// number of non-empty slots with a smaller first id (first occurrence, R8)
+__device__ __forceinline__ void rank_one(const BatchDev& b, uint64_t la, uint32_t lane, int32_t* s_first,
+                                         uint32_t* nc_out) {
   const uint32_t S = b.S;
-  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* s_first = reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * S;
   const uint64_t LA = (uint64_t)b.L * b.A;
-  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-  if (la >= LA) return;
   const SumLayout lay{LA * S, LA};
   const uint64_t base = la * S;
   uint32_t cnt = 0;
@@ -86,22 +102,29 @@ __global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
     b.rank[base + s] = r;
   }
   cnt = warp_sum32(cnt);
-  if (lane == 0) b.nc[la] = cnt;
+  if (lane == 0) *nc_out = cnt;
+  __syncwarp();
+}
+__global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char k3_smem[];
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (la >= (uint64_t)b.L * b.A) return;
+  rank_one(b, la, lane, reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * b.S, &b.nc[la]);
 }
 
-// K3b: child_begin = exclusive scan of nc over L*A (one CTA)
-__global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
-  __shared__ uint64_t wsum[32];
+// K3b body: child_begin = exclusive scan of nc (whole CTA) + status fields
+__device__ __forceinline__ void scan_children(const BatchDev& b, const uint32_t* nc, uint64_t* wsum) {
   const uint64_t LA = (uint64_t)b.L * b.A;
   const uint64_t per = (LA + blockDim.x - 1) / blockDim.x;
   const uint64_t i0 = (uint64_t)threadIdx.x * per;
   uint64_t loc = 0;
-  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += b.nc[i];
+  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += nc[i];
   uint64_t tot;
   uint64_t run = block_excl_scan(loc, wsum, tot);
   for (uint64_t i = i0; i < i0 + per && i < LA; ++i) {
     b.child_begin[i] = (uint32_t)run;
-    run += b.nc[i];
+    run += nc[i];
   }
   if (threadIdx.x == 0) {
     b.child_begin[LA] = (uint32_t)tot;
@@ -113,20 +136,21 @@ __global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
     b.status[3] = (uint32_t)(steps >> 32);
   }
 }
+__global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
+  __shared__ uint64_t wsum[32];
+  scan_children(b, b.nc, wsum);
+}
 
-// K3c: per (leaf, action) outputs, Eq. 11/12 child bounds, one-level Eq. 4
-__global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
+// K3c body: outputs of (leaf, action) la: Eq. 11/12 child bounds, one-level
+// Eq. 4, and the leaf's child-key table
+__device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32_t lane, uint32_t cb, uint32_t nc) {
   const uint32_t S = b.S, A = b.A;
-  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t LA = (uint64_t)b.L * A;
-  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-  if (la >= LA) return;
   const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
   const LeafDev& lf = b.leaves[leaf];
   const DevModel& dm = *b.model;
   const SumLayout lay{LA * S, LA};
   const uint64_t base = la * S;
-  const uint32_t cb = b.child_begin[la];
   int64_t wt = 0, nt = 0;
   for (uint32_t s = lane; s < S; s += 32) {
     const int64_t N = b.sums[lay.N(base + s)];
@@ -150,7 +174,7 @@ __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
   wt = warp_sum64(wt);
   nt = warp_sum64(nt);
   if (lane == 0) {
-    lf.nchild[a] = b.nc[la];
+    lf.nchild[a] = nc;
     const double Wd = (double)wt;
     b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
     b.act_upper[la] = (float)((double)b.sums[lay.Q(la, 1)] / Wd);
@@ -161,6 +185,28 @@ __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
       if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
     }
   }
+}
+__global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (la >= (uint64_t)b.L * b.A) return;
+  write_one(b, la, lane, b.child_begin[la], b.nc[la]);
+}
+
+// K3 for small batches (L*A <= kSmallLA): rank, scan and write in one CTA
+constexpr uint32_t kSmallLA = 4096;
+__global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char k3s_smem[];
+  __shared__ uint64_t wsum[32];
+  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const uint32_t LA = b.L * b.A;
+  uint32_t* nc = reinterpret_cast<uint32_t*>(k3s_smem);               // [LA]
+  int32_t* s_first = reinterpret_cast<int32_t*>(nc + LA) + (size_t)wid * b.S;
+  for (uint32_t la = wid; la < LA; la += nw) rank_one(b, la, lane, s_first, &nc[la]);
+  __syncthreads();
+  scan_children(b, nc, wsum);
+  __syncthreads();
+  for (uint32_t la = wid; la < LA; la += nw) write_one(b, la, lane, b.child_begin[la], nc[la]);
 }
 
 __global__ void k_stream_words(uint32_t k0, uint32_t k1, const uint32_t* ids, uint32_t n, uint32_t t,

@@ -4,6 +4,7 @@
 // (child order) -> K3b (CSR scan) -> K3c (outputs).  See DESIGN.md §4.
 #pragma once
 #include "common.cuh"
+#include "finalize.cuh"
 
 namespace hd {
 
@@ -21,56 +22,59 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
-    return;
-  }
-  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
-  const uint32_t nchild = lf.p_nchild[lf.action];
-  const bool valid_child = lf.child < nchild;
-  const uint32_t key = valid_child ? lf.p_keys[(uint64_t)lf.action * lf.p_kcap + lf.child] : 0xFFFFFFFFu;
-  if (threadIdx.x == 0) s_base = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t steps = 0;
-  for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
-    bool keep = false;
-    typename M::St s;
-    uint32_t id = 0;
-    if (i < lf.p_n && valid_child) {
-      s = M::load(sm, lf.p_states, lf.p_cap, i);
-      id = lf.p_ids[i];
-      uint32_t z;
-      if (M::terminal(s)) {
-        z = M::kTerminalObs;
-      } else {
-        float r;
-        M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, z, r);
-        ++steps;
+  } else {
+    M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+    const uint32_t nchild = lf.p_nchild[lf.action];
+    const bool valid_child = lf.child < nchild;
+    const uint32_t key = valid_child ? lf.p_keys[(uint64_t)lf.action * lf.p_kcap + lf.child] : 0xFFFFFFFFu;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t steps = 0;
+    for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      bool keep = false;
+      typename M::St s;
+      uint32_t id = 0;
+      if (i < lf.p_n && valid_child) {
+        s = M::load(sm, lf.p_states, lf.p_cap, i);
+        id = lf.p_ids[i];
+        uint32_t z;
+        if (M::terminal(s)) {
+          z = M::kTerminalObs;
+        } else {
+          float r;
+          M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, z, r);
+          ++steps;
+        }
+        keep = z == key;
       }
-      keep = z == key;
+      const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
+      if (lane == 0) warp_cnt[wid] = __popc(ballot);
+      __syncthreads();
+      uint32_t off = s_base;
+      for (int w = 0; w < wid; ++w) off += warp_cnt[w];
+      off += __popc(ballot & ((1u << lane) - 1u));
+      if (keep) {
+        lf.ids[off] = id;
+        lf.w[off] = lf.p_w[i];
+        M::store(sm, s, lf.states, lf.cap, off);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_cnt[w];
+        s_base += tot;
+      }
+      __syncthreads();
     }
-    const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) warp_cnt[wid] = __popc(ballot);
-    __syncthreads();
-    uint32_t off = s_base;
-    for (int w = 0; w < wid; ++w) off += warp_cnt[w];
-    off += __popc(ballot & ((1u << lane) - 1u));
-    if (keep) {
-      lf.ids[off] = id;
-      lf.w[off] = lf.p_w[i];
-      M::store(sm, s, lf.states, lf.cap, off);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t tot = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += warp_cnt[w];
-      s_base += tot;
-    }
-    __syncthreads();
+    const uint32_t ws = warp_sum32(steps);
+    if (lane == 0 && ws)
+      atomicAdd((unsigned long long*)&b.sums[SumLayout{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A}.steps()],
+                (unsigned long long)ws);
+    if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;  // may be 0 on a shard
   }
-  const uint32_t ws = warp_sum32(steps);
-  if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[SumLayout{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A}.steps()], (unsigned long long)ws);
-  if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;  // may be 0 on a shard
+  last_cta_prefix(b);  // K2pre folded in: the last CTA scans the leaf sizes
 }
 
 // ---------------------------------------------------------------------------
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
 // Persistent grid-stride loop over tiles.
 // ---------------------------------------------------------------------------
 template <class M, bool RECORD>
-__global__ void __launch_bounds__(128) k2_expand_dense(BatchDev b, uint32_t total_tiles_bound) {
+__global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, uint32_t total_tiles_bound) {
   extern __shared__ __align__(16) unsigned char k2_smem[];
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(k2_smem);
   uint32_t* tile_off = reinterpret_cast<uint32_t*>(k2_smem + ((sizeof(typename M::Sm) + 15) & ~size_t(15)));

@@ -15,6 +15,7 @@
 #pragma once
 #include "common.cuh"
 #include "model_car.cuh"
+#include "finalize.cuh"
 
 namespace hd {
 
@@ -39,7 +40,8 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
-    return;
+    last_cta_prefix(b);
+    return;  // uniform per CTA
   }
   M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
   const uint32_t OW = b.model->OW;
@@ -95,6 +97,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
     atomicAdd((unsigned long long*)&b.sums[SumLayout{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A}.steps()],
               (unsigned long long)ws);
   if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;
+  last_cta_prefix(b);
 }
 
 // item t -> (leaf, action, position) through the per-scenario prefix

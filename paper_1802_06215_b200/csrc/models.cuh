@@ -25,6 +25,7 @@ __device__ __forceinline__ void copy_words(void* dst, const void* src, int bytes
 // Tiger: state bit0 side, bit1 terminal; 0 LISTEN, 1 OPEN-LEFT, 2 OPEN-RIGHT
 // ===========================================================================
 struct Tiger {
+  static constexpr int kMinBlocks = 8;  // K2 occupancy target (CTAs of 128 per SM)
   struct Sm {
     uint64_t t_listen;
     uint32_t D;
@@ -101,6 +102,7 @@ struct Tiger {
 // ===========================================================================
 template <int R>
 struct RockSample {
+  static constexpr int kMinBlocks = 8;  // 64 registers: 32 warps per SM
   struct Sm {
     int32_t n, m, base, policy_east;
     uint32_t D;
@@ -310,6 +312,7 @@ struct RockSample {
 // ===========================================================================
 template <int NW>
 struct Nav {
+  static constexpr int kMinBlocks = 5;  // larger state: more registers, fewer warps
   struct Sm {
     int32_t n, wall_y, goal_x, goal_y;
     int32_t gate_x[2];

@@ -59,7 +59,7 @@ class Expansion(C.Structure):
                 ("scen_capacity", C.c_uint64), ("scen_obs", C.c_void_p), ("scen_reward", C.c_void_p),
                 ("scen_upper", C.c_void_p), ("scen_lower", C.c_void_p), ("scen_len", C.c_void_p),
                 ("scen_hash", C.c_void_p), ("scen_states", C.c_void_p),
-                ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("pad", C.c_uint32),
+                ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("launches", C.c_uint32),
                 ("phase_ms", C.c_float * 4)]
 
 
@@ -221,6 +221,7 @@ class Model:
         out["scenario_steps"] = int(E.scenario_steps)
         out["num_children"] = Cn
         out["phase_ms"] = [float(x) for x in E.phase_ms]
+        out["launches"] = int(E.launches)
         if not device:
             for k in ("child_count", "child_first", "child_weight", "child_upper", "child_lower"):
                 out[k] = o[k][:Cn]
