@@ -195,6 +195,8 @@ def main():
     ap.add_argument("--ref-leaves", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread"],
+                    help="driving kernel: factored warp per scenario, thread per scenario, or per-batch choice")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -215,7 +217,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
     c, kind, params, st, w, seed, L = workload(args.config, args.K)
-    model = Model(kind, params, device=local, rank=rank, world=world)
+    mflags = {"auto": 0, "thread": 1, "warp": 2}[args.car_variant]
+    model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags)
     stream = torch.cuda.current_stream(dev)
     if kind == "car":
         # config 4: L concurrent roots (inputs.car_roots)

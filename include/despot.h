@@ -74,9 +74,12 @@ typedef struct {
   uint32_t flags; /* DESPOT_MF_* below                                              */
 } despot_opts;
 
-/* Driving model: use the thread-per-scenario kernel instead of the factored
- * warp-per-scenario kernel (within-step parallelism). */
-#define DESPOT_MF_UNFACTORED 1u
+/* Driving model kernel variant.  Default: chosen per batch -- the factored
+ * warp-per-scenario kernel (lanes = pedestrians and the car, within-step
+ * parallelism) when the batch has too few (leaf, action, scenario)
+ * items to fill the GPU with one thread each, else thread-per-scenario. */
+#define DESPOT_MF_UNFACTORED 1u /* always thread per scenario */
+#define DESPOT_MF_FACTORED 2u   /* always warp per scenario   */
 
 typedef struct {
   uint32_t num_actions; /* |A|                                                     */

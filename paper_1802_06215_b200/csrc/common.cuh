@@ -43,12 +43,14 @@ struct DevModel {
   // navigation
   int32_t wall_y, gate_x[2], goal_x, goal_y, nav_words;
   uint64_t t_fail, t_flip;
-  uint8_t nbr[kNavMaxN * kNavMaxN][8];  // neighbour k of cell c: 0 free, 1 occupied,
-                                        // 2 gate0, 3 gate1, 4+idx unknown cell idx
+  int32_t nav_unknown;                   // number of unknown cells
+  uint32_t nav_known_rows[kNavMaxN + 2];  // padded rows: border + known obstacles
+  uint16_t nav_unk_pos[kNavMaxN * kNavMaxN];  // unknown idx -> (x+1) | (y+1) << 8
   // car
   int32_t peds;
   uint64_t t_car_fail;
   float noise_scale;
+  float2 car_rot[1021];  // heading-noise rotation (c, s) by byte sum - 510 + 510 (card §3.4)
 };
 
 // ---------------------------------------------------------------------------

@@ -303,7 +303,7 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
         mask |= 1u << pos;
         ++pos;
       }
-      dm.range_mask[r] = mask;
+      dm.range_mask[r] = dm.policy_east ? 0u : mask;  // always-east test policy: nothing to handle
     }
     rmax = 10.0 * dm.R;
     umax = 10.0 * (dm.m + dm.R);
@@ -344,19 +344,23 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
       }
     dm.nav_words = (nu + 31) / 32;
     if (dm.nav_words > kNavMaxWords || dm.nav_words < 1) return set_err(DESPOT_EINVAL, "nav: unknown cells");
-    const int DX[8] = {0, 1, 1, 1, 0, -1, -1, -1}, DY[8] = {-1, -1, 0, 1, 1, 1, 0, -1};
+    // padded occupancy rows: row y+1, bit x+1 = cell (x, y); the border is
+    // occupied (off-grid counts as occupied), gates are left open here (the
+    // closed one is added per scenario on the device)
+    dm.nav_unknown = nu;
+    for (int r = 0; r < dm.n + 2; ++r) {
+      uint32_t row = 0;
+      for (int c = 0; c < dm.n + 2; ++c) {
+        const int x = c - 1, y = r - 1;
+        bool occ = x < 0 || y < 0 || x >= dm.n || y >= dm.n;
+        if (!occ) occ = cls[y * dm.n + x] == 1;
+        row |= (uint32_t)occ << c;
+      }
+      dm.nav_known_rows[r] = row;
+    }
     for (int y = 0; y < dm.n; ++y)
       for (int x = 0; x < dm.n; ++x)
-        for (int kk = 0; kk < 8; ++kk) {
-          const int tx = x + DX[kk], ty = y + DY[kk];
-          uint8_t d;
-          if (tx < 0 || ty < 0 || tx >= dm.n || ty >= dm.n) d = 1;
-          else {
-            const int c = cls[ty * dm.n + tx];
-            d = c == 4 ? (uint8_t)(4 + idx[ty * dm.n + tx]) : (uint8_t)c;
-          }
-          dm.nbr[y * dm.n + x][kk] = d;
-        }
+        if (idx[y * dm.n + x] >= 0) dm.nav_unk_pos[idx[y * dm.n + x]] = (uint16_t)((x + 1) | ((y + 1) << 8));
     dm.A = 9; dm.SW = 1 + (uint32_t)dm.nav_words; dm.OW = 1; dm.slots = 257; dm.terminal_slot = 256;
     dm.D = (uint32_t)pi(params, "D", 90);
     dm.tail = (double)(-0.2f) / (1.0 - dm.gamma);  // stay forever (R6)
@@ -372,6 +376,16 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     dm.D = (uint32_t)pi(params, "D", 90);
     dm.elements = 1 + (uint32_t)dm.peds;
     dm.tail = (double)(-0.1f) / (1.0 - dm.gamma);
+    // heading-noise rotations for every byte sum (card §3.4), the card's fp32
+    // sequence evaluated here once per value (host fp contraction is off)
+    for (int v = 0; v <= 1020; ++v) {
+      volatile float tau = (float)(v - 510) * dm.noise_scale;
+      volatile float tt = tau * tau;
+      volatile float den = 1.0f + tt;
+      volatile float c = (1.0f - tt) / den;
+      volatile float sn = (tau + tau) / den;
+      dm.car_rot[v] = make_float2(c, sn);
+    }
     rmax = 1000.0 * 4.5 + 100.2;
     umax = 100;
   } else {
@@ -657,7 +671,11 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   uint64_t q_bound = 0;
   for (uint32_t l = 0; l < b->L; ++l) q_bound += (uint64_t)dm.A * b->leaf_node[l]->cap;
   b->mark(3);
-  if (m->flags & DESPOT_MF_UNFACTORED) {
+  // factored (warp per item) when the items cannot fill the SMs one thread
+  // each; otherwise thread per item (fewer issue slots per scenario-step)
+  const bool unfactored = (m->flags & DESPOT_MF_UNFACTORED) ||
+                          (!(m->flags & DESPOT_MF_FACTORED) && q_bound >= (uint64_t)m->num_sms * 256);
+  if (unfactored) {
     dispatch_car(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       const uint64_t g = std::min<uint64_t>((q_bound + 127) / 128, (uint64_t)m->num_sms * 16);
@@ -1066,26 +1084,28 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   const unsigned warps_per_cta = 4;
   const unsigned g3 = (unsigned)((LA + warps_per_cta - 1) / warps_per_cta);
   b->mark(5);
+  // small dense batches (few slots): rank + scan + write in one CTA
+  const bool small_k3 = !b->sparse && LA <= kSmallLA && b->S <= 32;
   if (!rc && b->sparse) {
     const size_t smem = 16 * (size_t)b->S;
     cudaFuncSetAttribute(k3_group_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io);
     ++b->launches;
     rc = check_launch(m, "K3a(sparse)");
-  } else if (!rc && LA <= kSmallLA) {
+  } else if (!rc && small_k3) {
     // small batch: rank + scan + write in one CTA (one launch instead of three)
-    const size_t smem = 4 * LA + 32 * 4 * (size_t)b->S;
+    const size_t smem = 4 * LA + 32 * 8 * (size_t)b->S;
     static std::once_flag once;
     std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
     k3_small_dense<<<1, 1024, smem, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3(small)");
   } else if (!rc) {
-    k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 4, st>>>(bd);
+    k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 8, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3a");
   }
-  if (!rc && (b->sparse || LA > kSmallLA)) {
+  if (!rc && !small_k3) {
     k3_scan<<<1, 1024, 0, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3b");
@@ -1094,7 +1114,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     k3_write_sparse<<<g3, 128, 0, st>>>(bd, b->io);
     ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
-  } else if (!rc && LA > kSmallLA) {
+  } else if (!rc && !small_k3) {
     k3_write_dense<<<g3, 128, 0, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3c");

@@ -80,28 +80,35 @@ __device__ __forceinline__ void last_cta_prefix(const BatchDev& b) {
 }
 
 // K3a body: child ordinal of each non-empty slot of (leaf, action) la =
-// number of non-empty slots with a smaller first id (first occurrence, R8)
+// number of non-empty slots with a smaller first id (first occurrence, R8).
+// The non-empty slots are compacted first (ballot prefix), so the cost is
+// S/32 + c^2/32 per lane for c children instead of S^2/32.
 __device__ __forceinline__ void rank_one(const BatchDev& b, uint64_t la, uint32_t lane, int32_t* s_first,
                                          uint32_t* nc_out) {
   const uint32_t S = b.S;
   const uint64_t LA = (uint64_t)b.L * b.A;
   const SumLayout lay{LA * S, LA};
   const uint64_t base = la * S;
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(s_first + S);
   uint32_t cnt = 0;
-  for (uint32_t s = lane; s < S; s += 32) {
-    const bool ne = b.sums[lay.N(base + s)] != 0;
-    s_first[s] = ne ? b.mins[base + s] : INT32_MAX;
-    cnt += ne;
+  for (uint32_t s0 = 0; s0 < S; s0 += 32) {
+    const uint32_t s = s0 + lane;
+    const bool ne = s < S && b.sums[lay.N(base + s)] != 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ne);
+    if (ne) {
+      const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
+      s_first[pos] = b.mins[base + s];
+      s_slot[pos] = s;
+    }
+    cnt += __popc(bal);
   }
   __syncwarp();
-  for (uint32_t s = lane; s < S; s += 32) {
-    const int32_t f = s_first[s];
-    if (f == INT32_MAX) continue;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const int32_t f = s_first[i];
     uint32_t r = 0;
-    for (uint32_t q = 0; q < S; ++q) r += s_first[q] < f;
-    b.rank[base + s] = r;
+    for (uint32_t q = 0; q < cnt; ++q) r += s_first[q] < f;
+    b.rank[base + s_slot[i]] = r;
   }
-  cnt = warp_sum32(cnt);
   if (lane == 0) *nc_out = cnt;
   __syncwarp();
 }
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   if (la >= (uint64_t)b.L * b.A) return;
-  rank_one(b, la, lane, reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * b.S, &b.nc[la]);
+  rank_one(b, la, lane, reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * 2 * b.S, &b.nc[la]);
 }
 
 // K3b body: child_begin = exclusive scan of nc (whole CTA) + status fields
@@ -201,7 +208,7 @@ __global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t LA = b.L * b.A;
   uint32_t* nc = reinterpret_cast<uint32_t*>(k3s_smem);               // [LA]
-  int32_t* s_first = reinterpret_cast<int32_t*>(nc + LA) + (size_t)wid * b.S;
+  int32_t* s_first = reinterpret_cast<int32_t*>(nc + LA) + (size_t)wid * 2 * b.S;
   for (uint32_t la = wid; la < LA; la += nw) rank_one(b, la, lane, s_first, &nc[la]);
   __syncthreads();
   scan_children(b, nc, wsum);

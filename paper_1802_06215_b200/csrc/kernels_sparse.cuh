@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
         for (uint32_t k = 1; k < OW; ++k) keep = keep && key[k] == 0u;
       } else {
         keep = true;
-        for (uint32_t k = 0; k < OW; ++k) keep = keep && M::obs_word(s, (int)k) == key[k];
+        M::for_obs_words(sm, s, [&](uint32_t k, uint32_t zk) { keep = keep && zk == key[k]; });
       }
     }
     const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
@@ -146,11 +146,15 @@ __global__ void __launch_bounds__(128) k2_car_thread(BatchDev b, SparseItemOut i
       ++steps_acc;
     }
     uint64_t hsh = 0;
-    for (uint32_t k = 0; k < OW; ++k) {
-      const uint32_t zk = term ? (k == 0 ? kCarTerminalWord0 : 0u) : M::obs_word(s, (int)k);
+    auto put = [&](uint32_t k, uint32_t zk) {
       io.keys[t * OW + k] = zk;
       if (RECORD) b.scen_obs[t * OW + k] = zk;
       hsh ^= key_mix(zk, k);
+    };
+    if (term) {
+      for (uint32_t k = 0; k < OW; ++k) put(k, k == 0 ? kCarTerminalWord0 : 0u);
+    } else {
+      M::for_obs_words(sm, s, put);
     }
     io.hash[t] = hsh;
     if (RECORD && b.scen_states) {
@@ -239,9 +243,8 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
       // 2. pedestrians, 3. collision
       bool hit = false;
       if (is_ped) {
-        float c, sn;
-        car_noise(u, sm.noise, c, sn);
-        car_ped_move(px, py, goal, c, sn);
+        const float2 cs = sm.rot[car_noise_index(u)];
+        car_ped_move(px, py, goal, cs.x, cs.y);
         const float dx = px - xc;
         hit = dx * dx + py * py < 1.0f;
       }

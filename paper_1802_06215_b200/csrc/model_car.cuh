@@ -17,15 +17,12 @@ __device__ __forceinline__ uint32_t car_bin(float v) {  // (int16) floor(2 v), a
 __device__ __forceinline__ int car_bin_i(float v) { return (int)(int16_t)(int)floorf(2.0f * v); }
 
 // heading-noise rotation (cos, sin) from one random word: tau = (sum of the
-// four bytes - 510) * noise, c = (1 - tau^2)/(1 + tau^2), s = 2 tau/(1 + tau^2)
-__device__ __forceinline__ void car_noise(uint32_t w, float noise, float& c, float& sn) {
-  const int sint = (int)(w & 0xFFu) + (int)((w >> 8) & 0xFFu) + (int)((w >> 16) & 0xFFu) +
-                   (int)((w >> 24) & 0xFFu) - 510;
-  const float tau = (float)sint * noise;
-  const float tt = tau * tau;
-  const float den = 1.0f + tt;
-  c = (1.0f - tt) / den;
-  sn = (tau + tau) / den;
+// four bytes - 510) * noise, c = (1 - tau^2)/(1 + tau^2), s = 2 tau/(1 + tau^2).
+// The byte sum has 1021 values, so the host evaluates that exact fp32
+// sequence once per value (libdespot's own table, built at model load) and the
+// kernels look it up in shared memory.
+__device__ __forceinline__ int car_noise_index(uint32_t w) {
+  return (int)(w & 0xFFu) + (int)((w >> 8) & 0xFFu) + (int)((w >> 16) & 0xFFu) + (int)((w >> 24) & 0xFFu);
 }
 // one pedestrian toward goal g with rotation (c, sn), speed 1 m/s, dt 0.25
 __device__ __forceinline__ void car_ped_move(float& x, float& y, uint32_t g, float c, float sn) {
@@ -53,6 +50,7 @@ __device__ __forceinline__ int car_policy_from_gap(int gap) { return gap <= 8 ? 
 
 template <int MAXP>
 struct CarThreadT {
+  static constexpr int kMaxP = MAXP;
   struct Sm {
     int32_t peds;
     uint64_t t_fail;
@@ -60,6 +58,7 @@ struct CarThreadT {
     uint32_t D, OW;
     double tail;
     double gpow[kGpowN];
+    float2 rot[1021];
   };
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     if (tid == 0) {
@@ -71,6 +70,7 @@ struct CarThreadT {
       sm.tail = dm.tail;
     }
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+    copy_words(sm.rot, dm.car_rot, sizeof(sm.rot), tid, nt);
   }
   struct St {
     float xc;
@@ -116,6 +116,15 @@ struct CarThreadT {
   static __device__ __forceinline__ uint32_t goal(const St& s, int p) {
     return ((p < 16 ? s.g0 : s.g1) >> (2 * (p & 15))) & 3u;
   }
+  // f(k, word) for every observation word of a non-terminal state, with
+  // compile-time pedestrian indices (no dynamic indexing of the state arrays)
+  template <class F>
+  static __device__ __forceinline__ void for_obs_words(const Sm& sm, const St& s, F&& f) {
+    f(0u, car_bin(s.xc) | (s.level << 16));
+#pragma unroll
+    for (int p = 0; p < MAXP; ++p)
+      if (p < sm.peds) f((uint32_t)(1 + p), car_bin(s.px[p]) | (car_bin(s.py[p]) << 16));
+  }
   // observation word k (0: car, 1+i: pedestrian i) of a non-terminal state
   static __device__ __forceinline__ uint32_t obs_word(const St& s, int k) {
     if (k == 0) return car_bin(s.xc) | (s.level << 16);
@@ -154,9 +163,8 @@ struct CarThreadT {
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
       if (p < sm.peds) {
-        float c, sn;
-        car_noise(u[1 + p], sm.noise, c, sn);
-        car_ped_move(s.px[p], s.py[p], goal(s, p), c, sn);
+        const float2 cs = sm.rot[car_noise_index(u[1 + p])];
+        car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
         const float dx = s.px[p] - s.xc;
         coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
       }

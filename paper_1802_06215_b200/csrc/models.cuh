@@ -174,9 +174,10 @@ struct RockSample {
   // one step with per-robot sub-actions b[r] and random words u[r].
   // Branch-free: every lane evaluates the move, sample and sense effects and
   // selects, so lanes of a warp taking different sub-actions in a roll-out do
-  // not diverge.  Same results as the card's case analysis.
+  // not diverge.  Same results as the card's case analysis.  zr[r] returns
+  // robot r's reading (0 none, 1 GOOD, 2 BAD).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
-                                                  uint32_t& z, float& rew) {
+                                                  uint32_t& z, float& rew, uint32_t* zrs = nullptr) {
     float reward = 0.0f;
     uint32_t zsum = 0;
 #pragma unroll
@@ -188,24 +189,25 @@ struct RockSample {
       const int nx = x + (sub == 2) - (sub == 3);
       const int ny = y + (sub == 1) - (sub == 0);
       const bool exits = act && sub == 2 && x == sm.n - 1;  // exit east
-      const bool inside = nx >= 0 && ny >= 0 && nx < sm.n && ny < sm.n;
-      const bool moves = act && inside;
+      const bool moves = act && (unsigned)nx < (unsigned)sm.n && (unsigned)ny < (unsigned)sm.n;
       // SAMPLE on the current cell
       const int jr = sm.rock_at[y * sm.n + x];
-      const bool samples = act && sub == 4 && jr >= 0;
-      const uint32_t gbit = samples ? ((s.good >> jr) & 1u) : 0u;
-      // SENSE j
-      const int js = sub >= 5 ? sub - 5 : 0;
+      const uint32_t samp = (act && sub == 4 && jr >= 0) ? 1u : 0u;
+      const uint32_t gbit = samp & (s.good >> (jr & 31));
+      // SENSE j (evaluated for every lane; masked)
+      const int js = max(sub - 5, 0);
       const int dx = x - sm.rx[js], dy = y - sm.ry[js];
-      const bool correct = u[r] <= sm.thr[dx * dx + dy * dy];
+      const uint32_t incorrect = u[r] > sm.thr[dx * dx + dy * dy] ? 1u : 0u;
       const uint32_t isgood = (s.good >> js) & 1u;
-      const uint32_t zr = (act && sub >= 5) ? (((isgood != 0u) == correct) ? 1u : 2u) : 0u;
+      const uint32_t sense = (act && sub >= 5) ? 1u : 0u;
+      const uint32_t zr = sense * (1u + ((isgood ^ incorrect) ^ 1u));  // GOOD iff good == correct
       reward = reward + (exits ? 10.0f : 0.0f);
-      reward = reward + (samples ? (gbit ? 10.0f : -10.0f) : 0.0f);
+      reward = reward + (samp ? (gbit ? 10.0f : -10.0f) : 0.0f);
       s.good &= ~(gbit << (jr & 31));
       s.x[r] = moves ? nx : x;
       s.y[r] = moves ? ny : y;
       s.ex[r] = s.ex[r] || exits;
+      if (zrs) zrs[r] = zr;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
     rew = reward;
@@ -247,17 +249,23 @@ struct RockSample {
 
   // default policy (card §3.2).  Memory over policy positions p (rocks sorted
   // by handling robot, then (x, y, j)): done bit = DONE, gm bit = GOOD.
+  // default policy (card §3.2), branch-free.  rmask[r]: policy positions of
+  // robot r (the host zeroes them for the always-east test policy).  Movement toward the target
+  // (E if x<tx, W if x>tx, S if y<ty, N if y>ty, SAMPLE on it) is looked up
+  // in a packed 9-entry table indexed by the signs of (tx-x, ty-y).
   static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
-                                                int* b, uint32_t* tbit) {
+                                                const uint32_t* rmask, int* b, uint32_t* tbit) {
+    constexpr uint32_t kMovePack = 3u | 3u << 3 | 3u << 6 | 0u << 9 | 4u << 12 | 1u << 15 | 2u << 18 |
+                                   2u << 21 | 2u << 24;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t open = ~done & sm.range_mask[r];
-      const bool has = open != 0u && !sm.policy_east && !s.ex[r];
-      const int p = has ? __ffs(open) - 1 : 0;
+      const uint32_t open = ~done & rmask[r];
+      const bool has = open != 0u && !s.ex[r];
+      const int p = __ffs(open | 0x80000000u) - 1;  // 31 when nothing is open
       const int j = sm.pos_rock[p];
-      const int tx = sm.rx[j], ty = sm.ry[j];
-      const int x = s.x[r], y = s.y[r];
-      const int mv = (x == tx && y == ty) ? 4 : x < tx ? 2 : x > tx ? 3 : y < ty ? 1 : 0;
+      const int ddx = sm.rx[j] - s.x[r], ddy = sm.ry[j] - s.y[r];
+      const int code = 3 * ((ddx > 0) - (ddx < 0) + 1) + ((ddy > 0) - (ddy < 0) + 1);
+      const int mv = (int)((kMovePack >> (3 * code)) & 7u);
       const bool known_good = (gm >> p) & 1u;
       b[r] = !has ? 2 : known_good ? mv : 5 + j;
       tbit[r] = has ? (1u << p) : 0u;
@@ -273,7 +281,7 @@ struct RockSample {
     while (t < sm.D && !term) {
       int b[R];
       uint32_t tb[R];
-      policy(sm, s, done, gm, b, tb);
+      policy(sm, s, done, gm, sm.range_mask, b, tb);
       if (TRACE) {
         int a = 0, mul = 1;
 #pragma unroll
@@ -286,15 +294,14 @@ struct RockSample {
       const uint4 w = philox4x32_10(id, t + 1, 0u, 0u, k0, k1);
       const uint32_t u[2] = {w.x, w.y};
       float r;
-      term = step_sub(sm, s, b, u, z, r);
+      uint32_t zr[R];
+      term = step_sub(sm, s, b, u, z, r, zr);
       // policy memory: a GOOD reading marks the rock GOOD, a BAD one DONE; a
       // sample marks it DONE
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        const uint32_t zr = (q == 0) ? (z % 3u) : (z / 3u) % 3u;
-        const bool sensed = b[q] >= 5, sampled = b[q] == 4;
-        gm |= (sensed && zr == 1u) ? tb[q] : 0u;
-        done |= ((sensed && zr != 1u) || sampled) ? tb[q] : 0u;
+        gm |= zr[q] == 1u ? tb[q] : 0u;
+        done |= (zr[q] == 2u || b[q] == 4) ? tb[q] : 0u;
       }
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
@@ -309,18 +316,28 @@ struct RockSample {
 // Navigation (card §3.3).  word 0: cell | gate<<8 | terminal<<9;
 // words 1..NW: occupancy bits of the unknown cells (row-major order).
 // actions 0 STAY, 1..8 = N, NE, E, SE, S, SW, W, NW.
+//
+// Device representation: when a state is loaded, the thread expands it into
+// a padded occupancy grid in shared memory (row y+1, bit x+1 = cell (x, y);
+// the border, known obstacles and the closed gate are 1).  A step then reads
+// three rows and extracts the 3x3 neighbourhood with shifts.
 // ===========================================================================
+constexpr int kNavRowStride = 19;      // padded rows (n + 2 <= 18), odd stride
+constexpr int kNavMaxThreads = 256;    // largest block of a kernel using Nav
+
 template <int NW>
 struct Nav {
-  static constexpr int kMinBlocks = 5;  // larger state: more registers, fewer warps
+  static constexpr int kMinBlocks = 5;
   struct Sm {
     int32_t n, wall_y, goal_x, goal_y;
     int32_t gate_x[2];
+    int32_t n_unknown;
     uint64_t t_fail, t_flip;
     uint32_t D;
     double tail;
     double gpow[kGpowN];
-    uint2 nbr[kNavMaxN * kNavMaxN];
+    uint32_t known_rows[kNavMaxN + 2];  // padded rows of the border + known obstacles (gates open)
+    uint16_t unk_pos[kNavMaxN * kNavMaxN];  // unknown index -> (x+1) | (y+1) << 8
   };
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     if (tid == 0) {
@@ -330,13 +347,19 @@ struct Nav {
       sm.goal_y = dm.goal_y;
       sm.gate_x[0] = dm.gate_x[0];
       sm.gate_x[1] = dm.gate_x[1];
+      sm.n_unknown = dm.nav_unknown;
       sm.t_fail = dm.t_fail;
       sm.t_flip = dm.t_flip;
       sm.D = dm.D;
       sm.tail = dm.tail;
     }
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
-    copy_words(sm.nbr, dm.nbr, 8 * dm.n * dm.n, tid, nt);
+    copy_words(sm.known_rows, dm.nav_known_rows, sizeof(sm.known_rows), tid, nt);
+    copy_words(sm.unk_pos, dm.nav_unk_pos, sizeof(sm.unk_pos), tid, nt);
+  }
+  static __device__ __forceinline__ uint32_t* grid() {
+    __shared__ uint32_t rows[kNavMaxThreads * kNavRowStride];
+    return rows + threadIdx.x * kNavRowStride;
   }
   struct St {
     int32_t x, y;
@@ -344,6 +367,22 @@ struct Nav {
     bool term;
     uint32_t occ[NW];
   };
+  static __device__ __forceinline__ void build_grid(const Sm& sm, const St& s) {
+    uint32_t* g = grid();
+    for (int r = 0; r < sm.n + 2; ++r) g[r] = sm.known_rows[r];
+    const int closed = sm.gate_x[1 - s.gate];
+    g[sm.wall_y + 1] |= 1u << (closed + 1);
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      uint32_t bits = s.occ[k];
+      while (bits) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        const uint32_t pos = sm.unk_pos[32 * k + bit];
+        g[pos >> 8] |= 1u << (pos & 0xFFu);
+      }
+    }
+  }
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
     St s;
     const uint32_t w0 = st[i];
@@ -354,6 +393,7 @@ struct Nav {
     s.term = (w0 >> 9) & 1u;
 #pragma unroll
     for (int k = 0; k < NW; ++k) s.occ[k] = st[(1 + k) * cap + i];
+    build_grid(sm, s);
     return s;
   }
   static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
@@ -365,23 +405,13 @@ struct Nav {
   static __device__ __forceinline__ bool terminal(const St& s) { return s.term; }
   static constexpr uint32_t kTerminalObs = 0x100u;
 
-  static __device__ __forceinline__ uint32_t unknown_bit(const St& s, uint32_t idx) {
-    // masked OR over the words (a select chain here is turned into an indexed
-    // local-memory load by the compiler)
-    const uint32_t wi = idx >> 5, b = idx & 31u;
-    uint32_t acc = 0;
-#pragma unroll
-    for (int k = 0; k < NW; ++k) acc |= (s.occ[k] >> b) & (0u - (uint32_t)(wi == (uint32_t)k));
-    return acc & 1u;
-  }
-  // occupancy of neighbour descriptor d (0 free, 1 occupied, 2/3 gate, 4+idx)
-  static __device__ __forceinline__ uint32_t occupied(const St& s, uint32_t d) {
-    const uint32_t ub = unknown_bit(s, d >= 4u ? d - 4u : 0u);
-    const uint32_t gb = (d - 2u) != s.gate ? 1u : 0u;
-    return d >= 4u ? ub : d >= 2u ? gb : d;
-  }
-  static __device__ __forceinline__ uint32_t desc(uint2 nb, int k) {
-    return ((k < 4 ? nb.x : nb.y) >> (8 * (k & 3))) & 0xFFu;
+  // occupancy of the 8 neighbours of (x, y), bit k = direction k+1
+  // (N, NE, E, SE, S, SW, W, NW); off-grid counts as occupied
+  static __device__ __forceinline__ uint32_t neighbours(int x, int y) {
+    const uint32_t* g = grid();
+    const uint32_t up = g[y] >> x, mid = g[y + 1] >> x, dn = g[y + 2] >> x;
+    return ((up >> 1) & 1u) | ((up >> 1) & 2u) | ((mid & 4u)) | ((dn & 4u) << 1) | ((dn & 2u) << 3) |
+           ((dn & 1u) << 5) | ((mid & 1u) << 6) | ((up & 1u) << 7);
   }
   // g(s, a, phi_t), branch-free so that roll-out lanes choosing different
   // actions do not diverge
@@ -394,7 +424,7 @@ struct Nav {
     const bool stay = a == 0;
     const bool fail = !stay && event(u[0], sm.t_fail);
     const int k = stay ? 0 : a - 1;  // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
-    const uint32_t occ = occupied(s, desc(sm.nbr[s.y * sm.n + s.x], k));
+    const uint32_t occ = (neighbours(s.x, s.y) >> k) & 1u;
     const bool moves = !stay && !fail && !occ;
     const int nx = s.x + ((a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0);
     const int ny = s.y + ((a == 1 || a == 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0);
@@ -404,13 +434,10 @@ struct Nav {
     // stay -0.2, failed move -0.1, crash -1 in place, move -0.1, goal +20
     r = stay ? -0.2f : fail ? -0.1f : occ ? -1.0f : goal ? 20.0f : -0.1f;
     s.term = goal;
-    const uint2 nb = sm.nbr[s.y * sm.n + s.x];
-    uint32_t obs = 0;
+    uint32_t flips = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t flip = event(u[1 + q], sm.t_flip) ? 1u : 0u;
-      obs |= (occupied(s, desc(nb, q)) ^ flip) << q;
-    }
+    for (int q = 0; q < 8; ++q) flips |= (event(u[1 + q], sm.t_flip) ? 1u : 0u) << q;
+    const uint32_t obs = neighbours(s.x, s.y) ^ flips;
     z = goal ? kTerminalObs : obs;
     return goal;
   }

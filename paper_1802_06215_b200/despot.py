@@ -18,6 +18,7 @@ DESPOT_X_DEVICE_OUTPUTS = 1
 DESPOT_X_RECORD_SCENARIO = 2
 DESPOT_X_TIMING = 4
 DESPOT_MF_UNFACTORED = 1
+DESPOT_MF_FACTORED = 2
 
 STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5: "ECUDA",
           -6: "ENCCL", -7: "ESHUTDOWN", -8: "EHASH"}

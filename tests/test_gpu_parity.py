@@ -274,7 +274,8 @@ def test_fake_ranks_equal_single_gpu():
 # ----------------------------------------------------------------------------
 def _car_models(peds=20, D=90):
     params = inputs.car_params(peds, D=D)
-    return (Model("car", params), Model("car", params, flags=1), oracle.Model("car", params))
+    # forced factored (warp per scenario) and unfactored (thread per scenario)
+    return (Model("car", params, flags=2), Model("car", params, flags=1), oracle.Model("car", params))
 
 
 def test_config4_car_64_roots_factored_and_unfactored():
