@@ -217,6 +217,80 @@ int despot_rollout_bounds(despot_model* model, despot_node node, float* upper_me
                           float* lower_mean, float* per_scen_upper, float* per_scen_lower,
                           void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Host tree driver (the north star's "thin host driver
+ * that coalesces many threads' leaves into one launch")                     */
+/* ------------------------------------------------------------------------ */
+/* Expansion backend: expands `L` leaves into host arrays of `out` (same
+ * contract as despot_expand_batch with host outputs).  libdespot's GPU
+ * backend is used by despot_plan; tests plug in the CPU oracle.  Called from
+ * one thread (the batcher) at a time.  Returns a despot_status. */
+typedef int (*despot_expand_fn)(void* ctx, const despot_leaf* leaves, uint32_t L, despot_expansion* out);
+typedef int (*despot_release_fn)(void* ctx, despot_node node);
+
+typedef struct {
+  uint32_t num_actions, obs_words, obs_slots, max_depth; /* as despot_model_info       */
+  double gamma;
+  despot_node root;          /* backend handle of the root belief (depth root_depth) */
+  uint32_t root_depth, root_scenarios;
+  double root_weight;        /* W_b0                                                  */
+  double root_upper, root_lower; /* initial bounds of the root (Eqs. 11-12)          */
+  despot_expand_fn expand;
+  despot_release_fn release; /* may be NULL                                           */
+  void* ctx;
+} despot_search_problem;
+
+typedef struct {
+  uint32_t workers;       /* CPU search threads                          */
+  uint32_t max_batch;     /* leaves per expansion launch                             */
+  uint32_t max_inflight;  /* trials a worker may have waiting for expansion          */
+  uint32_t batch_wait_us; /* the batcher waits at most this long to fill a batch     */
+  uint64_t max_trials;    /* 0 = no limit                                            */
+  double time_budget_s;   /* anytime budget; <= 0 = no limit              */
+  double xi;              /* WEU target factor (Eq. 6)                               */
+  double c_a;             /* PO-UCT exploration scale (Eq. 7)                        */
+  double c_o;             /* virtual-loss scale (Eq. 8)                              */
+  double target_gap;      /* stop when u(b0) - l(b0) <= target_gap                   */
+} despot_search_config;
+
+typedef struct {
+  int32_t action;         /* argmax_a l(b0, a), ties by the lowest index     */
+  float root_upper, root_lower;
+  uint64_t nodes;         /* belief nodes in the tree                                */
+  uint64_t expanded;      /* nodes expanded (leaves initialised)                     */
+  uint64_t trials;
+  uint64_t batches;       /* expansion launches                                      */
+  uint32_t max_depth;
+  uint32_t pad;
+  double seconds;
+  uint64_t scenario_steps;
+} despot_search_result;
+
+/* One tree node for tests and dumps (pre-order: a node follows its parent). */
+typedef struct {
+  int32_t parent;         /* index in the dump, -1 for the root                      */
+  int32_t action;         /* edge from the parent                                    */
+  uint32_t child, depth, n_scen, visits, branch_visits; /* N(b), sum_a N(b, a)      */
+  int32_t active;         /* virtual-loss markers still held (0 after a search)      */
+  int32_t expanded;
+  float weight, upper, lower, upper0, lower0;
+} despot_search_node;
+
+/* Anytime parallel DESPOT search from `problem->root`: workers descend with
+ * the scenario-based PO-UCT action rule (Eq. 7) and the WEU observation rule
+ * with virtual loss (Eqs. 6, 8), hand their leaves to a batcher that expands
+ * up to max_batch leaves per backend call, and back up Eq. 4 along each path
+ * (lower bounds floored at, upper bounds capped by the initial values).
+ * dump (optional, dump_capacity nodes) receives the final tree.  Every node
+ * the backend created is released before returning. */
+int despot_search(const despot_search_problem* problem, const despot_search_config* config,
+                  despot_search_result* result, despot_search_node* dump, uint32_t dump_capacity);
+
+/* despot_search on libdespot's GPU backend: root bounds by
+ * despot_rollout_bounds, expansions by despot_expand_batch on `stream`. */
+int despot_plan(despot_model* model, despot_node root, const despot_search_config* config,
+                despot_search_result* result, void* stream);
+
 /* Raw scenario stream words, for tests of the generator: out[i] = word k of
  * scenario ids[i] at depth t (tag 0), R13.  Host arrays, synchronous. */
 int despot_stream_words(despot_model* model, uint64_t stream_seed, const uint32_t* ids,

@@ -42,6 +42,10 @@ static int set_err(int code, const char* fmt, ...) {
   return code;
 }
 extern "C" const char* despot_last_error(void) { return g_err.c_str(); }
+extern "C" int despot__set_error(int code, const char* msg) {  // internal (search.cpp)
+  g_err = msg ? msg : "";
+  return code;
+}
 extern "C" int despot_abi_version(void) { return DESPOT_ABI_VERSION; }
 
 #define CU(call)                                                                              \

@@ -1,0 +1,492 @@
+// search.cpp -- host tree driver of libdespot: an anytime parallel DESPOT
+// search whose CPU workers coalesce their leaves into batched expansions.
+//
+//   workers  descend from the root: action by the scenario-based
+//                        PO-UCT rule (Eq. 7), observation branch by
+//                        the WEU rule with virtual loss (Eqs. 6, 8,
+//                        P:355-358); a trial ends at a leaf or when
+//                        every WEU is <= 0.
+//   batcher              collects the leaves of all workers' trials, expands
+//                        up to max_batch of them in ONE backend call
+//                        (node-level parallelism), creates the new
+//                        children (Eq. 10, done on the CPU as in P:435) and
+//                        backs up Eq. 4 along each trial's path.
+//
+// Readings: weights replace counts (R1); N(b,a) = 0 prefers the
+// branch, N(b) = 0 gives no bonus, natural log; the virtual
+// loss grows with the number of threads inside the branch; bounds are
+// floored / capped by their initial values during backup; a
+// node at depth D has the exact value l0 (its roll-out is the tail), so its
+// gap is 0; the root action is argmax_a l(b0, a).
+// Host-only C++: this file uses libdespot only through include/despot.h.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/despot.h"
+
+// sets the calling thread's despot_last_error message (despot.cu)
+extern "C" int despot__set_error(int code, const char* msg);
+
+namespace {
+
+struct TNode;
+struct TBranch {
+  double reward = 0.0, upper = 0.0, lower = 0.0;  // r(b,a), u(b,a), l(b,a)
+  uint32_t visits = 0;                            // N(b,a)
+  std::vector<TNode*> children;
+};
+
+struct TNode {
+  TNode* parent = nullptr;
+  int32_t action_in = -1;
+  uint32_t child_in = 0;
+  uint32_t depth = 0, n_scen = 0;
+  double weight = 0.0;
+  double u0 = 0.0, l0 = 0.0;
+  std::atomic<double> upper{0.0}, lower{0.0};
+  std::atomic<int> active{0};  // threads inside this branch (virtual loss)
+  uint32_t visits = 0;         // N(b), under mu
+  despot_node handle = 0;      // backend arena once expanded
+  enum State { kLeaf, kPending, kExpanded } state = kLeaf;  // under mu
+  std::vector<TBranch> branches;                            // [A] once expanded, under mu
+  std::mutex mu;
+};
+
+struct Pending {
+  TNode* leaf;
+  std::vector<TNode*> path;
+  std::atomic<uint32_t>* inflight;
+};
+
+struct Search {
+  const despot_search_problem& P;
+  const despot_search_config& C;
+  std::deque<TNode> nodes;  // stable addresses; appended by the batcher only
+  std::mutex nodes_mu;
+  TNode* root = nullptr;
+  std::atomic<bool> stop{false};
+  std::atomic<uint64_t> trials{0}, batches{0}, expanded{0}, steps{0};
+  std::atomic<uint32_t> max_depth{0};
+  std::mutex qmu;
+  std::condition_variable qcv;  // batcher wake-up
+  std::condition_variable dcv;  // a worker's trial finished expanding
+  std::deque<Pending> queue;
+  bool workers_done = false;
+  std::atomic<int> error{0};
+  std::string error_msg;
+
+  Search(const despot_search_problem& p, const despot_search_config& c) : P(p), C(c) {}
+
+  TNode* new_node() {
+    std::lock_guard<std::mutex> g(nodes_mu);
+    nodes.emplace_back();
+    return &nodes.back();
+  }
+  double root_gap() const { return root->upper.load() - root->lower.load(); }
+
+  // Eq. 4 one level: recompute node b's branch values and bounds from its
+  // children (clamped by the initial bounds)
+  void backup_node(TNode* b) {
+    std::lock_guard<std::mutex> g(b->mu);
+    if (b->state != TNode::kExpanded) return;
+    double bu = -std::numeric_limits<double>::infinity(), bl = bu;
+    for (TBranch& br : b->branches) {
+      double su = 0.0, sl = 0.0;
+      for (TNode* c : br.children) {
+        const double f = c->weight / b->weight;
+        su += f * c->upper.load(std::memory_order_relaxed);
+        sl += f * c->lower.load(std::memory_order_relaxed);
+      }
+      if (!br.children.empty()) {
+        br.upper = br.reward + P.gamma * su;
+        br.lower = br.reward + P.gamma * sl;
+      }
+      bu = std::max(bu, br.upper);
+      bl = std::max(bl, br.lower);
+    }
+    b->upper.store(std::min(b->u0, bu));
+    b->lower.store(std::max(b->l0, bl));
+  }
+  void backup(const std::vector<TNode*>& path) {
+    for (auto it = path.rbegin(); it != path.rend(); ++it) backup_node(*it);
+  }
+  static void release_markers(const std::vector<TNode*>& path) {
+    for (size_t i = 1; i < path.size(); ++i) path[i]->active.fetch_sub(1);
+  }
+
+  // ---------------------------------------------------------------- batcher
+  int expand(std::vector<Pending>& batch) {
+    const uint32_t L = (uint32_t)batch.size(), A = P.num_actions, OW = P.obs_words;
+    std::vector<despot_leaf> leaves(L);
+    uint64_t cap = 0;
+    for (uint32_t i = 0; i < L; ++i) {
+      TNode* b = batch[i].leaf;
+      if (b == root) leaves[i] = despot_leaf{P.root, -1, 0, P.root_depth, 0};
+      else leaves[i] = despot_leaf{b->parent->handle, b->action_in, b->child_in, b->depth, 0};
+      const uint32_t n = b->n_scen ? b->n_scen : 1;
+      cap += (uint64_t)A * (P.obs_slots ? std::min(n, P.obs_slots) : n);
+    }
+    if (cap > 0xFFFFFFFFull) return DESPOT_ECAPACITY;
+    std::vector<despot_node> hnode(L);
+    std::vector<uint32_t> n_scen(L), child_begin((size_t)L * A + 1), child_count(cap), child_first(cap),
+        child_obs(cap * OW);
+    std::vector<float> weight(L), ar((size_t)L * A), au((size_t)L * A), al((size_t)L * A), cw(cap), cu(cap),
+        cl(cap);
+    despot_expansion out;
+    memset(&out, 0, sizeof out);
+    out.node = hnode.data();
+    out.n_scen = n_scen.data();
+    out.weight = weight.data();
+    out.act_reward = ar.data();
+    out.act_upper = au.data();
+    out.act_lower = al.data();
+    out.child_begin = child_begin.data();
+    out.child_capacity = (uint32_t)cap;
+    out.child_count = child_count.data();
+    out.child_first = child_first.data();
+    out.child_weight = cw.data();
+    out.child_upper = cu.data();
+    out.child_lower = cl.data();
+    out.child_obs = child_obs.data();
+    const int rc = P.expand(P.ctx, leaves.data(), L, &out);
+    if (rc != DESPOT_OK) return rc;
+    batches.fetch_add(1);
+    steps.fetch_add(out.scenario_steps);
+    for (uint32_t i = 0; i < L; ++i) {
+      TNode* b = batch[i].leaf;
+      std::vector<TBranch> br(A);
+      for (uint32_t a = 0; a < A; ++a) {
+        const size_t la = (size_t)i * A + a;
+        br[a].reward = ar[la];
+        br[a].upper = au[la];
+        br[a].lower = al[la];
+        for (uint32_t c = child_begin[la]; c < child_begin[la + 1]; ++c) {
+          TNode* ch = new_node();
+          ch->parent = b;
+          ch->action_in = (int32_t)a;
+          ch->child_in = c - child_begin[la];
+          ch->depth = b->depth + 1;
+          ch->n_scen = child_count[c];
+          ch->weight = cw[c];
+          ch->u0 = cu[c];
+          ch->l0 = cl[c];
+          // at depth D the value is exactly the tail-based l0: gap 0
+          if (ch->depth >= P.max_depth) ch->u0 = ch->l0;
+          ch->upper.store(ch->u0);
+          ch->lower.store(ch->l0);
+          br[a].children.push_back(ch);
+        }
+      }
+      {
+        std::lock_guard<std::mutex> g(b->mu);
+        b->handle = hnode[i];
+        if (b->n_scen == 0) b->n_scen = n_scen[i];
+        if (b->weight == 0.0) b->weight = weight[i];
+        b->branches = std::move(br);
+        b->state = TNode::kExpanded;
+      }
+      expanded.fetch_add(1);
+      uint32_t d = b->depth + 1, m = max_depth.load();
+      while (d > m && !max_depth.compare_exchange_weak(m, d)) {
+      }
+    }
+    for (Pending& p : batch) {
+      backup(p.path);
+      release_markers(p.path);
+      if (p.inflight) p.inflight->fetch_sub(1);
+    }
+    return DESPOT_OK;
+  }
+
+  void batcher() {
+    const uint32_t max_batch = std::max<uint32_t>(1, C.max_batch);
+    for (;;) {
+      std::vector<Pending> batch;
+      {
+        std::unique_lock<std::mutex> lk(qmu);
+        qcv.wait(lk, [&] { return !queue.empty() || workers_done; });
+        if (queue.empty() && workers_done) break;
+        const auto deadline = std::chrono::steady_clock::now() + std::chrono::microseconds(C.batch_wait_us);
+        while (queue.size() < max_batch && !workers_done && !stop.load()) {
+          if (qcv.wait_until(lk, deadline) == std::cv_status::timeout) break;
+        }
+        while (!queue.empty() && batch.size() < max_batch) {
+          batch.push_back(std::move(queue.front()));
+          queue.pop_front();
+        }
+      }
+      const int rc = error.load() ? error.load() : expand(batch);
+      if (rc != DESPOT_OK) {
+        int expected = 0;
+        if (error.compare_exchange_strong(expected, rc)) error_msg = despot_last_error();
+        stop.store(true);
+        for (Pending& p : batch) {  // give the leaves back, release the markers
+          {
+            std::lock_guard<std::mutex> g(p.leaf->mu);
+            p.leaf->state = TNode::kLeaf;
+          }
+          release_markers(p.path);
+          if (p.inflight) p.inflight->fetch_sub(1);
+        }
+      }
+      {
+        std::lock_guard<std::mutex> g(qmu);  // pairs with the workers' dcv wait
+      }
+      dcv.notify_all();
+    }
+  }
+
+  // ---------------------------------------------------------------- workers
+  // Eq. 7: u(b,a) + c_a sqrt(log(|Phi_b| N(b)) / (|Phi_b| N(b,a)))
+  uint32_t choose_action(TNode* b) const {
+    const double phi = (double)std::max<uint32_t>(1, b->n_scen);
+    const double nb = phi * (double)b->visits;
+    uint32_t best = 0;
+    double bv = -std::numeric_limits<double>::infinity();
+    for (uint32_t a = 0; a < b->branches.size(); ++a) {
+      const TBranch& br = b->branches[a];
+      double v;
+      if (C.c_a > 0.0 && br.visits == 0) v = std::numeric_limits<double>::infinity();
+      else if (C.c_a > 0.0 && b->visits > 0)
+        v = br.upper + C.c_a * std::sqrt(std::log(nb) / (phi * (double)br.visits));
+      else v = br.upper;
+      if (v > bv) {
+        bv = v;
+        best = a;
+      }
+    }
+    return best;
+  }
+
+  void worker() {
+    std::atomic<uint32_t> inflight{0};
+    const uint32_t max_inflight = std::max<uint32_t>(1, C.max_inflight);
+    while (!stop.load()) {
+      if (inflight.load() >= max_inflight) {
+        std::unique_lock<std::mutex> lk(qmu);
+        dcv.wait(lk, [&] { return inflight.load() < max_inflight || stop.load(); });
+        continue;
+      }
+      if (C.max_trials && trials.fetch_add(1) >= C.max_trials) {
+        stop.store(true);
+        break;
+      }
+      if (!C.max_trials) trials.fetch_add(1);
+      std::vector<TNode*> path{root};
+      TNode* b = root;
+      TNode* leaf = nullptr;
+      for (;;) {
+        std::unique_lock<std::mutex> lk(b->mu);
+        if (b->state == TNode::kLeaf) {
+          if (b->depth < P.max_depth) {
+            b->state = TNode::kPending;  // claimed: this trial expands it
+            leaf = b;
+          }
+          break;
+        }
+        if (b->state == TNode::kPending) break;  // another trial is expanding it
+        const uint32_t a = choose_action(b);
+        b->visits += 1;  // counts bumped on entry
+        TBranch& br = b->branches[a];
+        br.visits += 1;
+        const double gap0 = root_gap();
+        TNode* next = nullptr;
+        double best = 0.0;  // the trial ends unless some WEU > 0
+        for (TNode* c : br.children) {
+          const double gap = c->upper.load(std::memory_order_relaxed) - c->lower.load(std::memory_order_relaxed);
+          const double weu = gap - (c->weight / root->weight) * C.xi * gap0;       // Eq. 6
+          const double aug = weu - (double)c->active.load() * C.c_o * gap0;        // Eq. 8
+          if (aug > best) {
+            best = aug;
+            next = c;
+          }
+        }
+        lk.unlock();
+        if (!next) break;
+        next->active.fetch_add(1);
+        path.push_back(next);
+        b = next;
+      }
+      if (leaf) {
+        inflight.fetch_add(1);
+        {
+          std::lock_guard<std::mutex> g(qmu);
+          queue.push_back(Pending{leaf, std::move(path), &inflight});
+        }
+        qcv.notify_one();
+      } else {
+        backup(path);
+        release_markers(path);
+      }
+    }
+    // wait for this worker's trials still in the batcher (inflight lives here)
+    std::unique_lock<std::mutex> lk(qmu);
+    qcv.notify_all();
+    dcv.wait(lk, [&] { return inflight.load() == 0; });
+  }
+
+  void dump_tree(despot_search_node* out, uint32_t cap, uint32_t& n) const {
+    std::vector<std::pair<const TNode*, int32_t>> stack{{root, -1}};
+    while (!stack.empty() && n < cap) {
+      auto [b, parent] = stack.back();
+      stack.pop_back();
+      despot_search_node& d = out[n];
+      d.parent = parent;
+      d.action = b->action_in;
+      d.child = b->child_in;
+      d.depth = b->depth;
+      d.n_scen = b->n_scen;
+      d.visits = b->visits;
+      uint32_t bv = 0;
+      for (const TBranch& br : b->branches) bv += br.visits;
+      d.branch_visits = bv;
+      d.active = b->active.load();
+      d.expanded = b->state == TNode::kExpanded;
+      d.weight = (float)b->weight;
+      d.upper = (float)b->upper.load();
+      d.lower = (float)b->lower.load();
+      d.upper0 = (float)b->u0;
+      d.lower0 = (float)b->l0;
+      const int32_t me = (int32_t)n++;
+      for (auto it = b->branches.rbegin(); it != b->branches.rend(); ++it)
+        for (auto c = it->children.rbegin(); c != it->children.rend(); ++c) stack.push_back({*c, me});
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" int despot_search(const despot_search_problem* P, const despot_search_config* C,
+                             despot_search_result* R, despot_search_node* dump, uint32_t dump_capacity) {
+  if (!P || !C || !R || !P->expand || P->num_actions == 0)
+    return despot__set_error(DESPOT_EINVAL, "despot_search: null argument or no actions");
+  if (P->root_depth >= P->max_depth) return despot__set_error(DESPOT_EINVAL, "despot_search: root depth >= D");
+  if (P->root_scenarios == 0) return despot__set_error(DESPOT_EINVAL, "despot_search: root_scenarios == 0");
+  const auto t0 = std::chrono::steady_clock::now();
+  Search S(*P, *C);
+  S.root = S.new_node();
+  TNode* root = S.root;
+  root->depth = P->root_depth;
+  root->n_scen = P->root_scenarios;
+  root->weight = P->root_weight;
+  root->u0 = P->root_upper;
+  root->l0 = P->root_lower;
+  root->upper.store(P->root_upper);
+  root->lower.store(P->root_lower);
+  root->handle = P->root;
+  // the root is expanded before any trial (and gives |Phi_b0| and W_b0)
+  {
+    std::vector<Pending> first{Pending{root, {root}, nullptr}};
+    root->state = TNode::kPending;
+    const int rc = S.expand(first);
+    if (rc != DESPOT_OK) return rc;
+  }
+  const uint32_t W = std::max<uint32_t>(1, C->workers);
+  std::thread batcher([&] { S.batcher(); });
+  std::vector<std::thread> workers;
+  for (uint32_t i = 0; i < W; ++i) workers.emplace_back([&] { S.worker(); });
+  // anytime loop: time budget, trial budget, target gap
+  for (;;) {
+    if (S.stop.load()) break;
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (C->time_budget_s > 0.0 && el >= C->time_budget_s) break;
+    if (S.root_gap() <= C->target_gap) break;
+    if (C->max_trials == 0 && C->time_budget_s <= 0.0) break;  // no budget at all
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  S.stop.store(true);
+  {
+    std::lock_guard<std::mutex> g(S.qmu);
+  }
+  S.dcv.notify_all();
+  for (auto& t : workers) t.join();
+  {
+    std::lock_guard<std::mutex> g(S.qmu);
+    S.workers_done = true;
+  }
+  S.qcv.notify_all();
+  batcher.join();
+  // result
+  R->action = 0;
+  double best = -std::numeric_limits<double>::infinity();
+  for (uint32_t a = 0; a < root->branches.size(); ++a)
+    if (root->branches[a].lower > best) {
+      best = root->branches[a].lower;
+      R->action = (int32_t)a;
+    }
+  R->root_upper = (float)root->upper.load();
+  R->root_lower = (float)root->lower.load();
+  R->nodes = S.nodes.size();
+  R->expanded = S.expanded.load();
+  R->trials = std::min<uint64_t>(S.trials.load(), C->max_trials ? C->max_trials : S.trials.load());
+  R->batches = S.batches.load();
+  R->max_depth = S.max_depth.load();
+  R->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  R->scenario_steps = S.steps.load();
+  if (dump && dump_capacity) {
+    uint32_t n = 0;
+    S.dump_tree(dump, dump_capacity, n);
+  }
+  // release the backend arenas this search created (not the caller's root)
+  if (P->release)
+    for (TNode& b : S.nodes)
+      if (&b != root && b.state == TNode::kExpanded && b.handle) P->release(P->ctx, b.handle);
+  if (S.error.load()) return despot__set_error(S.error.load(), S.error_msg.c_str());
+  return DESPOT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// despot_plan: the search on libdespot's GPU backend
+// ---------------------------------------------------------------------------
+namespace {
+struct GpuCtx {
+  despot_model* model;
+  void* stream;
+};
+int gpu_expand(void* ctx, const despot_leaf* leaves, uint32_t L, despot_expansion* out) {
+  GpuCtx* g = static_cast<GpuCtx*>(ctx);
+  out->flags = 0;  // host outputs
+  return despot_expand_batch(g->model, leaves, L, out, g->stream);
+}
+int gpu_release(void* ctx, despot_node n) { return despot_node_release(static_cast<GpuCtx*>(ctx)->model, n); }
+}  // namespace
+
+extern "C" int despot_plan(despot_model* model, despot_node root, const despot_search_config* config,
+                           despot_search_result* result, void* stream) {
+  if (!model || !config || !result) return DESPOT_EINVAL;
+  despot_model_info info;
+  int rc = despot_model_info_get(model, &info);
+  if (rc) return rc;
+  uint32_t n = 0, depth = 0;
+  if ((rc = despot_node_info(model, root, &n, &depth))) return rc;
+  float u0 = 0.0f, l0 = 0.0f;
+  if ((rc = despot_rollout_bounds(model, root, &u0, &l0, nullptr, nullptr, stream))) return rc;
+  GpuCtx ctx{model, stream};
+  despot_search_problem P;
+  memset(&P, 0, sizeof P);
+  P.num_actions = info.num_actions;
+  P.obs_words = info.obs_words;
+  P.obs_slots = info.obs_slots;
+  P.max_depth = info.max_depth;
+  P.gamma = info.gamma;
+  P.root = root;
+  P.root_depth = depth;
+  P.root_scenarios = n;  // this device's scenarios (the search is single-GPU)
+  P.root_weight = 0.0;
+  P.root_upper = u0;
+  P.root_lower = l0;
+  P.expand = gpu_expand;
+  P.release = gpu_release;
+  P.ctx = &ctx;
+  return despot_search(&P, config, result, nullptr, 0);
+}

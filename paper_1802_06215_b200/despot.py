@@ -27,7 +27,8 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5
 EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "despot_model_info_get",
            "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
            "despot_node_release", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
-           "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words"]
+           "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
+           "despot_search", "despot_plan"]
 
 
 class DespotError(RuntimeError):
@@ -64,6 +65,57 @@ class Expansion(C.Structure):
                 ("phase_ms", C.c_float * 4)]
 
 
+class SearchProblem(C.Structure):
+    _fields_ = [("num_actions", C.c_uint32), ("obs_words", C.c_uint32), ("obs_slots", C.c_uint32),
+                ("max_depth", C.c_uint32), ("gamma", C.c_double), ("root", C.c_uint64),
+                ("root_depth", C.c_uint32), ("root_scenarios", C.c_uint32), ("root_weight", C.c_double),
+                ("root_upper", C.c_double), ("root_lower", C.c_double), ("expand", C.c_void_p),
+                ("release", C.c_void_p), ("ctx", C.c_void_p)]
+
+
+class SearchConfig(C.Structure):
+    _fields_ = [("workers", C.c_uint32), ("max_batch", C.c_uint32), ("max_inflight", C.c_uint32),
+                ("batch_wait_us", C.c_uint32), ("max_trials", C.c_uint64), ("time_budget_s", C.c_double),
+                ("xi", C.c_double), ("c_a", C.c_double), ("c_o", C.c_double), ("target_gap", C.c_double)]
+
+
+class SearchResult(C.Structure):
+    _fields_ = [("action", C.c_int32), ("root_upper", C.c_float), ("root_lower", C.c_float),
+                ("nodes", C.c_uint64), ("expanded", C.c_uint64), ("trials", C.c_uint64), ("batches", C.c_uint64),
+                ("max_depth", C.c_uint32), ("pad", C.c_uint32), ("seconds", C.c_double),
+                ("scenario_steps", C.c_uint64)]
+
+
+class SearchNode(C.Structure):
+    _fields_ = [("parent", C.c_int32), ("action", C.c_int32), ("child", C.c_uint32), ("depth", C.c_uint32),
+                ("n_scen", C.c_uint32), ("visits", C.c_uint32), ("branch_visits", C.c_uint32),
+                ("active", C.c_int32), ("expanded", C.c_int32), ("weight", C.c_float), ("upper", C.c_float),
+                ("lower", C.c_float), ("upper0", C.c_float), ("lower0", C.c_float)]
+
+
+EXPAND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p)
+RELEASE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64)
+
+
+def search_config(workers=1, max_batch=64, max_inflight=1, batch_wait_us=200, max_trials=0, time_budget_s=0.0,
+                  xi=0.95, c_a=0.0, c_o=0.0, target_gap=0.0):
+    return SearchConfig(workers, max_batch, max_inflight, batch_wait_us, max_trials, time_budget_s, xi, c_a, c_o,
+                        target_gap)
+
+
+def result_dict(r: SearchResult):
+    return {k: getattr(r, k) for k, _ in SearchResult._fields_ if k != "pad"}
+
+
+def search(problem: SearchProblem, config: SearchConfig, dump_capacity=0):
+    """despot_search with a caller-provided backend (problem.expand/release
+    hold CFUNCTYPE pointers the caller keeps alive)."""
+    res = SearchResult()
+    dump = (SearchNode * dump_capacity)() if dump_capacity else None
+    _check(lib().despot_search(C.byref(problem), C.byref(config), C.byref(res), dump, dump_capacity))
+    return result_dict(res), (list(dump)[: min(res.nodes, dump_capacity)] if dump_capacity else None)
+
+
 class Exchange(C.Structure):
     _fields_ = [("sums", C.c_void_p), ("n_sums", C.c_uint64), ("mins", C.c_void_p), ("n_mins", C.c_uint64)]
 
@@ -94,6 +146,9 @@ def lib():
         L.despot_batch_abort.argtypes = [vp]
         L.despot_rollout_bounds.argtypes = [vp, u64, C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp, vp]
         L.despot_stream_words.argtypes = [vp, u64, vp, u32, u32, u32, vp, vp]
+        L.despot_search.argtypes = [C.POINTER(SearchProblem), C.POINTER(SearchConfig), C.POINTER(SearchResult),
+                                    vp, u32]
+        L.despot_plan.argtypes = [vp, u64, C.POINTER(SearchConfig), C.POINTER(SearchResult), vp]
         _lib = L
     return _lib
 
@@ -300,6 +355,13 @@ class Model:
         if per_scenario:
             return u.value, l.value, pu[:n], pl[:n]
         return u.value, l.value
+
+    def plan(self, root, config=None, stream=None, **kw):
+        """Parallel DESPOT search from `root` on the GPU backend (despot_plan)."""
+        cfg = config if config is not None else search_config(**kw)
+        res = SearchResult()
+        _check(lib().despot_plan(self.h, int(root), C.byref(cfg), C.byref(res), _stream_ptr(stream)))
+        return result_dict(res)
 
     def stream_words(self, seed, ids, t, k, stream=None):
         ids = np.ascontiguousarray(ids, dtype=np.uint32)
