@@ -78,6 +78,42 @@ __device__ __forceinline__ uint4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
   return make_uint4(c0, c1, c2, c3);
 }
 
+// The Philox key of a batch: either the seed (round keys added on the fly)
+// or the ten precomputed round keys passed as a kernel parameter, so that
+// the key schedule costs no per-lane instructions (it is read straight from
+// the constant bank by the LOP3s).
+struct SeedKey {
+  uint32_t k0, k1;
+};
+struct RoundKeys {
+  uint32_t k0[10], k1[10];
+};
+__host__ inline RoundKeys round_keys(uint32_t k0, uint32_t k1) {
+  RoundKeys rk;
+  for (int r = 0; r < 10; ++r) {
+    rk.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    rk.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  return rk;
+}
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const SeedKey& k) {
+  return philox4x32_10(c0, c1, c2, c3, k.k0, k.k1);
+}
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const RoundKeys& k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k.k0[r];
+    const uint32_t n2 = hi0 ^ c3 ^ k.k1[r];
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return make_uint4(c0, c1, c2, c3);
+}
+
 // event of probability p: (uint64)u < T(p), T(p) = floor(p 2^32) (R14)
 __device__ __forceinline__ bool event(uint32_t u, uint64_t T) { return (uint64_t)u < T; }
 

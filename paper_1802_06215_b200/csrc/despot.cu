@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -430,6 +431,29 @@ int dispatch_car(const DevModel& dm, F&& f) {
   if (dm.peds <= 8) return f(CarThreadT<8>{});
   if (dm.peds <= 20) return f(CarThreadT<20>{});
   return f(CarThreadT<31>{});
+}
+
+// Occupancy (CTAs per SM) of a kernel at a dynamic smem size, and the smem
+// attribute, cached per (kernel, smem): host calls are not free, and the
+// persistent grids must be sized with the launch's real shared memory.
+int kernel_occupancy(const void* kern, size_t smem, int block) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, size_t>, int> cache;
+  static std::map<const void*, size_t> smem_set;
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_pair(kern, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  size_t& cur = smem_set[kern];
+  if (smem > std::max<size_t>(cur, 48 << 10)) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cur = smem;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+  if (occ < 1) occ = 1;
+  cache[key] = occ;
+  return occ;
 }
 
 int check_launch(despot_model* m, const char* what) {
@@ -922,27 +946,10 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
-      auto kern = k2_expand_dense<M, false>;
-      // attribute + occupancy once per (instantiation, smem size); host calls
-      // are not free, and the occupancy must use the launch's real smem
-      static std::mutex mu;
-      static size_t smem_set = 48 << 10;
-      static size_t occ_smem = ~size_t(0);
-      static int occ_cached = 0;
-      int occ;
-      {
-        std::lock_guard<std::mutex> g(mu);
-        if (smem > smem_set) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          smem_set = smem;
-        }
-        if (occ_smem != smem) {
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cached, kern, 128, smem);
-          if (occ_cached < 1) occ_cached = 1;
-          occ_smem = smem;
-        }
-        occ = occ_cached;
-      }
+      bool uni = true;
+      for (uint32_t l = 1; l < L; ++l) uni = uni && ld[l].seed_lo == ld[0].seed_lo && ld[l].seed_hi == ld[0].seed_hi;
+      auto kern = uni ? k2_expand_dense<M, false, true> : k2_expand_dense<M, false, false>;
+      const int occ = kernel_occupancy((const void*)kern, smem, 128);
       uint64_t tiles_bound = 0;
       for (uint32_t l = 0; l < L; ++l) tiles_bound += (uint64_t)dm.A * ((parent[l]->cap + 31) / 32);
       uint64_t grid = (tiles_bound + 3) / 4;
@@ -950,7 +957,7 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       if (grid > maxg) grid = maxg;
       if (grid < 1) grid = 1;
       b->mark(3);
-      kern<<<(unsigned)grid, 128, smem, st>>>(bd, (uint32_t)tiles_bound);
+      kern<<<(unsigned)grid, 128, smem, st>>>(bd, round_keys(ld[0].seed_lo, ld[0].seed_hi));
       ++b->launches;
       b->mark(4);
       return check_launch(m, "K2");
@@ -1079,7 +1086,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
       auto kern = k2_expand_dense<M, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       b->mark(3);
-      kern<<<(unsigned)(m->num_sms * 4), 128, smem, st>>>(bd, 0);
+      kern<<<(unsigned)(m->num_sms * 4), 128, smem, st>>>(bd, RoundKeys{});
       ++b->launches;
       b->mark(4);
       return check_launch(m, "K2(record)");

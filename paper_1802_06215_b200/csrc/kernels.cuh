@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
           z = M::kTerminalObs;
         } else {
           float r;
-          M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, z, r);
+          M::step(sm, s, lf.action, id, lf.depth, SeedKey{lf.seed_lo, lf.seed_hi}, z, r);
           ++steps;
         }
         keep = z == key;
@@ -85,8 +85,11 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
 // (W, U, LAMBDA, N, first) per child slot and (R, Uq, Lq) per action.
 // Persistent grid-stride loop over tiles.
 // ---------------------------------------------------------------------------
-template <class M, bool RECORD>
-__global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, uint32_t total_tiles_bound) {
+// UNI_SEED: every leaf of the batch descends from the same belief, so the
+// Philox key is a kernel parameter (uniform registers; the key schedule costs
+// no per-lane instructions).
+template <class M, bool RECORD, bool UNI_SEED = false>
+__global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, const RoundKeys rk) {
   extern __shared__ __align__(16) unsigned char k2_smem[];
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(k2_smem);
   uint32_t* tile_off = reinterpret_cast<uint32_t*>(k2_smem + ((sizeof(typename M::Sm) + 15) & ~size_t(15)));
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     const bool valid = i < n;
     uint32_t z = 0xFFFFFFFFu, id = 0;
     int64_t qW = 0, qU = 0, qL = 0, qR = 0, qUq = 0, qLq = 0;
-    if (valid) {
+    auto item = [&](const auto& key) {
       typename M::St s = M::load(sm, lf.states, lf.cap, i);
       id = lf.ids[i];
       const double wn = (double)lf.w[i] * lf.inv_wroot;  // normalised weight
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
         z = M::kTerminalObs;
         term = true;
       } else {
-        term = M::step(sm, s, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, z, r);
+        term = M::step(sm, s, (int)a, id, lf.depth + 1, key, z, r);
         ++steps_acc;
       }
       double u = 0.0, lam = 0.0;
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
       uint64_t h = kFnvOffset;
       if (!term) {
         u = M::upper(sm, s);
-        M::template rollout<RECORD>(sm, s, z, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, lam, len, h);
+        M::template rollout<RECORD>(sm, s, z, id, lf.depth + 1, key, lam, len, h);
         steps_acc += len;
       }
       qW = fxq(wn, fx);
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
             if (!M::terminal(s2)) {
               uint32_t z2;
               float r2;
-              M::step(sm, s2, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, z2, r2);
+              M::step(sm, s2, (int)a, id, lf.depth + 1, key, z2, r2);
             }
             // scen_states is [S][SW] (row per scenario): write through a strided view
             uint32_t tmp[16];
@@ -171,6 +174,10 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
           atomicOr(b.err, kErrScenCap);
         }
       }
+    };
+    if (valid) {
+      if constexpr (UNI_SEED) item(rk);
+      else item(SeedKey{lf.seed_lo, lf.seed_hi});
     }
     // ---- per-action sums (R, Uq, Lq) -----------------------------------
     const uint64_t la = (uint64_t)leaf * b.A + a;
@@ -202,7 +209,6 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   }
   const uint32_t ws = warp_sum32(steps_acc);
   if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)ws);
-  (void)total_tiles_bound;
 }
 
 // ---------------------------------------------------------------------------
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, con
       u = M::upper(sm, s);
       uint32_t len;
       uint64_t h = kFnvOffset;
-      M::template rollout<false>(sm, s, M::initial_obs(sm, s), ids[i], depth, k0, k1, lam, len, h);
+      M::template rollout<false>(sm, s, M::initial_obs(sm, s), ids[i], depth, SeedKey{k0, k1}, lam, len, h);
     }
     if (per_u) per_u[i] = (float)u;
     if (per_l) per_l[i] = (float)lam;

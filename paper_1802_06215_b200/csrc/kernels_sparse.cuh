@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
       bool term = M::terminal(s);
       if (!term) {
         float r;
-        term = M::step(sm, s, lf.action, id, lf.depth, lf.seed_lo, lf.seed_hi, r);
+        term = M::step(sm, s, lf.action, id, lf.depth, SeedKey{lf.seed_lo, lf.seed_hi}, r);
         ++steps;
       }
       if (term) {
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(128) k2_car_thread(BatchDev b, SparseItemOut i
     float r = 0.0f;
     bool term = M::terminal(s);
     if (!term) {
-      term = M::step(sm, s, (int)a, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, r);
+      term = M::step(sm, s, (int)a, id, lf.depth + 1, SeedKey{lf.seed_lo, lf.seed_hi}, r);
       ++steps_acc;
     }
     uint64_t hsh = 0;
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(128) k2_car_thread(BatchDev b, SparseItemOut i
     uint64_t h = kFnvOffset;
     if (!term) {
       u = M::upper(sm, s);
-      M::template rollout<RECORD>(sm, s, 0u, id, lf.depth + 1, lf.seed_lo, lf.seed_hi, lam, len, h);
+      M::template rollout<RECORD>(sm, s, 0u, id, lf.depth + 1, SeedKey{lf.seed_lo, lf.seed_hi}, lam, len, h);
       steps_acc += len;
     }
     const double fx = dm.fx, gamma = dm.gamma;

@@ -137,14 +137,15 @@ struct CarThreadT {
       }
     return car_bin(x) | (car_bin(y) << 16);
   }
+  template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
-                                              uint32_t k0, uint32_t k1, float& r) {
+                                              const KeyT& key, float& r) {
     constexpr int NB = (MAXP + 1 + 3) / 4;
     uint32_t u[4 * NB];
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
       if (4 * bk < sm.peds + 1) {
-        const uint4 w = philox4x32_10(id, t, (uint32_t)bk, 0u, k0, k1);
+        const uint4 w = philox(id, t, (uint32_t)bk, 0u, key);
         u[4 * bk] = w.x;
         u[4 * bk + 1] = w.y;
         u[4 * bk + 2] = w.z;
@@ -192,9 +193,9 @@ struct CarThreadT {
     return car_policy_from_gap(gap);
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
-  template <bool TRACE>
+  template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t /*z: bins of s*/, uint32_t id, uint32_t t0,
-                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
     uint32_t t = t0;
     bool term = false;
@@ -202,7 +203,7 @@ struct CarThreadT {
       const int a = policy(sm, s);  // reads only the last observation's bins
       if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
       float r;
-      term = step(sm, s, a, id, t + 1, k0, k1, r);
+      term = step(sm, s, a, id, t + 1, key, r);
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
     }

@@ -68,16 +68,17 @@ struct Tiger {
     z = kTerminalObs;
     return true;
   }
+  template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
-                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
-    const uint4 u = philox4x32_10(id, t, 0u, 0u, k0, k1);
+                                              const KeyT& key, uint32_t& z, float& r) {
+    const uint4 u = philox(id, t, 0u, 0u, key);
     return step_u(sm, s, a, u.x, z, r);
   }
   static __device__ __forceinline__ double upper(const Sm&, const St&) { return 10.0; }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
-  template <bool TRACE>
+  template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
-                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
     uint32_t t = t0;
     bool term = false;
@@ -85,7 +86,7 @@ struct Tiger {
       const int a = 0;  // Listen always
       if (TRACE) h = (h ^ (uint64_t)a) * kFnvPrime;
       float r;
-      term = step(sm, s, a, id, t + 1, k0, k1, z, r);
+      term = step(sm, s, a, id, t + 1, key, z, r);
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
     }
@@ -110,6 +111,8 @@ struct RockSample {
     int8_t rx[32], ry[32];
     uint8_t pos_rock[32];
     uint32_t range_mask[2];
+    uint32_t rock_xy[32];   // rx | ry << 8                  (one load per sensing)
+    uint32_t pos_tgt[32];   // j | rx << 8 | ry << 16 of policy position p
     double gpow[kGpowN];
     int8_t rock_at[kRsMaxN * kRsMaxN];
     uint32_t thr[kRsMaxD2];
@@ -128,6 +131,12 @@ struct RockSample {
     copy_words(sm.rx, dm.rx, 32, tid, nt);
     copy_words(sm.ry, dm.ry, 32, tid, nt);
     copy_words(sm.pos_rock, dm.pos_rock, 32, tid, nt);
+    for (int j = tid; j < 32; j += nt) {
+      const uint32_t x = (uint8_t)dm.rx[j], y = (uint8_t)dm.ry[j];
+      sm.rock_xy[j] = x | (y << 8);
+      const int jj = dm.pos_rock[j];
+      sm.pos_tgt[j] = (uint32_t)jj | ((uint32_t)(uint8_t)dm.rx[jj] << 8) | ((uint32_t)(uint8_t)dm.ry[jj] << 16);
+    }
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
     copy_words(sm.rock_at, dm.rock_at, (dm.n * dm.n + 3) & ~3, tid, nt);
     copy_words(sm.thr, dm.sense_thr_m1, 4 * (dm.d2max + 1), tid, nt);
@@ -196,7 +205,8 @@ struct RockSample {
       const uint32_t gbit = samp & (s.good >> (jr & 31));
       // SENSE j (evaluated for every lane; masked)
       const int js = max(sub - 5, 0);
-      const int dx = x - sm.rx[js], dy = y - sm.ry[js];
+      const uint32_t xy = sm.rock_xy[js];
+      const int dx = x - (int)(xy & 0xFFu), dy = y - (int)(xy >> 8);
       const uint32_t incorrect = u[r] > sm.thr[dx * dx + dy * dy] ? 1u : 0u;
       const uint32_t isgood = (s.good >> js) & 1u;
       const uint32_t sense = (act && sub >= 5) ? 1u : 0u;
@@ -215,8 +225,9 @@ struct RockSample {
     z = term ? kTerminalObs : zsum;
     return term;
   }
+  template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
-                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
+                                              const KeyT& key, uint32_t& z, float& r) {
     int b[R];
     int rest = a;
 #pragma unroll
@@ -224,7 +235,7 @@ struct RockSample {
       b[q] = rest % sm.base;
       rest /= sm.base;
     }
-    const uint4 w = philox4x32_10(id, t, 0u, 0u, k0, k1);
+    const uint4 w = philox(id, t, 0u, 0u, key);
     const uint32_t u[2] = {w.x, w.y};
     return step_sub(sm, s, b, u, z, r);
   }
@@ -262,8 +273,9 @@ struct RockSample {
       const uint32_t open = ~done & rmask[r];
       const bool has = open != 0u && !s.ex[r];
       const int p = __ffs(open | 0x80000000u) - 1;  // 31 when nothing is open
-      const int j = sm.pos_rock[p];
-      const int ddx = sm.rx[j] - s.x[r], ddy = sm.ry[j] - s.y[r];
+      const uint32_t tg = sm.pos_tgt[p];
+      const int j = (int)(tg & 0xFFu);
+      const int ddx = (int)((tg >> 8) & 0xFFu) - s.x[r], ddy = (int)(tg >> 16) - s.y[r];
       const int code = 3 * ((ddx > 0) - (ddx < 0) + 1) + ((ddy > 0) - (ddy < 0) + 1);
       const int mv = (int)((kMovePack >> (3 * code)) & 7u);
       const bool known_good = (gm >> p) & 1u;
@@ -271,9 +283,9 @@ struct RockSample {
       tbit[r] = has ? (1u << p) : 0u;
     }
   }
-  template <bool TRACE>
+  template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
-                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
     uint32_t done = 0, gm = 0;
     uint32_t t = t0;
@@ -291,7 +303,7 @@ struct RockSample {
         }
         h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
       }
-      const uint4 w = philox4x32_10(id, t + 1, 0u, 0u, k0, k1);
+      const uint4 w = philox(id, t + 1, 0u, 0u, key);
       const uint32_t u[2] = {w.x, w.y};
       float r;
       uint32_t zr[R];
@@ -415,11 +427,12 @@ struct Nav {
   }
   // g(s, a, phi_t), branch-free so that roll-out lanes choosing different
   // actions do not diverge
+  template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
-                                              uint32_t k0, uint32_t k1, uint32_t& z, float& r) {
-    const uint4 u0 = philox4x32_10(id, t, 0u, 0u, k0, k1);
-    const uint4 u1 = philox4x32_10(id, t, 1u, 0u, k0, k1);
-    const uint4 u2 = philox4x32_10(id, t, 2u, 0u, k0, k1);
+                                              const KeyT& key, uint32_t& z, float& r) {
+    const uint4 u0 = philox(id, t, 0u, 0u, key);
+    const uint4 u1 = philox(id, t, 1u, 0u, key);
+    const uint4 u2 = philox(id, t, 2u, 0u, key);
     const uint32_t u[9] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x};
     const bool stay = a == 0;
     const bool fail = !stay && event(u[0], sm.t_fail);
@@ -459,9 +472,9 @@ struct Nav {
     return ((fr >> 4) & 1u) ? 5 : ((fr >> 3) & 1u) ? 4 : ((fr >> 5) & 1u) ? 6
          : ((fr >> (e1 - 1)) & 1u) ? e1 : ((fr >> (e2 - 1)) & 1u) ? e2 : 0;
   }
-  template <bool TRACE>
+  template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
-                                 uint32_t k0, uint32_t k1, double& ret, uint32_t& len, uint64_t& h) {
+                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
     uint32_t t = t0;
     bool term = false;
@@ -469,7 +482,7 @@ struct Nav {
       const int a = policy(z, t);
       if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
       float r;
-      term = step(sm, s, a, id, t + 1, k0, k1, z, r);
+      term = step(sm, s, a, id, t + 1, key, z, r);
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
     }

@@ -82,6 +82,8 @@ struct Search {
   std::condition_variable dcv;  // a worker's trial finished expanding
   std::deque<Pending> queue;
   bool workers_done = false;
+  uint32_t n_workers = 1;
+  uint32_t blocked = 0;  // workers waiting for their in-flight trials (under qmu)
   std::atomic<int> error{0};
   std::string error_msg;
 
@@ -216,8 +218,9 @@ struct Search {
         std::unique_lock<std::mutex> lk(qmu);
         qcv.wait(lk, [&] { return !queue.empty() || workers_done; });
         if (queue.empty() && workers_done) break;
+        // wait for more leaves only while some worker can still produce one
         const auto deadline = std::chrono::steady_clock::now() + std::chrono::microseconds(C.batch_wait_us);
-        while (queue.size() < max_batch && !workers_done && !stop.load()) {
+        while (queue.size() < max_batch && blocked < n_workers && !workers_done && !stop.load()) {
           if (qcv.wait_until(lk, deadline) == std::cv_status::timeout) break;
         }
         while (!queue.empty() && batch.size() < max_batch) {
@@ -274,7 +277,10 @@ struct Search {
     while (!stop.load()) {
       if (inflight.load() >= max_inflight) {
         std::unique_lock<std::mutex> lk(qmu);
+        ++blocked;
+        qcv.notify_one();  // the batcher need not wait for this worker's next leaf
         dcv.wait(lk, [&] { return inflight.load() < max_inflight || stop.load(); });
+        --blocked;
         continue;
       }
       if (C.max_trials && trials.fetch_add(1) >= C.max_trials) {
@@ -331,6 +337,7 @@ struct Search {
     }
     // wait for this worker's trials still in the batcher (inflight lives here)
     std::unique_lock<std::mutex> lk(qmu);
+    ++blocked;
     qcv.notify_all();
     dcv.wait(lk, [&] { return inflight.load() == 0; });
   }
@@ -392,6 +399,7 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
     if (rc != DESPOT_OK) return rc;
   }
   const uint32_t W = std::max<uint32_t>(1, C->workers);
+  S.n_workers = W;
   std::thread batcher([&] { S.batcher(); });
   std::vector<std::thread> workers;
   for (uint32_t i = 0; i < W; ++i) workers.emplace_back([&] { S.worker(); });
