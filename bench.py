@@ -35,7 +35,10 @@ from paper_1802_06215_b200 import inputs  # noqa: E402
 # thread-instructions per scenario-step of K2 (the "algorithmic" instruction
 # work of one step as implemented), from the ncu profile of round 1, see
 # DESIGN.md §7.  Used for the ALU roofline: achieved = I_step * steps / t_K2.
-I_STEP = {"rocksample": 260.0, "nav": 520.0, "car": 2000.0, "tiger": 120.0}
+# per config (ncu smsp__thread_inst_executed.sum / scenario-steps, round 1):
+# config 2/5 MARS 303, config 3 navigation 303, config 4 driving (thread per
+# scenario) 2054; config 1 RockSample(7,8) 184.
+I_STEP = {1: 184.0, 2: 303.0, 3: 303.0, 4: 2054.0, 5: 303.0}
 
 
 def load_peaks():
@@ -321,7 +324,7 @@ def main():
     peak_tinst = num_sms * 4 * 32 * sm_clock * 1e6 / 1e12  # issue slots, thread-instr/s (Tinst/s)
     k2_avg = float(np.mean(k2_ms))
     steps_local = total_steps / world
-    achieved = I_STEP[kind] * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
+    achieved = I_STEP[args.config] * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
     k2_share = float(np.sum(k2_ms) / np.sum(step_ms))
     if rank == 0:
         line = {
@@ -347,7 +350,7 @@ def main():
                          "peak": peak_tinst, "unit": "Tinst/s", "frac": achieved / peak_tinst,
                          "traffic": None,
                          "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
-                                 f"({peak_src} sm_max_mhz); achieved = {I_STEP[kind]} thread-instr per "
+                                 f"({peak_src} sm_max_mhz); achieved = {I_STEP[args.config]} thread-instr per "
                                  f"scenario-step (DESIGN.md §7) x steps / live K2 event time"},
             "e2e": {"value": e2e_steps / (e2e_ms / 1e3), "unit": "scenario-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_n,

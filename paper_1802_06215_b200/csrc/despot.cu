@@ -474,13 +474,15 @@ class PinnedPool {
   void* acquire(size_t bytes) {
     {
       std::lock_guard<std::mutex> g(mu_);
+      size_t best = free_.size();  // best fit: the smallest free buffer that holds `bytes`
       for (size_t i = 0; i < free_.size(); ++i)
-        if (free_[i].second >= bytes) {
-          void* p = free_[i].first;
-          sizes_[p] = free_[i].second;
-          free_.erase(free_.begin() + i);
-          return p;
-        }
+        if (free_[i].second >= bytes && (best == free_.size() || free_[i].second < free_[best].second)) best = i;
+      if (best < free_.size()) {
+        void* p = free_[best].first;
+        sizes_[p] = free_[best].second;
+        free_.erase(free_.begin() + best);
+        return p;
+      }
     }
     size_t sz = 4096;
     while (sz < bytes) sz <<= 1;
@@ -501,6 +503,36 @@ class PinnedPool {
   std::vector<std::pair<void*, size_t>> free_;
   std::unordered_map<void*, size_t> sizes_;
 };
+// timing events, reused across batches (creating 8 events per call costs more
+// than the phases of a small batch)
+class EventPool {
+ public:
+  bool acquire(cudaEvent_t* ev) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (int i = 0; i < 8; ++i) {
+      if (!free_.empty()) {
+        ev[i] = free_.back();
+        free_.pop_back();
+      } else if (cudaEventCreate(&ev[i]) != cudaSuccess) {
+        return false;
+      }
+    }
+    return true;
+  }
+  void release(cudaEvent_t* ev) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (int i = 0; i < 8; ++i)
+      if (ev[i]) free_.push_back(ev[i]);
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<cudaEvent_t> free_;
+};
+EventPool& event_pool() {
+  static EventPool* p = new EventPool();
+  return *p;
+}
 PinnedPool& pinned_pool() {
   static PinnedPool* p = new PinnedPool();  // never destroyed (process lifetime)
   return *p;
@@ -687,9 +719,7 @@ static void free_batch(despot_batch* b, bool drop_new_nodes) {
     cudaStreamSynchronize(b->stream);  // the H2D from it must have completed
     pinned_pool().release(b->pinned);
   }
-  if (b->timing)
-    for (auto& e : b->ev)
-      if (e) cudaEventDestroy(e);
+  if (b->timing) event_pool().release(b->ev);
   delete b;
 }
 
@@ -741,7 +771,7 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   b->leaves.assign(leaves, leaves + L);
   b->timing = flags & DESPOT_X_TIMING;
   if (b->timing) {
-    for (auto& e : b->ev) CU(cudaEventCreate(&e));
+    if (!event_pool().acquire(b->ev)) return set_err(DESPOT_ECUDA, "cudaEventCreate failed");
     b->mark(0);
   }
   b->leaf_node.assign(L, nullptr);
@@ -772,7 +802,8 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       smax = std::max(smax, parent[l]->cap);
       q_bound += (uint64_t)dm.A * parent[l]->cap;
     }
-    if (smax > 8192) return set_err(DESPOT_EINVAL, "sparse-key models: at most 8192 scenarios per leaf");
+    // the grouping table of k3_group_sparse: 12 B x 2^ceil(log2 2n) + 4n of shared memory
+    if (smax > 4096) return set_err(DESPOT_EINVAL, "sparse-key models: at most 4096 scenarios per leaf");
     b->S = smax;
   }
   cudaStream_t st = b->stream;
@@ -1098,9 +1129,12 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   // small dense batches (few slots): rank + scan + write in one CTA
   const bool small_k3 = !b->sparse && LA <= kSmallLA && b->S <= 32;
   if (!rc && b->sparse) {
-    const size_t smem = 16 * (size_t)b->S;
-    cudaFuncSetAttribute(k3_group_sparse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io);
+    uint32_t tbits = 1;
+    while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
+    const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
+    const int occ = kernel_occupancy((const void*)k3_group_sparse, smem, 512);
+    (void)occ;
+    k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io, tbits);
     ++b->launches;
     rc = check_launch(m, "K3a(sparse)");
   } else if (!rc && small_k3) {
@@ -1122,7 +1156,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     rc = check_launch(m, "K3b");
   }
   if (!rc && b->sparse) {
-    k3_write_sparse<<<g3, 128, 0, st>>>(bd, b->io);
+    k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);
     ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
   } else if (!rc && !small_k3) {
@@ -1143,22 +1177,24 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "status copy failed");
   }
+  // host outputs: the staging block [per-leaf | per-action | CSR | children]
+  // goes to one pinned buffer; when it is small (search-sized batches) the
+  // whole block travels in this first copy and no second round trip is needed
+  char* hp_out = nullptr;
+  const size_t head_bytes = o_cc, body_bytes = o_so;
+  const bool one_copy = body_bytes <= (1u << 20);  // else: head via pinned, children copied directly
+  struct PinRelease {
+    char*& p;
+    ~PinRelease() {
+      if (p) pinned_pool().release(p);
+    }
+  } pin_out_guard{hp_out};
   if (!rc && !dev_out) {
-    struct Cp {
-      void* dst;
-      const void* src;
-      size_t bytes;
-    } cps[] = {
-        {out->n_scen, bd.n_scen, 4 * (size_t)L},
-        {out->weight, bd.weight, 4 * (size_t)L},
-        {out->act_reward, bd.act_reward, 4 * LA},
-        {out->act_upper, bd.act_upper, 4 * LA},
-        {out->act_lower, bd.act_lower, 4 * LA},
-        {out->child_begin, bd.child_begin, 4 * (LA + 1)},
-    };
-    for (auto& c : cps)
-      if (cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        rc = set_err(DESPOT_ECUDA, "output copy failed");
+    hp_out = static_cast<char*>(pinned_pool().acquire(body_bytes));
+    if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
+    else if (cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st) !=
+             cudaSuccess)
+      rc = set_err(DESPOT_ECUDA, "output copy failed");
   }
   if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
     m->failed = true;
@@ -1180,22 +1216,35 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     else if (err & kErrScenCap) rc = set_err(DESPOT_ECAPACITY, "scen_capacity too small");
   }
   if (!rc && !dev_out) {
-    // children and per-scenario records: only the used part
     const uint64_t Cu = nchildren;
     uint64_t Su = 0;
     const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 24);
     for (uint32_t l = 0; l < L; ++l) Su += (uint64_t)dm.A * nl[l];
+    struct Part {
+      void* dst;
+      size_t off, bytes;
+    } parts[] = {
+        {out->n_scen, o_ns, 4 * (size_t)L},           {out->weight, o_w, 4 * (size_t)L},
+        {out->act_reward, o_ar, 4 * LA},              {out->act_upper, o_au, 4 * LA},
+        {out->act_lower, o_al, 4 * LA},               {out->child_begin, o_cb, 4 * (LA + 1)},
+        {out->child_count, o_cc, 4 * Cu},             {out->child_first, o_cf, 4 * Cu},
+        {out->child_weight, o_cw, 4 * Cu},            {out->child_upper, o_cu, 4 * Cu},
+        {out->child_lower, o_cl, 4 * Cu},             {out->child_obs, o_co, 4 * Cu * dm.OW},
+    };
+    if (!one_copy) {  // second round trip: the used part of each child array, straight to the caller
+      for (int k = 6; k < 12; ++k) {
+        if (parts[k].bytes && cudaMemcpyAsync(parts[k].dst, static_cast<char*>(stage) + parts[k].off,
+                                              parts[k].bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+          rc = set_err(DESPOT_ECUDA, "output copy failed");
+        parts[k].bytes = 0;  // nothing left to move on the host
+      }
+    }
+    // per-scenario records (validation mode): direct copies
     struct Cp {
       void* dst;
       const void* src;
       size_t bytes;
     } cps[] = {
-        {out->child_count, bd.child_count, 4 * Cu},
-        {out->child_first, bd.child_first, 4 * Cu},
-        {out->child_weight, bd.child_weight, 4 * Cu},
-        {out->child_upper, bd.child_upper, 4 * Cu},
-        {out->child_lower, bd.child_lower, 4 * Cu},
-        {out->child_obs, bd.child_obs, 4 * Cu * dm.OW},
         {record ? out->scen_obs : nullptr, bd.scen_obs, 4 * Su * dm.OW},
         {record ? out->scen_reward : nullptr, bd.scen_reward, 4 * Su},
         {record ? out->scen_upper : nullptr, bd.scen_upper, 4 * Su},
@@ -1205,10 +1254,14 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
         {record ? out->scen_states : nullptr, bd.scen_states, 4 * Su * dm.SW},
     };
     for (auto& c : cps)
-      if (c.dst && c.src && c.bytes &&
+      if (!rc && c.dst && c.src && c.bytes &&
           cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "output copy failed");
-    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) rc = set_err(DESPOT_ECUDA, "output copy sync failed");
+    if (!rc && (!one_copy || record) && cudaStreamSynchronize(st) != cudaSuccess)
+      rc = set_err(DESPOT_ECUDA, "output copy sync failed");
+    if (!rc)
+      for (auto& p : parts)
+        if (p.bytes) memcpy(p.dst, hp_out + p.off, p.bytes);
   }
   if (!rc && b->timing) {
     b->mark(7);

@@ -339,11 +339,20 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
 }
 
 // ---------------------------------------------------------------------------
-// K3s: group the items of one (leaf, action) by key (first occurrence)
+// K3s: group the items of one (leaf, action) by key (first occurrence).  An
+// open-addressing table in shared memory (2^k >= 2n slots) maps each 64-bit
+// key hash to the smallest item position carrying it (atomicMin), so the
+// representative of every item is found in O(1) probes; each item's full key
+// is then compared with its representative's (a hash collision is an error,
+// never a merge), representatives get their ordinal by a block scan in item
+// order (= first-occurrence order, R8), and every item adds its exact
+// fixed-point contributions to its child's row of the exchange block.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io) {
+__global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io, uint32_t tbits) {
   extern __shared__ __align__(16) unsigned char gs_smem[];
-  uint64_t* sh = reinterpret_cast<uint64_t*>(gs_smem);
+  const uint32_t tsize = 1u << tbits, tmask = tsize - 1u;
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gs_smem);  // [tsize]
+  uint32_t* titem = reinterpret_cast<uint32_t*>(tkey + tsize);              // [tsize]
   const uint64_t la = blockIdx.x;
   const uint32_t leaf = (uint32_t)(la / b.A), a = (uint32_t)(la - (uint64_t)leaf * b.A);
   const uint32_t n = b.n_leaf[leaf];
@@ -352,23 +361,41 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
   const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
   const uint64_t base = la * b.S;
   __shared__ uint64_t wsum[32];
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) sh[i] = io.hash[q0 + i];
+  constexpr unsigned long long kEmpty = 0ull;  // hash 0 is remapped to 1
+  uint32_t* ord = titem + tsize;  // [n] child ordinal of a representative
+  for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x) {
+    tkey[s] = kEmpty;
+    titem[s] = 0xFFFFFFFFu;
+  }
   __syncthreads();
-  uint32_t* rep_of = reinterpret_cast<uint32_t*>(sh + n);  // [n]
-  uint32_t* ord = rep_of + n;                              // [n] child ordinal of a representative
+  // 1. insert: slot of the hash, minimum item position per hash
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long h = io.hash[q0 + i];
+    h = h ? h : 1ull;
+    uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
+    for (;;) {
+      const unsigned long long prev = atomicCAS(&tkey[s], kEmpty, h);
+      if (prev == kEmpty || prev == h) break;
+      s = (s + 1u) & tmask;
+    }
+    atomicMin(&titem[s], i);
+  }
+  __syncthreads();
+  // 2. representative, exact-key check, ordinal of the representatives
   uint32_t run = 0;
   for (uint32_t c0 = 0; c0 < n; c0 += blockDim.x) {
     const uint32_t i = c0 + threadIdx.x;
-    uint32_t is_rep = 0;
+    uint32_t is_rep = 0, rep = 0;
     if (i < n) {
-      const uint64_t hi = sh[i];
-      uint32_t j = 0;
-      while (sh[j] != hi) ++j;  // first occurrence of the hash (j <= i)
-      rep_of[i] = j;
-      is_rep = j == i;
+      unsigned long long h = io.hash[q0 + i];
+      h = h ? h : 1ull;
+      uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
+      while (tkey[s] != h) s = (s + 1u) & tmask;
+      rep = titem[s];
+      is_rep = rep == i;
       if (!is_rep) {
         const uint32_t* ki = io.keys + (q0 + i) * OW;
-        const uint32_t* kj = io.keys + (q0 + j) * OW;
+        const uint32_t* kj = io.keys + (q0 + rep) * OW;
         for (uint32_t k = 0; k < OW; ++k)
           if (ki[k] != kj[k]) atomicOr(b.err, kErrHash);
       }
@@ -379,14 +406,20 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
     run += (uint32_t)tot;
   }
   __syncthreads();
+  // 3. exact sums per child
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint32_t c = ord[rep_of[i]];
+    unsigned long long h = io.hash[q0 + i];
+    h = h ? h : 1ull;
+    uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
+    while (tkey[s] != h) s = (s + 1u) & tmask;
+    const uint32_t rep = titem[s];
+    const uint32_t c = ord[rep];
     const uint64_t slot = base + c;
     atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 0]);
     atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 1]);
     atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 2]);
     atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], 1ull);
-    if (rep_of[i] == i) {
+    if (rep == i) {
       b.mins[slot] = (int32_t)b.leaves[leaf].ids[i];
       b.rank[slot] = c;
       b.sp_item[slot] = (uint32_t)(q0 + i);
@@ -395,13 +428,13 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
   if (threadIdx.x == 0) b.nc[la] = run;
 }
 
-// K3c for sparse keys: children are already in first-occurrence order
-__global__ void __launch_bounds__(128) k3_write_sparse(BatchDev b, SparseItemOut io) {
+// K3c for sparse keys: one CTA per (leaf, action), one thread per child
+// (children are already in first-occurrence order)
+__global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut io) {
+  __shared__ int64_t s_wt[8], s_nt[8];
   const uint32_t A = b.A;
-  const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t LA = (uint64_t)b.L * A;
-  const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-  if (la >= LA) return;
+  const uint64_t la = blockIdx.x;
   const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
   const LeafDev& lf = b.leaves[leaf];
   const DevModel& dm = *b.model;
@@ -411,7 +444,7 @@ __global__ void __launch_bounds__(128) k3_write_sparse(BatchDev b, SparseItemOut
   const uint32_t cb = b.child_begin[la];
   const uint32_t nc = b.nc[la];
   int64_t wt = 0, nt = 0;
-  for (uint32_t c = lane; c < nc; c += 32) {
+  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
     const int64_t N = b.sums[lay.N(base + c)];
     const int64_t W = b.sums[lay.W(base + c)];
     wt += W;
@@ -432,7 +465,16 @@ __global__ void __launch_bounds__(128) k3_write_sparse(BatchDev b, SparseItemOut
   }
   wt = warp_sum64(wt);
   nt = warp_sum64(nt);
-  if (lane == 0) {
+  if ((threadIdx.x & 31) == 0) {
+    s_wt[threadIdx.x >> 5] = wt;
+    s_nt[threadIdx.x >> 5] = nt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) {
+      wt += s_wt[w];
+      nt += s_nt[w];
+    }
     lf.nchild[a] = nc;
     const double Wd = (double)wt;
     b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
