@@ -339,3 +339,55 @@ def test_car_factored_equals_unfactored_1000_random_steps():
             Gs.append(gm.expand([(r, -1, 0, 0)], record=True))
         for k in ("scen_obs", "scen_reward", "scen_states", "scen_len", "scen_hash", "scen_upper", "scen_lower"):
             assert np.array_equal(Gs[0][k], Gs[1][k]), (peds, k)
+
+
+def test_concurrent_batches_from_host_threads():
+    """The model is shared by many host threads (8 concurrent
+    producers); every call uses its own scratch and stream and returns the
+    same bits as a serial call."""
+    import threading
+
+    import torch
+    gm, om, st, w, seed, L = setup(2, K=150, L=8)
+    root = gm.belief_load(st, w, seed)
+    R = gm.expand([(root, -1, 0, 0)])
+    lv = inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, 24)
+    jobs = [[(root, a, c, 1) for a, c in lv[i::8]] for i in range(8)]
+    ref = [gm.expand(j) for j in jobs]
+    got = [None] * 8
+    errs = []
+
+    def run(i):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(3):
+                    o = gm.expand(jobs[i], stream=s)
+                    for n in o["node"]:
+                        gm.node_release(n)
+                got[i] = gm.expand(jobs[i], stream=s)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(8):
+        for k in ("n_scen", "act_upper", "act_lower", "child_begin", "child_first", "child_upper", "child_lower"):
+            assert np.array_equal(got[i][k], ref[i][k]), (i, k)
+
+
+def test_sharded_model_rejects_record_and_sparse():
+    kind, params, st, w, seed, _ = inputs.config_inputs(2, K=40)
+    m = Model(kind, params, rank=0, world=2)
+    r = m.belief_load(st, w, seed)
+    assert m.node_info(r)[0] == 20  # ids 0, 2, 4, ... kept on rank 0 of 2
+    with pytest.raises(DespotError):
+        m.expand([(r, -1, 0, 0)])  # world > 1: begin / exchange / end only
+    with pytest.raises(DespotError):
+        m.expand_begin([(r, -1, 0, 0)], record=True)
+    with pytest.raises(DespotError):
+        Model("car", inputs.car_params(), rank=0, world=2)
