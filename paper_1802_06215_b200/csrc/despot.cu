@@ -471,21 +471,20 @@ int check_launch(despot_model* m, const char* what) {
 // one.
 class PinnedPool {
  public:
+  // power-of-two size classes: a request only reuses a buffer of its own
+  // class, so small staging never holds on to the large output buffer
   void* acquire(size_t bytes) {
+    size_t sz = 4096;
+    while (sz < bytes) sz <<= 1;
     {
       std::lock_guard<std::mutex> g(mu_);
-      size_t best = free_.size();  // best fit: the smallest free buffer that holds `bytes`
-      for (size_t i = 0; i < free_.size(); ++i)
-        if (free_[i].second >= bytes && (best == free_.size() || free_[i].second < free_[best].second)) best = i;
-      if (best < free_.size()) {
-        void* p = free_[best].first;
-        sizes_[p] = free_[best].second;
-        free_.erase(free_.begin() + best);
+      auto& fl = free_[sz];
+      if (!fl.empty()) {
+        void* p = fl.back();
+        fl.pop_back();
         return p;
       }
     }
-    size_t sz = 4096;
-    while (sz < bytes) sz <<= 1;
     void* p = nullptr;
     if (cudaMallocHost(&p, sz) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> g(mu_);
@@ -495,12 +494,12 @@ class PinnedPool {
   void release(void* p) {
     if (!p) return;
     std::lock_guard<std::mutex> g(mu_);
-    free_.push_back({p, sizes_[p]});
+    free_[sizes_[p]].push_back(p);
   }
 
  private:
   std::mutex mu_;
-  std::vector<std::pair<void*, size_t>> free_;
+  std::map<size_t, std::vector<void*>> free_;
   std::unordered_map<void*, size_t> sizes_;
 };
 // timing events, reused across batches (creating 8 events per call costs more
@@ -1190,7 +1189,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     }
   } pin_out_guard{hp_out};
   if (!rc && !dev_out) {
-    hp_out = static_cast<char*>(pinned_pool().acquire(body_bytes));
+    hp_out = static_cast<char*>(pinned_pool().acquire(one_copy ? body_bytes : head_bytes));
     if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
     else if (cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st) !=
              cudaSuccess)
