@@ -23,8 +23,15 @@ constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 
 enum Kind : int32_t { kTiger = 1, kRockSample = 2, kNav = 3, kCar = 4 };
 
+// Dynamic shared memory of every kernel that stages a model: the model's Sm
+// struct at offset 0, then the model's variable-size tables
+// (DevModel::sm_table_bytes, aligned to 16), then the kernel's own data.
+extern __shared__ __align__(16) unsigned char hd_dyn_smem[];
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
 struct DevModel {
   int32_t kind;
+  uint32_t sm_table_bytes;     // variable-size shared-memory tables after the model's Sm
   uint32_t A, SW, OW, slots, D, terminal_slot, elements;
   double gamma, tail;
   double fx, inv_fx;           // fixed-point scale of the exact reductions

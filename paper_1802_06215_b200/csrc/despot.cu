@@ -264,8 +264,8 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     dm.policy_east = get_param(params, "policy", pol) && pol == "east";
     dm.m = (int)rx.size();
     if (dm.R < 1 || dm.R > 2 || (int)sx.size() != dm.R || dm.m > kRsMaxRocks || dm.n < 1 ||
-        dm.n > kRsMaxN)
-      return set_err(DESPOT_EINVAL, "rocksample: need 1<=robots<=2, rocks<=31, n<=32");
+        dm.n > kRsMaxN || dm.n * dm.n * std::max(dm.m, 1) > RockSample<1>::kMaxTable)
+      return set_err(DESPOT_EINVAL, "rocksample: need 1<=robots<=2, rocks<=31, n<=32, n*n*rocks<=16384");
     dm.base = 5 + dm.m;
     dm.A = 1;
     for (int r = 0; r < dm.R; ++r) dm.A *= (uint32_t)dm.base;
@@ -312,6 +312,7 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     }
     rmax = 10.0 * dm.R;
     umax = 10.0 * (dm.m + dm.R);
+    dm.sm_table_bytes = (uint32_t)RockSample<1>::table_bytes(dm.n, dm.m, dm.d2max);
   } else if (k == "nav") {
     dm.kind = kNav;
     dm.n = (int)pi(params, "n", 13);
@@ -964,7 +965,9 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       using M = decltype(mdl);
       b->mark(1);
       if (!all_self) {
-        k1_update<M><<<L, 256, 0, st>>>(bd);  // + prefix in its last CTA
+        const size_t smem1 = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
+        kernel_occupancy((const void*)k1_update<M>, smem1, 256);  // sets the smem attribute if > 48 KB
+        k1_update<M><<<L, 256, smem1, st>>>(bd);  // + prefix in its last CTA
         ++b->launches;
       }
       b->mark(2);
@@ -975,7 +978,7 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
     // K2 now (the exchange block is complete after it)
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) + 4 * ((size_t)L + 1);
       bool uni = true;
       for (uint32_t l = 1; l < L; ++l) uni = uni && ld[l].seed_lo == ld[0].seed_lo && ld[l].seed_hi == ld[0].seed_hi;
       auto kern = uni ? k2_expand_dense<M, false, true> : k2_expand_dense<M, false, false>;
@@ -1112,7 +1115,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   } else if (record) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = ((sizeof(typename M::Sm) + 15) & ~size_t(15)) + 4 * ((size_t)L + 1);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) + 4 * ((size_t)L + 1);
       auto kern = k2_expand_dense<M, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       b->mark(3);
@@ -1319,7 +1322,7 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
   if (!rc) {
     auto launch = [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = sizeof(typename M::Sm);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
       auto kern = k_rollout_bounds<M>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>((n + 127) / 128, m->num_sms * 8));

@@ -16,7 +16,7 @@ namespace hd {
 // ---------------------------------------------------------------------------
 template <class M>
 __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
-  __shared__ typename M::Sm sm;
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_base;
   const LeafDev& lf = b.leaves[blockIdx.x];
@@ -90,9 +90,9 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
 // no per-lane instructions).
 template <class M, bool RECORD, bool UNI_SEED = false>
 __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, const RoundKeys rk) {
-  extern __shared__ __align__(16) unsigned char k2_smem[];
-  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(k2_smem);
-  uint32_t* tile_off = reinterpret_cast<uint32_t*>(k2_smem + ((sizeof(typename M::Sm) + 15) & ~size_t(15)));
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
+  uint32_t* tile_off =
+      reinterpret_cast<uint32_t*>(hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes));
   M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
   for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
   __syncthreads();
@@ -220,8 +220,7 @@ __global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, con
                                                         uint32_t cap, uint32_t n, uint32_t depth,
                                                         uint32_t k0, uint32_t k1, double inv_wroot,
                                                         float* per_u, float* per_l, int64_t* acc3) {
-  extern __shared__ __align__(16) unsigned char rb_smem[];
-  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(rb_smem);
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   M::load_sm(sm, *dmp, threadIdx.x, blockDim.x);
   __syncthreads();
   const double fx = dmp->fx;

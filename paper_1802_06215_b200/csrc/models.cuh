@@ -100,50 +100,98 @@ struct Tiger {
 // RockSample(n, m) with R in {1, 2} robots (card §3.2).
 // word 0: good-rock mask; word 1: 16 bits per robot (y*n+x, 0xFFFF exited).
 // sub-actions: 0 N, 1 S, 2 E, 3 W, 4 SAMPLE, 5+j SENSE j; a = b0 + base*b1.
+//
+// Device representation: a robot is its cell index; every geometric
+// question of a step (which moves stay on the grid, the rock on a cell, the
+// squared distance to a sensed rock, the policy's move toward its target
+// rock) is a shared-memory table lookup built per CTA from the layout.  This
+// moves the step's work from the ALU pipe (the kernel's limiter) to the
+// load/store pipe.
 // ===========================================================================
 template <int R>
 struct RockSample {
   static constexpr int kMinBlocks = 8;  // 64 registers: 32 warps per SM
+  static constexpr int kMaxTable = 16384;  // n*n*m entries of the per-cell rock tables
   struct Sm {
-    int32_t n, m, base, policy_east;
+    int32_t n, m, base, ncell;
     uint32_t D;
     double tail;
+    int32_t delta[4];        // cell offset of N, S, E, W
     int8_t rx[32], ry[32];
-    uint8_t pos_rock[32];
-    uint32_t range_mask[2];
-    uint32_t rock_xy[32];   // rx | ry << 8                  (one load per sensing)
-    uint32_t pos_tgt[32];   // j | rx << 8 | ry << 16 of policy position p
+    uint8_t pos_rock[32];    // default-policy position -> rock index
+    uint32_t range_mask[2];  // policy positions of robot r (0 for the always-east policy)
     double gpow[kGpowN];
-    int8_t rock_at[kRsMaxN * kRsMaxN];
-    uint32_t thr[kRsMaxD2];
+    // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m):
+    uint32_t off_info;  // u32 [cell]: bits 0-3 N,S,E,W stay on the grid; 8-15 rock (0xFF none); 16-23 x; 24-31 y
+    uint32_t off_dir;   // u8  [cell][j]: policy move toward rock j (4 = on it)
+    uint32_t off_d2;    // u16 [cell][j]: squared distance to rock j
+    uint32_t off_thr;   // u32 [d2]: sensing is correct iff u <= thr[d2]
   };
+  // table bytes (host and device agree): info | d2 | thr | dir
+  static __host__ __device__ size_t table_bytes(int n, int m, uint32_t d2max) {
+    return align16(4 * (size_t)n * n) + align16(2 * (size_t)n * n * m) + align16(4 * ((size_t)d2max + 1)) +
+           align16((size_t)n * n * m);
+  }
+  static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
+    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
+  }
+  static __device__ __forceinline__ uint32_t dir(const Sm& sm, int e) { return hd_dyn_smem[sm.off_dir + e]; }
+  static __device__ __forceinline__ uint32_t d2(const Sm& sm, int e) {
+    return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_d2)[e];
+  }
+  static __device__ __forceinline__ uint32_t thr(const Sm& sm, uint32_t d) {
+    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[d];
+  }
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
+    const int n = dm.n, mm = dm.m, nc = n * n;
+    const uint32_t base = (uint32_t)align16(sizeof(Sm));
+    const uint32_t off_info = base, off_d2 = off_info + (uint32_t)align16(4 * (size_t)nc),
+                   off_thr = off_d2 + (uint32_t)align16(2 * (size_t)nc * mm),
+                   off_dir = off_thr + (uint32_t)align16(4 * ((size_t)dm.d2max + 1));
+    uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
+    uint16_t* t_d2 = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_d2);
+    uint8_t* t_dir = hd_dyn_smem + off_dir;
     if (tid == 0) {
-      sm.n = dm.n;
-      sm.m = dm.m;
+      sm.off_info = off_info;
+      sm.off_dir = off_dir;
+      sm.off_d2 = off_d2;
+      sm.off_thr = off_thr;
+      sm.n = n;
+      sm.m = mm;
       sm.base = dm.base;
-      sm.policy_east = dm.policy_east;
+      sm.ncell = nc;
       sm.D = dm.D;
       sm.tail = dm.tail;
+      sm.delta[0] = -n;
+      sm.delta[1] = n;
+      sm.delta[2] = 1;
+      sm.delta[3] = -1;
       sm.range_mask[0] = dm.range_mask[0];
       sm.range_mask[1] = dm.range_mask[1];
     }
     copy_words(sm.rx, dm.rx, 32, tid, nt);
     copy_words(sm.ry, dm.ry, 32, tid, nt);
     copy_words(sm.pos_rock, dm.pos_rock, 32, tid, nt);
-    for (int j = tid; j < 32; j += nt) {
-      const uint32_t x = (uint8_t)dm.rx[j], y = (uint8_t)dm.ry[j];
-      sm.rock_xy[j] = x | (y << 8);
-      const int jj = dm.pos_rock[j];
-      sm.pos_tgt[j] = (uint32_t)jj | ((uint32_t)(uint8_t)dm.rx[jj] << 8) | ((uint32_t)(uint8_t)dm.ry[jj] << 16);
-    }
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
-    copy_words(sm.rock_at, dm.rock_at, (dm.n * dm.n + 3) & ~3, tid, nt);
-    copy_words(sm.thr, dm.sense_thr_m1, 4 * (dm.d2max + 1), tid, nt);
+    copy_words(hd_dyn_smem + off_thr, dm.sense_thr_m1, 4 * (dm.d2max + 1), tid, nt);
+    for (int c = tid; c < nc; c += nt) {
+      const int x = c % n, y = c / n;
+      const uint32_t rock = (uint32_t)(uint8_t)dm.rock_at[c];  // 0xFF: none
+      t_info[c] = (uint32_t)(y > 0) | ((uint32_t)(y < n - 1) << 1) | ((uint32_t)(x < n - 1) << 2) |
+                  ((uint32_t)(x > 0) << 3) | (rock << 8) | ((uint32_t)x << 16) | ((uint32_t)y << 24);
+    }
+    for (int e = tid; e < nc * mm; e += nt) {
+      const int c = e / mm, j = e - c * mm;
+      const int x = c % n, y = c / n;
+      const int dx = dm.rx[j] - x, dy = dm.ry[j] - y;
+      // E if x < tx, W if x > tx, S if y < ty, N if y > ty, on the rock: SAMPLE
+      t_dir[e] = (uint8_t)((dx == 0 && dy == 0) ? 4 : dx > 0 ? 2 : dx < 0 ? 3 : dy > 0 ? 1 : 0);
+      t_d2[e] = (uint16_t)(dx * dx + dy * dy);
+    }
   }
   struct St {
     uint32_t good;
-    int32_t x[R], y[R];
+    int32_t cell[R];
     bool ex[R];
   };
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
@@ -152,25 +200,19 @@ struct RockSample {
     const uint32_t pos = st[cap + i];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t cell = (pos >> (16 * r)) & 0xFFFFu;
-      s.ex[r] = cell == 0xFFFFu;
-      const uint32_t c = s.ex[r] ? 0u : cell;
-      s.y[r] = (int32_t)(c / (uint32_t)sm.n);
-      s.x[r] = (int32_t)c - s.y[r] * sm.n;
+      const uint32_t c = (pos >> (16 * r)) & 0xFFFFu;
+      s.ex[r] = c == 0xFFFFu;
+      s.cell[r] = s.ex[r] ? 0 : (int32_t)c;
     }
     return s;
   }
-  static __device__ __forceinline__ uint32_t pos_word(const Sm& sm, const St& s) {
-    uint32_t pos = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      pos |= (s.ex[r] ? 0xFFFFu : (uint32_t)(s.y[r] * sm.n + s.x[r])) << (16 * r);
-    return pos;
-  }
   static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
                                                uint32_t i) {
+    uint32_t pos = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) pos |= (s.ex[r] ? 0xFFFFu : (uint32_t)s.cell[r]) << (16 * r);
     st[i] = s.good;
-    st[cap + i] = pos_word(sm, s);
+    st[cap + i] = pos;
   }
   static __device__ __forceinline__ bool terminal(const St& s) {
     bool t = true;
@@ -180,11 +222,11 @@ struct RockSample {
   }
   static constexpr uint32_t kTerminalObs = (R == 1) ? 3u : 9u;
 
-  // one step with per-robot sub-actions b[r] and random words u[r].
-  // Branch-free: every lane evaluates the move, sample and sense effects and
-  // selects, so lanes of a warp taking different sub-actions in a roll-out do
-  // not diverge.  Same results as the card's case analysis.  zr[r] returns
-  // robot r's reading (0 none, 1 GOOD, 2 BAD).
+  // one step with per-robot sub-actions b[r] and random words u[r], robots in
+  // ascending order.  Branch-free: every lane evaluates the move, sample and
+  // sense effects and selects, so roll-out lanes choosing different
+  // sub-actions do not diverge.  zr[r] returns robot r's reading (0 none,
+  // 1 GOOD, 2 BAD).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
                                                   uint32_t& z, float& rew, uint32_t* zrs = nullptr) {
     float reward = 0.0f;
@@ -193,29 +235,28 @@ struct RockSample {
     for (int r = 0; r < R; ++r) {
       const bool act = !s.ex[r];
       const int sub = b[r];
-      const int x = s.x[r], y = s.y[r];
-      // moves: 0 N (y-1), 1 S (y+1), 2 E (x+1), 3 W (x-1); off-grid N/S/W stay
-      const int nx = x + (sub == 2) - (sub == 3);
-      const int ny = y + (sub == 1) - (sub == 0);
-      const bool exits = act && sub == 2 && x == sm.n - 1;  // exit east
-      const bool moves = act && (unsigned)nx < (unsigned)sm.n && (unsigned)ny < (unsigned)sm.n;
+      const int c = s.cell[r];
+      const uint32_t info = RockSample::info(sm, c);
+      // moves 0 N, 1 S, 2 E, 3 W: stay when the target is off the grid, except
+      // E at the east border, which exits (+10)
+      const bool is_move = sub < 4;
+      const bool inside = (info >> (sub & 3)) & 1u;
+      const bool moves = act && is_move && inside;
+      const bool exits = act && sub == 2 && !inside;
       // SAMPLE on the current cell
-      const int jr = sm.rock_at[y * sm.n + x];
-      const uint32_t samp = (act && sub == 4 && jr >= 0) ? 1u : 0u;
-      const uint32_t gbit = samp & (s.good >> (jr & 31));
+      const uint32_t jr = (info >> 8) & 0xFFu;
+      const uint32_t samp = (act && sub == 4 && jr != 0xFFu) ? 1u : 0u;
+      const uint32_t gbit = samp & (s.good >> (jr & 31u));
       // SENSE j (evaluated for every lane; masked)
       const int js = max(sub - 5, 0);
-      const uint32_t xy = sm.rock_xy[js];
-      const int dx = x - (int)(xy & 0xFFu), dy = y - (int)(xy >> 8);
-      const uint32_t incorrect = u[r] > sm.thr[dx * dx + dy * dy] ? 1u : 0u;
+      const uint32_t incorrect = u[r] > thr(sm, d2(sm, c * sm.m + js)) ? 1u : 0u;
       const uint32_t isgood = (s.good >> js) & 1u;
       const uint32_t sense = (act && sub >= 5) ? 1u : 0u;
       const uint32_t zr = sense * (1u + ((isgood ^ incorrect) ^ 1u));  // GOOD iff good == correct
       reward = reward + (exits ? 10.0f : 0.0f);
       reward = reward + (samp ? (gbit ? 10.0f : -10.0f) : 0.0f);
-      s.good &= ~(gbit << (jr & 31));
-      s.x[r] = moves ? nx : x;
-      s.y[r] = moves ? ny : y;
+      s.good &= ~(gbit << (jr & 31u));
+      s.cell[r] = moves ? c + sm.delta[sub & 3] : c;
       s.ex[r] = s.ex[r] || exits;
       if (zrs) zrs[r] = zr;
       zsum += zr * (r == 0 ? 1u : 3u);
@@ -241,43 +282,42 @@ struct RockSample {
   }
   // u(s) = sum_{good j} 10 g^{min_r |r-j|_1} + sum_{r active} 10 g^{n-1-x_r}
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
+    int x[R], y[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t info = RockSample::info(sm, s.cell[r]);
+      x[r] = (int)((info >> 16) & 0xFFu);
+      y[r] = (int)(info >> 24);
+    }
     double u = 0.0;
     for (int j = 0; j < sm.m; ++j) {  // uniform trip count; bad rocks add +0.0
       int dmin = 255;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int d = abs(s.x[r] - sm.rx[j]) + abs(s.y[r] - sm.ry[j]);
+        const int d = abs(x[r] - sm.rx[j]) + abs(y[r] - sm.ry[j]);
         dmin = (!s.ex[r] && d < dmin) ? d : dmin;
       }
       u += ((s.good >> j) & 1u) ? 10.0 * sm.gpow[dmin] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (!s.ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - s.x[r]];
+      if (!s.ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - x[r]];
     return u;
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
 
-  // default policy (card §3.2).  Memory over policy positions p (rocks sorted
-  // by handling robot, then (x, y, j)): done bit = DONE, gm bit = GOOD.
-  // default policy (card §3.2), branch-free.  rmask[r]: policy positions of
-  // robot r (the host zeroes them for the always-east test policy).  Movement toward the target
-  // (E if x<tx, W if x>tx, S if y<ty, N if y>ty, SAMPLE on it) is looked up
-  // in a packed 9-entry table indexed by the signs of (tx-x, ty-y).
+  // default policy (card §3.2), branch-free: memory over policy positions p
+  // (rocks sorted by handling robot, then (x, y, j)); done bit = DONE, gm bit
+  // = GOOD.  The move toward the target is the per-cell table lookup.
   static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
-                                                const uint32_t* rmask, int* b, uint32_t* tbit) {
-    constexpr uint32_t kMovePack = 3u | 3u << 3 | 3u << 6 | 0u << 9 | 4u << 12 | 1u << 15 | 2u << 18 |
-                                   2u << 21 | 2u << 24;
+                                                int* b, uint32_t* tbit) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t open = ~done & rmask[r];
+      const uint32_t open = ~done & sm.range_mask[r];
       const bool has = open != 0u && !s.ex[r];
       const int p = __ffs(open | 0x80000000u) - 1;  // 31 when nothing is open
-      const uint32_t tg = sm.pos_tgt[p];
-      const int j = (int)(tg & 0xFFu);
-      const int ddx = (int)((tg >> 8) & 0xFFu) - s.x[r], ddy = (int)(tg >> 16) - s.y[r];
-      const int code = 3 * ((ddx > 0) - (ddx < 0) + 1) + ((ddy > 0) - (ddy < 0) + 1);
-      const int mv = (int)((kMovePack >> (3 * code)) & 7u);
+      const int j = sm.pos_rock[p];
+      const int mv = (int)dir(sm, s.cell[r] * sm.m + j);
       const bool known_good = (gm >> p) & 1u;
       b[r] = !has ? 2 : known_good ? mv : 5 + j;
       tbit[r] = has ? (1u << p) : 0u;
@@ -293,7 +333,7 @@ struct RockSample {
     while (t < sm.D && !term) {
       int b[R];
       uint32_t tb[R];
-      policy(sm, s, done, gm, sm.range_mask, b, tb);
+      policy(sm, s, done, gm, b, tb);
       if (TRACE) {
         int a = 0, mul = 1;
 #pragma unroll
