@@ -141,7 +141,7 @@ def test_parallel_search_bounds_and_counts(case):
     om, root, be, res, nodes = run(kind, params, st, w, 11, cfg)
     check_invariants(nodes)
     v = om.brute_force(root)
-    tol = 1e-4
+    tol = 1e-5 * max(1.0, abs(v))  # the backend's outputs are fp32 (R12)
     assert res["root_lower"] <= v + tol and v <= res["root_upper"] + tol, (res, v)
     assert res["batches"] == be.calls and res["expanded"] == be.leaves_seen
     assert res["trials"] == 600
