@@ -36,9 +36,9 @@ from paper_1802_06215_b200 import inputs  # noqa: E402
 # work of one step as implemented), from the ncu profile of round 1, see
 # DESIGN.md §7.  Used for the ALU roofline: achieved = I_step * steps / t_K2.
 # per config (ncu smsp__thread_inst_executed.sum / scenario-steps, round 1):
-# config 2/5 MARS 303, config 3 navigation 303, config 4 driving (thread per
-# scenario) 2054; config 1 RockSample(7,8) 184.
-I_STEP = {1: 184.0, 2: 303.0, 3: 303.0, 4: 2054.0, 5: 303.0}
+# config 2/5 MARS 241, config 3 navigation 303, config 4 driving (thread per
+# scenario) 2054; config 1 RockSample(7,8) 177.
+I_STEP = {1: 177.0, 2: 241.0, 3: 303.0, 4: 2054.0, 5: 241.0}
 
 
 def load_peaks():
@@ -102,9 +102,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
-def workload(cfg, K=None):
-    c = inputs.CONFIGS[cfg]
-    kind, params, st, w, seed, L = inputs.config_inputs(cfg, K=K)
+def workload(cfg, K=None, peds=None):
+    c = dict(inputs.CONFIGS[cfg])
+    kind, params, st, w, seed, L = inputs.config_inputs(cfg, K=K, peds=peds)
+    if peds is not None and kind == "car":
+        c["name"] = f"car_{peds}peds_K{len(w)}_L{L}"
+        c["peds"] = peds
     return c, kind, params, st, w, seed, L
 
 
@@ -115,14 +118,14 @@ def make_leaves(model, root, L, cfg_kind, extra_roots=None):
     return [(root, a, c, 1) for a, c in lv]
 
 
-def cpu_baseline(kind, params, st, w, seed, leaves_ac, budget_s=12.0, L=64):
+def cpu_baseline(kind, params, st, w, seed, leaves_ac, budget_s=12.0, L=64, peds=20):
     """The oracle as it stands (single thread) on a bounded sample of the
     same workload: leaves expanded one at a time until ~budget_s of work."""
     import oracle
 
     om = oracle.Model(kind, params)
     if kind == "car":
-        croots = inputs.car_roots(L, int(len(w)))
+        croots = inputs.car_roots(L, int(len(w)), peds=peds)
         items = [("root", j) for j in range(L)]
     else:
         root = om.belief_load(st, w, seed)
@@ -144,6 +147,51 @@ def cpu_baseline(kind, params, st, w, seed, leaves_ac, budget_s=12.0, L=64):
     dt = time.perf_counter() - t0
     return {"value": steps / dt, "unit": "scenario-steps/s", "cores": 1, "kind": "oracle",
             "sample": f"{n} of {len(items)} leaves (all |A| actions each), {steps} scenario-steps in {dt:.1f} s"}
+
+
+def _oracle_share(job):
+    """one process of the all-cores oracle baseline: expand its share of the
+    leaves (every nproc-th) until the budget is spent"""
+    kind, params, st, w, seed, leaves_ac, budget_s, L, peds, rank, nproc = job
+    import oracle
+
+    om = oracle.Model(kind, params)
+    if kind == "car":
+        croots = inputs.car_roots(L, int(len(w)), peds=peds)
+        items = [("root", j) for j in range(L)][rank::nproc]
+    else:
+        root = om.belief_load(st, w, seed)
+        om.expand([(root, -1, 0, 0)])
+        items = leaves_ac[rank::nproc]
+    steps, n = 0, 0
+    t0 = time.perf_counter()
+    while True:
+        for (a, c) in items:
+            if kind == "car":
+                o = om.expand([(om.belief_load(*croots[c]), -1, 0, 0)])
+            else:
+                o = om.expand([(root, a, c, 1)])
+            steps += o["scenario_steps"]
+            n += 1
+            if time.perf_counter() - t0 > budget_s:
+                return steps, time.perf_counter() - t0, n
+        if not items:
+            return 0, time.perf_counter() - t0, 0
+
+
+def cpu_baseline_all_cores(kind, params, st, w, seed, leaves_ac, budget_s=8.0, L=64, peds=20):
+    """The same oracle in one process per host core (independent leaves)."""
+    import multiprocessing as mp
+
+    nproc = len(os.sched_getaffinity(0))
+    jobs = [(kind, params, st, w, seed, leaves_ac, budget_s, L, peds, r, nproc) for r in range(nproc)]
+    with mp.get_context("fork").Pool(nproc) as pool:
+        res = pool.map(_oracle_share, jobs)
+    steps = sum(r[0] for r in res)
+    secs = max(r[1] for r in res)
+    return {"value": steps / secs, "unit": "scenario-steps/s", "cores": nproc, "kind": "oracle",
+            "sample": f"{sum(r[2] for r in res)} leaf expansions in {nproc} processes, {steps} scenario-steps, "
+                      f"{secs:.1f} s"}
 
 
 def run_reference(args):
@@ -198,6 +246,10 @@ def main():
     ap.add_argument("--ref-leaves", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--all-cores-baseline", action="store_true", default=True,
+                    help="also time the oracle in one process per host core")
+    ap.add_argument("--no-all-cores-baseline", dest="all_cores_baseline", action="store_false")
+    ap.add_argument("--peds", type=int, default=None, help="pedestrians of the driving config (NEXT-3 study)")
     ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread"],
                     help="driving kernel: factored warp per scenario, thread per scenario, or per-batch choice")
     args = ap.parse_args()
@@ -219,7 +271,7 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    c, kind, params, st, w, seed, L = workload(args.config, args.K)
+    c, kind, params, st, w, seed, L = workload(args.config, args.K, args.peds)
     mflags = {"auto": 0, "thread": 1, "warp": 2}[args.car_variant]
     model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags)
     stream = torch.cuda.current_stream(dev)
@@ -227,7 +279,7 @@ def main():
         # config 4: L concurrent roots (inputs.car_roots)
         if world > 1:
             raise SystemExit("config 4 (sparse keys) runs on one GPU")
-        croots = inputs.car_roots(L, int(len(w)))
+        croots = inputs.car_roots(L, int(len(w)), peds=c.get("peds", 20))
         leaves = [(model.belief_load(s_, w_, sd_), -1, 0, 0) for s_, w_, sd_ in croots]
         lv_ac = None
     else:
@@ -359,7 +411,11 @@ def main():
             "clocks": clocks,
         }
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(kind, params, st, w, seed, lv_ac, args.cpu_budget, L)
+            line["cpu_baseline"] = cpu_baseline(kind, params, st, w, seed, lv_ac, args.cpu_budget, L,
+                                                c.get("peds", 20))
+            if args.all_cores_baseline:
+                line["cpu_baseline_all_cores"] = cpu_baseline_all_cores(kind, params, st, w, seed, lv_ac,
+                                                                        args.cpu_budget * 0.7, L, c.get("peds", 20))
         print(json.dumps(line))
     model.close()
     if world > 1:

@@ -140,21 +140,13 @@ struct CarThreadT {
   template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
                                               const KeyT& key, float& r) {
+    // random words are drawn one Philox block at a time (block k = words
+    // 4k..4k+3: the car's word 0, then pedestrian p's word 1+p), so only four
+    // are live at once; the element order (car, then pedestrians ascending)
+    // is the card's
     constexpr int NB = (MAXP + 1 + 3) / 4;
-    uint32_t u[4 * NB];
-#pragma unroll
-    for (int bk = 0; bk < NB; ++bk) {
-      if (4 * bk < sm.peds + 1) {
-        const uint4 w = philox(id, t, (uint32_t)bk, 0u, key);
-        u[4 * bk] = w.x;
-        u[4 * bk + 1] = w.y;
-        u[4 * bk + 2] = w.z;
-        u[4 * bk + 3] = w.w;
-      } else {
-        u[4 * bk] = u[4 * bk + 1] = u[4 * bk + 2] = u[4 * bk + 3] = 0u;
-      }
-    }
-    if (!event(u[0], sm.t_fail)) {  // Accelerate / Decelerate fail w.p. 0.01
+    const uint4 w0 = philox(id, t, 0u, 0u, key);
+    if (!event(w0.x, sm.t_fail)) {  // Accelerate / Decelerate fail w.p. 0.01
       if (a == 1 && s.level < 4u) s.level += 1u;
       if (a == 2 && s.level > 0u) s.level -= 1u;
     }
@@ -162,12 +154,19 @@ struct CarThreadT {
     s.xc = s.xc + v * 0.25f;
     bool coll = false;
 #pragma unroll
-    for (int p = 0; p < MAXP; ++p) {
-      if (p < sm.peds) {
-        const float2 cs = sm.rot[car_noise_index(u[1 + p])];
-        car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
-        const float dx = s.px[p] - s.xc;
-        coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
+    for (int bk = 0; bk < NB; ++bk) {
+      if (4 * bk >= sm.peds + 1) break;  // uniform
+      const uint4 w = bk == 0 ? w0 : philox(id, t, (uint32_t)bk, 0u, key);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int p = 4 * bk + q - 1;  // word 4bk+q belongs to pedestrian 4bk+q-1
+        if (p >= 0 && p < MAXP && p < sm.peds) {
+          const float2 cs = sm.rot[car_noise_index(ws[q])];
+          car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
+          const float dx = s.px[p] - s.xc;
+          coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
+        }
       }
     }
     const bool g = s.xc >= 20.0f;

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdespot.so")
+LIB_PATH = os.environ.get("DESPOT_LIB", os.path.join(HERE, "libdespot.so"))  # override: A/B builds
 
 DESPOT_X_DEVICE_OUTPUTS = 1
 DESPOT_X_RECORD_SCENARIO = 2

@@ -196,9 +196,12 @@ def car_roots(L, K, peds=20, base_seed=1004):
     return out
 
 
-def config_inputs(cfg: int, K=None, L=None, uniform=True, D=None):
-    """(kind, params, states_soa, weights, seed, L) of a BASELINE config."""
+def config_inputs(cfg: int, K=None, L=None, uniform=True, D=None, peds=None):
+    """(kind, params, states_soa, weights, seed, L) of a BASELINE config
+    (peds: pedestrian count of the driving config, default 20)."""
     c = dict(CONFIGS[cfg])
+    if peds is not None and c["kind"] == "car":
+        c["peds"] = peds
     K = c["K"] if K is None else K
     L = c["L"] if L is None else L
     D = c["D"] if D is None else D

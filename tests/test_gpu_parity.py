@@ -241,7 +241,7 @@ def test_fake_ranks_equal_single_gpu():
     R = g1.expand([(r1, -1, 0, 0)])
     lv = inputs.select_leaves(R["child_count"], R["child_begin"], g1.A, L)
     ref = g1.expand([(r1, a, c, 1) for a, c in lv])
-    for world in (2, 3):
+    for world in (2, 3, 4, 8):
         ms = [Model(kind, params, rank=r, world=world) for r in range(world)]
         roots = [m.belief_load(st, w, seed) for m in ms]
 
@@ -391,3 +391,14 @@ def test_sharded_model_rejects_record_and_sparse():
         m.expand_begin([(r, -1, 0, 0)], record=True)
     with pytest.raises(DespotError):
         Model("car", inputs.car_params(), rank=0, world=2)
+
+
+def test_gpu_scenario_prefix_is_stable_across_K():
+    kind, params, st, w, seed, _ = inputs.config_inputs(2, K=80, D=12)
+    gm = Model(kind, params)
+    big = gm.expand([(gm.belief_load(st, inputs.weights(80), seed), -1, 0, 0)], record=True)
+    small = gm.expand([(gm.belief_load(st[:, :50], inputs.weights(50), seed), -1, 0, 0)], record=True)
+    for a in range(0, gm.A, 13):
+        sb, ss = slice(a * 80, a * 80 + 50), slice(a * 50, a * 50 + 50)
+        for k in ("scen_obs", "scen_reward", "scen_len", "scen_hash", "scen_states", "scen_upper", "scen_lower"):
+            assert np.array_equal(big[k][sb], small[k][ss]), k

@@ -494,3 +494,18 @@ def test_car_failed_accelerate_keeps_speed_and_goals_unobserved():
     for i in range(20):
         bx, by = int(np.floor(2 * f[i, 0])), int(np.floor(2 * f[i, 1]))
         assert z[1 + i] == ((bx & 0xFFFF) | ((by & 0xFFFF) << 16))
+
+
+def test_scenario_prefix_is_stable_across_K():
+    """ids are global and the streams are keyed by (id, depth):
+    the first K scenarios of a larger belief reproduce every per-scenario
+    outcome of the K-scenario belief"""
+    for cfg, D in ((2, 12), (3, 30)):
+        kind, params, st, w, seed, _ = inputs.config_inputs(cfg, K=80, D=D)
+        m = oracle.Model(kind, params)
+        big = m.expand([(m.belief_load(st, inputs.weights(80), seed), -1, 0, 0)], record=True)
+        small = m.expand([(m.belief_load(st[:, :50], inputs.weights(50), seed), -1, 0, 0)], record=True)
+        for a in range(0, m.A, max(1, m.A // 7)):
+            sb, ss = slice(a * 80, a * 80 + 50), slice(a * 50, a * 50 + 50)
+            for k in ("scen_obs", "scen_reward", "scen_len", "scen_hash", "scen_states", "scen_upper", "scen_lower"):
+                np.testing.assert_array_equal(big[k][sb], small[k][ss])
