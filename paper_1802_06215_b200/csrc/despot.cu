@@ -731,8 +731,12 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   b->mark(3);
   // factored (warp per item) when the items cannot fill the SMs one thread
   // each; otherwise thread per item (fewer issue slots per scenario-step)
+  // (measured, profiles/r01/peds_sweep.jsonl: the warp kernel wins for >= 12
+  // pedestrians at 12k items, the thread kernel everywhere at 96k items and
+  // for 6 pedestrians, whose warps would leave 25 of 32 lanes idle)
   const bool unfactored = (m->flags & DESPOT_MF_UNFACTORED) ||
-                          (!(m->flags & DESPOT_MF_FACTORED) && q_bound >= (uint64_t)m->num_sms * 256);
+                          (!(m->flags & DESPOT_MF_FACTORED) &&
+                           (q_bound >= (uint64_t)m->num_sms * 256 || dm.peds < 8));
   if (unfactored) {
     dispatch_car(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);

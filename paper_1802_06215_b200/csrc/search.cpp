@@ -40,25 +40,38 @@ extern "C" int despot__set_error(int code, const char* msg);
 namespace {
 
 struct TNode;
-struct TBranch {
-  double reward = 0.0, upper = 0.0, lower = 0.0;  // r(b,a), u(b,a), l(b,a)
-  uint32_t visits = 0;                            // N(b,a)
-  std::vector<TNode*> children;
-};
 
-struct TNode {
-  TNode* parent = nullptr;
-  int32_t action_in = -1;
-  uint32_t child_in = 0;
-  uint32_t depth = 0, n_scen = 0;
-  double weight = 0.0;
+// A belief node's bounds and counts (every node, expanded or not, is one of
+// these; the root's lives in Search).  Children of an expanded node are a
+// contiguous array of records; a full TNode exists only once a trial
+// descends into the child.
+struct TChild {
+  float weight = 0.0f;  // W_b'
+  uint32_t n_scen = 0;  // |Phi_b'|
   double u0 = 0.0, l0 = 0.0;
   std::atomic<double> upper{0.0}, lower{0.0};
   std::atomic<int> active{0};  // threads inside this branch (virtual loss)
-  uint32_t visits = 0;         // N(b), under mu
-  despot_node handle = 0;      // backend arena once expanded
+  std::atomic<TNode*> node{nullptr};
+};
+
+struct TBranch {
+  double reward = 0.0, upper = 0.0, lower = 0.0;  // r(b,a), u(b,a), l(b,a)
+  uint32_t visits = 0;                            // N(b,a)
+  uint32_t first = 0, count = 0;                  // children: rec[first, first + count)
+};
+
+struct TNode {
+  TChild* rec = nullptr;  // this node's bounds
+  TNode* parent = nullptr;
+  int32_t action_in = -1;
+  uint32_t child_in = 0;
+  uint32_t depth = 0;
+  uint32_t visits = 0;     // N(b), under mu
+  despot_node handle = 0;  // backend arena once expanded
   enum State { kLeaf, kPending, kExpanded } state = kLeaf;  // under mu
   std::vector<TBranch> branches;                            // [A] once expanded, under mu
+  std::unique_ptr<TChild[]> children;                       // all children, action-major
+  uint32_t n_children = 0;
   std::mutex mu;
 };
 
@@ -71,11 +84,12 @@ struct Pending {
 struct Search {
   const despot_search_problem& P;
   const despot_search_config& C;
-  std::deque<TNode> nodes;  // stable addresses; appended by the batcher only
+  std::deque<TNode> nodes;  // full nodes (descended into); stable addresses
   std::mutex nodes_mu;
+  TChild root_rec;
   TNode* root = nullptr;
   std::atomic<bool> stop{false};
-  std::atomic<uint64_t> trials{0}, batches{0}, expanded{0}, steps{0};
+  std::atomic<uint64_t> trials{0}, batches{0}, expanded{0}, steps{0}, records{1};
   std::atomic<uint32_t> max_depth{0};
   std::mutex qmu;
   std::condition_variable qcv;  // batcher wake-up
@@ -94,36 +108,38 @@ struct Search {
     nodes.emplace_back();
     return &nodes.back();
   }
-  double root_gap() const { return root->upper.load() - root->lower.load(); }
+  double root_gap() const { return root_rec.upper.load() - root_rec.lower.load(); }
 
   // Eq. 4 one level: recompute node b's branch values and bounds from its
   // children (clamped by the initial bounds)
   void backup_node(TNode* b) {
     std::lock_guard<std::mutex> g(b->mu);
     if (b->state != TNode::kExpanded) return;
+    const double W = b->rec->weight;
     double bu = -std::numeric_limits<double>::infinity(), bl = bu;
     for (TBranch& br : b->branches) {
-      double su = 0.0, sl = 0.0;
-      for (TNode* c : br.children) {
-        const double f = c->weight / b->weight;
-        su += f * c->upper.load(std::memory_order_relaxed);
-        sl += f * c->lower.load(std::memory_order_relaxed);
-      }
-      if (!br.children.empty()) {
+      if (br.count) {
+        double su = 0.0, sl = 0.0;
+        for (uint32_t k = br.first; k < br.first + br.count; ++k) {
+          const TChild& c = b->children[k];
+          const double f = c.weight / W;
+          su += f * c.upper.load(std::memory_order_relaxed);
+          sl += f * c.lower.load(std::memory_order_relaxed);
+        }
         br.upper = br.reward + P.gamma * su;
         br.lower = br.reward + P.gamma * sl;
       }
       bu = std::max(bu, br.upper);
       bl = std::max(bl, br.lower);
     }
-    b->upper.store(std::min(b->u0, bu));
-    b->lower.store(std::max(b->l0, bl));
+    b->rec->upper.store(std::min(b->rec->u0, bu));
+    b->rec->lower.store(std::max(b->rec->l0, bl));
   }
   void backup(const std::vector<TNode*>& path) {
     for (auto it = path.rbegin(); it != path.rend(); ++it) backup_node(*it);
   }
   static void release_markers(const std::vector<TNode*>& path) {
-    for (size_t i = 1; i < path.size(); ++i) path[i]->active.fetch_sub(1);
+    for (size_t i = 1; i < path.size(); ++i) path[i]->rec->active.fetch_sub(1);
   }
 
   // ---------------------------------------------------------------- batcher
@@ -135,7 +151,7 @@ struct Search {
       TNode* b = batch[i].leaf;
       if (b == root) leaves[i] = despot_leaf{P.root, -1, 0, P.root_depth, 0};
       else leaves[i] = despot_leaf{b->parent->handle, b->action_in, b->child_in, b->depth, 0};
-      const uint32_t n = b->n_scen ? b->n_scen : 1;
+      const uint32_t n = b->rec->n_scen ? b->rec->n_scen : 1;
       cap += (uint64_t)A * (P.obs_slots ? std::min(n, P.obs_slots) : n);
     }
     if (cap > 0xFFFFFFFFull) return DESPOT_ECAPACITY;
@@ -166,35 +182,38 @@ struct Search {
     steps.fetch_add(out.scenario_steps);
     for (uint32_t i = 0; i < L; ++i) {
       TNode* b = batch[i].leaf;
+      const uint32_t c0 = child_begin[(size_t)i * A], c1 = child_begin[(size_t)i * A + A];
+      std::unique_ptr<TChild[]> ch(new TChild[c1 - c0]);
       std::vector<TBranch> br(A);
+      const bool at_horizon = b->depth + 1 >= P.max_depth;
       for (uint32_t a = 0; a < A; ++a) {
         const size_t la = (size_t)i * A + a;
         br[a].reward = ar[la];
         br[a].upper = au[la];
         br[a].lower = al[la];
-        for (uint32_t c = child_begin[la]; c < child_begin[la + 1]; ++c) {
-          TNode* ch = new_node();
-          ch->parent = b;
-          ch->action_in = (int32_t)a;
-          ch->child_in = c - child_begin[la];
-          ch->depth = b->depth + 1;
-          ch->n_scen = child_count[c];
-          ch->weight = cw[c];
-          ch->u0 = cu[c];
-          ch->l0 = cl[c];
-          // at depth D the value is exactly the tail-based l0: gap 0
-          if (ch->depth >= P.max_depth) ch->u0 = ch->l0;
-          ch->upper.store(ch->u0);
-          ch->lower.store(ch->l0);
-          br[a].children.push_back(ch);
-        }
+        br[a].first = child_begin[la] - c0;
+        br[a].count = child_begin[la + 1] - child_begin[la];
       }
+      for (uint32_t c = c0; c < c1; ++c) {
+        TChild& r = ch[c - c0];
+        r.weight = cw[c];
+        r.n_scen = child_count[c];
+        r.u0 = cu[c];
+        r.l0 = cl[c];
+        // at depth D the value is exactly the tail-based l0: gap 0
+        if (at_horizon) r.u0 = r.l0;
+        r.upper.store(r.u0, std::memory_order_relaxed);
+        r.lower.store(r.l0, std::memory_order_relaxed);
+      }
+      records.fetch_add(c1 - c0);
       {
         std::lock_guard<std::mutex> g(b->mu);
         b->handle = hnode[i];
-        if (b->n_scen == 0) b->n_scen = n_scen[i];
-        if (b->weight == 0.0) b->weight = weight[i];
+        if (b->rec->n_scen == 0) b->rec->n_scen = n_scen[i];
+        if (b->rec->weight == 0.0f) b->rec->weight = weight[i];
         b->branches = std::move(br);
+        b->children = std::move(ch);
+        b->n_children = c1 - c0;
         b->state = TNode::kExpanded;
       }
       expanded.fetch_add(1);
@@ -252,7 +271,7 @@ struct Search {
   // ---------------------------------------------------------------- workers
   // Eq. 7: u(b,a) + c_a sqrt(log(|Phi_b| N(b)) / (|Phi_b| N(b,a)))
   uint32_t choose_action(TNode* b) const {
-    const double phi = (double)std::max<uint32_t>(1, b->n_scen);
+    const double phi = (double)std::max<uint32_t>(1, b->rec->n_scen);
     const double nb = phi * (double)b->visits;
     uint32_t best = 0;
     double bv = -std::numeric_limits<double>::infinity();
@@ -306,22 +325,35 @@ struct Search {
         TBranch& br = b->branches[a];
         br.visits += 1;
         const double gap0 = root_gap();
-        TNode* next = nullptr;
+        TChild* next = nullptr;
+        uint32_t next_k = 0;
         double best = 0.0;  // the trial ends unless some WEU > 0
-        for (TNode* c : br.children) {
-          const double gap = c->upper.load(std::memory_order_relaxed) - c->lower.load(std::memory_order_relaxed);
-          const double weu = gap - (c->weight / root->weight) * C.xi * gap0;       // Eq. 6
-          const double aug = weu - (double)c->active.load() * C.c_o * gap0;        // Eq. 8
+        for (uint32_t k = br.first; k < br.first + br.count; ++k) {
+          TChild& c = b->children[k];
+          const double gap = c.upper.load(std::memory_order_relaxed) - c.lower.load(std::memory_order_relaxed);
+          const double weu = gap - ((double)c.weight / root_rec.weight) * C.xi * gap0;  // Eq. 6
+          const double aug = weu - (double)c.active.load() * C.c_o * gap0;              // Eq. 8
           if (aug > best) {
             best = aug;
-            next = c;
+            next = &c;
+            next_k = k;
           }
         }
-        lk.unlock();
         if (!next) break;
+        TNode* nd = next->node.load();
+        if (!nd) {  // first descent into this child: give it a full node
+          nd = new_node();
+          nd->rec = next;
+          nd->parent = b;
+          nd->action_in = (int32_t)a;
+          nd->child_in = next_k - br.first;
+          nd->depth = b->depth + 1;
+          next->node.store(nd);
+        }
+        lk.unlock();
         next->active.fetch_add(1);
-        path.push_back(next);
-        b = next;
+        path.push_back(nd);
+        b = nd;
       }
       if (leaf) {
         inflight.fetch_add(1);
@@ -342,31 +374,46 @@ struct Search {
     dcv.wait(lk, [&] { return inflight.load() == 0; });
   }
 
+  // pre-order dump: every belief node (a child record with or without a full node)
   void dump_tree(despot_search_node* out, uint32_t cap, uint32_t& n) const {
-    std::vector<std::pair<const TNode*, int32_t>> stack{{root, -1}};
+    struct Item {
+      const TChild* rec;
+      const TNode* node;
+      int32_t parent, action;
+      uint32_t child, depth;
+    };
+    std::vector<Item> stack{{&root_rec, root, -1, -1, 0, root->depth}};
     while (!stack.empty() && n < cap) {
-      auto [b, parent] = stack.back();
+      const Item it = stack.back();
       stack.pop_back();
       despot_search_node& d = out[n];
-      d.parent = parent;
-      d.action = b->action_in;
-      d.child = b->child_in;
-      d.depth = b->depth;
-      d.n_scen = b->n_scen;
-      d.visits = b->visits;
-      uint32_t bv = 0;
-      for (const TBranch& br : b->branches) bv += br.visits;
-      d.branch_visits = bv;
-      d.active = b->active.load();
-      d.expanded = b->state == TNode::kExpanded;
-      d.weight = (float)b->weight;
-      d.upper = (float)b->upper.load();
-      d.lower = (float)b->lower.load();
-      d.upper0 = (float)b->u0;
-      d.lower0 = (float)b->l0;
+      memset(&d, 0, sizeof d);
+      d.parent = it.parent;
+      d.action = it.action;
+      d.child = it.child;
+      d.depth = it.depth;
+      d.n_scen = it.rec->n_scen;
+      d.active = it.rec->active.load();
+      d.weight = it.rec->weight;
+      d.upper = (float)it.rec->upper.load();
+      d.lower = (float)it.rec->lower.load();
+      d.upper0 = (float)it.rec->u0;
+      d.lower0 = (float)it.rec->l0;
+      const TNode* b = it.node;
+      if (b) {
+        d.visits = b->visits;
+        for (const TBranch& br : b->branches) d.branch_visits += br.visits;
+        d.expanded = b->state == TNode::kExpanded;
+      }
       const int32_t me = (int32_t)n++;
-      for (auto it = b->branches.rbegin(); it != b->branches.rend(); ++it)
-        for (auto c = it->children.rbegin(); c != it->children.rend(); ++c) stack.push_back({*c, me});
+      if (b && b->state == TNode::kExpanded)
+        for (int a = (int)b->branches.size() - 1; a >= 0; --a) {
+          const TBranch& br = b->branches[a];
+          for (int k = (int)br.count - 1; k >= 0; --k) {
+            const TChild* c = &b->children[br.first + k];
+            stack.push_back({c, c->node.load(), me, a, (uint32_t)k, it.depth + 1});
+          }
+        }
     }
   }
 };
@@ -383,13 +430,14 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
   Search S(*P, *C);
   S.root = S.new_node();
   TNode* root = S.root;
+  root->rec = &S.root_rec;
   root->depth = P->root_depth;
-  root->n_scen = P->root_scenarios;
-  root->weight = P->root_weight;
-  root->u0 = P->root_upper;
-  root->l0 = P->root_lower;
-  root->upper.store(P->root_upper);
-  root->lower.store(P->root_lower);
+  S.root_rec.n_scen = P->root_scenarios;
+  S.root_rec.weight = (float)P->root_weight;
+  S.root_rec.u0 = P->root_upper;
+  S.root_rec.l0 = P->root_lower;
+  S.root_rec.upper.store(P->root_upper);
+  S.root_rec.lower.store(P->root_lower);
   root->handle = P->root;
   // the root is expanded before any trial (and gives |Phi_b0| and W_b0)
   {
@@ -432,9 +480,9 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
       best = root->branches[a].lower;
       R->action = (int32_t)a;
     }
-  R->root_upper = (float)root->upper.load();
-  R->root_lower = (float)root->lower.load();
-  R->nodes = S.nodes.size();
+  R->root_upper = (float)S.root_rec.upper.load();
+  R->root_lower = (float)S.root_rec.lower.load();
+  R->nodes = S.records.load();
   R->expanded = S.expanded.load();
   R->trials = std::min<uint64_t>(S.trials.load(), C->max_trials ? C->max_trials : S.trials.load());
   R->batches = S.batches.load();
