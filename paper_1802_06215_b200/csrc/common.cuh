@@ -161,7 +161,8 @@ struct BatchDev {
   int32_t* mins;             // exchange MIN block
   uint32_t* rank;            // [L*A*S] child ordinal of a slot
   uint32_t* nc;              // [L*A] children per (leaf, action)
-  uint32_t* status;          // [err, total children, steps lo, steps hi, n_leaf[L]]
+  uint32_t* status;          // [err, total children, steps lo, steps hi, K1 ticket, K2 ticket, n_leaf[L]]
+  uint32_t fused_k3;         // 1: K2's last CTA runs the small finalize
   uint32_t* err;
   // outputs (device)
   uint32_t* n_scen;

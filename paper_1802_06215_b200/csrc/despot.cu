@@ -182,6 +182,11 @@ struct despot_batch {
   BatchDev bd{};
   SparseItemOut io{};
   void* pinned = nullptr;  // leaf-table staging, owned until the batch syncs
+  void* stage = nullptr;   // device output staging (host outputs)
+  bool bound = false;      // outputs bound (bind_outputs)
+  bool k3_fused = false;   // the finalize runs in K2's last CTA
+  size_t o_ns = 0, o_w = 0, o_ar = 0, o_au = 0, o_al = 0, o_cb = 0, o_cc = 0, o_cf = 0, o_cw = 0, o_cu = 0,
+         o_cl = 0, o_co = 0, o_so = 0;  // staging layout
   bool sparse = false;
   uint64_t n_sums = 0, n_mins = 0;
   bool timing = false;
@@ -715,6 +720,7 @@ static void free_batch(despot_batch* b, bool drop_new_nodes) {
       }
   }
   if (b->scratch) cudaFreeAsync(b->scratch, b->stream);
+  if (b->stage) cudaFreeAsync(b->stage, b->stream);
   if (b->pinned) {
     cudaStreamSynchronize(b->stream);  // the H2D from it must have completed
     pinned_pool().release(b->pinned);
@@ -755,8 +761,10 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   return check_launch(m, "K2(car)");
 }
 
-extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags,
-                                   void* stream, despot_batch** out) {
+static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st);
+
+static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags, void* stream,
+                      despot_expansion* bind, despot_batch** out) {
   if (!m || !leaves || !out) return set_err(DESPOT_EINVAL, "null argument");
   if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
   if (L == 0 || L > kMaxLeaves) return set_err(DESPOT_EINVAL, "need 1 <= L <= %u", kMaxLeaves);
@@ -978,11 +986,27 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
       return check_launch(m, "K1");
     });
   }
+  // single-call batches bind their outputs now: a small dense batch then runs
+  // its finalize in K2's last CTA (no K3 launches)
+  if (!rc && bind) {
+    despot_batch* raw = b.release();
+    if ((rc = bind_outputs(raw, bind, st))) return rc;  // the batch is freed
+    b.reset(raw);
+    const uint64_t LAd = (uint64_t)L * dm.A;
+    // fused only when K2's 4 warps finish it in ~2 sweeps (else the 32-warp
+    // k3_small_dense is faster than the launch it saves)
+    const uint64_t G = 32 / small_group_width(b->S);
+    b->k3_fused = !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO) && m->world == 1 && b->S <= 32 &&
+                  LAd <= 4 * G * kSmallUnroll * 2;
+    b->bd.fused_k3 = b->k3_fused ? 1u : 0u;
+  }
   if (!rc && !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO)) {
     // K2 now (the exchange block is complete after it)
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) + 4 * ((size_t)L + 1);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
+                          align16(4 * ((size_t)L + 1)) +
+                          (b->k3_fused ? small_finalize_smem((uint64_t)L * dm.A) : 0);
       bool uni = true;
       for (uint32_t l = 1; l < L; ++l) uni = uni && ld[l].seed_lo == ld[0].seed_lo && ld[l].seed_hi == ld[0].seed_hi;
       auto kern = uni ? k2_expand_dense<M, false, true> : k2_expand_dense<M, false, false>;
@@ -1008,6 +1032,11 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   return DESPOT_OK;
 }
 
+extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags,
+                                   void* stream, despot_batch** out) {
+  return begin_impl(m, leaves, L, flags, stream, nullptr, out);
+}
+
 extern "C" int despot_batch_exchange(despot_batch* b, despot_exchange* out) {
   if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
   out->sums = b->bd.sums;
@@ -1024,12 +1053,11 @@ extern "C" int despot_batch_abort(despot_batch* b) {
   return DESPOT_OK;
 }
 
-extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* stream) {
-  if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
+// Binds the caller's outputs (or a device staging block for host outputs) to
+// the batch.  On error the batch is freed.
+static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st) {
   despot_model* m = b->model;
   const DevModel& dm = m->host;
-  CU(cudaSetDevice(m->device));
-  cudaStream_t st = (cudaStream_t)stream;
   b->stream = st;
   const uint32_t L = b->L;
   const uint64_t LA = (uint64_t)L * dm.A;
@@ -1051,7 +1079,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     return set_err(DESPOT_EINVAL, "RECORD_SCENARIO needs the scen_* arrays");
   }
   // output staging (host-output mode) in one allocation
-  void* stage = nullptr;
+  void*& stage = b->stage;
   size_t so = 0;
   auto take = [&](size_t bytes) {
     size_t o = so;
@@ -1059,14 +1087,18 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     return o;
   };
   const uint64_t S = bd.scen_capacity;
-  const size_t o_ns = take(4 * L), o_w = take(4 * L), o_ar = take(4 * LA), o_au = take(4 * LA),
-               o_al = take(4 * LA), o_cb = take(4 * (LA + 1)), o_cc = take(4 * (size_t)C),
-               o_cf = take(4 * (size_t)C), o_cw = take(4 * (size_t)C), o_cu = take(4 * (size_t)C),
-               o_cl = take(4 * (size_t)C), o_co = take(4 * (size_t)C * dm.OW),
-               o_so = take(record ? 4 * S * dm.OW : 0), o_sr = take(record ? 4 * S : 0),
-               o_su = take(record ? 4 * S : 0), o_sl = take(record ? 4 * S : 0),
-               o_sn = take(record ? 4 * S : 0), o_sh = take(record ? 8 * S : 0),
-               o_ss = take(record && out->scen_states ? 4 * S * dm.SW : 0);
+  auto& o_ns = b->o_ns; auto& o_w = b->o_w; auto& o_ar = b->o_ar; auto& o_au = b->o_au; auto& o_al = b->o_al;
+  auto& o_cb = b->o_cb; auto& o_cc = b->o_cc; auto& o_cf = b->o_cf; auto& o_cw = b->o_cw; auto& o_cu = b->o_cu;
+  auto& o_cl = b->o_cl; auto& o_co = b->o_co; auto& o_so = b->o_so;
+  size_t o_sr, o_su, o_sl, o_sn, o_sh, o_ss;
+  o_ns = take(4 * L), o_w = take(4 * L), o_ar = take(4 * LA), o_au = take(4 * LA),
+  o_al = take(4 * LA), o_cb = take(4 * (LA + 1)), o_cc = take(4 * (size_t)C),
+  o_cf = take(4 * (size_t)C), o_cw = take(4 * (size_t)C), o_cu = take(4 * (size_t)C),
+  o_cl = take(4 * (size_t)C), o_co = take(4 * (size_t)C * dm.OW),
+  o_so = take(record ? 4 * S * dm.OW : 0), o_sr = take(record ? 4 * S : 0),
+  o_su = take(record ? 4 * S : 0), o_sl = take(record ? 4 * S : 0),
+  o_sn = take(record ? 4 * S : 0), o_sh = take(record ? 8 * S : 0),
+  o_ss = take(record && out->scen_states ? 4 * S * dm.SW : 0);
   if (dev_out) {
     bd.n_scen = out->n_scen;
     bd.weight = out->weight;
@@ -1113,6 +1145,25 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     bd.scen_hash = reinterpret_cast<uint64_t*>(p + o_sh);
     bd.scen_states = (record && out->scen_states) ? reinterpret_cast<uint32_t*>(p + o_ss) : nullptr;
   }
+  b->bound = true;
+  return DESPOT_OK;
+}
+
+// Completes a bound batch: [K2 for RECORD] -> K3 (unless fused into K2) ->
+// status and outputs to the host -> frees the batch.
+static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st) {
+  despot_model* m = b->model;
+  const DevModel& dm = m->host;
+  const uint32_t L = b->L;
+  const uint64_t LA = (uint64_t)L * dm.A;
+  const bool dev_out = out->flags & DESPOT_X_DEVICE_OUTPUTS;
+  const bool record = b->flags & DESPOT_X_RECORD_SCENARIO;
+  BatchDev& bd = b->bd;
+  const uint32_t C = out->child_capacity;
+  void* stage = b->stage;
+  const size_t o_ns = b->o_ns, o_w = b->o_w, o_ar = b->o_ar, o_au = b->o_au, o_al = b->o_al, o_cb = b->o_cb,
+               o_cc = b->o_cc, o_cf = b->o_cf, o_cw = b->o_cw, o_cu = b->o_cu, o_cl = b->o_cl, o_co = b->o_co,
+               o_so = b->o_so;
   int rc = DESPOT_OK;
   if (record && b->sparse) {
     rc = launch_k2_sparse(m, b, true);
@@ -1132,9 +1183,11 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   const unsigned warps_per_cta = 4;
   const unsigned g3 = (unsigned)((LA + warps_per_cta - 1) / warps_per_cta);
   b->mark(5);
-  // small dense batches (few slots): rank + scan + write in one CTA
+  // small dense batches (few slots): rank + scan + write in one CTA (or in
+  // K2's last CTA, already done, when the batch was fused)
   const bool small_k3 = !b->sparse && LA <= kSmallLA && b->S <= 32;
-  if (!rc && b->sparse) {
+  if (b->k3_fused) {
+  } else if (!rc && b->sparse) {
     uint32_t tbits = 1;
     while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
     const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
@@ -1145,7 +1198,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     rc = check_launch(m, "K3a(sparse)");
   } else if (!rc && small_k3) {
     // small batch: rank + scan + write in one CTA (one launch instead of three)
-    const size_t smem = 4 * LA + 32 * 8 * (size_t)b->S;
+    const size_t smem = small_finalize_smem(LA);
     static std::once_flag once;
     std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
     k3_small_dense<<<1, 1024, smem, st>>>(bd);
@@ -1156,7 +1209,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
     ++b->launches;
     rc = check_launch(m, "K3a");
   }
-  if (!rc && !small_k3) {
+  if (!rc && !small_k3 && !b->k3_fused) {
     k3_scan<<<1, 1024, 0, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3b");
@@ -1279,7 +1332,6 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
       out->phase_ms[k] = ms;
     }
   }
-  if (stage) cudaFreeAsync(stage, st);
   if (rc) {
     free_batch(b, true);
     return rc;
@@ -1295,12 +1347,23 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
   return DESPOT_OK;
 }
 
+extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* stream) {
+  if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
+  CU(cudaSetDevice(b->model->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!b->bound) {
+    if (int rc = bind_outputs(b, out, st)) return rc;  // frees the batch on error
+  }
+  return finish_batch(b, out, st);
+}
+
 extern "C" int despot_expand_batch(despot_model* m, const despot_leaf* leaves, uint32_t L,
                                    despot_expansion* out, void* stream) {
   if (!m || !out) return set_err(DESPOT_EINVAL, "null argument");
   if (m->world > 1) return set_err(DESPOT_EINVAL, "world > 1: use despot_expand_begin/exchange/end");
   despot_batch* b = nullptr;
-  int rc = despot_expand_begin(m, leaves, L, out->flags, stream, &b);
+  // outputs are bound before K2 so that small batches finalize in K2's last CTA
+  int rc = begin_impl(m, leaves, L, out->flags, stream, out, &b);
   if (rc) return rc;
   return despot_expand_end(b, out, stream);
 }

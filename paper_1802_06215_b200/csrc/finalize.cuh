@@ -93,11 +93,11 @@ __device__ __forceinline__ void rank_one(const BatchDev& b, uint64_t la, uint32_
   uint32_t cnt = 0;
   for (uint32_t s0 = 0; s0 < S; s0 += 32) {
     const uint32_t s = s0 + lane;
-    const bool ne = s < S && b.sums[lay.N(base + s)] != 0;
+    const bool ne = s < S && __ldcg(&b.sums[lay.N(base + s)]) != 0;
     const uint32_t bal = __ballot_sync(0xffffffffu, ne);
     if (ne) {
       const uint32_t pos = cnt + __popc(bal & ((1u << lane) - 1u));
-      s_first[pos] = b.mins[base + s];
+      s_first[pos] = __ldcg(&b.mins[base + s]);
       s_slot[pos] = s;
     }
     cnt += __popc(bal);
@@ -138,7 +138,7 @@ __device__ __forceinline__ void scan_children(const BatchDev& b, const uint32_t*
     if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
     // status block for the host: total children and the step counter
     b.status[1] = (uint32_t)tot;
-    const uint64_t steps = (uint64_t)b.sums[SumLayout{LA * b.S, LA}.steps()];
+    const uint64_t steps = (uint64_t)__ldcg(&b.sums[SumLayout{LA * b.S, LA}.steps()]);
     b.status[2] = (uint32_t)steps;
     b.status[3] = (uint32_t)(steps >> 32);
   }
@@ -160,9 +160,9 @@ __device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32
   const uint64_t base = la * S;
   int64_t wt = 0, nt = 0;
   for (uint32_t s = lane; s < S; s += 32) {
-    const int64_t N = b.sums[lay.N(base + s)];
+    const int64_t N = __ldcg(&b.sums[lay.N(base + s)]);
     if (!N) continue;
-    const int64_t W = b.sums[lay.W(base + s)];
+    const int64_t W = __ldcg(&b.sums[lay.W(base + s)]);
     wt += W;
     nt += N;
     const uint32_t rk = b.rank[base + s];
@@ -170,10 +170,10 @@ __device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32
     if (c < b.child_capacity) {
       const double Wd = (double)W;
       b.child_count[c] = (uint32_t)N;
-      b.child_first[c] = (uint32_t)b.mins[base + s];
+      b.child_first[c] = (uint32_t)__ldcg(&b.mins[base + s]);
       b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
-      b.child_upper[c] = (float)((double)b.sums[lay.U(base + s)] / Wd);
-      b.child_lower[c] = (float)((double)b.sums[lay.Lm(base + s)] / Wd);
+      b.child_upper[c] = (float)((double)__ldcg(&b.sums[lay.U(base + s)]) / Wd);
+      b.child_lower[c] = (float)((double)__ldcg(&b.sums[lay.Lm(base + s)]) / Wd);
       b.child_obs[c] = s;
     }
     if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = s;  // key table for later updates
@@ -183,9 +183,9 @@ __device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32
   if (lane == 0) {
     lf.nchild[a] = nc;
     const double Wd = (double)wt;
-    b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
-    b.act_upper[la] = (float)((double)b.sums[lay.Q(la, 1)] / Wd);
-    b.act_lower[la] = (float)((double)b.sums[lay.Q(la, 2)] / Wd);
+    b.act_reward[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 0)]) / Wd);
+    b.act_upper[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 1)]) / Wd);
+    b.act_lower[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 2)]) / Wd);
     if (a == 0) {
       b.n_scen[leaf] = (uint32_t)nt;
       b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
@@ -200,20 +200,146 @@ __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
   write_one(b, la, lane, b.child_begin[la], b.nc[la]);
 }
 
-// K3 for small batches (L*A <= kSmallLA): rank, scan and write in one CTA
+// K3 for small batches (L*A <= kSmallLA, S <= 32): rank, scan and write in
+// one CTA -- a kernel of its own, or the tail of K2's last CTA.  The path is
+// latency bound (a few L2 round trips per (leaf, action)), so: one lane per
+// observation slot, 32/Sp (leaf, action) pairs per warp (Sp = S rounded up
+// to a power of two), the loads of kSmallUnroll pairs in flight at once, the
+// child ordinals (first occurrence, R8) recomputed in registers from the
+// first ids instead of stored, and child_begin scanned in shared memory.
 constexpr uint32_t kSmallLA = 4096;
-__global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
-  extern __shared__ __align__(16) unsigned char k3s_smem[];
+constexpr uint32_t kSmallUnroll = 4;
+__host__ __device__ inline uint32_t small_group_width(uint32_t S) {
+  uint32_t sp = 1;
+  while (sp < S) sp <<= 1;
+  return sp;
+}
+__host__ __device__ inline size_t small_finalize_smem(uint64_t LA) { return align16(4 * (LA + 1)); }
+__device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char* smem) {
   __shared__ uint64_t wsum[32];
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const uint32_t LA = b.L * b.A;
-  uint32_t* nc = reinterpret_cast<uint32_t*>(k3s_smem);               // [LA]
-  int32_t* s_first = reinterpret_cast<int32_t*>(nc + LA) + (size_t)wid * 2 * b.S;
-  for (uint32_t la = wid; la < LA; la += nw) rank_one(b, la, lane, s_first, &nc[la]);
+  const uint32_t S = b.S, A = b.A, LA = b.L * b.A;
+  const uint32_t Sp = small_group_width(S), G = 32 / Sp;
+  const uint32_t j = lane & (Sp - 1), gshift = lane & ~(Sp - 1);
+  const uint32_t gbits = Sp == 32 ? 0xffffffffu : (1u << Sp) - 1u;
+  const SumLayout lay{(uint64_t)LA * S, LA};
+  const uint32_t stride = nw * G;  // pairs per CTA-wide sweep
+  const uint32_t first = wid * G + lane / Sp;
+  uint32_t* cb = reinterpret_cast<uint32_t*>(smem);  // [LA + 1]: counts, then offsets
+  const double inv_fx = b.model->inv_fx;
+  // ---- children per (leaf, action), one-level Eq. 4 ---------------------
+  for (uint32_t la0 = first; la0 - lane / Sp < LA; la0 += stride * kSmallUnroll) {
+    int64_t n[kSmallUnroll], w[kSmallUnroll], Q[kSmallUnroll][3];
+#pragma unroll
+    for (uint32_t u = 0; u < kSmallUnroll; ++u) {
+      const uint32_t la = la0 + u * stride;
+      const bool v = la < LA && j < S;
+      n[u] = v ? __ldcg(&b.sums[lay.N((uint64_t)la * S + j)]) : 0;
+      w[u] = v ? __ldcg(&b.sums[lay.W((uint64_t)la * S + j)]) : 0;
+      const bool q = la < LA && j == 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) Q[u][k] = q ? __ldcg(&b.sums[lay.Q(la, k)]) : 0;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kSmallUnroll; ++u) {
+      const uint32_t la = la0 + u * stride;
+      const uint32_t gb = (__ballot_sync(0xffffffffu, n[u] != 0) >> gshift) & gbits;
+      int64_t wt = w[u], nt = n[u];
+      for (uint32_t o = Sp >> 1; o; o >>= 1) {
+        wt += __shfl_xor_sync(0xffffffffu, wt, o);
+        nt += __shfl_xor_sync(0xffffffffu, nt, o);
+      }
+      if (j == 0 && la < LA) {
+        const uint32_t leaf = la / A, a = la - leaf * A;
+        const LeafDev& lf = b.leaves[leaf];
+        cb[la] = __popc(gb);
+        lf.nchild[a] = __popc(gb);
+        const double Wd = (double)wt;
+        b.act_reward[la] = (float)((double)Q[u][0] / Wd);
+        b.act_upper[la] = (float)((double)Q[u][1] / Wd);
+        b.act_lower[la] = (float)((double)Q[u][2] / Wd);
+        if (a == 0) {
+          b.n_scen[leaf] = (uint32_t)nt;
+          b.weight[leaf] = (float)(Wd * inv_fx * lf.wroot);
+          if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+        }
+      }
+    }
+  }
   __syncthreads();
-  scan_children(b, nc, wsum);
+  // ---- child_begin: exclusive scan of the counts (in place) -----------
+  {
+    const uint32_t per = (LA + blockDim.x - 1) / blockDim.x;
+    const uint32_t i0 = threadIdx.x * per;
+    uint64_t loc = 0;
+    for (uint32_t i = i0; i < i0 + per && i < LA; ++i) loc += cb[i];
+    uint64_t tot;
+    uint64_t run = block_excl_scan(loc, wsum, tot);
+    for (uint32_t i = i0; i < i0 + per && i < LA; ++i) {
+      const uint32_t c = cb[i];
+      cb[i] = (uint32_t)run;
+      b.child_begin[i] = (uint32_t)run;
+      run += c;
+    }
+    if (threadIdx.x == 0) {
+      cb[LA] = (uint32_t)tot;
+      b.child_begin[LA] = (uint32_t)tot;
+      if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
+      b.status[1] = (uint32_t)tot;
+      const uint64_t steps = (uint64_t)__ldcg(&b.sums[lay.steps()]);
+      b.status[2] = (uint32_t)steps;
+      b.status[3] = (uint32_t)(steps >> 32);
+    }
+  }
   __syncthreads();
-  for (uint32_t la = wid; la < LA; la += nw) write_one(b, la, lane, b.child_begin[la], nc[la]);
+  // ---- children: Eq. 11/12 bounds, first ids, key tables --------------
+  for (uint32_t la0 = first; la0 - lane / Sp < LA; la0 += stride * kSmallUnroll) {
+    int64_t N[kSmallUnroll], W[kSmallUnroll], U[kSmallUnroll], Lm[kSmallUnroll];
+    int32_t mn[kSmallUnroll];
+#pragma unroll
+    for (uint32_t u = 0; u < kSmallUnroll; ++u) {
+      const uint32_t la = la0 + u * stride;
+      const bool v = la < LA && j < S;
+      const uint64_t slot = (uint64_t)la * S + j;
+      N[u] = v ? __ldcg(&b.sums[lay.N(slot)]) : 0;
+      W[u] = v ? __ldcg(&b.sums[lay.W(slot)]) : 0;
+      U[u] = v ? __ldcg(&b.sums[lay.U(slot)]) : 0;
+      Lm[u] = v ? __ldcg(&b.sums[lay.Lm(slot)]) : 0;
+      mn[u] = v ? __ldcg(&b.mins[slot]) : 0;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kSmallUnroll; ++u) {
+      const uint32_t la = la0 + u * stride;
+      const bool ne = N[u] != 0;
+      const uint32_t gb = (__ballot_sync(0xffffffffu, ne) >> gshift) & gbits;
+      // ordinal = number of non-empty slots of the pair with a smaller first id
+      uint32_t rk = 0;
+      for (uint32_t k = 0; k < Sp; ++k) {
+        const int32_t mk = __shfl_sync(0xffffffffu, mn[u], k, Sp);
+        rk += ((gb >> k) & 1u) && mk < mn[u];
+      }
+      if (!ne || la >= LA) continue;
+      const uint32_t leaf = la / A, a = la - leaf * A;
+      const LeafDev& lf = b.leaves[leaf];
+      const uint32_t c = cb[la] + rk;
+      if (c < b.child_capacity) {
+        const double Wd = (double)W[u];
+        b.child_count[c] = (uint32_t)N[u];
+        b.child_first[c] = (uint32_t)mn[u];
+        b.child_weight[c] = (float)(Wd * inv_fx * lf.wroot);
+        b.child_upper[c] = (float)((double)U[u] / Wd);
+        b.child_lower[c] = (float)((double)Lm[u] / Wd);
+        b.child_obs[c] = j;
+      }
+      if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = j;  // key table for later updates
+    }
+  }
+}
+// out of line for K2's tail: its registers do not constrain K2's main loop
+__device__ __noinline__ void small_finalize_tail(const BatchDev& b, unsigned char* smem) { small_finalize(b, smem); }
+__global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char k3s_smem[];
+  small_finalize(b, k3s_smem);
 }
 
 __global__ void k_stream_words(uint32_t k0, uint32_t k1, const uint32_t* ids, uint32_t n, uint32_t t,

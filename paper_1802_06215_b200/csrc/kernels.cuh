@@ -209,6 +209,21 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   }
   const uint32_t ws = warp_sum32(steps_acc);
   if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)ws);
+  if (b.fused_k3) {
+    // small batch: the last CTA to finish ranks, scans and writes the
+    // children (K3) -- one launch per expansion instead of two
+    __shared__ bool k2_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      k2_last = atomicAdd(&b.status[5], 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (k2_last) {
+      __threadfence();
+      small_finalize_tail(b, reinterpret_cast<unsigned char*>(tile_off) + align16(4 * ((size_t)b.L + 1)));
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

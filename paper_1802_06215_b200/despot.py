@@ -314,6 +314,26 @@ class Model:
         _check(lib().despot_expand_batch(self.h, lv, L, C.byref(E), _stream_ptr(stream)))
         return self._finish(o, E, L, nodes, record, device_outputs)
 
+    # ---- prepared calls (repeated batches: no per-call marshalling) ----
+    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False):
+        """Build the ctypes leaf table, output arrays and expansion struct of a
+        batch once; `run_prepared` then costs one foreign call."""
+        L = len(leaves)
+        C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
+        o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs)
+        nodes = (C.c_uint64 * L)()
+        E.node = C.addressof(nodes)
+        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_TIMING if timing else 0)
+        return {"lv": self._leaves(leaves), "L": L, "E": E, "o": o, "nodes": nodes, "ref": C.byref(E),
+                "leaves": list(leaves)}
+
+    def run_prepared(self, prep, stream=None):
+        """despot_expand_batch on a prepared batch; returns (scenario_steps,
+        launches, node handles); outputs are in prep["o"], prep["E"]."""
+        _check(lib().despot_expand_batch(self.h, prep["lv"], prep["L"], prep["ref"], _stream_ptr(stream)))
+        E = prep["E"]
+        return E.scenario_steps, E.launches, prep["nodes"]
+
     # ---- two-phase form for scenario sharding ----
     def alloc_outputs(self, leaves, device_outputs=False, child_capacity=None):
         C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)

@@ -42,8 +42,10 @@ int main(int argc, char** argv) {
   OK(despot_belief_load(m, st.data(), w.data(), K, 1001, s, &root));
   despot_leaf leaf{root, -1, 0, 0, 0};
   const uint32_t C = A * 4;
-  // host outputs (pinned) and device outputs
-  for (int dev = 0; dev < 2; ++dev) {
+  // host outputs (pinned) and device outputs; mode 2 = device outputs
+  // through the two-phase form (begin/end: separate K3, no fusion)
+  for (int mode = 0; mode < 3; ++mode) {
+    const int dev = mode > 0;
     despot_expansion out;
     memset(&out, 0, sizeof out);
     despot_node node;
@@ -72,15 +74,21 @@ int main(int argc, char** argv) {
     out.child_upper = (float*)take(4 * C);
     out.child_lower = (float*)take(4 * C);
     out.child_obs = (uint32_t*)take(4 * C);
-    for (int i = 0; i < 50; ++i) OK(despot_expand_batch(m, &leaf, 1, &out, s));
+    auto call = [&]() -> int {
+      if (mode < 2) return despot_expand_batch(m, &leaf, 1, &out, s);
+      despot_batch* b = nullptr;
+      if (int rc = despot_expand_begin(m, &leaf, 1, out.flags, s, &b)) return rc;
+      return despot_expand_end(b, &out, s);
+    };
+    for (int i = 0; i < 50; ++i) OK(call());
     const int N = argc > 1 ? atoi(argv[1]) : 2000;
     const auto t0 = std::chrono::steady_clock::now();
-    for (int i = 0; i < N; ++i) OK(despot_expand_batch(m, &leaf, 1, &out, s));
+    for (int i = 0; i < N; ++i) OK(call());
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / N;
     out.flags |= DESPOT_X_TIMING;
-    OK(despot_expand_batch(m, &leaf, 1, &out, s));
-    printf("{\"outputs\": \"%s\", \"us_per_call\": %.2f, \"scenario_steps\": %llu, \"phases_ms\": [%.4f, %.4f, %.4f, %.4f]}\n",
-           dev ? "device" : "host", us, (unsigned long long)out.scenario_steps, out.phase_ms[0], out.phase_ms[1],
+    OK(call());
+    printf("{\"outputs\": \"%s\", \"us_per_call\": %.2f, \"launches\": %u, \"scenario_steps\": %llu, \"phases_ms\": [%.4f, %.4f, %.4f, %.4f]}\n",
+           mode == 2 ? "device-two-phase" : dev ? "device" : "host", us, out.launches, (unsigned long long)out.scenario_steps, out.phase_ms[0], out.phase_ms[1],
            out.phase_ms[2], out.phase_ms[3]);
     if (dev) cudaFree(buf);
     else cudaFreeHost(buf);

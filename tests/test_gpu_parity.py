@@ -219,6 +219,47 @@ def test_determinism_and_device_outputs():
         assert np.array_equal(d.view(A1[k].dtype) if d.dtype != A1[k].dtype else d, A1[k]), k
 
 
+def test_fused_finalize_equals_separate_k3_and_prepared_calls():
+    """Small dense batches finalize in K2's last CTA when expanded in one call
+    (despot_expand_batch); the two-phase form (begin/end, world 1) runs the
+    separate small K3.  Both, and the prepared-call binding, agree bit for bit."""
+    import torch
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+            "child_first", "child_weight", "child_upper", "child_lower", "child_obs")
+    for cfg, K, L in ((1, 100, 1), (2, 30, 4), (3, 31, 3)):
+        gm, om, st, w, seed, _ = setup(cfg, K=K, L=L)
+        gr = gm.belief_load(st, w, seed)
+        R = gm.expand([(gr, -1, 0, 0)])
+        lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)]
+        for leaves in ([(gr, -1, 0, 0)], lv):
+            F = gm.expand(leaves)
+            b, _ = gm.expand_begin(leaves)
+            U = gm.expand_end(b, leaves)
+            prep = gm.prepare(leaves, device_outputs=False)
+            steps, launches, nodes = gm.run_prepared(prep)
+            torch.cuda.synchronize()
+            # the fused batch skips the K3 launch (small S and L*A: the RockSample(7,8) case)
+            assert F["launches"] < U["launches"] if cfg == 1 else F["launches"] <= U["launches"]
+            assert F["scenario_steps"] == U["scenario_steps"] == steps
+            for k in keys:
+                assert np.array_equal(F[k], U[k]), (cfg, k)
+                P = prep["o"][k]
+                f = np.asarray(F[k]).reshape(-1)
+                assert np.array_equal(np.asarray(P)[: len(f)], f), (cfg, k)
+            for n in list(F["node"]) + list(U["node"]) + list(nodes):
+                if n != gr:
+                    gm.node_release(n)
+        # the fused batch still matches the oracle
+        orr = om.belief_load(st, w, seed)
+        G = gm.expand([(gr, -1, 0, 0)])
+        O = om.expand([(orr, -1, 0, 0)], record=True)
+        compare_batch(G, O, gm, om, [(0, 0)])
+        for n in G["node"]:
+            if n != gr:
+                gm.node_release(n)
+        gm.close()
+
+
 def test_rollout_bounds_match_oracle():
     for cfg in (1, 3):
         gm, om, st, w, seed, _ = setup(cfg, K=150, uniform=False)
