@@ -90,6 +90,8 @@ struct Search {
   TNode* root = nullptr;
   std::atomic<bool> stop{false};
   std::atomic<uint64_t> trials{0}, batches{0}, expanded{0}, steps{0}, records{1};
+  std::atomic<uint64_t> done_batches{0};   // batches completed (workers wait on it)
+  std::atomic<uint32_t> inflight_total{0};  // leaves queued or being expanded
   std::atomic<uint32_t> max_depth{0};
   std::mutex qmu;
   std::condition_variable qcv;  // batcher wake-up
@@ -110,21 +112,25 @@ struct Search {
   }
   double root_gap() const { return root_rec.upper.load() - root_rec.lower.load(); }
 
-  // Eq. 4 one level: recompute node b's branch values and bounds from its
-  // children (clamped by the initial bounds)
-  void backup_node(TNode* b) {
+  // Eq. 4 one level: recompute node b's branch a (every branch when a < 0)
+  // from its children, then b's bounds as the max over its branches (clamped
+  // by the initial bounds).  A trial changes only the children below the
+  // branch it took, so the backup along its path recomputes that branch
+  // alone: O(A + |children of a|) per node instead of O(all children).
+  void backup_node(TNode* b, int32_t a) {
     std::lock_guard<std::mutex> g(b->mu);
     if (b->state != TNode::kExpanded) return;
     const double W = b->rec->weight;
     double bu = -std::numeric_limits<double>::infinity(), bl = bu;
-    for (TBranch& br : b->branches) {
-      if (br.count) {
+    for (uint32_t k = 0; k < b->branches.size(); ++k) {
+      TBranch& br = b->branches[k];
+      if (br.count && (a < 0 || (uint32_t)a == k)) {
         double su = 0.0, sl = 0.0;
-        for (uint32_t k = br.first; k < br.first + br.count; ++k) {
-          const TChild& c = b->children[k];
-          const double f = c.weight / W;
-          su += f * c.upper.load(std::memory_order_relaxed);
-          sl += f * c.lower.load(std::memory_order_relaxed);
+        for (uint32_t c = br.first; c < br.first + br.count; ++c) {
+          const TChild& ch = b->children[c];
+          const double f = ch.weight / W;
+          su += f * ch.upper.load(std::memory_order_relaxed);
+          sl += f * ch.lower.load(std::memory_order_relaxed);
         }
         br.upper = br.reward + P.gamma * su;
         br.lower = br.reward + P.gamma * sl;
@@ -136,7 +142,7 @@ struct Search {
     b->rec->lower.store(std::max(b->rec->l0, bl));
   }
   void backup(const std::vector<TNode*>& path) {
-    for (auto it = path.rbegin(); it != path.rend(); ++it) backup_node(*it);
+    for (size_t i = path.size(); i-- > 0;) backup_node(path[i], i + 1 < path.size() ? path[i + 1]->action_in : -1);
   }
   static void release_markers(const std::vector<TNode*>& path) {
     for (size_t i = 1; i < path.size(); ++i) path[i]->rec->active.fetch_sub(1);
@@ -225,6 +231,7 @@ struct Search {
       backup(p.path);
       release_markers(p.path);
       if (p.inflight) p.inflight->fetch_sub(1);
+      if (p.inflight) inflight_total.fetch_sub(1);
     }
     return DESPOT_OK;
   }
@@ -259,10 +266,12 @@ struct Search {
           }
           release_markers(p.path);
           if (p.inflight) p.inflight->fetch_sub(1);
+          if (p.inflight) inflight_total.fetch_sub(1);
         }
       }
       {
         std::lock_guard<std::mutex> g(qmu);  // pairs with the workers' dcv wait
+        done_batches.fetch_add(1);
       }
       dcv.notify_all();
     }
@@ -292,6 +301,7 @@ struct Search {
 
   void worker() {
     std::atomic<uint32_t> inflight{0};
+    uint32_t failed = 0;  // consecutive trials that found no leaf
     const uint32_t max_inflight = std::max<uint32_t>(1, C.max_inflight);
     while (!stop.load()) {
       if (inflight.load() >= max_inflight) {
@@ -356,15 +366,29 @@ struct Search {
         b = nd;
       }
       if (leaf) {
+        failed = 0;
         inflight.fetch_add(1);
+        inflight_total.fetch_add(1);
         {
           std::lock_guard<std::mutex> g(qmu);
           queue.push_back(Pending{leaf, std::move(path), &inflight});
         }
         qcv.notify_one();
       } else {
-        backup(path);
+        // no leaf (a pending node or every WEU <= 0): no bound changed, so
+        // no backup.  After a second miss in a row the tree will not change
+        // until a batch lands: wait for one instead of re-descending (the
+        // re-descents would only contend for the node locks).
         release_markers(path);
+        if (++failed >= 2 && inflight_total.load() > 0) {
+          const uint64_t seen = done_batches.load();
+          std::unique_lock<std::mutex> lk(qmu);
+          ++blocked;
+          qcv.notify_one();
+          dcv.wait_for(lk, std::chrono::milliseconds(2),
+                       [&] { return done_batches.load() != seen || stop.load(); });
+          --blocked;
+        }
       }
     }
     // wait for this worker's trials still in the batcher (inflight lives here)

@@ -144,7 +144,8 @@ def test_parallel_search_bounds_and_counts(case):
     tol = 1e-5 * max(1.0, abs(v))  # the backend's outputs are fp32 (R12)
     assert res["root_lower"] <= v + tol and v <= res["root_upper"] + tol, (res, v)
     assert res["batches"] == be.calls and res["expanded"] == be.leaves_seen
-    assert res["trials"] == 600
+    # the trial budget is spent, or the search stopped early on a closed root gap
+    assert res["trials"] == 600 or res["root_upper"] - res["root_lower"] <= tol, res
 
 
 def test_serial_search_is_deterministic():
