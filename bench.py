@@ -41,6 +41,24 @@ from paper_1802_06215_b200 import inputs  # noqa: E402
 I_STEP = {1: 177.0, 2: 241.0, 3: 303.0, 4: 2054.0, 5: 241.0}
 
 
+def ncu_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel,
+    per launch, from the committed `ncu --set full` raw page of this config
+    (profiles/r01/k2_config<C>_raw.csv); None if there is none."""
+    import csv
+    p = os.path.join(ROOT, "profiles", "r01", f"k2_config{config}_raw.csv")
+    try:
+        rows = list(csv.reader(open(p)))
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = rows[0].index(name)
+            tot += float(rows[2][i].replace(",", "")) * scale[rows[1][i]]
+        return {"bytes_per_launch": tot, "source": os.path.relpath(p, ROOT)}
+    except Exception:
+        return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -278,8 +296,6 @@ def main():
     torch.cuda.set_stream(stream)
     if kind == "car":
         # config 4: L concurrent roots (inputs.car_roots)
-        if world > 1:
-            raise SystemExit("config 4 (sparse keys) runs on one GPU")
         croots = inputs.car_roots(L, int(len(w)), peds=c.get("peds", 20))
         leaves = [(model.belief_load(s_, w_, sd_), -1, 0, 0) for s_, w_, sd_ in croots]
         lv_ac = None
@@ -301,10 +317,9 @@ def main():
 
     def one_step(outputs, device_outputs, timing=True):
         if world > 1:
-            from paper_1802_06215_b200.dist import exchange, exchange_views
+            from paper_1802_06215_b200.dist import run_exchange
             b, ex = model.expand_begin(leaves, timing=timing)
-            s, m = exchange_views(ex, dev)
-            exchange(s, m)
+            run_exchange(model, b, ex)  # one round (dense keys) or two (sparse: + record all-gather)
             o = model.expand_end(b, leaves, device_outputs=device_outputs, timing=timing, outputs=outputs)
             nodes = o["node"]
         else:
@@ -389,6 +404,14 @@ def main():
     steps_local = total_steps / world
     achieved = I_STEP[args.config] * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
     k2_share = float(np.sum(k2_ms) / np.sum(step_ms))
+    traffic = ncu_traffic(args.config)
+    if kind == "car":  # the variant rule of despot.cu (launch_k2_sparse) unless forced
+        q_bound = A * sum(model.node_info(lf[0])[0] for lf in leaves)
+        thread = args.car_variant == "thread" or (args.car_variant == "auto" and (
+            q_bound >= num_sms * 256 or c.get("peds", 20) < 8))
+        k2_name = "k2_car_thread" if thread else "k2_car_warp"
+    else:
+        k2_name = "k2_expand_dense"
     if rank == 0:
         line = {
             "metric": "scenario-steps/s",
@@ -409,9 +432,11 @@ def main():
                        "scenario_steps_per_batch": int(total_steps / args.steps)},
             "phases_ms": {"K1_update": float(np.mean(k1_ms)), "K2_expand_rollout": k2_avg,
                           "K3_finalize": float(np.mean(k3_ms)), "K2_share_of_step": k2_share},
-            "roofline": {"bound": "alu", "kernel": "k2_car_warp" if kind == "car" else "k2_expand_dense", "achieved": achieved,
+            "roofline": {"bound": "alu", "kernel": k2_name, "achieved": achieved,
                          "peak": peak_tinst, "unit": "Tinst/s", "frac": achieved / peak_tinst,
-                         "traffic": None,
+                         "traffic": traffic["bytes_per_launch"] if traffic else None,
+                         "traffic_unit": "DRAM bytes per K2 launch",
+                         "traffic_source": traffic["source"] if traffic else None,
                          "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
                                  f"({peak_src} sm_max_mhz); achieved = {I_STEP[args.config]} thread-instr per "
                                  f"scenario-step (DESIGN.md §7) x steps / live K2 event time"},

@@ -190,16 +190,30 @@ int despot_expand_batch(despot_model* model, const despot_leaf* leaves, uint32_t
                         despot_expansion* out, void* stream);
 
 /* Multi-GPU scenario sharding: every rank calls with identical
- * leaves; between begin and end the caller sums `sums` and mins `mins` over
- * the ranks in place (e.g. NCCL all-reduce on `stream`); `end` then produces
- * identical outputs on every rank.  The sums are exact int64 fixed-point
- * partials, so the result does not depend on the reduction order. */
+ * leaves; between begin and end the caller runs the collectives each
+ * exchange round names, in place, over the ranks (e.g. NCCL on `stream`):
+ * SUM over `sums`, MIN over `mins`, MAX over `maxs`, and an all-gather over
+ * `gather` (world blocks of gather_bytes; this rank's block, at
+ * rank * gather_bytes, is filled).  While `more` is nonzero it calls
+ * despot_batch_exchange again for the next round.  Dense-key models need one
+ * round (SUM + MIN); sparse-key models (driving) two (SUM + MAX, then the
+ * all-gather of the ranks' child records, merged by exact key in `end`).
+ * `end` then produces identical outputs on every rank, equal to world == 1
+ * bit for bit: the sums are exact int64 fixed-point partials, so nothing
+ * depends on the reduction order.  Null pointers / zero sizes: no such
+ * collective this round. */
 typedef struct despot_batch despot_batch;
 typedef struct {
   int64_t* sums;   /* device [n_sums]  all-reduce SUM (int64)  */
   uint64_t n_sums;
   int32_t* mins;   /* device [n_mins]  all-reduce MIN (int32)  */
   uint64_t n_mins;
+  int64_t* maxs;   /* device [n_maxs]  all-reduce MAX (int64)  */
+  uint64_t n_maxs;
+  void* gather;    /* device [world * gather_bytes]  all-gather (in place) */
+  uint64_t gather_bytes;
+  uint32_t round;  /* this round's index (0-based)                          */
+  uint32_t more;   /* nonzero: call despot_batch_exchange again after this  */
 } despot_exchange;
 int despot_expand_begin(despot_model* model, const despot_leaf* leaves, uint32_t L,
                         uint32_t flags, void* stream, despot_batch** batch_out);

@@ -151,6 +151,7 @@ struct Node {
   uint32_t* keys;
   uint32_t cap, kcap;
   uint32_t n;  // local scenarios (host copy, valid once the creating call returned)
+  uint32_t gn; // bound on the global scenario count (sizes the sharded sparse key table)
   uint32_t depth;
   uint64_t seed;
   double wroot;
@@ -189,6 +190,14 @@ struct despot_batch {
          o_cl = 0, o_co = 0, o_so = 0;  // staging layout
   bool sparse = false;
   uint64_t n_sums = 0, n_mins = 0;
+  // scenario-sharded sparse keys (world > 1): two exchange rounds, then a merge
+  bool sharded_sparse = false;
+  uint32_t xround = 0;            // exchange rounds handed out
+  int64_t* xmax = nullptr;        // device [2]: local record count, largest local child set
+  void* gbuf = nullptr;           // all-gather buffer: world blocks of gblk bytes
+  void* mscratch = nullptr;       // merge scratch (offsets, merged sums)
+  uint64_t gblk = 0, rmax = 0, ncmax = 0;
+  uint32_t hdr_pad = 0, rec_bytes = 0;
   bool timing = false;
   uint32_t launches = 0;  // kernels launched for this batch
   cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
@@ -231,6 +240,11 @@ void carve_node(Node* nd, const DevModel& dm, char*& p) {
 }
 uint32_t key_cap(const DevModel& dm, uint32_t cap) {
   return dm.slots ? dm.slots : (cap ? cap : 1);
+}
+// key-table capacity of a new child of p: a sharded sparse node keeps the
+// keys of the GLOBAL children, bounded by the global scenario count
+uint32_t child_kcap(const despot_model* m, const Node* p) {
+  return (m->world > 1 && !m->host.slots) ? std::max<uint32_t>(p->gn, 1) : key_cap(m->host, p->cap);
 }
 
 // fixed-point scale of the exact reductions: |sum of normalised values| <=
@@ -562,8 +576,7 @@ extern "C" int despot_model_load(const char* kind, const char* params, const des
     m->flags = opts->flags;
   }
   if (m->rank < 0 || m->rank >= m->world) return set_err(DESPOT_EINVAL, "rank outside [0, world)");
-  if (m->world > 1 && m->host.slots == 0)
-    return set_err(DESPOT_EINVAL, "scenario sharding needs a dense-observation model");
+  if (m->world > (int)kMaxMergeWorld) return set_err(DESPOT_EINVAL, "world > %u", kMaxMergeWorld);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return set_err(DESPOT_ECUDA, "no CUDA device (libdespot has no CPU fallback)");
@@ -636,13 +649,14 @@ extern "C" int despot_belief_load(despot_model* m, const uint32_t* states_soa, c
   cudaStream_t st = (cudaStream_t)stream;
   auto blk = std::make_shared<Block>();
   blk->stream = st;
-  const uint32_t kcap = key_cap(dm, cap);
+  const uint32_t kcap = (m->world > 1 && !dm.slots) ? std::max<uint32_t>(K, 1) : key_cap(dm, cap);
   CU(cudaMallocAsync(&blk->ptr, node_bytes(dm, cap, kcap), st));
   Node* nd = new Node();
   nd->model = m;
   nd->block = blk;
   nd->cap = cap;
   nd->kcap = kcap;
+  nd->gn = K;
   char* p = static_cast<char*>(blk->ptr);
   carve_node(nd, dm, p);
   nd->n = n;
@@ -721,12 +735,24 @@ static void free_batch(despot_batch* b, bool drop_new_nodes) {
   }
   if (b->scratch) cudaFreeAsync(b->scratch, b->stream);
   if (b->stage) cudaFreeAsync(b->stage, b->stream);
+  if (b->gbuf) cudaFreeAsync(b->gbuf, b->stream);
+  if (b->mscratch) cudaFreeAsync(b->mscratch, b->stream);
   if (b->pinned) {
     cudaStreamSynchronize(b->stream);  // the H2D from it must have completed
     pinned_pool().release(b->pinned);
   }
   if (b->timing) event_pool().release(b->ev);
   delete b;
+}
+
+static int launch_group_sparse(despot_model* m, despot_batch* b) {
+  uint32_t tbits = 1;
+  while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
+  const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
+  kernel_occupancy((const void*)k3_group_sparse, smem, 512);  // sets the smem attribute if > 48 KB
+  k3_group_sparse<<<(unsigned)((uint64_t)b->L * b->A), 512, smem, b->stream>>>(b->bd, b->io, tbits, b->xmax);
+  ++b->launches;
+  return check_launch(m, "K3a(sparse)");
 }
 
 static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
@@ -779,6 +805,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   b->A = dm.A;
   b->S = dm.slots;
   b->sparse = dm.slots == 0;
+  b->sharded_sparse = b->sparse && m->world > 1;
   b->flags = flags;
   b->leaves.assign(leaves, leaves + L);
   b->timing = flags & DESPOT_X_TIMING;
@@ -801,7 +828,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     if (lf.action >= 0) {
       if (!p->expanded) return set_err(DESPOT_EINVAL, "leaf %u: parent not expanded", l);
       if (lf.depth != p->depth + 1) return set_err(DESPOT_EINVAL, "leaf %u: depth != parent depth + 1", l);
-      new_bytes += node_bytes(dm, p->cap, key_cap(dm, p->cap));
+      new_bytes += node_bytes(dm, p->cap, child_kcap(m, p));
     } else if (lf.depth != p->depth) {
       return set_err(DESPOT_EINVAL, "leaf %u: depth != node depth", l);
     }
@@ -835,7 +862,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       nd->model = m;
       nd->block = b->new_block;
       nd->cap = p->cap;
-      nd->kcap = key_cap(dm, p->cap);
+      nd->kcap = child_kcap(m, p);
+      nd->gn = p->gn;
       carve_node(nd, dm, np);
       nd->n = 0;
       nd->depth = lf.depth;
@@ -895,7 +923,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   off += (stat_bytes + 7) & ~size_t(7);
   const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
                o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
-               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound);
+               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound),
+               o_xmax = take(b->sharded_sparse ? 16 : 0);
   if (cudaMallocAsync(&b->scratch, off, st) != cudaSuccess) {
     free_batch(b.release(), true);
     return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
@@ -921,6 +950,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     b->io.hash = reinterpret_cast<uint64_t*>(s + o_hash);
     b->io.keys = reinterpret_cast<uint32_t*>(s + o_keys);
     b->io.q3 = reinterpret_cast<int64_t*>(s + o_q3);
+    b->io.kstride = dm.OW;
+    if (b->sharded_sparse) b->xmax = reinterpret_cast<int64_t*>(s + o_xmax);
   }
   // all leaves are nodes themselves (e.g. roots): their sizes are known on the
   // host, so the update kernel and the prefix are skipped and the host ships
@@ -954,6 +985,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     }
     if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
         cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
+        (b->xmax && cudaMemsetAsync(b->xmax, 0, 16, st) != cudaSuccess) ||
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
   }
@@ -972,6 +1004,10 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       return check_launch(m, "K1");
     });
     if (!rc && !(flags & DESPOT_X_RECORD_SCENARIO)) rc = launch_k2_sparse(m, b.get(), false);
+    if (!rc && b->sharded_sparse) {  // local grouping now: its records are what the ranks exchange
+      b->mark(5);
+      rc = launch_group_sparse(m, b.get());
+    }
   } else if (!rc) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
@@ -1037,13 +1073,117 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   return begin_impl(m, leaves, L, flags, stream, nullptr, out);
 }
 
+// Exchange rounds of a sharded batch.  Dense keys: one round (SUM of the exact
+// partials, MIN of the first ids).  Sparse keys: round 0 sums the per-action
+// partials and the step count and MAXes (local record count, largest local
+// child set); round 1 hands out the all-gather buffer with this rank's
+// records packed into its block.
 extern "C" int despot_batch_exchange(despot_batch* b, despot_exchange* out) {
   if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
-  out->sums = b->bd.sums;
-  out->n_sums = b->n_sums;
-  out->mins = b->bd.mins;
-  out->n_mins = b->n_mins;
+  memset(out, 0, sizeof *out);
+  const uint64_t LA = (uint64_t)b->L * b->A;
+  const SumLayout lay{LA * b->S, LA};
+  out->round = b->xround;
+  if (!b->sharded_sparse) {
+    if (b->xround >= 1) return set_err(DESPOT_EINVAL, "exchange: no further round (more == 0)");
+    out->sums = b->bd.sums;
+    out->n_sums = b->n_sums;
+    out->mins = b->bd.mins;
+    out->n_mins = b->n_mins;
+    b->xround = 1;
+    return DESPOT_OK;
+  }
+  if (b->xround == 0) {
+    out->sums = b->bd.sums + lay.Q(0, 0);  // [L*A][3] per-action partials + the step count
+    out->n_sums = 3 * LA + 1;
+    out->maxs = b->xmax;
+    out->n_maxs = 2;
+    out->more = 1;
+    b->xround = 1;
+    return DESPOT_OK;
+  }
+  if (b->xround != 1) return set_err(DESPOT_EINVAL, "exchange: no further round (more == 0)");
+  despot_model* m = b->model;
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = b->stream;
+  // the all-reduced maxima size the blocks (identical on every rank)
+  int64_t* hx = static_cast<int64_t*>(pinned_pool().acquire(16));
+  if (!hx) return set_err(DESPOT_ENOMEM, "pinned staging");
+  const bool ok = cudaMemcpyAsync(hx, b->xmax, 16, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+                  cudaStreamSynchronize(st) == cudaSuccess;
+  b->rmax = (uint64_t)hx[0];
+  b->ncmax = (uint64_t)hx[1];
+  pinned_pool().release(hx);
+  if (!ok) return set_err(DESPOT_ECUDA, "exchange: reading the reduced maxima failed");
+  b->rec_bytes = sparse_record_bytes(m->host.OW);
+  b->hdr_pad = (uint32_t)(((4 * LA + b->rec_bytes - 1) / b->rec_bytes) * b->rec_bytes);
+  b->gblk = b->hdr_pad + b->rmax * b->rec_bytes;
+  const size_t gbytes = (size_t)m->world * b->gblk;
+  if (cudaMallocAsync(&b->gbuf, gbytes, st) != cudaSuccess || cudaMallocAsync(&b->mscratch, 4 * LA, st) != cudaSuccess)
+    return set_err(DESPOT_ENOMEM, "exchange: all-gather buffer (%zu bytes)", gbytes);
+  PackDev pk{static_cast<unsigned char*>(b->gbuf) + (size_t)m->rank * b->gblk, b->hdr_pad, b->rec_bytes,
+             static_cast<uint32_t*>(b->mscratch)};
+  k_pack_sparse_scan<<<1, 1024, 0, st>>>(b->bd, pk);
+  k_pack_sparse<<<(unsigned)LA, 128, 0, st>>>(b->bd, b->io, pk);
+  b->launches += 2;
+  if (int rc = check_launch(m, "exchange pack")) return rc;
+  out->gather = b->gbuf;
+  out->gather_bytes = b->gblk;
+  b->xround = 2;
   return DESPOT_OK;
+}
+
+// End of a sharded sparse batch: merge the gathered records into global
+// children (b->bd then points at the merged rows, b->io at the records' keys).
+static int merge_sparse(despot_model* m, despot_batch* b) {
+  if (b->xround != 2) return set_err(DESPOT_EINVAL, "sharded sparse batch: exchange rounds not completed");
+  cudaStream_t st = b->stream;
+  BatchDev& bd = b->bd;
+  const uint64_t LA = (uint64_t)b->L * b->A;
+  const uint32_t W = (uint32_t)m->world;
+  const uint64_t nmax = std::max<uint64_t>(1, W * b->ncmax);  // items (and children) per (leaf, action)
+  if (nmax > 4096) return set_err(DESPOT_EINVAL, "sharded sparse merge: more than 4096 children per (leaf, action)");
+  const SumLayout old_lay{LA * b->S, LA};
+  const uint32_t mS = (uint32_t)nmax;
+  const SumLayout lay{LA * mS, LA};
+  // merged rows: offsets [W][LA] | sums | mins | sp_item | nc
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align256(bytes);
+    return o;
+  };
+  const size_t o_offs = take(4 * W * LA), o_sums = take(8 * lay.total()), o_mins = take(4 * LA * mS),
+               o_item = take(4 * LA * mS), o_nc = take(4 * LA);
+  void* ms = nullptr;
+  if (cudaMallocAsync(&ms, off, st) != cudaSuccess) return set_err(DESPOT_ENOMEM, "merge scratch (%zu bytes)", off);
+  cudaFreeAsync(b->mscratch, st);  // the pack offsets are no longer needed
+  b->mscratch = ms;
+  char* s = static_cast<char*>(ms);
+  int64_t* nsums = reinterpret_cast<int64_t*>(s + o_sums);
+  if (cudaMemsetAsync(nsums, 0, 8 * lay.Q(0, 0), st) != cudaSuccess ||
+      cudaMemcpyAsync(nsums + lay.Q(0, 0), bd.sums + old_lay.Q(0, 0), 8 * (3 * LA + 1), cudaMemcpyDeviceToDevice,
+                      st) != cudaSuccess ||
+      cudaMemsetAsync(s + o_mins, 0x7F, 4 * LA * mS, st) != cudaSuccess)
+    return set_err(DESPOT_ECUDA, "merge setup failed");
+  bd.sums = nsums;
+  bd.mins = reinterpret_cast<int32_t*>(s + o_mins);
+  bd.sp_item = reinterpret_cast<uint32_t*>(s + o_item);
+  bd.nc = reinterpret_cast<uint32_t*>(s + o_nc);
+  bd.S = mS;
+  b->S = mS;
+  MergeDev g{static_cast<const unsigned char*>(b->gbuf), b->gblk, b->hdr_pad, b->rec_bytes, W,
+             reinterpret_cast<uint32_t*>(s + o_offs)};
+  k_merge_offsets<<<1, 1024, 0, st>>>(bd, g);
+  uint32_t tbits = 1;
+  while ((1ull << tbits) < 2 * nmax) ++tbits;
+  const size_t smem = 16 * ((size_t)1 << tbits) + 12 * nmax;
+  kernel_occupancy((const void*)k3_merge_sparse, smem, 512);  // sets the smem attribute if > 48 KB
+  k3_merge_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, g, tbits);
+  b->launches += 2;
+  b->io.keys = reinterpret_cast<uint32_t*>(static_cast<char*>(b->gbuf) + kRecKey);
+  b->io.kstride = b->rec_bytes / 4;
+  return check_launch(m, "K3a(merge)");
 }
 
 extern "C" int despot_batch_abort(despot_batch* b) {
@@ -1187,15 +1327,10 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   // K2's last CTA, already done, when the batch was fused)
   const bool small_k3 = !b->sparse && LA <= kSmallLA && b->S <= 32;
   if (b->k3_fused) {
+  } else if (!rc && b->sharded_sparse) {
+    rc = merge_sparse(m, b);  // the ranks' records -> global children
   } else if (!rc && b->sparse) {
-    uint32_t tbits = 1;
-    while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
-    const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
-    const int occ = kernel_occupancy((const void*)k3_group_sparse, smem, 512);
-    (void)occ;
-    k3_group_sparse<<<(unsigned)LA, 512, smem, st>>>(bd, b->io, tbits);
-    ++b->launches;
-    rc = check_launch(m, "K3a(sparse)");
+    rc = launch_group_sparse(m, b);
   } else if (!rc && small_k3) {
     // small batch: rank + scan + write in one CTA (one launch instead of three)
     const size_t smem = small_finalize_smem(LA);
@@ -1215,7 +1350,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     rc = check_launch(m, "K3b");
   }
   if (!rc && b->sparse) {
-    k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);
+    k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);  // (merged: keys from the gathered records)
     ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
   } else if (!rc && !small_k3) {

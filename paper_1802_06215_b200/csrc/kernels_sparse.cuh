@@ -112,9 +112,10 @@ __device__ __forceinline__ uint32_t find_leaf(const uint64_t* off, uint32_t L, u
 }
 
 struct SparseItemOut {
-  uint64_t* hash;  // [Q]
-  uint32_t* keys;  // [Q*OW]
-  int64_t* q3;     // [Q*3]  W, U, LAMBDA contributions
+  uint64_t* hash;    // [Q]
+  uint32_t* keys;    // [Q*OW]  (item q's key at keys + q * kstride)
+  int64_t* q3;       // [Q*3]  W, U, LAMBDA contributions
+  uint32_t kstride;  // words between consecutive keys: OW, or a merged record's size
 };
 
 // ---------------------------------------------------------------------------
@@ -348,7 +349,8 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
 // order (= first-occurrence order, R8), and every item adds its exact
 // fixed-point contributions to its child's row of the exchange block.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io, uint32_t tbits) {
+__global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io, uint32_t tbits,
+                                                       int64_t* xmax) {
   extern __shared__ __align__(16) unsigned char gs_smem[];
   const uint32_t tsize = 1u << tbits, tmask = tsize - 1u;
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gs_smem);  // [tsize]
@@ -425,7 +427,13 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
       b.sp_item[slot] = (uint32_t)(q0 + i);
     }
   }
-  if (threadIdx.x == 0) b.nc[la] = run;
+  if (threadIdx.x == 0) {
+    b.nc[la] = run;
+    if (xmax) {  // sharded: this rank's record count and largest child set
+      atomicAdd((unsigned long long*)&xmax[0], (unsigned long long)run);
+      atomicMax((unsigned long long*)&xmax[1], (unsigned long long)run);
+    }
+  }
 }
 
 // K3c for sparse keys: one CTA per (leaf, action), one thread per child
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut
     wt += W;
     nt += N;
     const uint32_t oc = cb + c;
-    const uint32_t* key = io.keys + (uint64_t)b.sp_item[base + c] * OW;
+    const uint32_t* key = io.keys + (uint64_t)b.sp_item[base + c] * io.kstride;
     if (oc < b.child_capacity) {
       const double Wd = (double)W;
       b.child_count[oc] = (uint32_t)N;
@@ -486,6 +494,191 @@ __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut
       if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Scenario-sharded sparse keys (world > 1).  Every rank groups
+// its own scenarios (k3_group_sparse), packs its local children as fixed-size
+// records into its block of an all-gather buffer, the caller all-gathers the
+// blocks, and every rank merges the same P blocks the same way: records with
+// equal keys are one child (exact compare; the 64-bit hash only indexes),
+// the child's sums are exact int64 sums, its first id the minimum, and the
+// children are ordered by first id -- the world == 1 result, bit for bit.
+//
+// block of rank r: [nc[L*A] u32 | pad to hdr_pad | records, (leaf, action)-major]
+// record: hash u64 | N, W, U, LAMBDA i64 | first i32 | key[OW] u32 (8-aligned)
+// ---------------------------------------------------------------------------
+constexpr uint32_t kRecN = 8, kRecFirst = 40, kRecKey = 44;
+__host__ __device__ inline uint32_t sparse_record_bytes(uint32_t OW) { return (kRecKey + 4 * OW + 7) & ~7u; }
+
+struct PackDev {
+  unsigned char* blk;  // this rank's block
+  uint32_t hdr_pad, rec_bytes;
+  uint32_t* loc_off;   // [L*A] record offset of each (leaf, action)
+};
+// header + record offsets (one CTA)
+__global__ void __launch_bounds__(1024) k_pack_sparse_scan(BatchDev b, PackDev p) {
+  __shared__ uint64_t wsum[32];
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const uint64_t per = (LA + blockDim.x - 1) / blockDim.x, i0 = (uint64_t)threadIdx.x * per;
+  uint64_t loc = 0;
+  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += b.nc[i];
+  uint64_t tot;
+  uint64_t run = block_excl_scan(loc, wsum, tot);
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(p.blk);
+  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) {
+    p.loc_off[i] = (uint32_t)run;
+    hdr[i] = b.nc[i];
+    run += b.nc[i];
+  }
+}
+// records: one CTA per (leaf, action)
+__global__ void __launch_bounds__(128) k_pack_sparse(BatchDev b, SparseItemOut io, PackDev p) {
+  const uint64_t la = blockIdx.x;
+  const uint32_t OW = b.model->OW;
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  const uint64_t base = la * b.S;
+  const uint32_t nc = b.nc[la];
+  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
+    unsigned char* r = p.blk + p.hdr_pad + (uint64_t)(p.loc_off[la] + c) * p.rec_bytes;
+    const uint32_t it = b.sp_item[base + c];
+    int64_t* q = reinterpret_cast<int64_t*>(r + kRecN);
+    *reinterpret_cast<uint64_t*>(r) = io.hash[it];
+    q[0] = b.sums[lay.N(base + c)];
+    q[1] = b.sums[lay.W(base + c)];
+    q[2] = b.sums[lay.U(base + c)];
+    q[3] = b.sums[lay.Lm(base + c)];
+    *reinterpret_cast<int32_t*>(r + kRecFirst) = b.mins[base + c];
+    uint32_t* key = reinterpret_cast<uint32_t*>(r + kRecKey);
+    for (uint32_t k = 0; k < OW; ++k) key[k] = io.keys[(uint64_t)it * OW + k];
+  }
+}
+
+struct MergeDev {
+  const unsigned char* gbuf;  // world blocks
+  uint64_t blk;               // bytes per block
+  uint32_t hdr_pad, rec_bytes, world;
+  uint32_t* offs;             // [world][L*A] record offset of (rank, leaf, action)
+};
+constexpr uint32_t kMaxMergeWorld = 64;
+// per-rank record offsets of every (leaf, action) (one CTA, ranks in turn)
+__global__ void __launch_bounds__(1024) k_merge_offsets(BatchDev b, MergeDev g) {
+  __shared__ uint64_t wsum[32];
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const uint64_t per = (LA + blockDim.x - 1) / blockDim.x, i0 = (uint64_t)threadIdx.x * per;
+  for (uint32_t r = 0; r < g.world; ++r) {
+    const uint32_t* hdr = reinterpret_cast<const uint32_t*>(g.gbuf + r * g.blk);
+    uint64_t loc = 0;
+    for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += hdr[i];
+    uint64_t tot;
+    uint64_t run = block_excl_scan(loc, wsum, tot);
+    for (uint64_t i = i0; i < i0 + per && i < LA; ++i) {
+      g.offs[r * LA + i] = (uint32_t)run;
+      run += hdr[i];
+    }
+  }
+}
+// one CTA per (leaf, action): union of the ranks' records -> global children
+// in b.sums/mins/sp_item/nc (b.S = merged row capacity); sp_item holds the
+// representative's record index in gbuf units of rec_bytes
+__global__ void __launch_bounds__(512) k3_merge_sparse(BatchDev b, MergeDev g, uint32_t tbits) {
+  extern __shared__ __align__(16) unsigned char mg_smem[];
+  const uint32_t tsize = 1u << tbits, tmask = tsize - 1u;
+  unsigned long long* tkey = reinterpret_cast<unsigned long long*>(mg_smem);  // [tsize]
+  unsigned long long* trep = tkey + tsize;                                     // [tsize] (first << 32 | item)
+  __shared__ uint32_t rs[kMaxMergeWorld + 1], nrep;
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const uint64_t la = blockIdx.x;
+  const uint32_t OW = b.model->OW;
+  const SumLayout lay{LA * b.S, LA};
+  const uint64_t base = la * b.S;
+  if (threadIdx.x == 0) {
+    rs[0] = 0;
+    for (uint32_t r = 0; r < g.world; ++r)
+      rs[r + 1] = rs[r] + reinterpret_cast<const uint32_t*>(g.gbuf + r * g.blk)[la];
+    nrep = 0;
+  }
+  for (uint32_t s = threadIdx.x; s < tsize; s += blockDim.x) {
+    tkey[s] = 0ull;
+    trep[s] = ~0ull;
+  }
+  __syncthreads();
+  const uint32_t n = rs[g.world];
+  uint32_t* ord = reinterpret_cast<uint32_t*>(trep + tsize);  // [n] ordinal of a representative
+  int32_t* rfirst = reinterpret_cast<int32_t*>(ord + n);      // [n] representatives' first ids
+  uint32_t* ritem = reinterpret_cast<uint32_t*>(rfirst + n);  // [n] representatives' items
+  auto rec_index = [&](uint32_t i) -> uint64_t {  // global record index of item i
+    uint32_t r = 0;
+    while (rs[r + 1] <= i) ++r;
+    return (r * g.blk + g.hdr_pad) / g.rec_bytes + g.offs[r * LA + la] + (i - rs[r]);
+  };
+  auto rec = [&](uint64_t gi) { return g.gbuf + gi * g.rec_bytes; };
+  auto slot_of = [&](unsigned long long h) {
+    uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
+    while (tkey[s] != h) s = (s + 1u) & tmask;
+    return s;
+  };
+  // 1. insert: per hash, the item with the smallest first id
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned char* r = rec(rec_index(i));
+    unsigned long long h = *reinterpret_cast<const unsigned long long*>(r);
+    h = h ? h : 1ull;
+    uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
+    for (;;) {
+      const unsigned long long prev = atomicCAS(&tkey[s], 0ull, h);
+      if (prev == 0ull || prev == h) break;
+      s = (s + 1u) & tmask;
+    }
+    const uint32_t first = (uint32_t)*reinterpret_cast<const int32_t*>(r + kRecFirst);
+    atomicMin(&trep[s], ((unsigned long long)first << 32) | i);
+  }
+  __syncthreads();
+  // 2. representatives; every other item's key must equal its representative's
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t gi = rec_index(i);
+    const unsigned char* r = rec(gi);
+    unsigned long long h = *reinterpret_cast<const unsigned long long*>(r);
+    const unsigned long long t = trep[slot_of(h ? h : 1ull)];
+    const uint32_t rep = (uint32_t)t;
+    if (rep == i) {
+      const uint32_t j = atomicAdd(&nrep, 1u);
+      rfirst[j] = (int32_t)(t >> 32);
+      ritem[j] = i;
+    } else {
+      const uint32_t* ki = reinterpret_cast<const uint32_t*>(r + kRecKey);
+      const uint32_t* kj = reinterpret_cast<const uint32_t*>(rec(rec_index(rep)) + kRecKey);
+      for (uint32_t k = 0; k < OW; ++k)
+        if (ki[k] != kj[k]) atomicOr(b.err, kErrHash);
+    }
+  }
+  __syncthreads();
+  // 3. ordinal = number of representatives with a smaller first id (R8)
+  const uint32_t nr = nrep;
+  for (uint32_t j = threadIdx.x; j < nr; j += blockDim.x) {
+    const int32_t f = rfirst[j];
+    uint32_t o = 0;
+    for (uint32_t q = 0; q < nr; ++q) o += rfirst[q] < f;
+    ord[ritem[j]] = o;
+  }
+  __syncthreads();
+  // 4. exact sums per global child
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t gi = rec_index(i);
+    const unsigned char* r = rec(gi);
+    unsigned long long h = *reinterpret_cast<const unsigned long long*>(r);
+    const uint32_t rep = (uint32_t)trep[slot_of(h ? h : 1ull)];
+    const uint64_t slot = base + ord[rep];
+    const int64_t* q = reinterpret_cast<const int64_t*>(r + kRecN);
+    atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], (unsigned long long)q[0]);
+    atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)q[1]);
+    atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)q[2]);
+    atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)q[3]);
+    if (rep == i) {
+      b.mins[slot] = *reinterpret_cast<const int32_t*>(r + kRecFirst);
+      b.sp_item[slot] = (uint32_t)gi;
+    }
+  }
+  if (threadIdx.x == 0) b.nc[la] = nr;
 }
 
 }  // namespace hd

@@ -117,7 +117,9 @@ def search(problem: SearchProblem, config: SearchConfig, dump_capacity=0):
 
 
 class Exchange(C.Structure):
-    _fields_ = [("sums", C.c_void_p), ("n_sums", C.c_uint64), ("mins", C.c_void_p), ("n_mins", C.c_uint64)]
+    _fields_ = [("sums", C.c_void_p), ("n_sums", C.c_uint64), ("mins", C.c_void_p), ("n_mins", C.c_uint64),
+                ("maxs", C.c_void_p), ("n_maxs", C.c_uint64), ("gather", C.c_void_p), ("gather_bytes", C.c_uint64),
+                ("round", C.c_uint32), ("more", C.c_uint32)]
 
 
 _lib = None
@@ -235,11 +237,17 @@ class Model:
         return lv
 
     def child_capacity_bound(self, leaves):
+        """Children bound of a batch: A * min(|Phi|, slots) per leaf.  Under
+        sharding |Phi| is global and only the local count is known here, so
+        the bound is (n + 1) * world -- exact for interleaved roots; a
+        filtered node may need more, which the call reports as ECAPACITY."""
         per = self.slots if self.slots else None
+        W = max(self.world, 1)
         tot = 0
         for (p, a, c, d) in leaves:
             n, _ = self.node_info(p)
-            tot += self.A * (min(n * max(self.world, 1), per) if per else n)
+            g = n if W == 1 else (n + 1) * W
+            tot += self.A * (min(g, per) if per else g)
         return max(tot, 1)
 
     def _alloc_outputs(self, L, C_cap, S_cap, record, device):
@@ -361,6 +369,13 @@ class Model:
         E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_TIMING if timing else 0)
         _check(lib().despot_expand_end(batch, C.byref(E), _stream_ptr(stream)))
         return self._finish(o, E, L, nodes, False, device_outputs)
+
+    def batch_exchange(self, batch):
+        """The next exchange round of a sharded batch (after the caller ran
+        the previous round's collectives); see dist.run_exchange."""
+        ex = Exchange()
+        _check(lib().despot_batch_exchange(batch, C.byref(ex)))
+        return ex
 
     def batch_abort(self, batch):
         _check(lib().despot_batch_abort(batch))

@@ -4,8 +4,10 @@ Every rank loads the same belief with despot_opts{rank, world}; the library
 keeps the scenarios with global id % world == rank.  A batch then runs
 begin (update + expansion + roll-outs + grouping on the local shard) ->
 exchange (all-reduce SUM of the exact int64 fixed-point partials and MIN of
-the first-occurrence ids, here via torch.distributed / NCCL over NVLink) ->
-end (child order, CSR and outputs, identical on every rank).
+the first-occurrence ids, here via torch.distributed / NCCL over NVLink; for
+the driving model's sparse keys a second round all-gathers the ranks' child
+records) -> end (merge, child order, CSR and outputs, identical on every
+rank).
 """
 from __future__ import annotations
 
@@ -28,22 +30,65 @@ class _CudaArray:
 
 
 def exchange_views(ex, device):
-    sums = torch.as_tensor(_CudaArray(ex.sums, ex.n_sums, "<i8"), device=device)
-    mins = torch.as_tensor(_CudaArray(ex.mins, ex.n_mins, "<i4"), device=device)
-    return sums, mins
+    """(sums, mins) views of a dense-key exchange round (kept for callers of
+    the one-round form); see round_views for every collective of a round."""
+    v = round_views(ex, device)
+    return v["sums"], v["mins"]
 
 
-def exchange(sums: torch.Tensor, mins: torch.Tensor, group=None):
-    """The one collective step of a sharded batch: exact, order-independent."""
-    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+def round_views(ex, device):
+    """Zero-copy tensors of one exchange round: sums (SUM), mins (MIN), maxs
+    (MAX), gather (all-gather, uint8 [world * gather_bytes]); None if unused."""
+    def view(ptr, n, typestr):
+        return torch.as_tensor(_CudaArray(ptr, n, typestr), device=device) if ptr and n else None
+    return {"sums": view(ex.sums, ex.n_sums, "<i8"), "mins": view(ex.mins, ex.n_mins, "<i4"),
+            "maxs": view(ex.maxs, ex.n_maxs, "<i8"), "gather": None if not ex.gather_bytes else
+            (int(ex.gather), int(ex.gather_bytes))}
+
+
+def exchange(sums: torch.Tensor, mins: torch.Tensor, group=None, maxs=None, gather=None):
+    """The collectives of one exchange round, in place: exact integer sums,
+    minima and maxima (order-independent), and the all-gather of the ranks'
+    blocks (`gather` = the whole [world * block] byte tensor; this rank's block
+    is already filled)."""
+    if sums is not None:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    if mins is not None:
+        dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
+    if maxs is not None:
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+    if gather is not None:
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        blk = gather.numel() // world
+        mine = gather[rank * blk:(rank + 1) * blk]
+        if gather.is_cuda:
+            dist.all_gather_into_tensor(gather, mine.clone(), group=group)
+        else:  # gloo: list form
+            parts = list(gather.split(blk))
+            dist.all_gather(parts, mine.clone(), group=group)
+
+
+def run_exchange(model, batch, ex, group=None):
+    """Every exchange round of a sharded batch (one for dense keys, two for
+    the driving model's sparse keys)."""
+    device = torch.device("cuda", model.device)
+    world = dist.get_world_size(group)
+    while True:
+        v = round_views(ex, device)
+        gather = None
+        if v["gather"] is not None:
+            ptr, blk = v["gather"]
+            gather = torch.as_tensor(_CudaArray(ptr, world * blk, "|u1"), device=device)
+        exchange(v["sums"], v["mins"], group, maxs=v["maxs"], gather=gather)
+        if not ex.more:
+            return
+        ex = model.batch_exchange(batch)
 
 
 def expand_sharded(model, leaves, group=None, device_outputs=False, child_capacity=None, stream=None):
     batch, ex = model.expand_begin(leaves, stream=stream)
     try:
-        sums, mins = exchange_views(ex, torch.device("cuda", model.device))
-        exchange(sums, mins, group)
+        run_exchange(model, batch, ex, group)
     except Exception:
         model.batch_abort(batch)
         raise

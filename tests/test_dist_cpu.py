@@ -29,6 +29,11 @@ def _partials(rank, n_sums=1000, n_mins=300):
     return sums, mins
 
 
+def _block(rank, nbytes=1024):
+    """this rank's all-gather block (the sparse-key records, §6.2)"""
+    return np.random.default_rng(500 + rank).integers(0, 256, nbytes, dtype=np.uint8)
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -36,12 +41,19 @@ def _worker(rank, world, port, q):
     s, m = _partials(rank)
     ts, tm = torch.from_numpy(s.copy()), torch.from_numpy(m.copy())
     ddist.exchange(ts, tm)
-    q.put((rank, ts.numpy().copy(), tm.numpy().copy()))
+    # the sparse-key rounds: MAX of (record count, largest child set), then
+    # the in-place all-gather of every rank's block
+    tx = torch.tensor([100 + 7 * rank, 3 - rank], dtype=torch.int64)
+    blk = _block(rank)
+    g = torch.zeros(world * blk.size, dtype=torch.uint8)
+    g[rank * blk.size:(rank + 1) * blk.size] = torch.from_numpy(blk)
+    ddist.exchange(None, None, maxs=tx, gather=g)
+    q.put((rank, ts.numpy().copy(), tm.numpy().copy(), tx.numpy().copy(), g.numpy().copy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_exchange_sum_min_world2_gloo():
+def test_exchange_sum_min_max_gather_world2_gloo():
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
@@ -56,9 +68,13 @@ def test_exchange_sum_min_world2_gloo():
     parts = [_partials(r) for r in range(world)]
     want_s = sum(p[0] for p in parts)  # int64 wrap-around arithmetic is exact either way
     want_m = np.minimum(parts[0][1], parts[1][1])
-    for _, s, m in res:
+    want_x = np.array([100 + 7 * (world - 1), 3], dtype=np.int64)
+    want_g = np.concatenate([_block(r) for r in range(world)])
+    for _, s, m, x, g in res:
         assert np.array_equal(s, want_s)
         assert np.array_equal(m, want_m)
+        assert np.array_equal(x, want_x)
+        assert np.array_equal(g, want_g)
     # order independence: reversing the ranks' contributions gives the same bits
     assert np.array_equal(parts[1][0] + parts[0][0], want_s)
 

@@ -421,7 +421,7 @@ def test_concurrent_batches_from_host_threads():
             assert np.array_equal(got[i][k], ref[i][k]), (i, k)
 
 
-def test_sharded_model_rejects_record_and_sparse():
+def test_sharded_model_rejects_record_and_single_call():
     kind, params, st, w, seed, _ = inputs.config_inputs(2, K=40)
     m = Model(kind, params, rank=0, world=2)
     r = m.belief_load(st, w, seed)
@@ -430,8 +430,79 @@ def test_sharded_model_rejects_record_and_sparse():
         m.expand([(r, -1, 0, 0)])  # world > 1: begin / exchange / end only
     with pytest.raises(DespotError):
         m.expand_begin([(r, -1, 0, 0)], record=True)
+    mc = Model("car", inputs.car_params(), rank=0, world=2)  # sparse keys shard too (two exchange rounds)
+    rc = mc.belief_load(*inputs.car_roots(1, 30)[0])
     with pytest.raises(DespotError):
-        Model("car", inputs.car_params(), rank=0, world=2)
+        mc.expand([(rc, -1, 0, 0)])
+
+
+def _emulate_ranks(ms, leaf_lists):
+    """The ranks of a sharded batch emulated one after the other on one GPU:
+    every exchange round's SUM / MIN / MAX and all-gather done with torch."""
+    import torch
+    from paper_1802_06215_b200.dist import _CudaArray, round_views
+    dev = torch.device("cuda", 0)
+    begun = [m.expand_begin(ll) for m, ll in zip(ms, leaf_lists)]
+    exs = [ex for _, ex in begun]
+    W = len(ms)
+    while True:
+        views = [round_views(ex, dev) for ex in exs]
+        torch.cuda.synchronize()
+        for key in ("sums", "mins", "maxs"):
+            vs = [v[key] for v in views]
+            if vs[0] is None:
+                continue
+            s = torch.stack(vs)
+            red = s.sum(0) if key == "sums" else s.min(0).values if key == "mins" else s.max(0).values
+            for v in vs:
+                v.copy_(red)
+        if views[0]["gather"] is not None:
+            blk = views[0]["gather"][1]
+            assert all(v["gather"][1] == blk for v in views)  # identical block size on every rank
+            bufs = [torch.as_tensor(_CudaArray(v["gather"][0], W * blk, "|u1"), device=dev) for v in views]
+            for r in range(W):
+                for q in range(W):
+                    if q != r:
+                        bufs[q][r * blk:(r + 1) * blk].copy_(bufs[r][r * blk:(r + 1) * blk])
+        torch.cuda.synchronize()
+        if not exs[0].more:
+            assert not any(ex.more for ex in exs)
+            break
+        exs = [m.batch_exchange(b) for m, (b, _) in zip(ms, begun)]
+    cap = 4 * max(m.child_capacity_bound(ll) for m, ll in zip(ms, leaf_lists))  # filtered nodes: see the bound
+    return [m.expand_end(b, ll, child_capacity=cap) for m, (b, _), ll in zip(ms, begun, leaf_lists)]
+
+
+def test_car_sharded_equals_single_gpu():
+    """Driving (sparse 21-word keys) scenario-sharded over 2/3/4 emulated ranks:
+    local grouping, MAX round, record all-gather, exact-key merge -- equal to
+    world == 1 bit for bit, for 6 roots and for depth-1 children (K1 filters
+    by the merged global child keys)."""
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+            "child_first", "child_weight", "child_upper", "child_lower", "child_obs")
+    params = inputs.car_params(6, D=30)
+    croots = inputs.car_roots(6, 80, peds=6)
+    g1 = Model("car", params)
+    r1 = [g1.belief_load(s, w_, sd) for s, w_, sd in croots]
+    ref0 = g1.expand([(r, -1, 0, 0) for r in r1])
+    R = g1.expand([(r1[0], -1, 0, 0)])
+    lv = inputs.select_leaves(R["child_count"], R["child_begin"], g1.A, 5)
+    ref1 = g1.expand([(r1[0], a, c, 1) for a, c in lv])
+
+    def same(o, ref, tag):
+        for k in keys:
+            assert np.array_equal(o[k], ref[k]), (tag, k)
+        assert o["scenario_steps"] == ref["scenario_steps"], tag
+
+    for world in (2, 3, 4):
+        ms = [Model("car", params, rank=r, world=world) for r in range(world)]
+        roots = [[m.belief_load(s, w_, sd) for s, w_, sd in croots] for m in ms]
+        for o in _emulate_ranks(ms, [[(r, -1, 0, 0) for r in rt] for rt in roots]):
+            same(o, ref0, (world, "roots"))
+        for o in _emulate_ranks(ms, [[(rt[0], -1, 0, 0)] for rt in roots]):
+            same(o, R, (world, "root 0"))
+        for o in _emulate_ranks(ms, [[(rt[0], a, c, 1) for a, c in lv] for rt in roots]):
+            same(o, ref1, (world, "children"))
 
 
 def test_gpu_scenario_prefix_is_stable_across_K():
