@@ -150,6 +150,12 @@ struct LeafDev {
 // error bits of a batch
 enum : uint32_t { kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u };
 
+// status block of a batch (zeroed per batch; the host reads it back in one copy)
+enum : uint32_t {
+  kStatErr = 0, kStatChildren = 1, kStatSteps = 2 /* u64: 2-3 */, kStatK1Ticket = 4, kStatK2Ticket = 5,
+  kStatK2Tile = 6 /* K2's dynamic tile counter */, kStatWords = 8 /* then n_leaf[L] */
+};
+
 struct BatchDev {
   const DevModel* model;
   const LeafDev* leaves;
@@ -161,7 +167,7 @@ struct BatchDev {
   int32_t* mins;             // exchange MIN block
   uint32_t* rank;            // [L*A*S] child ordinal of a slot
   uint32_t* nc;              // [L*A] children per (leaf, action)
-  uint32_t* status;          // [err, total children, steps lo, steps hi, K1 ticket, K2 ticket, n_leaf[L]]
+  uint32_t* status;          // [kStatWords header (kStat*), n_leaf[L]]
   uint32_t fused_k3;         // 1: K2's last CTA runs the small finalize
   uint32_t* err;
   // outputs (device)

@@ -916,7 +916,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   // status block [err u32 | total children u32 | steps u64 | K1 ticket u32 |
   // pad | n_leaf[L] u32] sits right before the SUM block: one memset zeroes
   // both, one D2H reads it
-  const size_t stat_bytes = 24 + 4 * (size_t)L;
+  const size_t stat_bytes = 4 * kStatWords + 4 * (size_t)L;
   const size_t o_leaves = take(sizeof(LeafDev) * L), o_tile = take(4 * ((size_t)L + 1)),
                o_scen = take(8 * ((size_t)L + 1));
   const size_t o_stat = off;
@@ -938,7 +938,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   bd.S = b->S;
   bd.status = reinterpret_cast<uint32_t*>(s + o_stat);
   bd.err = bd.status;
-  bd.n_leaf = bd.status + 6;
+  bd.n_leaf = bd.status + kStatWords;
   bd.tile_off = reinterpret_cast<uint32_t*>(s + o_tile);
   bd.scen_off = reinterpret_cast<uint64_t*>(s + o_scen);
   bd.sums = reinterpret_cast<int64_t*>(s + o_sums);
@@ -974,7 +974,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       uint64_t tacc = 0, sacc = 0;
       for (uint32_t l = 0; l < L; ++l) {
         const uint32_t n = parent[l]->n;
-        stat[6 + l] = n;
+        stat[kStatWords + l] = n;
         tile[l] = (uint32_t)tacc;
         scen[l] = sacc;
         tacc += (uint64_t)dm.A * ((n + 31) / 32);
@@ -1360,7 +1360,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   }
   b->mark(6);
   // status block: err | total children | steps | ticket | pad | n_leaf[L]
-  const size_t stat_bytes = 24 + 4 * (size_t)L;
+  const size_t stat_bytes = 4 * kStatWords + 4 * (size_t)L;
   char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
   struct PinGuard {
     void* p;
@@ -1412,7 +1412,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   if (!rc && !dev_out) {
     const uint64_t Cu = nchildren;
     uint64_t Su = 0;
-    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 24);
+    const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4 * kStatWords);
     for (uint32_t l = 0; l < L; ++l) Su += (uint64_t)dm.A * nl[l];
     struct Part {
       void* dst;
@@ -1471,7 +1471,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     free_batch(b, true);
     return rc;
   }
-  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 24);
+  const uint32_t* nl = reinterpret_cast<const uint32_t*>(hs + 4 * kStatWords);
   for (uint32_t l = 0; l < L; ++l) {
     Node* nd = b->leaf_node[l];
     if (b->is_new[l]) nd->n = nl[l];

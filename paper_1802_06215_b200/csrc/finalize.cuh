@@ -70,7 +70,7 @@ __device__ __forceinline__ void last_cta_prefix(const BatchDev& b) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    am_last = atomicAdd(&b.status[4], 1u) == gridDim.x - 1;
+    am_last = atomicAdd(&b.status[kStatK1Ticket], 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (am_last) {

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
         s = M::load(sm, lf.p_states, lf.p_cap, i);
         id = lf.p_ids[i];
         uint32_t z;
-        if (M::terminal(s)) {
+        if (M::terminal(sm, s)) {
           z = M::kTerminalObs;
         } else {
           float r;
@@ -88,6 +88,11 @@ __global__ void __launch_bounds__(256) k1_update(BatchDev b) {
 // UNI_SEED: every leaf of the batch descends from the same belief, so the
 // Philox key is a kernel parameter (uniform registers; the key schedule costs
 // no per-lane instructions).
+__device__ __forceinline__ uint32_t next_tile(const BatchDev& b, uint32_t nwarps, uint32_t lane) {
+  uint32_t t = 0;
+  if (lane == 0) t = nwarps + atomicAdd(&b.status[kStatK2Tile], 1u);
+  return __shfl_sync(0xffffffffu, t, 0);
+}
 template <class M, bool RECORD, bool UNI_SEED = false>
 __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, const RoundKeys rk) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
@@ -103,7 +108,12 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   const double fx = dm.fx, gamma = dm.gamma;
   const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
   uint32_t steps_acc = 0;
-  for (uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < total; t += nwarps) {
+  // dynamic tile scheduling: a warp's first tile is its index, every later
+  // one comes from a global counter, so the warps finish within about one
+  // tile of each other (a static stride leaves the slowest of ~5000 warps'
+  // sums of ~100 random tile times ~35% above the mean)
+  uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  for (; t < total; t = next_tile(b, nwarps, lane)) {
     // tile -> (leaf, action, chunk)
     uint32_t lo = 0, hi = b.L;  // tile_off[lo] <= t < tile_off[hi]
     while (hi - lo > 1) {
@@ -127,7 +137,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
       const double wn = (double)lf.w[i] * lf.inv_wroot;  // normalised weight
       float r = 0.0f;
       bool term;
-      if (M::terminal(s)) {  // R7: terminal scenarios stay terminal, reward 0
+      if (M::terminal(sm, s)) {  // R7: terminal scenarios stay terminal, reward 0
         z = M::kTerminalObs;
         term = true;
       } else {
@@ -160,7 +170,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
           if (b.scen_states) {
             // s' after the expansion step: recompute (the roll-out consumed s)
             typename M::St s2 = M::load(sm, lf.states, lf.cap, i);
-            if (!M::terminal(s2)) {
+            if (!M::terminal(sm, s2)) {
               uint32_t z2;
               float r2;
               M::step(sm, s2, (int)a, id, lf.depth + 1, key, z2, r2);
@@ -216,7 +226,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      k2_last = atomicAdd(&b.status[5], 1u) == gridDim.x - 1;
+      k2_last = atomicAdd(&b.status[kStatK2Ticket], 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (k2_last) {
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, con
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     typename M::St s = M::load(sm, states, cap, i);
     double u = 0.0, lam = 0.0;
-    if (!M::terminal(s)) {
+    if (!M::terminal(sm, s)) {
       u = M::upper(sm, s);
       uint32_t len;
       uint64_t h = kFnvOffset;

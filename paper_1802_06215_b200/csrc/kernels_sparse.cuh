@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
     if (i < lf.p_n && valid_child) {
       s = M::load(sm, lf.p_states, lf.p_cap, i);
       id = lf.p_ids[i];
-      bool term = M::terminal(s);
+      bool term = M::terminal(sm, s);
       if (!term) {
         float r;
         term = M::step(sm, s, lf.action, id, lf.depth, SeedKey{lf.seed_lo, lf.seed_hi}, r);
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(128) k2_car_thread(BatchDev b, SparseItemOut i
     const uint32_t id = lf.ids[i];
     const double wn = (double)lf.w[i] * lf.inv_wroot;
     float r = 0.0f;
-    bool term = M::terminal(s);
+    bool term = M::terminal(sm, s);
     if (!term) {
       term = M::step(sm, s, (int)a, id, lf.depth + 1, SeedKey{lf.seed_lo, lf.seed_hi}, r);
       ++steps_acc;

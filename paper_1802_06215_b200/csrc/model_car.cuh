@@ -112,7 +112,7 @@ struct CarThreadT {
         st[(5 + 2 * p) * cap + i] = __float_as_uint(s.py[p]);
       }
   }
-  static __device__ __forceinline__ bool terminal(const St& s) { return s.term; }
+  static __device__ __forceinline__ bool terminal(const Sm&, const St& s) { return s.term; }
   static __device__ __forceinline__ uint32_t goal(const St& s, int p) {
     return ((p < 16 ? s.g0 : s.g1) >> (2 * (p & 15))) & 3u;
   }

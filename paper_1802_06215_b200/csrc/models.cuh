@@ -6,7 +6,7 @@
 //   M::Sm                 shared-memory copy of the hot tables
 //   M::load_sm(sm, dm)    cooperative copy (caller syncs)
 //   M::St                 per-thread register state; load/store SoA rows
-//   M::terminal(s)        terminal flag of a state
+//   M::terminal(sm, s)    terminal flag of a state
 //   M::step(...)          g(s, a, phi_t) on a non-terminal state (Eq. 9)
 //   M::upper(...)         per-scenario u(s) of Eq. 11 (non-terminal state)
 //   M::rollout<TRACE>     default-policy roll-out of Eq. 12 to depth D
@@ -50,7 +50,7 @@ struct Tiger {
                                                uint32_t i) {
     st[i] = s.s;
   }
-  static __device__ __forceinline__ bool terminal(const St& s) { return (s.s >> 1) & 1u; }
+  static __device__ __forceinline__ bool terminal(const Sm&, const St& s) { return (s.s >> 1) & 1u; }
   static constexpr uint32_t kTerminalObs = 3u;
   static __device__ __forceinline__ bool step_u(const Sm& sm, St& s, int a, uint32_t u0, uint32_t& z,
                                                 float& r) {
@@ -101,99 +101,121 @@ struct Tiger {
 // word 0: good-rock mask; word 1: 16 bits per robot (y*n+x, 0xFFFF exited).
 // sub-actions: 0 N, 1 S, 2 E, 3 W, 4 SAMPLE, 5+j SENSE j; a = b0 + base*b1.
 //
-// Device representation: a robot is its cell index; every geometric
-// question of a step (which moves stay on the grid, the rock on a cell, the
-// squared distance to a sensed rock, the policy's move toward its target
-// rock) is a shared-memory table lookup built per CTA from the layout.  This
-// moves the step's work from the ALU pipe (the kernel's limiter) to the
-// load/store pipe.
+// Device representation: a robot is its cell index, an exited robot the
+// pseudo-cell EXIT = n*n whose every action is a no-op.  Every geometric
+// question of a step is a shared-memory table lookup built per CTA from the
+// layout: the target cell of each move (with the +10 exit through the east
+// border as a flag bit), the rock on a cell, the sensing threshold of every
+// (cell, rock), and the default policy's move toward each policy position.
+// This moves the step's work from the ALU pipe (the kernel's limiter) to the
+// load/store pipe, and the pseudo-cell removes the per-robot "exited" selects.
 // ===========================================================================
 template <int R>
 struct RockSample {
   static constexpr int kMinBlocks = 8;  // 64 registers: 32 warps per SM
   static constexpr int kMaxTable = 16384;  // n*n*m entries of the per-cell rock tables
+  static constexpr uint32_t kExitFlag = 0x8000u;  // move target flag: the robot exits (+10)
   struct Sm {
-    int32_t n, m, base, ncell;
+    int32_t n, m, mm, base, ncell, exitc;  // exitc = EXIT pseudo-cell = n*n; mm = max(m, 1)
     uint32_t D;
     double tail;
-    int32_t delta[4];        // cell offset of N, S, E, W
     int8_t rx[32], ry[32];
-    uint8_t pos_rock[32];    // default-policy position -> rock index
+    uint8_t senseb[32];      // policy position p -> SENSE sub-action 5 + rock(p); [31] = E (nothing open)
     uint32_t range_mask[2];  // policy positions of robot r (0 for the always-east policy)
     double gpow[kGpowN];
     // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m):
-    uint32_t off_info;  // u32 [cell]: bits 0-3 N,S,E,W stay on the grid; 8-15 rock (0xFF none); 16-23 x; 24-31 y
-    uint32_t off_dir;   // u8  [cell][j]: policy move toward rock j (4 = on it)
-    uint32_t off_d2;    // u16 [cell][j]: squared distance to rock j
-    uint32_t off_thr;   // u32 [d2]: sensing is correct iff u <= thr[d2]
+    uint32_t off_nb;    // u16 [cell][4]: target of N, S, E, W (kExitFlag | EXIT: exits east)
+    uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
+    uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
+    uint32_t off_pol;   // u8  [cell][32]: policy move toward the rock of position p (4 = on it); [31] = E
   };
-  // table bytes (host and device agree): info | d2 | thr | dir
-  static __host__ __device__ size_t table_bytes(int n, int m, uint32_t d2max) {
-    return align16(4 * (size_t)n * n) + align16(2 * (size_t)n * n * m) + align16(4 * ((size_t)d2max + 1)) +
-           align16((size_t)n * n * m);
+  // table bytes (host and device agree): nb | info | thr | pol, all with the EXIT row
+  static __host__ __device__ size_t table_bytes(int n, int m, uint32_t) {
+    const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1;
+    return align16(8 * c) + align16(4 * c) + align16(4 * c * mm) + align16(32 * c);
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
   }
-  static __device__ __forceinline__ uint32_t dir(const Sm& sm, int e) { return hd_dyn_smem[sm.off_dir + e]; }
-  static __device__ __forceinline__ uint32_t d2(const Sm& sm, int e) {
-    return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_d2)[e];
+  static __device__ __forceinline__ uint32_t target(const Sm& sm, int c, int mv) {
+    return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_nb)[c * 4 + mv];
   }
-  static __device__ __forceinline__ uint32_t thr(const Sm& sm, uint32_t d) {
-    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[d];
+  static __device__ __forceinline__ uint32_t thr(const Sm& sm, int c, int j) {
+    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + j];
+  }
+  static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int p) {
+    return hd_dyn_smem[sm.off_pol + c * 32 + p];
   }
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
-    const int n = dm.n, mm = dm.m, nc = n * n;
+    const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc;
     const uint32_t base = (uint32_t)align16(sizeof(Sm));
-    const uint32_t off_info = base, off_d2 = off_info + (uint32_t)align16(4 * (size_t)nc),
-                   off_thr = off_d2 + (uint32_t)align16(2 * (size_t)nc * mm),
-                   off_dir = off_thr + (uint32_t)align16(4 * ((size_t)dm.d2max + 1));
+    const uint32_t off_nb = base, off_info = off_nb + (uint32_t)align16(8 * (size_t)(nc + 1)),
+                   off_thr = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
+                   off_pol = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm);
+    uint16_t* t_nb = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_nb);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
-    uint16_t* t_d2 = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_d2);
-    uint8_t* t_dir = hd_dyn_smem + off_dir;
+    uint32_t* t_thr = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_thr);
+    uint8_t* t_pol = hd_dyn_smem + off_pol;
     if (tid == 0) {
+      sm.off_nb = off_nb;
       sm.off_info = off_info;
-      sm.off_dir = off_dir;
-      sm.off_d2 = off_d2;
       sm.off_thr = off_thr;
+      sm.off_pol = off_pol;
       sm.n = n;
-      sm.m = mm;
+      sm.m = dm.m;
+      sm.mm = mm;
       sm.base = dm.base;
       sm.ncell = nc;
+      sm.exitc = exitc;
       sm.D = dm.D;
       sm.tail = dm.tail;
-      sm.delta[0] = -n;
-      sm.delta[1] = n;
-      sm.delta[2] = 1;
-      sm.delta[3] = -1;
       sm.range_mask[0] = dm.range_mask[0];
       sm.range_mask[1] = dm.range_mask[1];
     }
+    if (tid < 32) sm.senseb[tid] = tid < dm.m ? (uint8_t)(5 + dm.pos_rock[tid]) : (uint8_t)2;
     copy_words(sm.rx, dm.rx, 32, tid, nt);
     copy_words(sm.ry, dm.ry, 32, tid, nt);
-    copy_words(sm.pos_rock, dm.pos_rock, 32, tid, nt);
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
-    copy_words(hd_dyn_smem + off_thr, dm.sense_thr_m1, 4 * (dm.d2max + 1), tid, nt);
-    for (int c = tid; c < nc; c += nt) {
+    for (int c = tid; c <= nc; c += nt) {
+      if (c == exitc) {  // the pseudo-cell: every move stays, no rock
+        for (int k = 0; k < 4; ++k) t_nb[4 * c + k] = (uint16_t)exitc;
+        t_info[c] = 0;
+        continue;
+      }
       const int x = c % n, y = c / n;
-      const uint32_t rock = (uint32_t)(uint8_t)dm.rock_at[c];  // 0xFF: none
-      t_info[c] = (uint32_t)(y > 0) | ((uint32_t)(y < n - 1) << 1) | ((uint32_t)(x < n - 1) << 2) |
-                  ((uint32_t)(x > 0) << 3) | (rock << 8) | ((uint32_t)x << 16) | ((uint32_t)y << 24);
+      t_nb[4 * c + 0] = (uint16_t)(y > 0 ? c - n : c);                                 // N
+      t_nb[4 * c + 1] = (uint16_t)(y < n - 1 ? c + n : c);                             // S
+      t_nb[4 * c + 2] = (uint16_t)(x < n - 1 ? c + 1 : (int)(kExitFlag | exitc));      // E (exit)
+      t_nb[4 * c + 3] = (uint16_t)(x > 0 ? c - 1 : c);                                 // W
+      const int8_t rock = dm.rock_at[c];
+      t_info[c] = (rock >= 0 ? ((uint32_t)rock | 32u) : 0u) | ((uint32_t)x << 8) | ((uint32_t)y << 16);
     }
-    for (int e = tid; e < nc * mm; e += nt) {
+    for (int e = tid; e < (nc + 1) * mm; e += nt) {
       const int c = e / mm, j = e - c * mm;
-      const int x = c % n, y = c / n;
-      const int dx = dm.rx[j] - x, dy = dm.ry[j] - y;
-      // E if x < tx, W if x > tx, S if y < ty, N if y > ty, on the rock: SAMPLE
-      t_dir[e] = (uint8_t)((dx == 0 && dy == 0) ? 4 : dx > 0 ? 2 : dx < 0 ? 3 : dy > 0 ? 1 : 0);
-      t_d2[e] = (uint16_t)(dx * dx + dy * dy);
+      uint32_t t = 0;
+      if (c < nc && j < dm.m) {
+        const int dx = dm.rx[j] - c % n, dy = dm.ry[j] - c / n;
+        t = dm.sense_thr_m1[dx * dx + dy * dy];
+      }
+      t_thr[e] = t;
+    }
+    for (int e = tid; e < (nc + 1) * 32; e += nt) {
+      const int c = e >> 5, p = e & 31;
+      uint8_t v = 2;  // E: nothing open, or the EXIT pseudo-cell
+      if (c < nc && p < dm.m) {
+        const int j = dm.pos_rock[p];
+        const int dx = dm.rx[j] - c % n, dy = dm.ry[j] - c / n;
+        // E if x < tx, W if x > tx, S if y < ty, N if y > ty, on the rock: SAMPLE
+        v = (uint8_t)((dx == 0 && dy == 0) ? 4 : dx > 0 ? 2 : dx < 0 ? 3 : dy > 0 ? 1 : 0);
+      }
+      t_pol[e] = v;
     }
   }
   struct St {
     uint32_t good;
-    int32_t cell[R];
-    bool ex[R];
+    int32_t cell[R];  // EXIT pseudo-cell once exited
   };
+  static __device__ __forceinline__ bool exited(const Sm& sm, const St& s, int r) { return s.cell[r] == sm.exitc; }
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
     St s;
     s.good = st[i];
@@ -201,8 +223,7 @@ struct RockSample {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t c = (pos >> (16 * r)) & 0xFFFFu;
-      s.ex[r] = c == 0xFFFFu;
-      s.cell[r] = s.ex[r] ? 0 : (int32_t)c;
+      s.cell[r] = c == 0xFFFFu ? sm.exitc : (int32_t)c;
     }
     return s;
   }
@@ -210,14 +231,15 @@ struct RockSample {
                                                uint32_t i) {
     uint32_t pos = 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) pos |= (s.ex[r] ? 0xFFFFu : (uint32_t)s.cell[r]) << (16 * r);
+    for (int r = 0; r < R; ++r) pos |= (exited(sm, s, r) ? 0xFFFFu : (uint32_t)s.cell[r]) << (16 * r);
     st[i] = s.good;
     st[cap + i] = pos;
   }
-  static __device__ __forceinline__ bool terminal(const St& s) {
+  // terminal iff every robot has exited
+  static __device__ __forceinline__ bool terminal(const Sm& sm, const St& s) {
     bool t = true;
 #pragma unroll
-    for (int r = 0; r < R; ++r) t = t && s.ex[r];
+    for (int r = 0; r < R; ++r) t = t && exited(sm, s, r);
     return t;
   }
   static constexpr uint32_t kTerminalObs = (R == 1) ? 3u : 9u;
@@ -225,44 +247,40 @@ struct RockSample {
   // one step with per-robot sub-actions b[r] and random words u[r], robots in
   // ascending order.  Branch-free: every lane evaluates the move, sample and
   // sense effects and selects, so roll-out lanes choosing different
-  // sub-actions do not diverge.  zr[r] returns robot r's reading (0 none,
-  // 1 GOOD, 2 BAD).
+  // sub-actions do not diverge.  zrs[r] returns robot r's reading (0 none,
+  // 1 GOOD, 2 BAD).  Rewards are integers (exact in fp32).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
                                                   uint32_t& z, float& rew, uint32_t* zrs = nullptr) {
-    float reward = 0.0f;
+    int reward = 0;
     uint32_t zsum = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool act = !s.ex[r];
       const int sub = b[r];
       const int c = s.cell[r];
-      const uint32_t info = RockSample::info(sm, c);
-      // moves 0 N, 1 S, 2 E, 3 W: stay when the target is off the grid, except
-      // E at the east border, which exits (+10)
+      // moves 0 N, 1 S, 2 E, 3 W: the table's target (itself when blocked;
+      // EXIT with the flag through the east border)
+      const uint32_t tg = target(sm, c, sub & 3);
       const bool is_move = sub < 4;
-      const bool inside = (info >> (sub & 3)) & 1u;
-      const bool moves = act && is_move && inside;
-      const bool exits = act && sub == 2 && !inside;
       // SAMPLE on the current cell
-      const uint32_t jr = (info >> 8) & 0xFFu;
-      const uint32_t samp = (act && sub == 4 && jr != 0xFFu) ? 1u : 0u;
-      const uint32_t gbit = samp & (s.good >> (jr & 31u));
-      // SENSE j (evaluated for every lane; masked)
+      const uint32_t inf = info(sm, c);
+      const uint32_t jr = inf & 31u;
+      const uint32_t samp = (sub == 4) ? (inf >> 5) & 1u : 0u;
+      const uint32_t gbit = samp & (s.good >> jr);
+      // SENSE j (evaluated for every lane; masked; none from EXIT)
       const int js = max(sub - 5, 0);
-      const uint32_t incorrect = u[r] > thr(sm, d2(sm, c * sm.m + js)) ? 1u : 0u;
+      const uint32_t incorrect = u[r] > thr(sm, c, js) ? 1u : 0u;
       const uint32_t isgood = (s.good >> js) & 1u;
-      const uint32_t sense = (act && sub >= 5) ? 1u : 0u;
-      const uint32_t zr = sense * (1u + ((isgood ^ incorrect) ^ 1u));  // GOOD iff good == correct
-      reward = reward + (exits ? 10.0f : 0.0f);
-      reward = reward + (samp ? (gbit ? 10.0f : -10.0f) : 0.0f);
-      s.good &= ~(gbit << (jr & 31u));
-      s.cell[r] = moves ? c + sm.delta[sub & 3] : c;
-      s.ex[r] = s.ex[r] || exits;
+      const uint32_t sense = (sub >= 5 && c != sm.exitc) ? 1u : 0u;
+      const uint32_t zr = sense * (2u - (isgood ^ incorrect));  // GOOD (1) iff good == correct
+      reward += is_move ? 10 * (int)(tg >> 15) : 0;
+      reward += (int)samp * (20 * (int)gbit - 10);
+      s.good &= ~(gbit << jr);
+      s.cell[r] = is_move ? (int)(tg & 0x7FFFu) : c;
       if (zrs) zrs[r] = zr;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
-    rew = reward;
-    const bool term = terminal(s);
+    rew = (float)reward;
+    const bool term = terminal(sm, s);
     z = term ? kTerminalObs : zsum;
     return term;
   }
@@ -283,11 +301,13 @@ struct RockSample {
   // u(s) = sum_{good j} 10 g^{min_r |r-j|_1} + sum_{r active} 10 g^{n-1-x_r}
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
     int x[R], y[R];
+    bool ex[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t info = RockSample::info(sm, s.cell[r]);
-      x[r] = (int)((info >> 16) & 0xFFu);
-      y[r] = (int)(info >> 24);
+      const uint32_t inf = info(sm, s.cell[r]);
+      x[r] = (int)((inf >> 8) & 0xFFu);
+      y[r] = (int)((inf >> 16) & 0xFFu);
+      ex[r] = exited(sm, s, r);
     }
     double u = 0.0;
     for (int j = 0; j < sm.m; ++j) {  // uniform trip count; bad rocks add +0.0
@@ -295,32 +315,37 @@ struct RockSample {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int d = abs(x[r] - sm.rx[j]) + abs(y[r] - sm.ry[j]);
-        dmin = (!s.ex[r] && d < dmin) ? d : dmin;
+        dmin = (!ex[r] && d < dmin) ? d : dmin;
       }
       u += ((s.good >> j) & 1u) ? 10.0 * sm.gpow[dmin] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (!s.ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - x[r]];
+      if (!ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - x[r]];
     return u;
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
 
   // default policy (card §3.2), branch-free: memory over policy positions p
   // (rocks sorted by handling robot, then (x, y, j)); done bit = DONE, gm bit
-  // = GOOD.  The move toward the target is the per-cell table lookup.
+  // = GOOD.  Robot r targets its first open position p: a known-GOOD rock is
+  // approached (the table's move; SAMPLE on it), an unknown one is sensed;
+  // nothing open: E.  tbit = the target's bit (0 when nothing is open).  An
+  // exited robot's sub-action is immaterial (every action is a no-op at
+  // EXIT, the table gives E there, never SAMPLE); TRACE reports E for it.
+  template <bool TRACE = false>
   static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
                                                 int* b, uint32_t* tbit) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t open = ~done & sm.range_mask[r];
-      const bool has = open != 0u && !s.ex[r];
       const int p = __ffs(open | 0x80000000u) - 1;  // 31 when nothing is open
-      const int j = sm.pos_rock[p];
-      const int mv = (int)dir(sm, s.cell[r] * sm.m + j);
-      const bool known_good = (gm >> p) & 1u;
-      b[r] = !has ? 2 : known_good ? mv : 5 + j;
-      tbit[r] = has ? (1u << p) : 0u;
+      const uint32_t tb = open & (0u - open);        // lowest open bit, 0 when none
+      const int mv = (int)pol(sm, s.cell[r], p);
+      const int sn = (int)sm.senseb[p];
+      b[r] = (gm & tb) ? mv : sn;
+      if (TRACE && exited(sm, s, r)) b[r] = 2;
+      tbit[r] = tb;
     }
   }
   template <bool TRACE, class KeyT>
@@ -333,7 +358,7 @@ struct RockSample {
     while (t < sm.D && !term) {
       int b[R];
       uint32_t tb[R];
-      policy(sm, s, done, gm, b, tb);
+      policy<TRACE>(sm, s, done, gm, b, tb);
       if (TRACE) {
         int a = 0, mul = 1;
 #pragma unroll
@@ -352,8 +377,8 @@ struct RockSample {
       // sample marks it DONE
 #pragma unroll
       for (int q = 0; q < R; ++q) {
-        gm |= zr[q] == 1u ? tb[q] : 0u;
-        done |= (zr[q] == 2u || b[q] == 4) ? tb[q] : 0u;
+        gm |= tb[q] & (0u - (zr[q] & 1u));
+        done |= ((zr[q] >> 1) | (uint32_t)(b[q] == 4)) ? tb[q] : 0u;
       }
       acc += sm.gpow[t - t0] * (double)r;
       ++t;
@@ -454,7 +479,7 @@ struct Nav {
 #pragma unroll
     for (int k = 0; k < NW; ++k) st[(1 + k) * cap + i] = s.occ[k];
   }
-  static __device__ __forceinline__ bool terminal(const St& s) { return s.term; }
+  static __device__ __forceinline__ bool terminal(const Sm&, const St& s) { return s.term; }
   static constexpr uint32_t kTerminalObs = 0x100u;
 
   // occupancy of the 8 neighbours of (x, y), bit k = direction k+1
