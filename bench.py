@@ -41,6 +41,17 @@ from paper_1802_06215_b200 import inputs  # noqa: E402
 I_STEP = {1: 177.0, 2: 223.0, 3: 303.0, 4: 2054.0, 5: 223.0}
 
 
+def i_step(config):
+    """thread-instructions per scenario-step of K2 for this config: the
+    committed measurement (scripts/measure_istep.py -> profiles/r01/i_step.json)
+    if present, else the table above."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "i_step.json")) as f:
+            return float(json.load(f)[str(config)]["i_step"]), "profiles/r01/i_step.json"
+    except Exception:
+        return I_STEP[config], "bench.py I_STEP"
+
+
 def ncu_traffic(config):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel,
     per launch, from the committed `ncu --set full` raw page of this config
@@ -402,7 +413,8 @@ def main():
     peak_tinst = num_sms * 4 * 32 * sm_clock * 1e6 / 1e12  # issue slots, thread-instr/s (Tinst/s)
     k2_avg = float(np.mean(k2_ms))
     steps_local = total_steps / world
-    achieved = I_STEP[args.config] * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
+    istep, istep_src = i_step(args.config)
+    achieved = istep * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
     k2_share = float(np.sum(k2_ms) / np.sum(step_ms))
     traffic = ncu_traffic(args.config)
     if kind == "car":  # the variant rule of despot.cu (launch_k2_sparse) unless forced
@@ -438,8 +450,8 @@ def main():
                          "traffic_unit": "DRAM bytes per K2 launch",
                          "traffic_source": traffic["source"] if traffic else None,
                          "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
-                                 f"({peak_src} sm_max_mhz); achieved = {I_STEP[args.config]} thread-instr per "
-                                 f"scenario-step (DESIGN.md §7) x steps / live K2 event time"},
+                                 f"({peak_src} sm_max_mhz); achieved = {istep:.1f} thread-instr per "
+                                 f"scenario-step ({istep_src}, DESIGN.md §7.1) x steps / live K2 event time"},
             "e2e": {"value": e2e_steps / (e2e_ms / 1e3), "unit": "scenario-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_n,
                     "wall_ms_per_step": 1e3 * e2e_wall / e2e_n},
