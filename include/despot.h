@@ -120,6 +120,9 @@ int despot_node_info(despot_model* model, despot_node node, uint32_t* n, uint32_
 int despot_node_read(despot_model* model, despot_node node, uint32_t* ids, float* weights,
                      uint32_t* states_soa, void* stream);
 int despot_node_release(despot_model* model, despot_node node);
+/* despot_node_release of n nodes (host array), in order, in one call.  Stops
+ * at the first unknown node (EINVAL); the ones before it are released. */
+int despot_node_release_many(despot_model* model, const despot_node* nodes, uint32_t n);
 
 /* ------------------------------------------------------------------------ */
 /* Batched leaf expansion (the hot path)                                    */
@@ -139,6 +142,9 @@ typedef struct {
 #define DESPOT_X_RECORD_SCENARIO 2u /* fill the per-scenario scen_* arrays         */
 #define DESPOT_X_TIMING 4u          /* fill phase_ms with CUDA-event times of the
                                        phases, recorded on the call's stream       */
+#define DESPOT_X_TIMING_K2 8u       /* only phase_ms[1] (K2), two events: the cheap
+                                       form for timing loops (8 events cost ~30 us
+                                       of host time per call)                     */
 
 /* Caller-owned outputs.  Sizes: L leaves, A = |A|, C = child_capacity,
  * S = scen_capacity.  Children of (l, a) are child_begin[l*A+a] ..

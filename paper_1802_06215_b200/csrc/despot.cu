@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -141,6 +142,38 @@ struct Block {
   }
 };
 
+// Host-side trace of one expansion call (env DESPOT_HOST_TRACE=1): the time
+// since the call's start at named points, printed to stderr at its end.  A
+// diagnostic for the per-call host overhead; off by default (one branch).
+struct HostTrace {
+  bool on = false;
+  int n = 0;
+  double t[40];
+  const char* name[40];
+  static double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+  void mark(const char* s) {
+    if (on && n < 40) {
+      t[n] = now_us();
+      name[n++] = s;
+    }
+  }
+  void start() {
+    static const bool env = getenv("DESPOT_HOST_TRACE") != nullptr;
+    on = env;
+    n = 0;
+    mark("start");
+  }
+  void dump() {
+    if (!on) return;
+    fprintf(stderr, "[despot host trace]");
+    for (int i = 1; i < n; ++i) fprintf(stderr, " %s=%.1f", name[i], t[i] - t[0]);
+    fprintf(stderr, " (us)\n");
+  }
+};
+static thread_local HostTrace g_ht;
+
 struct Node {
   despot_model* model;
   std::shared_ptr<Block> block;
@@ -198,11 +231,11 @@ struct despot_batch {
   void* mscratch = nullptr;       // merge scratch (offsets, merged sums)
   uint64_t gblk = 0, rmax = 0, ncmax = 0;
   uint32_t hdr_pad = 0, rec_bytes = 0;
-  bool timing = false;
+  bool timing = false, timing_k2 = false;  // DESPOT_X_TIMING / DESPOT_X_TIMING_K2 (K2 events only)
   uint32_t launches = 0;  // kernels launched for this batch
   cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
   void mark(int i) {
-    if (timing) cudaEventRecord(ev[i], stream);
+    if (timing && (!timing_k2 || i == 3 || i == 4)) cudaEventRecord(ev[i], stream);
   }
 };
 
@@ -719,6 +752,13 @@ extern "C" int despot_node_release(despot_model* m, despot_node h) {
   return DESPOT_OK;
 }
 
+extern "C" int despot_node_release_many(despot_model* m, const despot_node* nodes, uint32_t n) {
+  if (!m || (n && !nodes)) return set_err(DESPOT_EINVAL, "null argument");
+  for (uint32_t i = 0; i < n; ++i)
+    if (int rc = despot_node_release(m, nodes[i])) return rc;
+  return DESPOT_OK;
+}
+
 // ---------------------------------------------------------------------------
 // batches
 // ---------------------------------------------------------------------------
@@ -808,7 +848,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   b->sharded_sparse = b->sparse && m->world > 1;
   b->flags = flags;
   b->leaves.assign(leaves, leaves + L);
-  b->timing = flags & DESPOT_X_TIMING;
+  b->timing = flags & (DESPOT_X_TIMING | DESPOT_X_TIMING_K2);
+  b->timing_k2 = (flags & DESPOT_X_TIMING_K2) && !(flags & DESPOT_X_TIMING);
   if (b->timing) {
     if (!event_pool().acquire(b->ev)) return set_err(DESPOT_ECUDA, "cudaEventCreate failed");
     b->mark(0);
@@ -845,12 +886,14 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     if (smax > 4096) return set_err(DESPOT_EINVAL, "sparse-key models: at most 4096 scenarios per leaf");
     b->S = smax;
   }
+  g_ht.mark("validated");
   cudaStream_t st = b->stream;
   if (new_bytes) {
     b->new_block = std::make_shared<Block>();
     b->new_block->stream = st;
     CU(cudaMallocAsync(&b->new_block->ptr, new_bytes, st));
   }
+  g_ht.mark("arena_alloc");
   char* np = b->new_block ? static_cast<char*>(b->new_block->ptr) : nullptr;
   std::vector<LeafDev> ld(L);
   for (uint32_t l = 0; l < L; ++l) {
@@ -902,6 +945,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     for (uint32_t l = 0; l < L; ++l)
       if (b->is_new[l]) m->nodes.insert(b->leaf_node[l]);
   }
+  g_ht.mark("leaf_table");
   // scratch: leaves | n_leaf | tile_off | scen_off | sums | mins | rank | nc | err
   const uint64_t LA = (uint64_t)L * dm.A, LAS = LA * b->S;
   const SumLayout lay{LAS, LA};
@@ -929,6 +973,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     free_batch(b.release(), true);
     return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
   }
+  g_ht.mark("scratch_alloc");
   char* s = static_cast<char*>(b->scratch);
   BatchDev& bd = b->bd;
   bd.model = m->dev;
@@ -989,6 +1034,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
   }
+  g_ht.mark("setup_copies");
   // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
   // are bound in despot_expand_end (K2 runs there when RECORD is set, since
   // the record pointers arrive with the output struct).
@@ -1022,6 +1068,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       return check_launch(m, "K1");
     });
   }
+  g_ht.mark("k1");
   // single-call batches bind their outputs now: a small dense batch then runs
   // its finalize in K2's last CTA (no K3 launches)
   if (!rc && bind) {
@@ -1036,6 +1083,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
                   LAd <= 4 * G * kSmallUnroll * 2;
     b->bd.fused_k3 = b->k3_fused ? 1u : 0u;
   }
+  g_ht.mark("bind");
   if (!rc && !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO)) {
     // K2 now (the exchange block is complete after it)
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
@@ -1064,6 +1112,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     free_batch(b.release(), true);
     return rc;
   }
+  g_ht.mark("k2");
   *out = b.release();
   return DESPOT_OK;
 }
@@ -1289,6 +1338,29 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
   return DESPOT_OK;
 }
 
+// every host output array of `out` is page-locked (cudaHostAlloc /
+// cudaHostRegister): the D2H copies can then go straight into them
+static bool outputs_pinned(const despot_expansion* out, uint32_t C) {
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  const void* head[] = {out->n_scen, out->weight, out->act_reward, out->act_upper, out->act_lower, out->child_begin};
+  for (const void* p : head)
+    if (!pinned(p)) return false;
+  if (C) {
+    const void* ch[] = {out->child_count, out->child_first, out->child_weight, out->child_upper, out->child_lower,
+                        out->child_obs};
+    for (const void* p : ch)
+      if (!pinned(p)) return false;
+  }
+  return true;
+}
+
 // Completes a bound batch: [K2 for RECORD] -> K3 (unless fused into K2) ->
 // status and outputs to the host -> frees the batch.
 static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st) {
@@ -1358,6 +1430,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     ++b->launches;
     rc = check_launch(m, "K3c");
   }
+  g_ht.mark("k3");
   b->mark(6);
   // status block: err | total children | steps | ticket | pad | n_leaf[L]
   const size_t stat_bytes = 4 * kStatWords + 4 * (size_t)L;
@@ -1376,24 +1449,45 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   // whole block travels in this first copy and no second round trip is needed
   char* hp_out = nullptr;
   const size_t head_bytes = o_cc, body_bytes = o_so;
-  const bool one_copy = body_bytes <= (1u << 20);  // else: head via pinned, children copied directly
+  // page-locked caller buffers: every array is copied straight into them (no
+  // staging, no host memcpy); else the head goes through the library's pinned
+  // staging (with the whole block when it is small) and the children directly
+  // (small blocks: one staging copy beats a dozen small DMA copies)
+  const bool small = body_bytes <= (1u << 20);  // every array at capacity in the first round trip
+  const bool pinned_out = !dev_out && !record && !small && outputs_pinned(out, C);
+  const bool one_copy = small;
   struct PinRelease {
     char*& p;
     ~PinRelease() {
       if (p) pinned_pool().release(p);
     }
   } pin_out_guard{hp_out};
-  if (!rc && !dev_out) {
+  if (!rc && pinned_out) {
+    const struct {
+      void* dst;
+      size_t off, bytes;
+    } head[] = {{out->n_scen, o_ns, 4 * (size_t)L},  {out->weight, o_w, 4 * (size_t)L},
+                {out->act_reward, o_ar, 4 * LA},     {out->act_upper, o_au, 4 * LA},
+                {out->act_lower, o_al, 4 * LA},      {out->child_begin, o_cb, 4 * (LA + 1)}};
+    for (const auto& h : head)
+      if (!rc && h.dst && h.bytes &&
+          cudaMemcpyAsync(h.dst, static_cast<char*>(stage) + h.off, h.bytes, cudaMemcpyDeviceToHost, st) !=
+              cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "output copy failed");
+  } else if (!rc && !dev_out) {
     hp_out = static_cast<char*>(pinned_pool().acquire(one_copy ? body_bytes : head_bytes));
     if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
     else if (cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st) !=
              cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "output copy failed");
   }
+  g_ht.mark("d2h_enqueued");
+  b->mark(7);  // end of the call's device work (before the host waits: no extra round trip)
   if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
     m->failed = true;
     rc = set_err(DESPOT_ECUDA, "batch failed: %s", cudaGetErrorString(cudaGetLastError()));
   }
+  g_ht.mark("synced");
   uint32_t err = 0, nchildren = 0;
   uint64_t steps = 0;
   if (!rc) {
@@ -1425,7 +1519,9 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
         {out->child_weight, o_cw, 4 * Cu},            {out->child_upper, o_cu, 4 * Cu},
         {out->child_lower, o_cl, 4 * Cu},             {out->child_obs, o_co, 4 * Cu * dm.OW},
     };
-    if (!one_copy) {  // second round trip: the used part of each child array, straight to the caller
+    if (pinned_out)
+      for (int k = 0; k < 6; ++k) parts[k].bytes = 0;  // already in the caller's buffers
+    if (!small) {  // second round trip: the used part of each child array, straight to the caller
       for (int k = 6; k < 12; ++k) {
         if (parts[k].bytes && cudaMemcpyAsync(parts[k].dst, static_cast<char*>(stage) + parts[k].off,
                                               parts[k].bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -1451,19 +1547,17 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       if (!rc && c.dst && c.src && c.bytes &&
           cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "output copy failed");
-    if (!rc && (!one_copy || record) && cudaStreamSynchronize(st) != cudaSuccess)
+    if (!rc && (!small || record) && cudaStreamSynchronize(st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "output copy sync failed");
     if (!rc)
       for (auto& p : parts)
         if (p.bytes) memcpy(p.dst, hp_out + p.off, p.bytes);
   }
-  if (!rc && b->timing) {
-    b->mark(7);
-    cudaEventSynchronize(b->ev[7]);
+  if (!rc && b->timing) {  // the events are complete: the stream was synchronised
     const int pairs[4][2] = {{1, 2}, {3, 4}, {5, 6}, {0, 7}};
     for (int k = 0; k < 4; ++k) {
       float ms = 0.0f;
-      cudaEventElapsedTime(&ms, b->ev[pairs[k][0]], b->ev[pairs[k][1]]);
+      if (!b->timing_k2 || k == 1) cudaEventElapsedTime(&ms, b->ev[pairs[k][0]], b->ev[pairs[k][1]]);
       out->phase_ms[k] = ms;
     }
   }
@@ -1478,7 +1572,10 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     nd->expanded = true;
     out->node[l] = reinterpret_cast<despot_node>(nd);
   }
+  g_ht.mark("outputs");
   free_batch(b, false);
+  g_ht.mark("freed");
+  g_ht.dump();
   return DESPOT_OK;
 }
 
@@ -1494,6 +1591,7 @@ extern "C" int despot_expand_end(despot_batch* b, despot_expansion* out, void* s
 
 extern "C" int despot_expand_batch(despot_model* m, const despot_leaf* leaves, uint32_t L,
                                    despot_expansion* out, void* stream) {
+  g_ht.start();
   if (!m || !out) return set_err(DESPOT_EINVAL, "null argument");
   if (m->world > 1) return set_err(DESPOT_EINVAL, "world > 1: use despot_expand_begin/exchange/end");
   despot_batch* b = nullptr;

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("DESPOT_LIB", os.path.join(HERE, "libdespot.so"))  # o
 DESPOT_X_DEVICE_OUTPUTS = 1
 DESPOT_X_RECORD_SCENARIO = 2
 DESPOT_X_TIMING = 4
+DESPOT_X_TIMING_K2 = 8
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
 
@@ -26,9 +27,15 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5
 # every function declared in include/despot.h (checked by the CPU tests)
 EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "despot_model_info_get",
            "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
-           "despot_node_release", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
+           "despot_node_release", "despot_node_release_many", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
            "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
            "despot_search", "despot_plan"]
+
+
+def _tflag(timing):
+    """timing=True: every phase (8 CUDA events); "k2": K2 only (2 events, the
+    cheap form for timing loops); False: none."""
+    return DESPOT_X_TIMING_K2 if timing == "k2" else DESPOT_X_TIMING if timing else 0
 
 
 class DespotError(RuntimeError):
@@ -141,6 +148,7 @@ def lib():
         L.despot_node_info.argtypes = [vp, u64, C.POINTER(u32), C.POINTER(u32)]
         L.despot_node_read.argtypes = [vp, u64, vp, vp, vp, vp]
         L.despot_node_release.argtypes = [vp, u64]
+        L.despot_node_release_many.argtypes = [vp, C.POINTER(C.c_uint64), C.c_uint32]
         L.despot_expand_batch.argtypes = [vp, C.POINTER(Leaf), u32, C.POINTER(Expansion), vp]
         L.despot_expand_begin.argtypes = [vp, C.POINTER(Leaf), u32, u32, vp, C.POINTER(vp)]
         L.despot_batch_exchange.argtypes = [vp, C.POINTER(Exchange)]
@@ -227,6 +235,11 @@ class Model:
     def node_release(self, node):
         _check(lib().despot_node_release(self.h, int(node)))
 
+    def node_release_many(self, nodes):
+        """Releases every node in `nodes` (one foreign call)."""
+        arr = (C.c_uint64 * len(nodes))(*[int(n) for n in nodes])
+        _check(lib().despot_node_release_many(self.h, arr, len(nodes)))
+
     # ---- expansion ----
     @staticmethod
     def _leaves(leaves):
@@ -250,9 +263,22 @@ class Model:
             tot += self.A * (min(g, per) if per else g)
         return max(tot, 1)
 
-    def _alloc_outputs(self, L, C_cap, S_cap, record, device):
+    def _alloc_outputs(self, L, C_cap, S_cap, record, device, pinned=False):
         A, OW, SW = self.A, self.OW, self.SW
-        if device:
+        keep = []
+        if pinned and not device:
+            # page-locked host arrays (numpy views of pinned torch buffers): the
+            # library copies the results straight into them
+            import torch
+
+            def z(n, dt):
+                n = max(int(n), 1)
+                t = torch.zeros(n * np.dtype(dt).itemsize, dtype=torch.uint8, pin_memory=True)
+                keep.append(t)
+                return t.numpy().view(dt)
+            u32, f32, i64 = np.uint32, np.float32, np.uint64
+            ptr = lambda t: t.ctypes.data  # noqa: E731
+        elif device:
             import torch
             dev = torch.device("cuda", self.device)
             z = lambda n, dt: torch.zeros(max(int(n), 1), dtype=dt, device=dev)  # noqa: E731
@@ -273,6 +299,8 @@ class Model:
         E = Expansion()
         for k, v in o.items():
             setattr(E, k, ptr(v))
+        if keep:
+            o["_pinned"] = keep  # owners of the page-locked memory
         E.child_capacity = int(C_cap)
         E.scen_capacity = int(S_cap) if record else 0
         return o, E
@@ -318,20 +346,21 @@ class Model:
         nodes = (C.c_uint64 * L)()
         E.node = C.addressof(nodes)
         E.flags = ((DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_RECORD_SCENARIO if record else 0)
-                   | (DESPOT_X_TIMING if timing else 0))
+                   | _tflag(timing))
         _check(lib().despot_expand_batch(self.h, lv, L, C.byref(E), _stream_ptr(stream)))
         return self._finish(o, E, L, nodes, record, device_outputs)
 
     # ---- prepared calls (repeated batches: no per-call marshalling) ----
-    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False):
+    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False, pinned=False):
         """Build the ctypes leaf table, output arrays and expansion struct of a
-        batch once; `run_prepared` then costs one foreign call."""
+        batch once; `run_prepared` then costs one foreign call.  pinned: host
+        outputs in page-locked memory (copied into directly)."""
         L = len(leaves)
         C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
-        o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs)
+        o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs, pinned=pinned)
         nodes = (C.c_uint64 * L)()
         E.node = C.addressof(nodes)
-        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_TIMING if timing else 0)
+        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | _tflag(timing)
         return {"lv": self._leaves(leaves), "L": L, "E": E, "o": o, "nodes": nodes, "ref": C.byref(E),
                 "leaves": list(leaves)}
 
@@ -343,14 +372,14 @@ class Model:
         return E.scenario_steps, E.launches, prep["nodes"]
 
     # ---- two-phase form for scenario sharding ----
-    def alloc_outputs(self, leaves, device_outputs=False, child_capacity=None):
+    def alloc_outputs(self, leaves, device_outputs=False, child_capacity=None, pinned=False):
         C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
-        return self._alloc_outputs(len(leaves), C_cap, 0, False, device_outputs)
+        return self._alloc_outputs(len(leaves), C_cap, 0, False, device_outputs, pinned=pinned)
 
     def expand_begin(self, leaves, record=False, stream=None, timing=False):
         lv = self._leaves(leaves)
         b = C.c_void_p()
-        flags = (DESPOT_X_RECORD_SCENARIO if record else 0) | (DESPOT_X_TIMING if timing else 0)
+        flags = (DESPOT_X_RECORD_SCENARIO if record else 0) | _tflag(timing)
         _check(lib().despot_expand_begin(self.h, lv, len(leaves), flags, _stream_ptr(stream), C.byref(b)))
         ex = Exchange()
         _check(lib().despot_batch_exchange(b, C.byref(ex)))
@@ -366,7 +395,7 @@ class Model:
             o, E = outputs
         nodes = (C.c_uint64 * L)()
         E.node = C.addressof(nodes)
-        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_TIMING if timing else 0)
+        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | _tflag(timing)
         _check(lib().despot_expand_end(batch, C.byref(E), _stream_ptr(stream)))
         return self._finish(o, E, L, nodes, False, device_outputs)
 

@@ -175,7 +175,7 @@ def select_leaves(child_count, child_begin, num_actions, L, root=0):
 # Configs of BASELINE.json
 # --------------------------------------------------------------------------
 CONFIGS = {
-    1: dict(kind="rocksample", name="rocksample_7_8_K100", n=7, m=8, robots=1, K=100, L=1, D=20),
+    1: dict(kind="rocksample", name="rocksample_7_8_K100_root", n=7, m=8, robots=1, K=100, L=1, D=20, root=True),
     2: dict(kind="rocksample", name="mars_15_15_K500_L64", n=15, m=15, robots=2, K=500, L=64, D=20),
     3: dict(kind="nav", name="nav_13_K500_L64", n=13, K=500, L=64, D=90),
     4: dict(kind="car", name="car_20peds_K500_L64", peds=20, K=500, L=64, D=90),

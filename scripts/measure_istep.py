@@ -51,7 +51,9 @@ def main():
         if r.returncode:
             print(json.dumps({"config": cfg, "error": r.stderr[-400:]}), flush=True)
             continue
-        rows = list(csv.DictReader(io.StringIO(open(csvp).read())))
+        text = open(csvp).read()
+        text = text[text.index('"ID"'):]  # skip ncu's own log lines before the CSV header
+        rows = list(csv.DictReader(io.StringIO(text)))
         vals, units = {}, {}
         for row in rows:
             vals.setdefault(row["ID"], {})[row["Metric Name"]] = float(row["Metric Value"].replace(",", ""))

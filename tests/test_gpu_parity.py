@@ -260,6 +260,33 @@ def test_fused_finalize_equals_separate_k3_and_prepared_calls():
         gm.close()
 
 
+def test_pinned_host_outputs_equal_pageable():
+    """Page-locked caller buffers take the direct-copy path (no staging): the
+    results equal the pageable-buffer path bit for bit (dense and sparse)."""
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+            "child_first", "child_weight", "child_upper", "child_lower", "child_obs")
+    gm, om, st, w, seed, L = setup(2, K=300, L=16)
+    gr = gm.belief_load(st, w, seed)
+    R = gm.expand([(gr, -1, 0, 0)])
+    lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)]
+    params = inputs.car_params(6, D=30)
+    cm = Model("car", params)
+    cl = [(cm.belief_load(s, w_, sd), -1, 0, 0) for s, w_, sd in inputs.car_roots(4, 60, peds=6)]
+    for m, leaves in ((gm, lv), (gm, [(gr, -1, 0, 0)]), (cm, cl)):
+        ref = m.expand(leaves)
+        P = m.prepare(leaves, pinned=True)
+        steps, launches, nodes = m.run_prepared(P)
+        assert steps == ref["scenario_steps"]
+        n = int(P["E"].num_children)
+        assert n == ref["num_children"]
+        for k in keys:
+            a = np.asarray(P["o"][k])
+            r = np.asarray(ref[k]).reshape(-1)
+            assert np.array_equal(a[: len(r)], r), k
+        m.node_release_many([nd for lf, nd in zip(leaves, ref["node"]) if lf[1] >= 0] +
+                            [nd for lf, nd in zip(leaves, nodes) if lf[1] >= 0])
+
+
 def test_rollout_bounds_match_oracle():
     for cfg in (1, 3):
         gm, om, st, w, seed, _ = setup(cfg, K=150, uniform=False)
