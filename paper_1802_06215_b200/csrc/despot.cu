@@ -1426,7 +1426,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
   } else if (!rc && !small_k3) {
-    k3_write_dense<<<g3, 128, 0, st>>>(bd);
+    if (b->S > kWideS) k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
+    else k3_write_dense<<<g3, 128, 0, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3c");
   }

@@ -199,6 +199,64 @@ __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
   if (la >= (uint64_t)b.L * b.A) return;
   write_one(b, la, lane, b.child_begin[la], b.nc[la]);
 }
+// K3c for many observation slots (S > 32: navigation's 257): one CTA per
+// (leaf, action), one thread per slot -- a warp per (leaf, action) would walk
+// its slots in S/32 dependent rounds
+constexpr uint32_t kWideS = 32;
+__global__ void __launch_bounds__(256) k3_write_wide(BatchDev b) {
+  __shared__ int64_t s_wt[8], s_nt[8];
+  const uint32_t S = b.S, A = b.A;
+  const uint64_t LA = (uint64_t)b.L * A, la = blockIdx.x;
+  const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
+  const LeafDev& lf = b.leaves[leaf];
+  const DevModel& dm = *b.model;
+  const SumLayout lay{LA * S, LA};
+  const uint64_t base = la * S;
+  const uint32_t cb = b.child_begin[la];
+  int64_t wt = 0, nt = 0;
+  for (uint32_t s = threadIdx.x; s < S; s += blockDim.x) {
+    const int64_t N = b.sums[lay.N(base + s)];
+    if (!N) continue;
+    const int64_t W = b.sums[lay.W(base + s)];
+    wt += W;
+    nt += N;
+    const uint32_t rk = b.rank[base + s];
+    const uint32_t c = cb + rk;
+    if (c < b.child_capacity) {
+      const double Wd = (double)W;
+      b.child_count[c] = (uint32_t)N;
+      b.child_first[c] = (uint32_t)b.mins[base + s];
+      b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
+      b.child_upper[c] = (float)((double)b.sums[lay.U(base + s)] / Wd);
+      b.child_lower[c] = (float)((double)b.sums[lay.Lm(base + s)] / Wd);
+      b.child_obs[c] = s;
+    }
+    if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = s;  // key table for later updates
+  }
+  wt = warp_sum64(wt);
+  nt = warp_sum64(nt);
+  if ((threadIdx.x & 31) == 0) {
+    s_wt[threadIdx.x >> 5] = wt;
+    s_nt[threadIdx.x >> 5] = nt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < (blockDim.x >> 5); ++w) {
+      wt += s_wt[w];
+      nt += s_nt[w];
+    }
+    lf.nchild[a] = b.nc[la];
+    const double Wd = (double)wt;
+    b.act_reward[la] = (float)((double)b.sums[lay.Q(la, 0)] / Wd);
+    b.act_upper[la] = (float)((double)b.sums[lay.Q(la, 1)] / Wd);
+    b.act_lower[la] = (float)((double)b.sums[lay.Q(la, 2)] / Wd);
+    if (a == 0) {
+      b.n_scen[leaf] = (uint32_t)nt;
+      b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
+      if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+    }
+  }
+}
 
 // K3 for small batches (L*A <= kSmallLA, S <= 32): rank, scan and write in
 // one CTA -- a kernel of its own, or the tail of K2's last CTA.  The path is
