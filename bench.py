@@ -403,6 +403,8 @@ def main():
     tw1 = time.monotonic()
     clk.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("BENCH_STEP_LOG"):
+        print("step_ms", [round(x, 4) for x in step_ms], file=sys.stderr)
     t_local = float(np.sum(step_ms))
     if world > 1:
         t = torch.tensor([t_local], device=dev)

@@ -8,11 +8,11 @@ timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; echo "pyt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1
 timeout 1800 python scripts/measure_istep.py --out $O/i_step.json > $O/i_step.log 2>&1
 mkdir -p profiles/r01 && cp $O/i_step.json profiles/r01/i_step.json
+timeout 900 python bench.py > $O/bench_default.log 2>&1   # the driver's default command, first
 for c in 1 2 3 4; do
   timeout 600 python bench.py --config $c --steps 20 --warmup 3 --cpu-budget 10 > $O/bench_config$c.log 2>&1
 done
 timeout 900 python bench.py --config 5 --K 32768 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_config5.log 2>&1
-timeout 900 python bench.py > $O/bench_default.log 2>&1
 timeout 900 python bench.py --impl reference > $O/bench_reference.log 2>&1
 # launch list of the default command (cold cache, serialised: shares only)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_config2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_launch.log 2>&1
