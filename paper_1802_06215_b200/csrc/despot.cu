@@ -364,7 +364,7 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     }
     rmax = 10.0 * dm.R;
     umax = 10.0 * (dm.m + dm.R);
-    dm.sm_table_bytes = (uint32_t)RockSample<1>::table_bytes(dm.n, dm.m, dm.d2max);
+    dm.sm_table_bytes = (uint32_t)RockSample<1>::table_bytes(dm.n, dm.m, dm.D);
   } else if (k == "nav") {
     dm.kind = kNav;
     dm.n = (int)pi(params, "n", 13);

@@ -119,20 +119,24 @@ struct RockSample {
     int32_t n, m, mm, base, ncell, exitc;  // exitc = EXIT pseudo-cell = n*n; mm = max(m, 1)
     uint32_t D;
     double tail;
-    int8_t rx[32], ry[32];
-    uint8_t senseb[32];      // policy position p -> SENSE sub-action 5 + rock(p); [31] = E (nothing open)
+    uint8_t senseb[32];      // policy position p -> SENSE sub-action 5 + rock(p); [m] = E (nothing open)
+    uint32_t none_bit;       // 1 << m: __ffs(open | none_bit) - 1 = m when nothing is open
     uint32_t range_mask[2];  // policy positions of robot r (0 for the always-east policy)
-    double gpow[kGpowN];
-    // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m):
+    // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m, D):
     uint32_t off_nb;    // u16 [cell][4]: target of N, S, E, W (kExitFlag | EXIT: exits east)
     uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
     uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
-    uint32_t off_pol;   // u8  [cell][32]: policy move toward the rock of position p (4 = on it); [31] = E
+    uint32_t off_pol;   // u8  [cell][m+1]: policy move toward the rock of position p (4 = on it); [m] = E
+    uint32_t off_dist;  // u8  [cell][mm]: |x - x_j| + |y - y_j| (255 from EXIT)
+    uint32_t off_gp;    // f64 [G]: gamma^k;  off_gp10: f64 [G]: 10 gamma^k (G = max(D, 2n) + 1)
+    uint32_t off_gp10;
   };
-  // table bytes (host and device agree): nb | info | thr | pol, all with the EXIT row
-  static __host__ __device__ size_t table_bytes(int n, int m, uint32_t) {
-    const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1;
-    return align16(8 * c) + align16(4 * c) + align16(4 * c * mm) + align16(32 * c);
+  static __host__ __device__ int gpow_len(int n, uint32_t D) { return (int)(D > (uint32_t)(2 * n) ? D : 2 * n) + 1; }
+  // table bytes (host and device agree): nb | info | thr | pol | dist | gp | gp10, with the EXIT row
+  static __host__ __device__ size_t table_bytes(int n, int m, uint32_t D) {
+    const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
+    return align16(8 * c) + align16(4 * c) + align16(4 * c * mm) + align16(c * (m + 1)) + align16(c * mm) +
+           align16(8 * G) + align16(8 * G);
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
@@ -144,23 +148,42 @@ struct RockSample {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + j];
   }
   static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int p) {
-    return hd_dyn_smem[sm.off_pol + c * 32 + p];
+    return hd_dyn_smem[sm.off_pol + c * (sm.m + 1) + p];
+  }
+  static __device__ __forceinline__ const uint8_t* dist_row(const Sm& sm, int c) {
+    return hd_dyn_smem + sm.off_dist + c * sm.mm;
+  }
+  static __device__ __forceinline__ double gp(const Sm& sm, int k) {
+    return reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp)[k];
+  }
+  static __device__ __forceinline__ double gp10(const Sm& sm, int k) {
+    return reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10)[k];
   }
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
-    const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc;
+    const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc, G = gpow_len(n, dm.D);
     const uint32_t base = (uint32_t)align16(sizeof(Sm));
     const uint32_t off_nb = base, off_info = off_nb + (uint32_t)align16(8 * (size_t)(nc + 1)),
                    off_thr = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
-                   off_pol = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm);
+                   off_pol = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
+                   off_dist = off_pol + (uint32_t)align16((size_t)(nc + 1) * (dm.m + 1)),
+                   off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * mm),
+                   off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
     uint16_t* t_nb = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_nb);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
     uint32_t* t_thr = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_thr);
     uint8_t* t_pol = hd_dyn_smem + off_pol;
+    uint8_t* t_dist = hd_dyn_smem + off_dist;
+    double* t_gp = reinterpret_cast<double*>(hd_dyn_smem + off_gp);
+    double* t_gp10 = reinterpret_cast<double*>(hd_dyn_smem + off_gp10);
     if (tid == 0) {
       sm.off_nb = off_nb;
       sm.off_info = off_info;
       sm.off_thr = off_thr;
       sm.off_pol = off_pol;
+      sm.off_dist = off_dist;
+      sm.off_gp = off_gp;
+      sm.off_gp10 = off_gp10;
+      sm.none_bit = 1u << dm.m;
       sm.n = n;
       sm.m = dm.m;
       sm.mm = mm;
@@ -173,9 +196,14 @@ struct RockSample {
       sm.range_mask[1] = dm.range_mask[1];
     }
     if (tid < 32) sm.senseb[tid] = tid < dm.m ? (uint8_t)(5 + dm.pos_rock[tid]) : (uint8_t)2;
-    copy_words(sm.rx, dm.rx, 32, tid, nt);
-    copy_words(sm.ry, dm.ry, 32, tid, nt);
-    copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
+    for (int k = tid; k < G; k += nt) {
+      t_gp[k] = dm.gpow[k];
+      t_gp10[k] = 10.0 * dm.gpow[k];  // the product upper() used to form per rock
+    }
+    for (int e = tid; e < (nc + 1) * mm; e += nt) {
+      const int c = e / mm, j = e - c * mm;
+      t_dist[e] = (c < nc && j < dm.m) ? (uint8_t)(abs(c % n - dm.rx[j]) + abs(c / n - dm.ry[j])) : (uint8_t)255;
+    }
     for (int c = tid; c <= nc; c += nt) {
       if (c == exitc) {  // the pseudo-cell: every move stays, no rock
         for (int k = 0; k < 4; ++k) t_nb[4 * c + k] = (uint16_t)exitc;
@@ -199,9 +227,9 @@ struct RockSample {
       }
       t_thr[e] = t;
     }
-    for (int e = tid; e < (nc + 1) * 32; e += nt) {
-      const int c = e >> 5, p = e & 31;
-      uint8_t v = 2;  // E: nothing open, or the EXIT pseudo-cell
+    for (int e = tid; e < (nc + 1) * (dm.m + 1); e += nt) {
+      const int c = e / (dm.m + 1), p = e - c * (dm.m + 1);
+      uint8_t v = 2;  // E: nothing open (p = m), or the EXIT pseudo-cell
       if (c < nc && p < dm.m) {
         const int j = dm.pos_rock[p];
         const int dx = dm.rx[j] - c % n, dy = dm.ry[j] - c / n;
@@ -299,29 +327,25 @@ struct RockSample {
     return step_sub(sm, s, b, u, z, r);
   }
   // u(s) = sum_{good j} 10 g^{min_r |r-j|_1} + sum_{r active} 10 g^{n-1-x_r}
+  // (per rock: the robots' table distances, the nearest's 10 gamma^d from
+  // the premultiplied table; an exited robot's row is 255, never the min
+  // while some robot is active -- upper() is only asked of non-terminal states)
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
-    int x[R], y[R];
-    bool ex[R];
+    const uint8_t* dr[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t inf = info(sm, s.cell[r]);
-      x[r] = (int)((inf >> 8) & 0xFFu);
-      y[r] = (int)((inf >> 16) & 0xFFu);
-      ex[r] = exited(sm, s, r);
-    }
+    for (int r = 0; r < R; ++r) dr[r] = dist_row(sm, s.cell[r]);
+    const double* g10 = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10);
     double u = 0.0;
-    for (int j = 0; j < sm.m; ++j) {  // uniform trip count; bad rocks add +0.0
-      int dmin = 255;
+    for (int j = 0; j < sm.m; ++j) {  // uniform trip count, branch-free; bad rocks add +0.0
+      uint32_t dmin = dr[0][j];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int d = abs(x[r] - sm.rx[j]) + abs(y[r] - sm.ry[j]);
-        dmin = (!ex[r] && d < dmin) ? d : dmin;
-      }
-      u += ((s.good >> j) & 1u) ? 10.0 * sm.gpow[dmin] : 0.0;
+      for (int r = 1; r < R; ++r) dmin = min(dmin, (uint32_t)dr[r][j]);
+      const double v = g10[dmin];
+      u += ((s.good >> j) & 1u) ? v : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (!ex[r]) u += 10.0 * sm.gpow[sm.n - 1 - x[r]];
+      if (!exited(sm, s, r)) u += gp10(sm, sm.n - 1 - (int)((info(sm, s.cell[r]) >> 8) & 0xFFu));
     return u;
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
@@ -339,7 +363,7 @@ struct RockSample {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const uint32_t open = ~done & sm.range_mask[r];
-      const int p = __ffs(open | 0x80000000u) - 1;  // 31 when nothing is open
+      const int p = __ffs(open | sm.none_bit) - 1;  // m when nothing is open
       const uint32_t tb = open & (0u - open);        // lowest open bit, 0 when none
       const int mv = (int)pol(sm, s.cell[r], p);
       const int sn = (int)sm.senseb[p];
@@ -380,10 +404,10 @@ struct RockSample {
         gm |= tb[q] & (0u - (zr[q] & 1u));
         done |= ((zr[q] >> 1) | (uint32_t)(b[q] == 4)) ? tb[q] : 0u;
       }
-      acc += sm.gpow[t - t0] * (double)r;
+      acc += gp(sm, (int)(t - t0)) * (double)r;
       ++t;
     }
-    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    if (!term) acc += gp(sm, (int)(t - t0)) * sm.tail;
     ret = acc;
     len = t - t0;
   }
