@@ -226,6 +226,66 @@ def cpu_baseline_all_cores(kind, params, st, w, seed, leaves_ac, budget_s=8.0, L
                       f"{secs:.1f} s"}
 
 
+def run_plan(args):
+    """--plan: tree size per planning time (the paper's speedup metric, P:566;
+    SURVEY §8(f) NEXT-1/2) of the host tree driver (despot_plan) on the GPU
+    backend vs the same driver on the CPU oracle backend with one worker (the
+    serial DESPOT analog: this mode's cpu_baseline leg).  One JSON line per
+    run, then the speedups.  Studies: "configs" (the BASELINE configs), "K"
+    (navigation, K = 100 ... 5000, P:611-617), "A" (MARS |A| = 256/400/625,
+    P:625-627)."""
+    from paper_1802_06215_b200 import despot as D
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    points = []
+    if args.plan_study == "configs":
+        for cfg in args.plan_configs:
+            kind, params, st, w, seed, _ = inputs.config_inputs(cfg, K=args.K)
+            points.append((f"config{cfg}", cfg, kind, params, st, w, seed))
+    elif args.plan_study == "K":
+        for K in args.plan_K:
+            kind, params, st, w, seed, _ = inputs.config_inputs(3, K=K)
+            points.append(("K_nav13", K, kind, params, st, w, seed))
+    else:
+        for n, m in ((11, 11), (15, 15), (20, 20)):  # |A| = (5 + m)^2 = 256, 400, 625 (P:627)
+            params = inputs.rocksample_params(n, m, 2, D=20)
+            K = args.K or 500
+            points.append(("A_mars", f"MARS({n},{n}) |A|={(5 + m) ** 2}", "rocksample", params,
+                           inputs.rocksample_belief(n, m, 2, K, 1002), inputs.weights(K), 1002))
+    for study, point, kind, params, st, w, seed in points:
+        rows = []
+        gm = D.Model(kind, params)
+        root = gm.belief_load(st, w, seed)
+        for W in args.plan_workers:
+            c = D.search_config(workers=W, max_inflight=8 if W > 1 else 1, max_batch=64, batch_wait_us=300,
+                                time_budget_s=args.plan_budget, xi=0.95, c_a=0.3, c_o=0.1)
+            r = gm.plan(root, c)
+            r.update(study=study, point=point, backend="gpu", workers=W, K=len(w), A=gm.A,
+                     nodes_per_s=r["nodes"] / r["seconds"], leaves_per_batch=r["expanded"] / max(1, r["batches"]))
+            rows.append(r)
+            print(json.dumps(r), flush=True)
+        gm.close()
+        if args.no_cpu_baseline:
+            continue
+        import oracle
+        from test_search_cpu import OracleBackend
+        om = oracle.Model(kind, params)
+        orr = om.belief_load(st, w, seed)
+        u0, l0 = om.rollout_bounds(orr)
+        be = OracleBackend(om)
+        c = D.search_config(workers=1, max_inflight=1, max_batch=1, time_budget_s=args.plan_budget, xi=0.95,
+                            c_a=0.3, c_o=0.1)
+        r, _ = D.search(be.problem(orr, u0, l0, K=len(w)), c)
+        r.update(study=study, point=point, backend="oracle-serial", workers=1, K=len(w), A=om.A,
+                 nodes_per_s=r["nodes"] / r["seconds"], cores=1)
+        print(json.dumps(r), flush=True)
+        for g in rows:
+            print(json.dumps({"study": study, "point": point, "workers": g["workers"],
+                              "speedup_tree_size_per_time": g["nodes_per_s"] / r["nodes_per_s"],
+                              "gpu_max_depth": g["max_depth"], "oracle_max_depth": r["max_depth"]}), flush=True)
+    return 0
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle, timed on this box's host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -285,9 +345,18 @@ def main():
     ap.add_argument("--peds", type=int, default=None, help="pedestrians of the driving config (NEXT-3 study)")
     ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread"],
                     help="driving kernel: factored warp per scenario, thread per scenario, or per-batch choice")
+    ap.add_argument("--plan", action="store_true",
+                    help="tree size per planning time: despot_plan vs the serial oracle-backed driver (NEXT-1/2)")
+    ap.add_argument("--plan-study", default="configs", choices=["configs", "K", "A"])
+    ap.add_argument("--plan-configs", type=int, nargs="*", default=[1, 2, 3, 4])
+    ap.add_argument("--plan-K", type=int, nargs="*", default=[100, 500, 1000, 2000, 5000])
+    ap.add_argument("--plan-workers", type=int, nargs="*", default=[1, 8])
+    ap.add_argument("--plan-budget", type=float, default=1.0)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.plan:
+        return run_plan(args)
 
     import torch
 

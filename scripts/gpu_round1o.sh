@@ -1,5 +1,4 @@
 set -x
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python scripts/peds_sweep.py > gpurun_out/peds_sweep.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_default.log
+timeout 300 python bench.py --plan --plan-configs 1 2 --plan-budget 0.3 > gpurun_out/plan_mode.log 2>&1; echo "rc=$?" >> gpurun_out/plan_mode.log
+timeout 900 python scripts/online_bench.py --episodes 3 --budgets 0.02 0.1 --steps 20 > gpurun_out/online.jsonl 2> gpurun_out/online.err; echo "rc=$?" >> gpurun_out/online.err
