@@ -24,6 +24,8 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <limits>
@@ -81,6 +83,39 @@ struct Pending {
   std::atomic<uint32_t>* inflight;
 };
 
+// The batcher's output arrays, grown on demand and reused across batches.
+struct OutBuf {
+  size_t L = 0, LA = 0, C = 0, OW = 0;
+  std::unique_ptr<despot_node[]> node;
+  std::unique_ptr<uint32_t[]> n_scen, child_begin, child_count, child_first, child_obs;
+  std::unique_ptr<float[]> weight, ar, au, al, cw, cu, cl;
+  void reserve(size_t l, size_t la, size_t c, size_t ow) {
+    if (l > L) {
+      L = l;
+      node.reset(new despot_node[l]);
+      n_scen.reset(new uint32_t[l]);
+      weight.reset(new float[l]);
+    }
+    if (la > LA) {
+      LA = la;
+      child_begin.reset(new uint32_t[la + 1]);
+      ar.reset(new float[la]);
+      au.reset(new float[la]);
+      al.reset(new float[la]);
+    }
+    if (c > C || ow != OW) {
+      C = std::max(c, (size_t)1);
+      OW = ow;
+      child_count.reset(new uint32_t[C]);
+      child_first.reset(new uint32_t[C]);
+      child_obs.reset(new uint32_t[C * ow]);
+      cw.reset(new float[C]);
+      cu.reset(new float[C]);
+      cl.reset(new float[C]);
+    }
+  }
+};
+
 struct Search {
   const despot_search_problem& P;
   const despot_search_config& C;
@@ -102,6 +137,11 @@ struct Search {
   uint32_t blocked = 0;  // workers waiting for their in-flight trials (under qmu)
   std::atomic<int> error{0};
   std::string error_msg;
+  // batcher time split in ns (DESPOT_SEARCH_TRACE)
+  std::atomic<uint64_t> t_call{0}, t_children{0}, t_backup{0};
+  static uint64_t ns(std::chrono::steady_clock::duration d) {
+    return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count();
+  }
 
   Search(const despot_search_problem& p, const despot_search_config& c) : P(p), C(c) {}
 
@@ -149,7 +189,7 @@ struct Search {
   }
 
   // ---------------------------------------------------------------- batcher
-  int expand(std::vector<Pending>& batch) {
+  int expand(std::vector<Pending>& batch, OutBuf& ob) {
     const uint32_t L = (uint32_t)batch.size(), A = P.num_actions, OW = P.obs_words;
     std::vector<despot_leaf> leaves(L);
     uint64_t cap = 0;
@@ -161,28 +201,34 @@ struct Search {
       cap += (uint64_t)A * (P.obs_slots ? std::min(n, P.obs_slots) : n);
     }
     if (cap > 0xFFFFFFFFull) return DESPOT_ECAPACITY;
-    std::vector<despot_node> hnode(L);
-    std::vector<uint32_t> n_scen(L), child_begin((size_t)L * A + 1), child_count(cap), child_first(cap),
-        child_obs(cap * OW);
-    std::vector<float> weight(L), ar((size_t)L * A), au((size_t)L * A), al((size_t)L * A), cw(cap), cu(cap),
-        cl(cap);
+    // output arrays: the batcher's own grow-only buffers (no per-batch
+    // allocation or zero fill; the backend writes every element we read)
+    ob.reserve(L, (size_t)L * A, cap, OW);
+    despot_node* hnode = ob.node.get();
+    uint32_t *n_scen = ob.n_scen.get(), *child_begin = ob.child_begin.get(), *child_count = ob.child_count.get(),
+             *child_first = ob.child_first.get(), *child_obs = ob.child_obs.get();
+    float *weight = ob.weight.get(), *ar = ob.ar.get(), *au = ob.au.get(), *al = ob.al.get(), *cw = ob.cw.get(),
+          *cu = ob.cu.get(), *cl = ob.cl.get();
     despot_expansion out;
     memset(&out, 0, sizeof out);
-    out.node = hnode.data();
-    out.n_scen = n_scen.data();
-    out.weight = weight.data();
-    out.act_reward = ar.data();
-    out.act_upper = au.data();
-    out.act_lower = al.data();
-    out.child_begin = child_begin.data();
+    out.node = hnode;
+    out.n_scen = n_scen;
+    out.weight = weight;
+    out.act_reward = ar;
+    out.act_upper = au;
+    out.act_lower = al;
+    out.child_begin = child_begin;
     out.child_capacity = (uint32_t)cap;
-    out.child_count = child_count.data();
-    out.child_first = child_first.data();
-    out.child_weight = cw.data();
-    out.child_upper = cu.data();
-    out.child_lower = cl.data();
-    out.child_obs = child_obs.data();
+    out.child_count = child_count;
+    out.child_first = child_first;
+    out.child_weight = cw;
+    out.child_upper = cu;
+    out.child_lower = cl;
+    out.child_obs = child_obs;
+    const auto tc0 = std::chrono::steady_clock::now();
     const int rc = P.expand(P.ctx, leaves.data(), L, &out);
+    const auto tc1 = std::chrono::steady_clock::now();
+    t_call += ns(tc1 - tc0);
     if (rc != DESPOT_OK) return rc;
     batches.fetch_add(1);
     steps.fetch_add(out.scenario_steps);
@@ -227,16 +273,23 @@ struct Search {
       while (d > m && !max_depth.compare_exchange_weak(m, d)) {
       }
     }
+    const auto tc2 = std::chrono::steady_clock::now();
+    t_children += ns(tc2 - tc1);
     for (Pending& p : batch) {
       backup(p.path);
       release_markers(p.path);
       if (p.inflight) p.inflight->fetch_sub(1);
       if (p.inflight) inflight_total.fetch_sub(1);
     }
+    t_backup += ns(std::chrono::steady_clock::now() - tc2);
     return DESPOT_OK;
   }
 
+  // Batchers take turns: while one waits for its expansion call the other
+  // creates the children and backs up the previous batch (the host work and
+  // the device work of consecutive batches overlap).
   void batcher() {
+    OutBuf ob;
     const uint32_t max_batch = std::max<uint32_t>(1, C.max_batch);
     for (;;) {
       std::vector<Pending> batch;
@@ -254,7 +307,8 @@ struct Search {
           queue.pop_front();
         }
       }
-      const int rc = error.load() ? error.load() : expand(batch);
+      if (batch.empty()) continue;  // the other batcher took the leaves while this one waited
+      const int rc = error.load() ? error.load() : expand(batch, ob);
       if (rc != DESPOT_OK) {
         int expected = 0;
         if (error.compare_exchange_strong(expected, rc)) error_msg = despot_last_error();
@@ -467,12 +521,16 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
   {
     std::vector<Pending> first{Pending{root, {root}, nullptr}};
     root->state = TNode::kPending;
-    const int rc = S.expand(first);
+    OutBuf ob;
+    const int rc = S.expand(first, ob);
     if (rc != DESPOT_OK) return rc;
   }
   const uint32_t W = std::max<uint32_t>(1, C->workers);
   S.n_workers = W;
-  std::thread batcher([&] { S.batcher(); });
+  // two batchers when several workers produce leaves (overlap of host and device work)
+  const uint32_t n_batchers = W > 1 ? 2 : 1;
+  std::vector<std::thread> batchers;
+  for (uint32_t i = 0; i < n_batchers; ++i) batchers.emplace_back([&] { S.batcher(); });
   std::vector<std::thread> workers;
   for (uint32_t i = 0; i < W; ++i) workers.emplace_back([&] { S.worker(); });
   // anytime loop: time budget, trial budget, target gap
@@ -495,7 +553,7 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
     S.workers_done = true;
   }
   S.qcv.notify_all();
-  batcher.join();
+  for (auto& t : batchers) t.join();
   // result
   R->action = 0;
   double best = -std::numeric_limits<double>::infinity();
@@ -513,6 +571,11 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
   R->max_depth = S.max_depth.load();
   R->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   R->scenario_steps = S.steps.load();
+  if (getenv("DESPOT_SEARCH_TRACE"))
+    fprintf(stderr, "[despot search] %.3f s: batchers in the expansion call %.3f s, creating children %.3f s, "
+                    "backups %.3f s, %llu batches\n",
+            R->seconds, 1e-9 * (double)S.t_call.load(), 1e-9 * (double)S.t_children.load(),
+            1e-9 * (double)S.t_backup.load(), (unsigned long long)R->batches);
   if (dump && dump_capacity) {
     uint32_t n = 0;
     S.dump_tree(dump, dump_capacity, n);
