@@ -1060,8 +1060,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       b->mark(1);
       if (!all_self) {
         const size_t smem1 = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
-        kernel_occupancy((const void*)k1_update<M>, smem1, 256);  // sets the smem attribute if > 48 KB
-        k1_update<M><<<L, 256, smem1, st>>>(bd);  // + prefix in its last CTA
+        kernel_occupancy((const void*)k1_update<M>, smem1, M::kK1Threads);  // sets the smem attribute if > 48 KB
+        k1_update<M><<<L, M::kK1Threads, smem1, st>>>(bd);  // + prefix in its last CTA
         ++b->launches;
       }
       b->mark(2);
@@ -1417,7 +1417,13 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     rc = check_launch(m, "K3a");
   }
   if (!rc && !small_k3 && !b->k3_fused) {
-    k3_scan<<<1, 1024, 0, st>>>(bd);
+    if (LA <= kScanSmemLA) {
+      const size_t smem = 4 * (LA + 1);
+      kernel_occupancy((const void*)k3_scan_smem, smem, 1024);  // sets the smem attribute if > 48 KB
+      k3_scan_smem<<<1, 1024, smem, st>>>(bd);
+    } else {
+      k3_scan<<<1, 1024, 0, st>>>(bd);
+    }
     ++b->launches;
     rc = check_launch(m, "K3b");
   }

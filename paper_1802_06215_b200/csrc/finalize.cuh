@@ -147,6 +147,38 @@ __global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
   __shared__ uint64_t wsum[32];
   scan_children(b, b.nc, wsum);
 }
+// The same scan with the counts staged in shared memory (L*A <= kScanSmemLA):
+// coalesced loads and stores instead of each thread walking a contiguous
+// chunk of global memory in dependent steps (config 2: 20 -> a few us)
+constexpr uint32_t kScanSmemLA = 49152;
+__global__ void __launch_bounds__(1024) k3_scan_smem(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char sc_smem[];
+  __shared__ uint64_t wsum[32];
+  uint32_t* v = reinterpret_cast<uint32_t*>(sc_smem);  // [LA + 1]
+  const uint32_t LA = b.L * b.A;
+  for (uint32_t i = threadIdx.x; i < LA; i += blockDim.x) v[i] = b.nc[i];
+  __syncthreads();
+  const uint32_t per = (LA + blockDim.x - 1) / blockDim.x, i0 = threadIdx.x * per;
+  uint64_t loc = 0;
+  for (uint32_t i = i0; i < i0 + per && i < LA; ++i) loc += v[i];
+  uint64_t tot;
+  uint64_t run = block_excl_scan(loc, wsum, tot);  // (synchronises the block)
+  for (uint32_t i = i0; i < i0 + per && i < LA; ++i) {
+    const uint32_t c = v[i];
+    v[i] = (uint32_t)run;
+    run += c;
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < LA; i += blockDim.x) b.child_begin[i] = v[i];
+  if (threadIdx.x == 0) {
+    b.child_begin[LA] = (uint32_t)tot;
+    if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
+    b.status[1] = (uint32_t)tot;
+    const uint64_t steps = (uint64_t)__ldcg(&b.sums[SumLayout{(uint64_t)LA * b.S, LA}.steps()]);
+    b.status[2] = (uint32_t)steps;
+    b.status[3] = (uint32_t)(steps >> 32);
+  }
+}
 
 // K3c body: outputs of (leaf, action) la: Eq. 11/12 child bounds, one-level
 // Eq. 4, and the leaf's child-key table

@@ -15,9 +15,9 @@ namespace hd {
 // (order kept) into the leaf arena.  Leaves with action == -1 only publish n.
 // ---------------------------------------------------------------------------
 template <class M>
-__global__ void __launch_bounds__(256) k1_update(BatchDev b) {
+__global__ void __launch_bounds__(512) k1_update(BatchDev b) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
-  __shared__ uint32_t warp_cnt[8];
+  __shared__ uint32_t warp_cnt[16];
   __shared__ uint32_t s_base;
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {

@@ -25,6 +25,7 @@ __device__ __forceinline__ void copy_words(void* dst, const void* src, int bytes
 // Tiger: state bit0 side, bit1 terminal; 0 LISTEN, 1 OPEN-LEFT, 2 OPEN-RIGHT
 // ===========================================================================
 struct Tiger {
+  static constexpr int kK1Threads = 512;  // K1 block: one round over K = 500 scenarios
   static constexpr int kMinBlocks = 8;  // K2 occupancy target (CTAs of 128 per SM)
   struct Sm {
     uint64_t t_listen;
@@ -113,6 +114,7 @@ struct Tiger {
 template <int R>
 struct RockSample {
   static constexpr int kMinBlocks = 8;  // 64 registers: 32 warps per SM
+  static constexpr int kK1Threads = 512;  // K1 block: one round over K = 500 scenarios
   static constexpr int kMaxTable = 16384;  // n*n*m entries of the per-cell rock tables
   static constexpr uint32_t kExitFlag = 0x8000u;  // move target flag: the robot exits (+10)
   struct Sm {
@@ -429,6 +431,7 @@ constexpr int kNavMaxThreads = 256;    // largest block of a kernel using Nav
 template <int NW>
 struct Nav {
   static constexpr int kMinBlocks = 5;
+  static constexpr int kK1Threads = kNavMaxThreads;  // the per-thread grids are sized for it
   struct Sm {
     int32_t n, wall_y, goal_x, goal_y;
     int32_t gate_x[2];
