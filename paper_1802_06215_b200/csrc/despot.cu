@@ -1432,8 +1432,14 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     ++b->launches;
     rc = check_launch(m, "K3c(sparse)");
   } else if (!rc && !small_k3) {
-    if (b->S > kWideS) k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
-    else k3_write_dense<<<g3, 128, 0, st>>>(bd);
+    if (b->S > kWideS) {
+      k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
+    } else if (b->S <= 16) {
+      const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
+      k3_write_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+    } else {
+      k3_write_dense<<<g3, 128, 0, st>>>(bd);
+    }
     ++b->launches;
     rc = check_launch(m, "K3c");
   }

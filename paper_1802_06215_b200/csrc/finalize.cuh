@@ -231,6 +231,81 @@ __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
   if (la >= (uint64_t)b.L * b.A) return;
   write_one(b, la, lane, b.child_begin[la], b.nc[la]);
 }
+// S rounded up to a power of two: the lanes of one (leaf, action) in the
+// lane-per-slot finalize kernels
+__host__ __device__ inline uint32_t small_group_width(uint32_t S) {
+  uint32_t sp = 1;
+  while (sp < S) sp <<= 1;
+  return sp;
+}
+
+// K3c for few observation slots (S <= 16: RockSample/MARS, Tiger): a lane per
+// slot and 32/S' (leaf, action) pairs per warp (S' = S rounded up to a power
+// of two), the child ordinals recomputed in registers from the first ids
+// (the rank array is not read), every load of a pair issued at once
+__global__ void __launch_bounds__(128) k3_write_grouped(BatchDev b) {
+  const uint32_t lane = threadIdx.x & 31, S = b.S, A = b.A;
+  const uint32_t LA = b.L * A;
+  const uint32_t Sp = small_group_width(S), G = 32 / Sp;
+  const uint32_t j = lane & (Sp - 1), gshift = lane & ~(Sp - 1);
+  const uint32_t gbits = Sp == 32 ? 0xffffffffu : (1u << Sp) - 1u;
+  const uint32_t la = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G + lane / Sp;
+  if ((la - lane / Sp) >= LA) return;  // warp-uniform
+  const SumLayout lay{(uint64_t)LA * S, LA};
+  const bool v = la < LA && j < S;
+  const uint64_t slot = (uint64_t)la * S + j;
+  const int64_t N = v ? b.sums[lay.N(slot)] : 0;
+  const int64_t W = v ? b.sums[lay.W(slot)] : 0;
+  const int64_t U = v ? b.sums[lay.U(slot)] : 0;
+  const int64_t Lm = v ? b.sums[lay.Lm(slot)] : 0;
+  const int32_t mn = v ? b.mins[slot] : 0;
+  const bool q = la < LA && j == 0;
+  const int64_t Q0 = q ? b.sums[lay.Q(la, 0)] : 0, Q1 = q ? b.sums[lay.Q(la, 1)] : 0,
+                Q2 = q ? b.sums[lay.Q(la, 2)] : 0;
+  const uint32_t cb = la < LA ? b.child_begin[la] : 0;
+  const bool ne = N != 0;
+  const uint32_t gb = (__ballot_sync(0xffffffffu, ne) >> gshift) & gbits;
+  uint32_t rk = 0;  // first occurrence (R8): non-empty slots with a smaller first id
+  for (uint32_t k = 0; k < Sp; ++k) {
+    const int32_t mk = __shfl_sync(0xffffffffu, mn, k, Sp);
+    rk += ((gb >> k) & 1u) && mk < mn;
+  }
+  int64_t wt = W, nt = N;
+  for (uint32_t o = Sp >> 1; o; o >>= 1) {
+    wt += __shfl_xor_sync(0xffffffffu, wt, o);
+    nt += __shfl_xor_sync(0xffffffffu, nt, o);
+  }
+  if (la >= LA) return;
+  const uint32_t leaf = la / A, a = la - leaf * A;
+  const LeafDev& lf = b.leaves[leaf];
+  const DevModel& dm = *b.model;
+  if (ne) {
+    const uint32_t c = cb + rk;
+    if (c < b.child_capacity) {
+      const double Wd = (double)W;
+      b.child_count[c] = (uint32_t)N;
+      b.child_first[c] = (uint32_t)mn;
+      b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
+      b.child_upper[c] = (float)((double)U / Wd);
+      b.child_lower[c] = (float)((double)Lm / Wd);
+      b.child_obs[c] = j;
+    }
+    if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = j;  // key table for later updates
+  }
+  if (j == 0) {
+    lf.nchild[a] = __popc(gb);
+    const double Wd = (double)wt;
+    b.act_reward[la] = (float)((double)Q0 / Wd);
+    b.act_upper[la] = (float)((double)Q1 / Wd);
+    b.act_lower[la] = (float)((double)Q2 / Wd);
+    if (a == 0) {
+      b.n_scen[leaf] = (uint32_t)nt;
+      b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
+      if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+    }
+  }
+}
+
 // K3c for many observation slots (S > 32: navigation's 257): one CTA per
 // (leaf, action), one thread per slot -- a warp per (leaf, action) would walk
 // its slots in S/32 dependent rounds
@@ -299,11 +374,6 @@ __global__ void __launch_bounds__(256) k3_write_wide(BatchDev b) {
 // first ids instead of stored, and child_begin scanned in shared memory.
 constexpr uint32_t kSmallLA = 4096;
 constexpr uint32_t kSmallUnroll = 4;
-__host__ __device__ inline uint32_t small_group_width(uint32_t S) {
-  uint32_t sp = 1;
-  while (sp < S) sp <<= 1;
-  return sp;
-}
 __host__ __device__ inline size_t small_finalize_smem(uint64_t LA) { return align16(4 * (LA + 1)); }
 __device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char* smem) {
   __shared__ uint64_t wsum[32];
