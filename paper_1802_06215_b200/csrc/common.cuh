@@ -167,6 +167,7 @@ struct BatchDev {
   int32_t* mins;             // exchange MIN block
   uint32_t* rank;            // [L*A*S] child ordinal of a slot
   uint32_t* nc;              // [L*A] children per (leaf, action)
+  unsigned long long* scan_flags;  // K3b look-back: [0] tile counter, [1 + t] tile t's (flag, prefix)
   uint32_t* status;          // [kStatWords header (kStat*), n_leaf[L]]
   uint32_t fused_k3;         // 1: K2's last CTA runs the small finalize
   uint32_t* err;

@@ -965,6 +965,10 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
                o_scen = take(8 * ((size_t)L + 1));
   const size_t o_stat = off;
   off += (stat_bytes + 7) & ~size_t(7);
+  // K3b's look-back flags (tile counter + one word per 1024 (leaf, action)
+  // pairs), zeroed by the same memset as the status block and the sums
+  const size_t o_scan = off;
+  off += 8 * (LA / kScanTile + 2);
   const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
                o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
                o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound),
@@ -990,6 +994,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   bd.mins = reinterpret_cast<int32_t*>(s + o_mins);
   bd.rank = reinterpret_cast<uint32_t*>(s + o_rank);
   bd.nc = reinterpret_cast<uint32_t*>(s + o_nc);
+  bd.scan_flags = reinterpret_cast<unsigned long long*>(s + o_scan);
   if (b->sparse) {
     bd.sp_item = reinterpret_cast<uint32_t*>(s + o_item);
     b->io.hash = reinterpret_cast<uint64_t*>(s + o_hash);
@@ -1417,13 +1422,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     rc = check_launch(m, "K3a");
   }
   if (!rc && !small_k3 && !b->k3_fused) {
-    if (LA <= kScanSmemLA) {
-      const size_t smem = 4 * (LA + 1);
-      kernel_occupancy((const void*)k3_scan_smem, smem, 1024);  // sets the smem attribute if > 48 KB
-      k3_scan_smem<<<1, 1024, smem, st>>>(bd);
-    } else {
-      k3_scan<<<1, 1024, 0, st>>>(bd);
-    }
+    k3_scan_lookback<<<(unsigned)((LA + kScanTile - 1) / kScanTile), kScanTile, 0, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3b");
   }

@@ -120,61 +120,51 @@ __global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
   rank_one(b, la, lane, reinterpret_cast<int32_t*>(k3_smem) + (size_t)wid * 2 * b.S, &b.nc[la]);
 }
 
-// K3b body: child_begin = exclusive scan of nc (whole CTA) + status fields
-__device__ __forceinline__ void scan_children(const BatchDev& b, const uint32_t* nc, uint64_t* wsum) {
+// K3b as a multi-CTA scan with decoupled look-back: each CTA takes the next
+// tile of kScanTile counts (an atomic ticket, so every tile it waits on is
+// already running), publishes its aggregate, walks back over its
+// predecessors' published words until an inclusive prefix, and publishes its
+// own inclusive prefix (flag 2).  A (flag, value) pair is one 64-bit word.
+constexpr uint32_t kScanTile = 1024;
+__global__ void __launch_bounds__(kScanTile) k3_scan_lookback(BatchDev b) {
+  __shared__ uint64_t wsum[32];
+  __shared__ uint32_t tile_sh;
+  __shared__ uint64_t excl_sh;
+  constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kVal = (1ull << 62) - 1;
   const uint64_t LA = (uint64_t)b.L * b.A;
-  const uint64_t per = (LA + blockDim.x - 1) / blockDim.x;
-  const uint64_t i0 = (uint64_t)threadIdx.x * per;
-  uint64_t loc = 0;
-  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) loc += nc[i];
+  if (threadIdx.x == 0) tile_sh = (uint32_t)atomicAdd(&b.scan_flags[0], 1ull);
+  __syncthreads();
+  const uint32_t tile = tile_sh;
+  const uint64_t i = (uint64_t)tile * kScanTile + threadIdx.x;
+  const uint32_t v = i < LA ? b.nc[i] : 0u;
   uint64_t tot;
-  uint64_t run = block_excl_scan(loc, wsum, tot);
-  for (uint64_t i = i0; i < i0 + per && i < LA; ++i) {
-    b.child_begin[i] = (uint32_t)run;
-    run += nc[i];
-  }
+  const uint64_t pre = block_excl_scan(v, wsum, tot);
+  unsigned long long* st = b.scan_flags + 1;
   if (threadIdx.x == 0) {
-    b.child_begin[LA] = (uint32_t)tot;
-    if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
-    // status block for the host: total children and the step counter
-    b.status[1] = (uint32_t)tot;
+    uint64_t excl = 0;
+    if (tile == 0) {
+      atomicExch(&st[0], kIncl | tot);
+    } else {
+      atomicExch(&st[tile], kAgg | tot);
+      for (int p = (int)tile - 1;;) {
+        const unsigned long long f = atomicAdd(&st[p], 0ull);  // device-scope read
+        if (!(f >> 62)) continue;                               // predecessor not published yet
+        excl += f & kVal;
+        if ((f >> 62) == 2) break;                              // an inclusive prefix: done
+        --p;
+      }
+      atomicExch(&st[tile], kIncl | (excl + tot));
+    }
+    excl_sh = excl;
+  }
+  __syncthreads();
+  if (i < LA) b.child_begin[i] = (uint32_t)(excl_sh + pre);
+  if (threadIdx.x == 0 && (uint64_t)(tile + 1) * kScanTile >= LA) {  // the last tile: totals
+    const uint64_t total = excl_sh + tot;
+    b.child_begin[LA] = (uint32_t)total;
+    if (total > b.child_capacity) atomicOr(b.err, kErrChildCap);
+    b.status[1] = (uint32_t)total;
     const uint64_t steps = (uint64_t)__ldcg(&b.sums[SumLayout{LA * b.S, LA}.steps()]);
-    b.status[2] = (uint32_t)steps;
-    b.status[3] = (uint32_t)(steps >> 32);
-  }
-}
-__global__ void __launch_bounds__(1024) k3_scan(BatchDev b) {
-  __shared__ uint64_t wsum[32];
-  scan_children(b, b.nc, wsum);
-}
-// The same scan with the counts staged in shared memory (L*A <= kScanSmemLA):
-// coalesced loads and stores instead of each thread walking a contiguous
-// chunk of global memory in dependent steps (config 2: 20 -> a few us)
-constexpr uint32_t kScanSmemLA = 49152;
-__global__ void __launch_bounds__(1024) k3_scan_smem(BatchDev b) {
-  extern __shared__ __align__(16) unsigned char sc_smem[];
-  __shared__ uint64_t wsum[32];
-  uint32_t* v = reinterpret_cast<uint32_t*>(sc_smem);  // [LA + 1]
-  const uint32_t LA = b.L * b.A;
-  for (uint32_t i = threadIdx.x; i < LA; i += blockDim.x) v[i] = b.nc[i];
-  __syncthreads();
-  const uint32_t per = (LA + blockDim.x - 1) / blockDim.x, i0 = threadIdx.x * per;
-  uint64_t loc = 0;
-  for (uint32_t i = i0; i < i0 + per && i < LA; ++i) loc += v[i];
-  uint64_t tot;
-  uint64_t run = block_excl_scan(loc, wsum, tot);  // (synchronises the block)
-  for (uint32_t i = i0; i < i0 + per && i < LA; ++i) {
-    const uint32_t c = v[i];
-    v[i] = (uint32_t)run;
-    run += c;
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < LA; i += blockDim.x) b.child_begin[i] = v[i];
-  if (threadIdx.x == 0) {
-    b.child_begin[LA] = (uint32_t)tot;
-    if (tot > b.child_capacity) atomicOr(b.err, kErrChildCap);
-    b.status[1] = (uint32_t)tot;
-    const uint64_t steps = (uint64_t)__ldcg(&b.sums[SumLayout{(uint64_t)LA * b.S, LA}.steps()]);
     b.status[2] = (uint32_t)steps;
     b.status[3] = (uint32_t)(steps >> 32);
   }
