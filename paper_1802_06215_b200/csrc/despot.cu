@@ -1416,6 +1416,11 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     k3_small_dense<<<1, 1024, smem, st>>>(bd);
     ++b->launches;
     rc = check_launch(m, "K3(small)");
+  } else if (!rc && b->S <= 16) {  // counts only: k3_write_grouped recomputes the ordinals
+    const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
+    k3_count_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+    ++b->launches;
+    rc = check_launch(m, "K3a");
   } else if (!rc) {
     k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 8, st>>>(bd);
     ++b->launches;

@@ -229,6 +229,22 @@ __host__ __device__ inline uint32_t small_group_width(uint32_t S) {
   return sp;
 }
 
+// K3a for few observation slots (S <= 16): only the child count of each
+// (leaf, action) -- k3_write_grouped recomputes the ordinals -- a lane per
+// slot, 32/S' pairs per warp
+__global__ void __launch_bounds__(128) k3_count_grouped(BatchDev b) {
+  const uint32_t lane = threadIdx.x & 31, S = b.S, LA = b.L * b.A;
+  const uint32_t Sp = small_group_width(S);
+  const uint32_t j = lane & (Sp - 1), gshift = lane & ~(Sp - 1);
+  const uint32_t gbits = Sp == 32 ? 0xffffffffu : (1u << Sp) - 1u;
+  const uint32_t la = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 / Sp) + lane / Sp;
+  if ((la - lane / Sp) >= LA) return;  // warp-uniform
+  const SumLayout lay{(uint64_t)LA * S, LA};
+  const bool ne = la < LA && j < S && b.sums[lay.N((uint64_t)la * S + j)] != 0;
+  const uint32_t gb = (__ballot_sync(0xffffffffu, ne) >> gshift) & gbits;
+  if (j == 0 && la < LA) b.nc[la] = __popc(gb);
+}
+
 // K3c for few observation slots (S <= 16: RockSample/MARS, Tiger): a lane per
 // slot and 32/S' (leaf, action) pairs per warp (S' = S rounded up to a power
 // of two), the child ordinals recomputed in registers from the first ids
