@@ -1402,7 +1402,10 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   b->mark(5);
   // small dense batches (few slots): rank + scan + write in one CTA (or in
   // K2's last CTA, already done, when the batch was fused)
-  const bool small_k3 = !b->sparse && LA <= kSmallLA && b->S <= 32;
+  // the single-CTA finalize when its 32 warps cover the pairs in about one
+  // sweep; beyond that the multi-CTA kernels win (their launches overlap)
+  const bool small_k3 = !b->sparse && b->S <= 32 &&
+                        LA <= std::min<uint64_t>(kSmallLA, 32 * (32 / small_group_width(b->S)) * 2);
   if (b->k3_fused) {
   } else if (!rc && b->sharded_sparse) {
     rc = merge_sparse(m, b);  // the ranks' records -> global children
