@@ -21,6 +21,10 @@
  */
 #include "oracle.h"
 
+/* per-scenario word buffers: state words <= 4 + 2*31 = 66 (driving, 31
+ * pedestrians), observation words <= 32 */
+#define ORACLE_MAXW 128
+
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -663,7 +667,7 @@ static int policy_action(const oracle_model* M, const uint32_t* s, const uint32_
 static void rollout(const oracle_model* M, const uint32_t* s_in, const uint32_t* z_in, uint32_t id,
                     uint32_t d0, uint64_t seed, double* ret_out, uint32_t* len_out,
                     uint64_t* hash_out, uint64_t* steps) {
-  uint32_t s[64], s2[64], z[64];
+  uint32_t s[ORACLE_MAXW], s2[ORACLE_MAXW], z[ORACLE_MAXW];
   memcpy(s, s_in, M->SW * 4);
   memcpy(z, z_in, M->OW * 4);
   double ret = 0.0, disc = 1.0;
@@ -859,7 +863,7 @@ double oracle_upper(const oracle_model* M, const uint32_t* s) { return upper_of(
 int oracle_rollout(const oracle_model* M, const uint32_t* s, const uint32_t* z, uint32_t id,
                    uint32_t depth, uint64_t seed, double* ret, uint32_t* len, uint64_t* hash,
                    uint64_t* steps) {
-  uint32_t z0[64];
+  uint32_t z0[ORACLE_MAXW];
   if (!z) {
     initial_obs(M, s, z0);
     z = z0;
@@ -991,7 +995,7 @@ int oracle_expand_batch(oracle_model* M, const oracle_leaf* leaves, uint32_t L,
       tmp->seed = seed;
       uint32_t kept = 0;
       for (uint32_t i = 0; i < P->n; ++i) {
-        uint32_t s2[64], z[64];
+        uint32_t s2[ORACLE_MAXW], z[ORACLE_MAXW];
         float r;
         int term;
         steps += (uint64_t)step_or_term(M, P->states + (size_t)i * SW, lf->action, P->ids[i],
@@ -1035,7 +1039,7 @@ int oracle_expand_batch(oracle_model* M, const oracle_leaf* leaves, uint32_t L,
       uint32_t* gkey = (uint32_t*)malloc((size_t)S->n * OW * 4);
       uint32_t cbase = nchildren;
       for (uint32_t i = 0; i < S->n; ++i) {
-        uint32_t s2[64], z[64];
+        uint32_t s2[ORACLE_MAXW], z[ORACLE_MAXW];
         float r;
         int term;
         steps += (uint64_t)step_or_term(M, S->states + (size_t)i * SW, (int)a, S->ids[i],
@@ -1114,7 +1118,7 @@ int oracle_rollout_bounds(const oracle_model* M, int64_t h, double* upper_mean, 
   double W = 0.0, U = 0.0, Lm = 0.0;
   for (uint32_t i = 0; i < nd->n; ++i) {
     const uint32_t* s = nd->states + (size_t)i * M->SW;
-    uint32_t z[64];
+    uint32_t z[ORACLE_MAXW];
     initial_obs(M, s, z);
     double u = is_terminal(M, s) ? 0.0 : upper_of(M, s);
     double lam = 0.0;
