@@ -343,7 +343,7 @@ def main():
                     help="also time the oracle in one process per host core")
     ap.add_argument("--no-all-cores-baseline", dest="all_cores_baseline", action="store_false")
     ap.add_argument("--peds", type=int, default=None, help="pedestrians of the driving config (NEXT-3 study)")
-    ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread"],
+    ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread", "group"],
                     help="driving kernel: factored warp per scenario, thread per scenario, or per-batch choice")
     ap.add_argument("--plan", action="store_true",
                     help="tree size per planning time: despot_plan vs the serial oracle-backed driver (NEXT-1/2)")
@@ -374,7 +374,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
     c, kind, params, st, w, seed, L = workload(args.config, args.K, args.peds)
-    mflags = {"auto": 0, "thread": 1, "warp": 2}[args.car_variant]
+    mflags = {"auto": 0, "thread": 1, "warp": 2, "group": 4}[args.car_variant]
     model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags)
     stream = torch.cuda.Stream(dev)  # a non-blocking stream of our own (not the legacy default stream)
     torch.cuda.set_stream(stream)
@@ -521,7 +521,7 @@ def main():
         q_bound = A * sum(model.node_info(lf[0])[0] for lf in leaves)
         thread = args.car_variant == "thread" or (args.car_variant == "auto" and (
             q_bound >= num_sms * 256 or c.get("peds", 20) < 8))
-        k2_name = "k2_car_thread" if thread else "k2_car_warp"
+        k2_name = "k2_car_group" if args.car_variant == "group" else "k2_car_thread" if thread else "k2_car_warp"
     else:
         k2_name = "k2_expand_dense"
     if rank == 0:

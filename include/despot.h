@@ -80,6 +80,9 @@ typedef struct {
  * items to fill the GPU with one thread each, else thread-per-scenario. */
 #define DESPOT_MF_UNFACTORED 1u /* always thread per scenario */
 #define DESPOT_MF_FACTORED 2u   /* always warp per scenario   */
+#define DESPOT_MF_GROUPED 4u    /* a lane group per scenario: lane q owns Philox block q
+                                   (the car's word and pedestrians 4q-1 .. 4q+2),
+                                   32 / ceil((P+1)/4) scenarios per warp */
 
 typedef struct {
   uint32_t num_actions; /* |A|                                                     */

@@ -806,10 +806,18 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   // (measured, profiles/r01/peds_sweep.jsonl: the warp kernel wins for >= 12
   // pedestrians at 12k items, the thread kernel everywhere at 96k items and
   // for 6 pedestrians, whose warps would leave 25 of 32 lanes idle)
-  const bool unfactored = (m->flags & DESPOT_MF_UNFACTORED) ||
-                          (!(m->flags & DESPOT_MF_FACTORED) &&
-                           (q_bound >= (uint64_t)m->num_sms * 256 || dm.peds < 8));
-  if (unfactored) {
+  const bool grouped = m->flags & DESPOT_MF_GROUPED;
+  const bool unfactored = !grouped && ((m->flags & DESPOT_MF_UNFACTORED) ||
+                                       (!(m->flags & DESPOT_MF_FACTORED) &&
+                                        (q_bound >= (uint64_t)m->num_sms * 256 || dm.peds < 8)));
+  if (grouped) {
+    const uint64_t G = ((uint64_t)dm.peds + 4) / 4, gpw = 32 / G;
+    const uint64_t warps = (q_bound + gpw - 1) / gpw;
+    auto kern = record ? k2_car_group<true> : k2_car_group<false>;
+    const int occ = kernel_occupancy((const void*)kern, 0, 128);
+    const uint64_t g = std::min<uint64_t>((warps + 3) / 4, (uint64_t)m->num_sms * occ);
+    kern<<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+  } else if (unfactored) {
     dispatch_car(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       const uint64_t g = std::min<uint64_t>((q_bound + 127) / 128, (uint64_t)m->num_sms * 16);

@@ -340,6 +340,219 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
 }
 
 // ---------------------------------------------------------------------------
+// K2g: several scenarios per warp (NEXT-3's "packing several small-element
+// scenarios per warp"): a group of G = ceil((P + 1) / 4) lanes per
+// (leaf, action, scenario), lane q of the group owning Philox block q of the
+// step -- the random words 4q .. 4q+3: word 0 is the car's, word 1 + p
+// pedestrian p's -- so each lane draws exactly one block per step (as many
+// blocks per scenario as the thread kernel) and moves its (up to) four
+// pedestrians; the car is tracked by every lane of the group, the failure
+// draw comes from lane 0, collisions are a ballot over the group, the
+// policy's gap a minimum over the group.  32 / G scenarios per warp (five
+// for 20 pedestrians).  Bit-identical to K2t (same operation sequence per
+// element).  The group loops run warp-uniformly (shuffles need every lane).
+// ---------------------------------------------------------------------------
+#ifndef HD_CARG_MINB
+#define HD_CARG_MINB 6  // 80 registers: the best of 1, 5, 6, 8 CTAs per SM (config 4)
+#endif
+template <bool RECORD>
+__global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, SparseItemOut io) {
+  __shared__ typename CarThreadT<1>::Sm sm;  // scalar parameters + gamma table + rotations
+  CarThreadT<1>::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const DevModel& dm = *b.model;
+  const uint32_t OW = dm.OW, SW = dm.SW;
+  const int P = sm.peds;
+  const uint32_t G = (uint32_t)(P + 1 + 3) / 4, GPW = 32 / G;  // lanes per scenario, scenarios per warp
+  const uint32_t lane = threadIdx.x & 31, gw = lane / G, q = lane - gw * G;
+  const bool in_group = gw < GPW;                 // the last 32 mod G lanes idle
+  const uint32_t g0 = gw * G;                     // first lane of the group
+  const uint32_t gmask = in_group ? ((G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << g0) : 0u;
+  const uint64_t Q = b.scen_off[b.L];
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  const uint64_t wglobal = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  uint32_t steps_acc = 0;
+  for (uint64_t base = wglobal * GPW; base < Q; base += nwarps * GPW) {
+    const uint64_t t = base + gw;
+    const bool valid = in_group && t < Q;
+    uint32_t leaf = 0, a0 = 0, i = 0, id = 0, cap = 1;
+    const LeafDev* lfp = b.leaves;
+    if (valid) {
+      leaf = find_leaf(b.scen_off, b.L, t);
+      lfp = &b.leaves[leaf];
+      const uint32_t n = b.n_leaf[leaf];
+      const uint64_t local = t - b.scen_off[leaf];
+      a0 = (uint32_t)(local / n);
+      i = (uint32_t)(local - (uint64_t)a0 * n);
+      id = lfp->ids[i];
+      cap = lfp->cap;
+    }
+    const LeafDev& lf = *lfp;
+    // element state: the car (every lane), this lane's pedestrians p = 4q + k - 1
+    float xc = 0.0f;
+    uint32_t level = 0;
+    bool term = true;
+    float px[4] = {0.0f, 0.0f, 0.0f, 0.0f}, py[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    uint32_t goal[4] = {0u, 0u, 0u, 0u};
+    if (valid) {
+      xc = __uint_as_float(lf.states[i]);
+      const uint32_t w1 = lf.states[cap + i];
+      level = w1 & 0xFFu;
+      term = (w1 >> 8) & 1u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = (int)(4 * q) + k - 1;
+        if (p >= 0 && p < P) {
+          px[k] = __uint_as_float(lf.states[(4 + 2 * p) * cap + i]);
+          py[k] = __uint_as_float(lf.states[(5 + 2 * p) * cap + i]);
+          goal[k] = (lf.states[(2 + (p >> 4)) * cap + i] >> (2 * (p & 15))) & 3u;
+        }
+      }
+    }
+    // one factored step g(s, a, phi_tt) of this lane's group (active: the
+    // group still steps; inactive groups run the shuffles only)
+    auto step = [&](bool active, int a, uint32_t tt, float& r) {
+      const uint4 wv = philox4x32_10(id, tt, q, 0u, lf.seed_lo, lf.seed_hi);  // words 4q .. 4q+3
+      const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+      // 1. the car: lane 0's word 0 decides the failure
+      const int fail0 = event(wv.x, sm.t_fail) ? 1 : 0;
+      const bool fail = __shfl_sync(0xffffffffu, fail0, in_group ? g0 : lane) != 0;
+      if (active && !fail) {
+        if (a == 1 && level < 4u) level += 1u;
+        if (a == 2 && level > 0u) level -= 1u;
+      }
+      const float v = 0.5f * (float)level;
+      if (active) xc = xc + v * 0.25f;
+      // 2. pedestrians, 3. collision
+      bool hit = false;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = (int)(4 * q) + k - 1;
+        if (active && p >= 0 && p < P) {
+          const float2 cs = sm.rot[car_noise_index(ws[k])];
+          car_ped_move(px[k], py[k], goal[k], cs.x, cs.y);
+          const float dx = px[k] - xc;
+          hit = hit || (dx * dx + py[k] * py[k] < 1.0f);
+        }
+      }
+      const bool coll = (__ballot_sync(0xffffffffu, hit) & gmask) != 0u;
+      const bool g = xc >= 20.0f;  // 4. goal
+      r = car_reward(a, coll, g, v);
+      if (active) term = coll || g;
+    };
+    float r0 = 0.0f;
+    const bool live0 = valid && !term;
+    step(live0, (int)a0, lf.depth + 1, r0);
+    if (!live0) r0 = 0.0f;
+    if (live0 && q == 0) ++steps_acc;
+    // the child's key: this lane's words 4q .. 4q+3 (word 0: the car)
+    uint64_t hk = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t w = 4 * q + (uint32_t)k;
+      if (valid && w < OW) {
+        const int p = (int)w - 1;
+        uint32_t zw;
+        if (term) zw = w == 0 ? kCarTerminalWord0 : 0u;
+        else if (w == 0) zw = car_bin(xc) | (level << 16);
+        else zw = car_bin(px[k]) | (car_bin(py[k]) << 16);
+        (void)p;
+        io.keys[t * OW + w] = zw;
+        if (RECORD) b.scen_obs[t * OW + w] = zw;
+        hk ^= key_mix(zw, w);
+      }
+    }
+    {  // XOR over the group (the group's lanes in turn)
+      uint64_t tot = 0;
+      for (uint32_t k = 0; k < G; ++k) tot ^= __shfl_sync(0xffffffffu, hk, in_group ? g0 + k : lane);
+      hk = tot;
+    }
+    if (valid && q == 0) io.hash[t] = hk;
+    if (RECORD && valid && b.scen_states) {
+      uint32_t* dst = b.scen_states + t * SW;
+      if (q == 0) {
+        dst[0] = __float_as_uint(xc);
+        dst[1] = level | ((uint32_t)term << 8);
+        dst[2] = lf.states[2 * cap + i];
+        dst[3] = lf.states[3 * cap + i];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = (int)(4 * q) + k - 1;
+        if (p >= 0 && p < P) {
+          dst[4 + 2 * p] = __float_as_uint(px[k]);
+          dst[5 + 2 * p] = __float_as_uint(py[k]);
+        }
+      }
+    }
+    double u = 0.0, lam = 0.0;
+    uint32_t len = 0;
+    uint64_t h = kFnvOffset;
+    const bool rolled = valid && !term;  // a roll-out from the non-terminal child state
+    bool live = rolled;
+    if (live) {
+      int k = (int)ceilf((20.0f - xc) * 2.0f);
+      k = k < 1 ? 1 : k;
+      u = 100.0 * sm.gpow[k - 1];  // Eq. 11
+    }
+    // roll-out (Eq. 12): pi0 reads the last observation's bins
+    const uint32_t t0 = lf.depth + 1;
+    uint32_t tt = t0;
+    double acc = 0.0;
+    live = live && tt < sm.D;
+    while (__any_sync(0xffffffffu, live)) {
+      const int cxb = car_bin_i(xc);
+      int gap = 255;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int p = (int)(4 * q) + k - 1;
+        if (p >= 0 && p < P) {
+          const int pxb = car_bin_i(px[k]), pyb = car_bin_i(py[k]);
+          if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
+        }
+      }
+      for (uint32_t k = 0; k < G; ++k) gap = min(gap, __shfl_sync(0xffffffffu, gap, in_group ? g0 + k : lane));
+      const int a = car_policy_from_gap(gap);
+      if (RECORD && live) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+      float r;
+      step(live, a, tt + 1, r);
+      if (live) {
+        acc += sm.gpow[tt - t0] * (double)r;
+        ++tt;
+        live = !term && tt < sm.D;
+      }
+    }
+    if (rolled) {
+      if (!term) acc += sm.gpow[tt - t0] * sm.tail;  // reached D non-terminal
+      lam = acc;
+      len = tt - t0;
+    }
+    if (valid && q == 0) {
+      steps_acc += len;
+      const double wn = (double)lf.w[i] * lf.inv_wroot;
+      const double fx = dm.fx, gamma = dm.gamma;
+      io.q3[3 * t + 0] = fxq(wn, fx);
+      io.q3[3 * t + 1] = fxq(wn * u, fx);
+      io.q3[3 * t + 2] = fxq(wn * lam, fx);
+      const uint64_t la = (uint64_t)leaf * b.A + a0;
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r0, fx));
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r0 + gamma * u), fx));
+      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r0 + gamma * lam), fx));
+      if (RECORD) {
+        b.scen_reward[t] = r0;
+        b.scen_upper[t] = (float)u;
+        b.scen_lower[t] = (float)lam;
+        b.scen_len[t] = len;
+        b.scen_hash[t] = h;
+      }
+    }
+  }
+  const uint32_t ws = warp_sum32(steps_acc);
+  if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)ws);
+}
+
+// ---------------------------------------------------------------------------
 // K3s: group the items of one (leaf, action) by key (first occurrence).  An
 // open-addressing table in shared memory (2^k >= 2n slots) maps each 64-bit
 // key hash to the smallest item position carrying it (atomicMin), so the

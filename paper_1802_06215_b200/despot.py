@@ -20,6 +20,7 @@ DESPOT_X_TIMING = 4
 DESPOT_X_TIMING_K2 = 8
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
+DESPOT_MF_GROUPED = 4
 
 STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5: "ECUDA",
           -6: "ENCCL", -7: "ESHUTDOWN", -8: "EHASH"}

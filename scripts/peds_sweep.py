@@ -3,7 +3,8 @@
  and the two kernel variants -- factored warp per
 scenario (lanes = pedestrians + car) vs thread per scenario -- at
 the full batch (64 roots x K=500) and a small one (8 roots x K=64, where the
-factored kernel's extra parallelism matters).  One JSON line per run."""
+factored kernel's extra parallelism matters), plus the grouped kernel (a lane
+group per scenario, several scenarios per warp).  One JSON line per run."""
 import json
 import os
 import subprocess
@@ -12,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for K in (500, 64):
     for peds in (6, 12, 20):
-        for variant in ("warp", "thread"):
+        for variant in ("warp", "group", "thread"):
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "4", "--peds", str(peds), "--K", str(K),
                    "--car-variant", variant, "--steps", "10", "--warmup", "3", "--no-cpu-baseline"]
             out = subprocess.run(cmd, capture_output=True, text=True)

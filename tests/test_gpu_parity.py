@@ -340,14 +340,17 @@ def test_fake_ranks_equal_single_gpu():
 # ----------------------------------------------------------------------------
 # driving (config 4): sparse 21-word keys, factored warp kernel
 # ----------------------------------------------------------------------------
-def _car_models(peds=20, D=90):
+def _car_models(peds=20, D=90, grouped=False):
     params = inputs.car_params(peds, D=D)
-    # forced factored (warp per scenario) and unfactored (thread per scenario)
-    return (Model("car", params, flags=2), Model("car", params, flags=1), oracle.Model("car", params))
+    # forced factored (warp per scenario) -- or grouped (a lane group per
+    # scenario, several scenarios per warp) -- and unfactored (thread per scenario)
+    return (Model("car", params, flags=4 if grouped else 2), Model("car", params, flags=1),
+            oracle.Model("car", params))
 
 
-def test_config4_car_64_roots_factored_and_unfactored():
-    gw, gt, om = _car_models()
+@pytest.mark.parametrize("grouped", [False, True])
+def test_config4_car_64_roots_factored_and_unfactored(grouped):
+    gw, gt, om = _car_models(grouped=grouped)
     roots = inputs.car_roots(64, 500)
     gws = [gw.belief_load(st, w, sd) for st, w, sd in roots]
     gts = [gt.belief_load(st, w, sd) for st, w, sd in roots]
@@ -363,9 +366,11 @@ def test_config4_car_64_roots_factored_and_unfactored():
     compare_batch(Gw, O, gw, om, list(zip(sample, range(len(sample)))))
 
 
-@pytest.mark.parametrize("peds,K,D", [(20, 64, 40), (6, 45, 90), (2, 7, 12), (12, 33, 30)])
-def test_car_small_full_parity_with_records(peds, K, D):
-    gw, gt, om = _car_models(peds, D)
+@pytest.mark.parametrize("peds,K,D,grouped", [(20, 64, 40, False), (6, 45, 90, False), (2, 7, 12, False),
+                                               (12, 33, 30, False), (20, 64, 40, True), (3, 37, 25, True),
+                                               (31, 20, 20, True)])
+def test_car_small_full_parity_with_records(peds, K, D, grouped):
+    gw, gt, om = _car_models(peds, D, grouped)
     st = inputs.car_belief(K, 5 + K, peds)
     st[0] = np.float32(12.0).view(np.uint32)  # closer to the goal: goal and collision outcomes occur
     w = inputs.weights(K, K, uniform=False)
@@ -391,7 +396,7 @@ def test_car_factored_equals_unfactored_1000_random_steps():
     rng = np.random.default_rng(6)
     for trial in range(10):
         peds = int(rng.choice([1, 6, 12, 20, 31]))
-        gw, gt, _ = _car_models(peds, D=2)
+        gw, gt, _ = _car_models(peds, D=2, grouped=trial % 2 == 1)
         K = 100
         st = inputs.car_belief(K, trial, peds, layout_seed=trial)
         xs = rng.uniform(0, 20, K).astype(np.float32)
