@@ -419,7 +419,7 @@ def main():
             steps, launches, nodes = model.run_prepared(prep, stream=stream)
             E = prep["E"]
             o = {"scenario_steps": steps, "launches": launches, "phase_ms": list(E.phase_ms),
-                 "num_children": E.num_children}
+                 "num_children": E.num_children, "h2d_bytes": int(E.h2d_bytes), "d2h_bytes": int(E.d2h_bytes)}
         o["new_nodes"] = [n for (lf, n) in zip(leaves, nodes) if lf[1] >= 0]  # self leaves return their own node
         return o
 
@@ -500,11 +500,9 @@ def main():
     barrier()
     e2e_ms = ee[0].elapsed_time(ee[1])
     e2e_wall = time.perf_counter() - t0
-    import ctypes
-    h2d = L * ctypes.sizeof(__import__("paper_1802_06215_b200.despot", fromlist=["Leaf"]).Leaf)
-    nch = int(o["num_children"])
+    # the library's own count of what one call copied (leaf table in; status and results out)
+    h2d, d2h = o["h2d_bytes"], o["d2h_bytes"]
     A = model.A
-    d2h = 4 * (2 * L + 3 * L * A + L * A + 1) + nch * (5 * 4 + 4 * model.OW) + 4 + 4 * L + 4 + 8
     # ---- roofline of the dominant kernel (K2), live CUDA-event time ----
     peaks, peak_src = load_peaks()
     clocks = clk.summary(tw0, tw1)

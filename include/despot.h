@@ -187,6 +187,8 @@ typedef struct {
    * grouping (K2), [2] child order / CSR / outputs (K3a-c), [3] whole call
    * from the first enqueued operation to the last (device time, ms)          */
   float phase_ms[4];
+  uint64_t h2d_bytes;      /* out: bytes this call copied host -> device / device -> */
+  uint64_t d2h_bytes;      /*      host (leaf table, status, results; begin + end)   */
 } despot_expansion;
 
 /* One batch: update (world-local) -> expansion + bounds + roll-outs + grouping

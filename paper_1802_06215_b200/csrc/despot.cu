@@ -233,6 +233,7 @@ struct despot_batch {
   uint32_t hdr_pad = 0, rec_bytes = 0;
   bool timing = false, timing_k2 = false;  // DESPOT_X_TIMING / DESPOT_X_TIMING_K2 (K2 events only)
   uint32_t launches = 0;  // kernels launched for this batch
+  uint64_t h2d = 0, d2h = 0;  // host <-> device bytes copied for this batch
   cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
   void mark(int i) {
     if (timing && (!timing_k2 || i == 3 || i == 4)) cudaEventRecord(ev[i], stream);
@@ -1046,6 +1047,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
         (b->xmax && cudaMemsetAsync(b->xmax, 0, 16, st) != cudaSuccess) ||
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
+    b->h2d += h2d_bytes - o_leaves;
   }
   g_ht.mark("setup_copies");
   // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
@@ -1171,6 +1173,7 @@ extern "C" int despot_batch_exchange(despot_batch* b, despot_exchange* out) {
   // the all-reduced maxima size the blocks (identical on every rank)
   int64_t* hx = static_cast<int64_t*>(pinned_pool().acquire(16));
   if (!hx) return set_err(DESPOT_ENOMEM, "pinned staging");
+  b->d2h += 16;
   const bool ok = cudaMemcpyAsync(hx, b->xmax, 16, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
                   cudaStreamSynchronize(st) == cudaSuccess;
   b->rmax = (uint64_t)hx[0];
@@ -1469,6 +1472,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   } pin_guard{hs};
   if (!rc && !hs) rc = set_err(DESPOT_ENOMEM, "pinned staging");
   if (!rc) {
+    b->d2h += stat_bytes;
     if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "status copy failed");
   }
@@ -1497,6 +1501,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     } head[] = {{out->n_scen, o_ns, 4 * (size_t)L},  {out->weight, o_w, 4 * (size_t)L},
                 {out->act_reward, o_ar, 4 * LA},     {out->act_upper, o_au, 4 * LA},
                 {out->act_lower, o_al, 4 * LA},      {out->child_begin, o_cb, 4 * (LA + 1)}};
+    for (const auto& h : head) b->d2h += h.bytes;
     for (const auto& h : head)
       if (!rc && h.dst && h.bytes &&
           cudaMemcpyAsync(h.dst, static_cast<char*>(stage) + h.off, h.bytes, cudaMemcpyDeviceToHost, st) !=
@@ -1505,7 +1510,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   } else if (!rc && !dev_out) {
     hp_out = static_cast<char*>(pinned_pool().acquire(one_copy ? body_bytes : head_bytes));
     if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
-    else if (cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st) !=
+    else if ((b->d2h += one_copy ? body_bytes : head_bytes,
+              cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st)) !=
              cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "output copy failed");
   }
@@ -1551,6 +1557,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       for (int k = 0; k < 6; ++k) parts[k].bytes = 0;  // already in the caller's buffers
     if (!small) {  // second round trip: the used part of each child array, straight to the caller
       for (int k = 6; k < 12; ++k) {
+        b->d2h += parts[k].bytes;
         if (parts[k].bytes && cudaMemcpyAsync(parts[k].dst, static_cast<char*>(stage) + parts[k].off,
                                               parts[k].bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
           rc = set_err(DESPOT_ECUDA, "output copy failed");
@@ -1573,7 +1580,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     };
     for (auto& c : cps)
       if (!rc && c.dst && c.src && c.bytes &&
-          cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+          (b->d2h += c.bytes, cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "output copy failed");
     if (!rc && (!small || record) && cudaStreamSynchronize(st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "output copy sync failed");
@@ -1600,6 +1607,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     nd->expanded = true;
     out->node[l] = reinterpret_cast<despot_node>(nd);
   }
+  out->h2d_bytes = b->h2d;
+  out->d2h_bytes = b->d2h;
   g_ht.mark("outputs");
   free_batch(b, false);
   g_ht.mark("freed");

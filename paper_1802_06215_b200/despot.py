@@ -70,7 +70,7 @@ class Expansion(C.Structure):
                 ("scen_upper", C.c_void_p), ("scen_lower", C.c_void_p), ("scen_len", C.c_void_p),
                 ("scen_hash", C.c_void_p), ("scen_states", C.c_void_p),
                 ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("launches", C.c_uint32),
-                ("phase_ms", C.c_float * 4)]
+                ("phase_ms", C.c_float * 4), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 class SearchProblem(C.Structure):
@@ -315,6 +315,7 @@ class Model:
         out["num_children"] = Cn
         out["phase_ms"] = [float(x) for x in E.phase_ms]
         out["launches"] = int(E.launches)
+        out["h2d_bytes"], out["d2h_bytes"] = int(E.h2d_bytes), int(E.d2h_bytes)
         if not device:
             for k in ("child_count", "child_first", "child_weight", "child_upper", "child_lower"):
                 out[k] = o[k][:Cn]
