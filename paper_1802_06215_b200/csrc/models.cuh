@@ -557,12 +557,19 @@ struct Nav {
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
   // pi0: first of [S, SE, SW, t even ? E : W, t even ? W : E] read FREE
+  // (branch-free: the candidates are selected in reverse priority order, so
+  // roll-out lanes reading different observations do not diverge)
   static __device__ __forceinline__ int policy(uint32_t z, uint32_t t) {
     const uint32_t fr = ~z;
     const bool even = (t & 1u) == 0u;
     const int e1 = even ? 3 : 7, e2 = even ? 7 : 3;
-    return ((fr >> 4) & 1u) ? 5 : ((fr >> 3) & 1u) ? 4 : ((fr >> 5) & 1u) ? 6
-         : ((fr >> (e1 - 1)) & 1u) ? e1 : ((fr >> (e2 - 1)) & 1u) ? e2 : 0;
+    int a = 0;
+    a = ((fr >> (e2 - 1)) & 1u) ? e2 : a;
+    a = ((fr >> (e1 - 1)) & 1u) ? e1 : a;
+    a = ((fr >> 5) & 1u) ? 6 : a;
+    a = ((fr >> 3) & 1u) ? 4 : a;
+    a = ((fr >> 4) & 1u) ? 5 : a;
+    return a;
   }
   template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
