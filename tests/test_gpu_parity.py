@@ -87,6 +87,75 @@ def test_config5_sweep_k4096_256_leaves():
     _full_config(5, K=4096, sample=(0, -1), action_mask=mask)
 
 
+def test_config5_max_k32768_invariants_and_sampled_leaves():
+    """The sweep's largest size (K = 32768, 256 leaves, the bench batch):
+    invariants over every (leaf, action) -- the children partition the leaf
+    (counts sum to |Phi|, weights to W), first ids strictly increase (first
+    occurrence order), l <= u -- and two leaves against the oracle on a few
+    actions (the oracle root expanded only for their actions)."""
+    gm, om, st, w, seed, L = setup(5, K=32768)
+    A = gm.A
+    gr, orr = gm.belief_load(st, w, seed), om.belief_load(st, w, seed)
+    G0 = gm.expand([(gr, -1, 0, 0)])
+    glv = inputs.select_leaves(G0["child_count"], G0["child_begin"], A, L)
+    G = gm.expand([(gr, a, c, 1) for a, c in glv])
+    cb, cnt, first = G["child_begin"], G["child_count"], G["child_first"]
+    for i in range(L):
+        n = int(G["n_scen"][i])
+        assert n == int(G0["child_count"][G0["child_begin"][glv[i][0]] + glv[i][1]])
+        for a in range(A):
+            b0, b1 = int(cb[i * A + a]), int(cb[i * A + a + 1])
+            assert b1 > b0 and int(cnt[b0:b1].sum()) == n
+            assert np.all(np.diff(first[b0:b1].astype(np.int64)) > 0)
+            np.testing.assert_allclose(G["child_weight"][b0:b1].sum(), G["weight"][i], rtol=1e-5)
+        assert np.all(G["act_lower"][i * A:(i + 1) * A] <= G["act_upper"][i * A:(i + 1) * A] + 1e-5)
+    idx = [0, L - 1]
+    mroot = np.zeros(A, np.uint8)
+    for i in idx:
+        mroot[glv[i][0]] = 1
+    O0 = om.expand([(orr, -1, 0, 0)], action_mask=mroot)
+    for i in idx:  # the same child under the same (action, ordinal) on both sides
+        a, c = glv[i]
+        assert int(O0["child_first"][O0["child_begin"][a] + c]) == int(G0["child_first"][G0["child_begin"][a] + c])
+    mleaf = np.zeros(A, np.uint8)
+    mleaf[::131] = 1
+    O = om.expand([(orr, glv[i][0], glv[i][1], 1) for i in idx], action_mask=mleaf)
+    for j, i in enumerate(idx):
+        assert int(G["n_scen"][i]) == int(O["n_scen"][j])
+        for a in np.nonzero(mleaf)[0]:
+            gb, ge = G["child_begin"][i * A + a], G["child_begin"][i * A + a + 1]
+            ob, oe = O["child_begin"][j * A + a], O["child_begin"][j * A + a + 1]
+            assert np.array_equal(G["child_first"][gb:ge], O["child_first"][ob:oe])
+            assert np.array_equal(G["child_count"][gb:ge], O["child_count"][ob:oe])
+            np.testing.assert_allclose(G["child_upper"][gb:ge], O["child_upper"][ob:oe], rtol=1e-5, atol=1e-5)
+            np.testing.assert_allclose(G["child_lower"][gb:ge], O["child_lower"][ob:oe], rtol=1e-5, atol=1e-5)
+            np.testing.assert_allclose(G["act_upper"][i * A + a], O["act_upper"][j * A + a], rtol=1e-5, atol=1e-5)
+            np.testing.assert_allclose(G["act_lower"][i * A + a], O["act_lower"][j * A + a], rtol=1e-5, atol=1e-5)
+            np.testing.assert_allclose(G["act_reward"][i * A + a], O["act_reward"][j * A + a], rtol=1e-5, atol=1e-5)
+    gm.close()
+
+
+def test_max_leaves_per_batch():
+    """kMaxLeaves = 4096 leaves in one batch (RockSample(7,8), K = 24): equal
+    to the same leaves expanded in 8 batches of 512, and a batch of 4097 is
+    refused."""
+    gm, om, st, w, seed, _ = setup(1, K=24)
+    gr = gm.belief_load(st, w, seed)
+    R = gm.expand([(gr, -1, 0, 0)])
+    pairs = [(a, c) for a in range(gm.A) for c in range(int(R["child_begin"][a + 1] - R["child_begin"][a]))]
+    leaves = [(gr, a, c, 1) for a, c in (pairs * (4096 // len(pairs) + 1))[:4096]]
+    big = gm.expand(leaves)
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_count", "child_first",
+            "child_weight", "child_upper", "child_lower")
+    parts = [gm.expand(leaves[k:k + 512]) for k in range(0, 4096, 512)]
+    for k in keys:
+        ref = np.concatenate([np.asarray(p[k]).reshape(-1) for p in parts])
+        assert np.array_equal(np.asarray(big[k]).reshape(-1), ref), k
+    gm.node_release_many([n for n in big["node"]] + [n for p in parts for n in p["node"]])
+    with pytest.raises(DespotError):
+        gm.expand(leaves + leaves[:1])
+
+
 # ----------------------------------------------------------------------------
 # small cases compared completely, incl. per-scenario records
 # ----------------------------------------------------------------------------
