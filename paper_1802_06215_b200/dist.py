@@ -50,22 +50,35 @@ def exchange(sums: torch.Tensor, mins: torch.Tensor, group=None, maxs=None, gath
     """The collectives of one exchange round, in place: exact integer sums,
     minima and maxima (order-independent), and the all-gather of the ranks'
     blocks (`gather` = the whole [world * block] byte tensor; this rank's block
-    is already filled)."""
-    if sums is not None:
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
-    if mins is not None:
-        dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
-    if maxs is not None:
-        dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
+    is already filled).  NCCL works on the device views directly; a host
+    backend (gloo: the CPU tests, or device tensors staged through host
+    memory) gets host copies."""
+    nccl = dist.get_backend(group) == "nccl"
+
+    def reduce(t, op):
+        if t is None:
+            return
+        if nccl or not t.is_cuda:
+            dist.all_reduce(t, op=op, group=group)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=group)
+            t.copy_(h)
+
+    reduce(sums, dist.ReduceOp.SUM)
+    reduce(mins, dist.ReduceOp.MIN)
+    reduce(maxs, dist.ReduceOp.MAX)
     if gather is not None:
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         blk = gather.numel() // world
-        mine = gather[rank * blk:(rank + 1) * blk]
-        if gather.is_cuda:
-            dist.all_gather_into_tensor(gather, mine.clone(), group=group)
-        else:  # gloo: list form
-            parts = list(gather.split(blk))
-            dist.all_gather(parts, mine.clone(), group=group)
+        if nccl:
+            dist.all_gather_into_tensor(gather, gather[rank * blk:(rank + 1) * blk].clone(), group=group)
+        else:  # list form on host memory
+            h = gather.cpu() if gather.is_cuda else gather
+            parts = list(h.split(blk))
+            dist.all_gather(parts, h[rank * blk:(rank + 1) * blk].clone(), group=group)
+            if gather.is_cuda:
+                gather.copy_(h)
 
 
 def run_exchange(model, batch, ex, group=None):
