@@ -248,8 +248,11 @@ int despot_rollout_bounds(despot_model* model, despot_node node, float* upper_me
 /* ------------------------------------------------------------------------ */
 /* Expansion backend: expands `L` leaves into host arrays of `out` (same
  * contract as despot_expand_batch with host outputs).  libdespot's GPU
- * backend is used by despot_plan; tests plug in the CPU oracle.  Called from
- * one thread (the batcher) at a time.  Returns a despot_status. */
+ * backend is used by despot_plan; tests plug in the CPU oracle.  With one
+ * worker it is called from one thread at a time; with several, two batcher
+ * threads may call it concurrently (one waits for its expansion while the
+ * other builds the previous batch's children), so the backend must be
+ * thread-safe -- libdespot's is.  Returns a despot_status. */
 typedef int (*despot_expand_fn)(void* ctx, const despot_leaf* leaves, uint32_t L, despot_expansion* out);
 typedef int (*despot_release_fn)(void* ctx, despot_node node);
 

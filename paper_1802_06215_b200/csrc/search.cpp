@@ -30,9 +30,12 @@
 #include <deque>
 #include <limits>
 #include <mutex>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "../../include/despot.h"
 
@@ -54,6 +57,46 @@ struct TChild {
   std::atomic<double> upper{0.0}, lower{0.0};
   std::atomic<int> active{0};  // threads inside this branch (virtual loss)
   std::atomic<TNode*> node{nullptr};
+  TChild() = default;
+  TChild(float w, uint32_t n, double u, double l)
+      : weight(w), n_scen(n), u0(u), l0(l), upper(u), lower(l), active(0), node(nullptr) {}
+};
+
+// Bump allocator for the child records of a search (all freed with it; a
+// TChild needs no destructor): one construction per record instead of a
+// zero-initialised array per node and a second pass over it.
+class ChildArena {
+ public:
+  ~ChildArena() {
+    for (auto& c : chunks_) munmap(c.first, c.second);
+  }
+  TChild* alloc(size_t n) {
+    const size_t bytes = (n ? n : 1) * sizeof(TChild);
+    std::lock_guard<std::mutex> g(mu_);
+    if (bytes > left_) {
+      // 2 MB-aligned chunks with transparent huge pages, populated up front:
+      // a search grows its tree by ~1 GB/s, and 4 KB first-touch faults cost
+      // more than writing the records
+      const size_t chunk = ((std::max<size_t>(bytes, size_t(64) << 20)) + (size_t(2) << 20) - 1) &
+                           ~((size_t(2) << 20) - 1);
+      void* p = mmap(nullptr, chunk, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_POPULATE, -1, 0);
+      if (p == MAP_FAILED) return nullptr;
+      madvise(p, chunk, MADV_HUGEPAGE);
+      chunks_.emplace_back(p, chunk);
+      cur_ = static_cast<unsigned char*>(p);
+      left_ = chunk;
+    }
+    TChild* r = reinterpret_cast<TChild*>(cur_);
+    cur_ += bytes;
+    left_ -= bytes;
+    return r;
+  }
+
+ private:
+  std::mutex mu_;
+  std::vector<std::pair<void*, size_t>> chunks_;
+  unsigned char* cur_ = nullptr;
+  size_t left_ = 0;
 };
 
 struct TBranch {
@@ -72,7 +115,7 @@ struct TNode {
   despot_node handle = 0;  // backend arena once expanded
   enum State { kLeaf, kPending, kExpanded } state = kLeaf;  // under mu
   std::vector<TBranch> branches;                            // [A] once expanded, under mu
-  std::unique_ptr<TChild[]> children;                       // all children, action-major
+  TChild* children = nullptr;                               // all children, action-major (arena)
   uint32_t n_children = 0;
   std::mutex mu;
 };
@@ -137,6 +180,7 @@ struct Search {
   uint32_t blocked = 0;  // workers waiting for their in-flight trials (under qmu)
   std::atomic<int> error{0};
   std::string error_msg;
+  ChildArena arena;  // the child records of every node (all batchers)
   // batcher time split in ns (DESPOT_SEARCH_TRACE)
   std::atomic<uint64_t> t_call{0}, t_children{0}, t_backup{0};
   static uint64_t ns(std::chrono::steady_clock::duration d) {
@@ -235,7 +279,8 @@ struct Search {
     for (uint32_t i = 0; i < L; ++i) {
       TNode* b = batch[i].leaf;
       const uint32_t c0 = child_begin[(size_t)i * A], c1 = child_begin[(size_t)i * A + A];
-      std::unique_ptr<TChild[]> ch(new TChild[c1 - c0]);
+      TChild* ch = arena.alloc(c1 - c0);
+      if (!ch) return DESPOT_ENOMEM;
       std::vector<TBranch> br(A);
       const bool at_horizon = b->depth + 1 >= P.max_depth;
       for (uint32_t a = 0; a < A; ++a) {
@@ -246,17 +291,8 @@ struct Search {
         br[a].first = child_begin[la] - c0;
         br[a].count = child_begin[la + 1] - child_begin[la];
       }
-      for (uint32_t c = c0; c < c1; ++c) {
-        TChild& r = ch[c - c0];
-        r.weight = cw[c];
-        r.n_scen = child_count[c];
-        r.u0 = cu[c];
-        r.l0 = cl[c];
-        // at depth D the value is exactly the tail-based l0: gap 0
-        if (at_horizon) r.u0 = r.l0;
-        r.upper.store(r.u0, std::memory_order_relaxed);
-        r.lower.store(r.l0, std::memory_order_relaxed);
-      }
+      for (uint32_t c = c0; c < c1; ++c)  // at depth D the value is exactly the tail-based l0: gap 0
+        new (&ch[c - c0]) TChild(cw[c], child_count[c], at_horizon ? cl[c] : cu[c], cl[c]);
       records.fetch_add(c1 - c0);
       {
         std::lock_guard<std::mutex> g(b->mu);
@@ -264,7 +300,7 @@ struct Search {
         if (b->rec->n_scen == 0) b->rec->n_scen = n_scen[i];
         if (b->rec->weight == 0.0f) b->rec->weight = weight[i];
         b->branches = std::move(br);
-        b->children = std::move(ch);
+        b->children = ch;
         b->n_children = c1 - c0;
         b->state = TNode::kExpanded;
       }

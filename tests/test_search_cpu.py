@@ -27,7 +27,9 @@ class OracleBackend:
     """despot_expand_fn / despot_release_fn backed by oracle.Model."""
 
     def __init__(self, om: oracle.Model):
+        import threading
         self.om = om
+        self.lock = threading.Lock()  # the oracle is single-threaded; the search may call from two batchers
         self.calls = 0
         self.leaves_seen = 0
         self.released = []
@@ -35,6 +37,10 @@ class OracleBackend:
         self._release = D.RELEASE_FN(self.release)
 
     def expand(self, ctx, leaves_p, L, out_p):
+        with self.lock:
+            return self._expand_locked(ctx, leaves_p, L, out_p)
+
+    def _expand_locked(self, ctx, leaves_p, L, out_p):
         try:
             lv = C.cast(leaves_p, C.POINTER(D.Leaf))
             out = C.cast(out_p, C.POINTER(D.Expansion)).contents
