@@ -7,6 +7,7 @@ timeout 1500 python scripts/sweep.py > $O/sweep_config5.jsonl 2>&1
 timeout 900 python scripts/peds_sweep.py > $O/peds_sweep.jsonl 2>&1
 timeout 900 python scripts/plan_bench.py --configs 1 2 3 4 --workers 1 4 8 > $O/plan_bench.jsonl 2>&1
 timeout 1000 python scripts/next2_sweeps.py > $O/next2_sweeps.jsonl 2>&1
+timeout 1200 python scripts/online_bench.py --episodes 6 --budgets 0.02 0.1 0.3 --steps 30 > $O/online.jsonl 2>&1
 g++ -O2 -std=c++17 scripts/latency.cpp -Iinclude -I/usr/local/cuda/include -Lpaper_1802_06215_b200 -ldespot \
   -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,$PWD/paper_1802_06215_b200 -o /tmp/latency && \
   timeout 120 /tmp/latency > $O/latency.jsonl 2>&1
