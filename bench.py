@@ -517,9 +517,9 @@ def main():
     traffic = ncu_traffic(args.config)
     if kind == "car":  # the variant rule of despot.cu (launch_k2_sparse) unless forced
         q_bound = A * sum(model.node_info(lf[0])[0] for lf in leaves)
-        thread = args.car_variant == "thread" or (args.car_variant == "auto" and (
-            q_bound >= num_sms * 256 or c.get("peds", 20) < 8))
-        k2_name = "k2_car_group" if args.car_variant == "group" else "k2_car_thread" if thread else "k2_car_warp"
+        big, tiny = q_bound >= num_sms * 256, q_bound < num_sms * 4
+        k2_name = {"thread": "k2_car_thread", "warp": "k2_car_warp", "group": "k2_car_group",
+                   "auto": "k2_car_thread" if big else "k2_car_warp" if tiny else "k2_car_group"}[args.car_variant]
     else:
         k2_name = "k2_expand_dense"
     if rank == 0:

@@ -807,10 +807,15 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   // (measured, profiles/r01/peds_sweep.jsonl: the warp kernel wins for >= 12
   // pedestrians at 12k items, the thread kernel everywhere at 96k items and
   // for 6 pedestrians, whose warps would leave 25 of 32 lanes idle)
-  const bool grouped = m->flags & DESPOT_MF_GROUPED;
-  const bool unfactored = !grouped && ((m->flags & DESPOT_MF_UNFACTORED) ||
-                                       (!(m->flags & DESPOT_MF_FACTORED) &&
-                                        (q_bound >= (uint64_t)m->num_sms * 256 || dm.peds < 8)));
+  // automatic choice (no variant flag), by the items the batch has: thread
+  // per scenario when they fill the GPU one thread each; the grouped kernel
+  // in between (its packed lane groups beat both others at 8 roots x K = 64,
+  // profiles/r01/peds_sweep.jsonl); a warp per scenario for the few-item
+  // batches of a tree search (latency: all pedestrians of a step in parallel)
+  const bool forced = m->flags & (DESPOT_MF_UNFACTORED | DESPOT_MF_FACTORED | DESPOT_MF_GROUPED);
+  const bool big = q_bound >= (uint64_t)m->num_sms * 256, tiny = q_bound < (uint64_t)m->num_sms * 4;
+  const bool grouped = (m->flags & DESPOT_MF_GROUPED) || (!forced && !big && !tiny);
+  const bool unfactored = !grouped && ((m->flags & DESPOT_MF_UNFACTORED) || (!forced && big));
   if (grouped) {
     const uint64_t G = ((uint64_t)dm.peds + 4) / 4, gpw = 32 / G;
     const uint64_t warps = (q_bound + gpw - 1) / gpw;
