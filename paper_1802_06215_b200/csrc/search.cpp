@@ -35,8 +35,6 @@
 #include <thread>
 #include <vector>
 
-#include <sys/mman.h>
-
 #include "../../include/despot.h"
 
 // sets the calling thread's despot_last_error message (despot.cu)
@@ -67,23 +65,16 @@ struct TChild {
 // zero-initialised array per node and a second pass over it.
 class ChildArena {
  public:
-  ~ChildArena() {
-    for (auto& c : chunks_) munmap(c.first, c.second);
-  }
   TChild* alloc(size_t n) {
     const size_t bytes = (n ? n : 1) * sizeof(TChild);
     std::lock_guard<std::mutex> g(mu_);
     if (bytes > left_) {
-      // 2 MB-aligned chunks with transparent huge pages, populated up front:
-      // a search grows its tree by ~1 GB/s, and 4 KB first-touch faults cost
-      // more than writing the records
-      const size_t chunk = ((std::max<size_t>(bytes, size_t(64) << 20)) + (size_t(2) << 20) - 1) &
-                           ~((size_t(2) << 20) - 1);
-      void* p = mmap(nullptr, chunk, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_POPULATE, -1, 0);
-      if (p == MAP_FAILED) return nullptr;
-      madvise(p, chunk, MADV_HUGEPAGE);
-      chunks_.emplace_back(p, chunk);
-      cur_ = static_cast<unsigned char*>(p);
+      const size_t chunk = std::max<size_t>(bytes, size_t(32) << 20);
+      chunks_.emplace_back(new (std::nothrow) unsigned char[chunk + alignof(TChild)]);
+      if (!chunks_.back()) return nullptr;
+      uintptr_t p = reinterpret_cast<uintptr_t>(chunks_.back().get());
+      p = (p + alignof(TChild) - 1) & ~(uintptr_t)(alignof(TChild) - 1);
+      cur_ = reinterpret_cast<unsigned char*>(p);
       left_ = chunk;
     }
     TChild* r = reinterpret_cast<TChild*>(cur_);
@@ -94,7 +85,7 @@ class ChildArena {
 
  private:
   std::mutex mu_;
-  std::vector<std::pair<void*, size_t>> chunks_;
+  std::vector<std::unique_ptr<unsigned char[]>> chunks_;
   unsigned char* cur_ = nullptr;
   size_t left_ = 0;
 };
@@ -182,7 +173,7 @@ struct Search {
   std::string error_msg;
   ChildArena arena;  // the child records of every node (all batchers)
   // batcher time split in ns (DESPOT_SEARCH_TRACE)
-  std::atomic<uint64_t> t_call{0}, t_children{0}, t_backup{0};
+  std::atomic<uint64_t> t_call{0}, t_children{0}, t_backup{0}, t_alloc{0}, t_branch{0}, t_rec{0};
   static uint64_t ns(std::chrono::steady_clock::duration d) {
     return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(d).count();
   }
@@ -279,9 +270,12 @@ struct Search {
     for (uint32_t i = 0; i < L; ++i) {
       TNode* b = batch[i].leaf;
       const uint32_t c0 = child_begin[(size_t)i * A], c1 = child_begin[(size_t)i * A + A];
+      const auto ta = std::chrono::steady_clock::now();
       TChild* ch = arena.alloc(c1 - c0);
       if (!ch) return DESPOT_ENOMEM;
       std::vector<TBranch> br(A);
+      const auto tb = std::chrono::steady_clock::now();
+      t_alloc += ns(tb - ta);
       const bool at_horizon = b->depth + 1 >= P.max_depth;
       for (uint32_t a = 0; a < A; ++a) {
         const size_t la = (size_t)i * A + a;
@@ -291,9 +285,13 @@ struct Search {
         br[a].first = child_begin[la] - c0;
         br[a].count = child_begin[la + 1] - child_begin[la];
       }
+      const auto tcc = std::chrono::steady_clock::now();
+      t_branch += ns(tcc - tb);
       for (uint32_t c = c0; c < c1; ++c)  // at depth D the value is exactly the tail-based l0: gap 0
         new (&ch[c - c0]) TChild(cw[c], child_count[c], at_horizon ? cl[c] : cu[c], cl[c]);
       records.fetch_add(c1 - c0);
+      const auto td = std::chrono::steady_clock::now();
+      t_rec += ns(td - tcc);
       {
         std::lock_guard<std::mutex> g(b->mu);
         b->handle = hnode[i];
@@ -612,6 +610,9 @@ extern "C" int despot_search(const despot_search_problem* P, const despot_search
                     "backups %.3f s, %llu batches\n",
             R->seconds, 1e-9 * (double)S.t_call.load(), 1e-9 * (double)S.t_children.load(),
             1e-9 * (double)S.t_backup.load(), (unsigned long long)R->batches);
+  if (getenv("DESPOT_SEARCH_TRACE"))
+    fprintf(stderr, "[despot search]   children: alloc %.3f s, branches %.3f s, records %.3f s\n",
+            1e-9 * (double)S.t_alloc.load(), 1e-9 * (double)S.t_branch.load(), 1e-9 * (double)S.t_rec.load());
   if (dump && dump_capacity) {
     uint32_t n = 0;
     S.dump_tree(dump, dump_capacity, n);
