@@ -367,12 +367,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional test of the N > 1 path on a one-GPU box (never a measurement):
+    # every rank on device 0, gloo collectives through host memory
+    one_gpu_test = world > 1 and os.environ.get("DESPOT_BENCH_ONE_GPU_TEST") == "1"
+    if one_gpu_test:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     c, kind, params, st, w, seed, L = workload(args.config, args.K, args.peds)
     mflags = {"auto": 0, "thread": 1, "warp": 2, "group": 4}[args.car_variant]
     model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags)
@@ -476,7 +484,7 @@ def main():
         print("step_ms", [round(x, 4) for x in step_ms], file=sys.stderr)
     t_local = float(np.sum(step_ms))
     if world > 1:
-        t = torch.tensor([t_local], device=dev)
+        t = torch.tensor([t_local], device="cpu" if one_gpu_test else dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_total = float(t.item())
     else:
@@ -524,6 +532,8 @@ def main():
         k2_name = "k2_expand_dense"
     if rank == 0:
         line = {
+            **({"note": "functional test of the N > 1 path on one GPU (DESPOT_BENCH_ONE_GPU_TEST): not a "
+                        "measurement"} if one_gpu_test else {}),
             "metric": "scenario-steps/s",
             "value": value,
             "unit": "scenario-steps/s",
