@@ -1,5 +1,5 @@
 // kernels.cuh -- the batched leaf-expansion kernels (sm_100a), templated on
-// the model.  One batch = K1 (update/filter) -> K2pre (tile prefix) -> K2
+// the model.  One batch = K1 (update/filter + tile prefix) -> K2
 // (expansion + bounds + roll-outs + grouping, fused) -> [exchange] -> K3a
 // (child order) -> K3b (CSR scan) -> K3c (outputs).  See DESIGN.md §4.
 #pragma once
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
 // Delta+1, u(s') (Eq. 11), roll-out (Eq. 12), then the warp groups its lanes
 // by observation and adds exact int64 fixed-point partial sums of
 // (W, U, LAMBDA, N, first) per child slot and (R, Uq, Lq) per action.
-// Persistent grid-stride loop over tiles.
+// Persistent grid; tiles handed out dynamically (next_tile).
 // ---------------------------------------------------------------------------
 // UNI_SEED: every leaf of the batch descends from the same belief, so the
 // Philox key is a kernel parameter (uniform registers; the key schedule costs
