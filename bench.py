@@ -73,6 +73,37 @@ def ncu_traffic(config):
         return None
 
 
+NCU_K2_METRICS = {
+    "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "alu_pipe_pct": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "fma_pipe_pct": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "lanes_per_warp_instr": "smsp__thread_inst_executed_per_inst_executed.ratio",
+    "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "registers": "launch__registers_per_thread",
+}
+
+
+def ncu_k2_summary(config):
+    """The per-pipe picture of the dominant kernel from the same committed
+    `ncu --set full` raw page as `traffic` (SURVEY §8(d) metric list)."""
+    import csv
+    p = os.path.join(ROOT, "profiles", "r01", f"k2_config{config}_raw.csv")
+    try:
+        rows = list(csv.reader(open(p)))
+        out = {}
+        for k, name in NCU_K2_METRICS.items():
+            out[k] = float(rows[2][rows[0].index(name)].replace(",", ""))
+        out["source"] = os.path.relpath(p, ROOT)
+        return out
+    except Exception:
+        return None
+
+
+# Philox4x32-10 blocks drawn per scenario-step (DESIGN.md §3 model cards)
+def philox_blocks_per_step(kind, peds):
+    return {"tiger": 1, "rocksample": 1, "nav": 3}.get(kind, (peds + 1 + 3) // 4)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -521,6 +552,13 @@ def main():
     steps_local = total_steps / world
     istep, istep_src = i_step(args.config)
     achieved = istep * steps_local / (k2_avg / 1e3) / 1e12 / args.steps
+    # K0: the measured Philox ceiling (RNG only, full occupancy) vs K2's own
+    # Philox block rate (ceiling 2)
+    k0_threads, k0_blocks = num_sms * 2048, 128
+    k0_ms, _ = model.philox_ceiling(seed if kind != "car" else 1004, k0_threads, k0_blocks, reps=5, stream=stream)
+    k0_rate = k0_threads * k0_blocks / (k0_ms / 1e3)
+    bps = philox_blocks_per_step(kind, c.get("peds", 20))
+    k2_blocks = bps * steps_local / args.steps / (k2_avg / 1e3)
     k2_share = float(np.sum(k2_ms) / np.sum(step_ms))
     traffic = ncu_traffic(args.config)
     if kind == "car":  # the variant rule of despot.cu (launch_k2_sparse) unless forced
@@ -562,6 +600,12 @@ def main():
                          "traffic": traffic["bytes_per_launch"] if traffic else None,
                          "traffic_unit": "DRAM bytes per K2 launch",
                          "traffic_source": traffic["source"] if traffic else None,
+                         "ncu_k2": ncu_k2_summary(args.config),
+                         "k0_philox": {"ceiling_blocks_per_s": k0_rate, "k2_blocks_per_s": k2_blocks,
+                                       "k2_over_k0": k2_blocks / k0_rate, "blocks_per_scenario_step": bps,
+                                       "k0_ms": k0_ms, "k0_blocks_per_launch": k0_threads * k0_blocks},
+                         "hbm_frac": (traffic["bytes_per_launch"] / (k2_avg / 1e3) / 1e9 / peaks.get("hbm_gbs", 6650.0))
+                         if traffic else None,
                          "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
                                  f"({peak_src} sm_max_mhz); achieved = {istep:.1f} thread-instr per "
                                  f"scenario-step ({istep_src}, DESIGN.md §7.1) x steps / live K2 event time"},

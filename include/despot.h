@@ -324,6 +324,18 @@ int despot_plan(despot_model* model, despot_node root, const despot_search_confi
 int despot_stream_words(despot_model* model, uint64_t stream_seed, const uint32_t* ids,
                         uint32_t n, uint32_t t, uint32_t k, uint32_t* out, void* stream);
 
+/* K0, the measured Philox ceiling (SURVEY §8(d) "Ceilings"): a persistent
+ * grid (256-thread CTAs, full occupancy) in which thread g of n_threads draws
+ * the Philox4x32-10 blocks ctr = (g, t, 0, 0), t = 1 .. blocks, key = the seed
+ * (the R13 addressing of the scenario streams, round keys as a kernel
+ * parameter as in K2) and XOR-folds their words.  One warm-up launch, then
+ * `reps` launches timed with CUDA events on `stream`: *out_ms = mean ms per
+ * launch (n_threads * blocks blocks), *out_checksum = XOR of every word of
+ * one launch (tests compare it with the oracle's generator).  Synchronous.
+ * Errors: EINVAL (null output, zero sizes), ECUDA. */
+int despot_philox_ceiling(despot_model* model, uint64_t stream_seed, uint32_t n_threads, uint32_t blocks,
+                          uint32_t reps, void* stream, double* out_ms, uint32_t* out_checksum);
+
 #ifdef __cplusplus
 }
 #endif

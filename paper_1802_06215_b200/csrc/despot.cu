@@ -1710,3 +1710,41 @@ extern "C" int despot_stream_words(despot_model* m, uint64_t seed, const uint32_
   cudaFreeAsync(d, st);
   return rc;
 }
+
+extern "C" int despot_philox_ceiling(despot_model* m, uint64_t seed, uint32_t n_threads, uint32_t blocks,
+                                     uint32_t reps, void* stream, double* out_ms, uint32_t* out_checksum) {
+  if (!m || !out_ms || !out_checksum) return set_err(DESPOT_EINVAL, "null argument");
+  if (n_threads == 0 || blocks == 0 || reps == 0) return set_err(DESPOT_EINVAL, "empty K0 launch");
+  CU(cudaSetDevice(m->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int occ = kernel_occupancy((const void*)k0_philox, 0, 256);
+  const uint64_t full = (uint64_t)m->num_sms * occ;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(full, (n_threads + 255) / 256));
+  const RoundKeys rk = round_keys((uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t* d = nullptr;
+  CU(cudaMallocAsync(&d, 4 * (size_t)(reps + 1), st));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  int rc = DESPOT_OK;
+  if (cudaMemsetAsync(d, 0, 4 * (size_t)(reps + 1), st) != cudaSuccess || cudaEventCreate(&e0) != cudaSuccess ||
+      cudaEventCreate(&e1) != cudaSuccess)
+    rc = set_err(DESPOT_ECUDA, "K0 setup");
+  if (!rc) {
+    k0_philox<<<grid, 256, 0, st>>>(rk, n_threads, blocks, d);  // warm-up
+    cudaEventRecord(e0, st);
+    for (uint32_t r = 0; r < reps; ++r) k0_philox<<<grid, 256, 0, st>>>(rk, n_threads, blocks, d + 1 + r);
+    cudaEventRecord(e1, st);
+    rc = check_launch(m, "K0");
+  }
+  uint32_t cs = 0;
+  float ms = 0.0f;
+  if (!rc && (cudaMemcpyAsync(&cs, d + 1, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess || cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess))
+    rc = set_err(DESPOT_ECUDA, "K0 read back");
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  cudaFreeAsync(d, st);
+  if (rc) return rc;
+  *out_ms = (double)ms / reps;
+  *out_checksum = cs;
+  return DESPOT_OK;
+}

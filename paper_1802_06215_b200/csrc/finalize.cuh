@@ -517,4 +517,21 @@ __global__ void k_stream_words(uint32_t k0, uint32_t k1, const uint32_t* ids, ui
   out[i] = sel == 0 ? w.x : sel == 1 ? w.y : sel == 2 ? w.z : w.w;
 }
 
+// K0, the measured Philox ceiling (ceiling 2): thread g of the
+// grid-stride loop draws the stream blocks (ctr = (g, t, 0, 0), t = 1 ..
+// blocks) with the round keys as a kernel parameter -- K2's best case -- and
+// XOR-folds every word; one atomicXor per warp keeps the work observable.
+__global__ void __launch_bounds__(256) k0_philox(const RoundKeys rk, uint32_t n_threads, uint32_t blocks,
+                                                 uint32_t* checksum) {
+  uint32_t x = 0;
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < n_threads; g += gridDim.x * blockDim.x) {
+    for (uint32_t t = 1; t <= blocks; ++t) {
+      const uint4 w = philox(g, t, 0u, 0u, rk);
+      x ^= w.x ^ w.y ^ w.z ^ w.w;
+    }
+  }
+  x = __reduce_xor_sync(0xffffffffu, x);
+  if ((threadIdx.x & 31) == 0) atomicXor(checksum, x);
+}
+
 }  // namespace hd

@@ -30,7 +30,7 @@ EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "desp
            "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
            "despot_node_release", "despot_node_release_many", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
            "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
-           "despot_search", "despot_plan"]
+           "despot_search", "despot_plan", "despot_philox_ceiling"]
 
 
 def _tflag(timing):
@@ -157,6 +157,8 @@ def lib():
         L.despot_batch_abort.argtypes = [vp]
         L.despot_rollout_bounds.argtypes = [vp, u64, C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp, vp]
         L.despot_stream_words.argtypes = [vp, u64, vp, u32, u32, u32, vp, vp]
+        L.despot_philox_ceiling.argtypes = [vp, u64, u32, u32, u32, vp, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_uint32)]
         L.despot_search.argtypes = [C.POINTER(SearchProblem), C.POINTER(SearchConfig), C.POINTER(SearchResult),
                                     vp, u32]
         L.despot_plan.argtypes = [vp, u64, C.POINTER(SearchConfig), C.POINTER(SearchResult), vp]
@@ -428,6 +430,14 @@ class Model:
         res = SearchResult()
         _check(lib().despot_plan(self.h, int(root), C.byref(cfg), C.byref(res), _stream_ptr(stream)))
         return result_dict(res)
+
+    def philox_ceiling(self, seed, n_threads, blocks, reps=5, stream=None):
+        """K0 (despot_philox_ceiling): (ms per launch of n_threads * blocks
+        Philox blocks, XOR checksum of one launch's words)."""
+        ms, cs = C.c_double(), C.c_uint32()
+        _check(lib().despot_philox_ceiling(self.h, int(seed), int(n_threads), int(blocks), int(reps),
+                                           _stream_ptr(stream), C.byref(ms), C.byref(cs)))
+        return ms.value, cs.value
 
     def stream_words(self, seed, ids, t, k, stream=None):
         ids = np.ascontiguousarray(ids, dtype=np.uint32)

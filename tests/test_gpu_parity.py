@@ -30,6 +30,23 @@ def test_stream_words_match_oracle_philox():
         assert np.array_equal(g, o)
 
 
+def test_k0_philox_ceiling_checksum_matches_oracle():
+    """K0 draws the stream blocks (g, t) of every thread g and XOR-folds them:
+    its checksum equals the oracle generator's over the same blocks."""
+    gm = Model("tiger", inputs.tiger_params())
+    for seed, n, blocks in ((1002, 1000, 3), (0xDEADBEEF12345678, 333, 7)):
+        ms, cs = gm.philox_ceiling(seed, n, blocks, reps=2)
+        key = [seed & 0xFFFFFFFF, seed >> 32]
+        x = 0
+        for g in range(n):
+            for t in range(1, blocks + 1):
+                for v in oracle.philox([g, t, 0, 0], key):
+                    x ^= int(v)
+        assert cs == x and ms > 0.0
+    with pytest.raises(DespotError):
+        gm.philox_ceiling(1, 0, 1)
+
+
 # ----------------------------------------------------------------------------
 # full configs (BASELINE.json), in the launch configuration bench.py times;
 # the oracle checks a sample of the leaves (each leaf's outputs depend only on
