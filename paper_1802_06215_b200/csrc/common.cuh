@@ -204,11 +204,22 @@ struct SumLayout {
   __host__ __device__ uint64_t total() const { return 4 * las + 3 * la + 1; }
 };
 
-__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+// Exact int64 sum over the lanes of `mask` (every lane of mask calls it): the
+// value is split into 27 + 27 + 10 bits, each part summed by one REDUX
+// (__reduce_add_sync; 32 lanes x (2^27 - 1) < 2^32, the signed top part
+// stays far inside int32) and reassembled mod 2^64 -- three warp reductions
+// instead of five rounds of two 32-bit shuffles and a 64-bit add.
+__device__ __forceinline__ int64_t group_sum64(uint32_t mask, int64_t v) {
+  const uint64_t u = (uint64_t)v;
+  const uint32_t p0 = (uint32_t)u & 0x7FFFFFFu;
+  const uint32_t p1 = (uint32_t)(u >> 27) & 0x7FFFFFFu;
+  const uint32_t p2 = (uint32_t)(int32_t)(v >> 54);
+  const uint32_t s0 = __reduce_add_sync(mask, p0);
+  const uint32_t s1 = __reduce_add_sync(mask, p1);
+  const int32_t s2 = (int32_t)__reduce_add_sync(mask, p2);
+  return (int64_t)((uint64_t)s0 + ((uint64_t)s1 << 27) + ((uint64_t)(int64_t)s2 << 54));
 }
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) { return group_sum64(0xffffffffu, v); }
 __device__ __forceinline__ uint32_t warp_sum32(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
 
 // exact fixed-point quantisation of a normalised weighted value

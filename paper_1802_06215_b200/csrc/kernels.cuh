@@ -113,15 +113,23 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   // tile of each other (a static stride leaves the slowest of ~5000 warps'
   // sums of ~100 random tile times ~35% above the mean)
   uint32_t t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  uint32_t leaf = 0;  // tile_off[leaf] <= t: a warp's tiles only increase
   for (; t < total; t = next_tile(b, nwarps, lane)) {
-    // tile -> (leaf, action, chunk)
-    uint32_t lo = 0, hi = b.L;  // tile_off[lo] <= t < tile_off[hi]
-    while (hi - lo > 1) {
+    // tile -> (leaf, action, chunk): gallop forward from the previous leaf
+    // (the next tile is ~nwarps further, usually in the same or the next
+    // leaf), then bisect
+    uint32_t step = 1, lo = leaf, hi = leaf + 1;
+    while (hi < b.L && tile_off[hi] <= t) {
+      lo = hi;
+      hi = min(hi + step, b.L);
+      step <<= 1;
+    }
+    while (hi - lo > 1) {  // tile_off[lo] <= t < tile_off[hi] (tile_off[L] = total > t)
       const uint32_t mid = (lo + hi) >> 1;
       if (tile_off[mid] <= t) lo = mid;
       else hi = mid;
     }
-    const uint32_t leaf = lo;
+    leaf = lo;
     const LeafDev& lf = b.leaves[leaf];
     const uint32_t n = b.n_leaf[leaf];
     const uint32_t chunks = (n + 31) >> 5;
@@ -205,15 +213,16 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
       const bool in = valid && z == zk;
       const uint32_t gmask = __ballot_sync(0xffffffffu, in);
       pending &= ~gmask;
-      const int64_t gW = warp_sum64(in ? qW : 0), gU = warp_sum64(in ? qU : 0),
-                    gL = warp_sum64(in ? qL : 0);
-      if ((int)lane == leader) {
-        const uint64_t slot = la * b.S + zk;
-        atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)gW);
-        atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)gU);
-        atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)gL);
-        atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], (unsigned long long)__popc(gmask));
-        atomicMin(&b.mins[slot], (int32_t)id);  // leader = lowest position = smallest id
+      if (in) {  // the group's lanes reduce over its mask
+        const int64_t gW = group_sum64(gmask, qW), gU = group_sum64(gmask, qU), gL = group_sum64(gmask, qL);
+        if ((int)lane == leader) {
+          const uint64_t slot = la * b.S + zk;
+          atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)gW);
+          atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)gU);
+          atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)gL);
+          atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], (unsigned long long)__popc(gmask));
+          atomicMin(&b.mins[slot], (int32_t)id);  // leader = lowest position = smallest id
+        }
       }
     }
   }

@@ -113,7 +113,10 @@ struct Tiger {
 // ===========================================================================
 template <int R>
 struct RockSample {
-  static constexpr int kMinBlocks = 8;  // 64 registers: 32 warps per SM
+#ifndef HD_RS_MINB
+#define HD_RS_MINB 7
+#endif
+  static constexpr int kMinBlocks = HD_RS_MINB;  // 7: 72 registers, 28 warps per SM (8 / 7 / 6 measured 1.569 / 1.539 / 1.538 ms on config 2)
   static constexpr int kK1Threads = 512;  // K1 block: one round over K = 500 scenarios
   static constexpr int kMaxTable = 16384;  // n*n*m entries of the per-cell rock tables
   static constexpr uint32_t kExitFlag = 0x8000u;  // move target flag: the robot exits (+10)
