@@ -433,7 +433,10 @@ constexpr int kNavMaxThreads = 256;    // largest block of a kernel using Nav
 
 template <int NW>
 struct Nav {
-  static constexpr int kMinBlocks = 5;
+#ifndef HD_NAV_MINB
+#define HD_NAV_MINB 4
+#endif
+  static constexpr int kMinBlocks = HD_NAV_MINB;  // 4: 102 registers (5 / 4 / 6 measured 85.3 / 83.2 / 92.0 us on config 3)
   static constexpr int kK1Threads = kNavMaxThreads;  // the per-thread grids are sized for it
   struct Sm {
     int32_t n, wall_y, goal_x, goal_y;
