@@ -125,10 +125,7 @@ template <class M, bool RECORD>
 // 3 CTAs of 128 per SM: 168 registers, no spills (without the bound ptxas
 // may take 181, which leaves 2 CTAs: 0.96 -> 1.25 ms on config 4; 4 CTAs
 // spill: 1.06 ms)
-#ifndef HD_CART_MINB
-#define HD_CART_MINB 3
-#endif
-__global__ void __launch_bounds__(128, HD_CART_MINB) k2_car_thread(BatchDev b, SparseItemOut io) {
+__global__ void __launch_bounds__(128, 3) k2_car_thread(BatchDev b, SparseItemOut io) {
   __shared__ typename M::Sm sm;
   M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
   __syncthreads();

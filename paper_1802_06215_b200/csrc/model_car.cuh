@@ -72,13 +72,22 @@ struct CarThreadT {
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
     copy_words(sm.rot, dm.car_rot, sizeof(sm.rot), tid, nt);
   }
+  // gap: pi0's input for this state (the nearest pedestrian ahead in the
+  // lane, in bins; 255 = none), maintained by load() and step() as they
+  // write the positions, so that policy() needs no pass of its own over them
   struct St {
     float xc;
     uint32_t level;
     bool term;
     uint32_t g0, g1;
+    int gap;
     float px[MAXP], py[MAXP];
   };
+  // the default policy's view of pedestrian (x, y) from car bin cxb (card §3.4)
+  static __device__ __forceinline__ void gap_min(int& gap, int cxb, float x, float y) {
+    const int pxb = car_bin_i(x), pyb = car_bin_i(y);
+    if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
+  }
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
     St s;
     s.xc = __uint_as_float(st[i]);
@@ -87,11 +96,14 @@ struct CarThreadT {
     s.term = (w1 >> 8) & 1u;
     s.g0 = st[2 * cap + i];
     s.g1 = st[3 * cap + i];
+    s.gap = 255;
+    const int cxb = car_bin_i(s.xc);
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
       if (p < sm.peds) {
         s.px[p] = __uint_as_float(st[(4 + 2 * p) * cap + i]);
         s.py[p] = __uint_as_float(st[(5 + 2 * p) * cap + i]);
+        gap_min(s.gap, cxb, s.px[p], s.py[p]);
       } else {
         s.px[p] = 0.0f;
         s.py[p] = 0.0f;
@@ -153,6 +165,8 @@ struct CarThreadT {
     const float v = 0.5f * (float)s.level;
     s.xc = s.xc + v * 0.25f;
     bool coll = false;
+    const int cxb = car_bin_i(s.xc);
+    s.gap = 255;
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
       if (4 * bk >= sm.peds + 1) break;  // uniform
@@ -166,6 +180,7 @@ struct CarThreadT {
           car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
           const float dx = s.px[p] - s.xc;
           coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
+          gap_min(s.gap, cxb, s.px[p], s.py[p]);
         }
       }
     }
@@ -179,18 +194,9 @@ struct CarThreadT {
     k = k < 1 ? 1 : k;
     return 100.0 * sm.gpow[k - 1];
   }
-  static __device__ __forceinline__ int policy(const Sm& sm, const St& s) {
-    const int cxb = car_bin_i(s.xc);
-    int gap = 255;
-#pragma unroll
-    for (int p = 0; p < MAXP; ++p) {
-      if (p < sm.peds) {
-        const int pxb = car_bin_i(s.px[p]), pyb = car_bin_i(s.py[p]);
-        if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
-      }
-    }
-    return car_policy_from_gap(gap);
-  }
+  // pi0 (card §3.4): from the gap load() / step() formed over this state's
+  // positions (the bins of the last observation)
+  static __device__ __forceinline__ int policy(const Sm&, const St& s) { return car_policy_from_gap(s.gap); }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
   template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t /*z: bins of s*/, uint32_t id, uint32_t t0,
