@@ -481,7 +481,14 @@ int dispatch_dense(const DevModel& dm, F&& f) {
 
 template <class F>
 int dispatch_car(const DevModel& dm, F&& f) {
-  if (dm.peds <= 2) return f(CarThreadT<2>{});
+  // exact instantiations for the studied counts (6 / 12 / 20; 2 for tests)
+  switch (dm.peds) {
+    case 2: return f(CarThreadT<2, true>{});
+    case 6: return f(CarThreadT<6, true>{});
+    case 12: return f(CarThreadT<12, true>{});
+    case 20: return f(CarThreadT<20, true>{});
+    default: break;
+  }
   if (dm.peds <= 8) return f(CarThreadT<8>{});
   if (dm.peds <= 20) return f(CarThreadT<20>{});
   return f(CarThreadT<31>{});

@@ -48,7 +48,9 @@ __device__ __forceinline__ float car_reward(int a, bool coll, bool goal, float v
 }
 __device__ __forceinline__ int car_policy_from_gap(int gap) { return gap <= 8 ? 2 : gap <= 16 ? 0 : 1; }
 
-template <int MAXP>
+// EXACT: the model has exactly MAXP pedestrians (no per-pedestrian runtime
+// test of the count)
+template <int MAXP, bool EXACT = false>
 struct CarThreadT {
   static constexpr int kMaxP = MAXP;
   struct Sm {
@@ -88,6 +90,7 @@ struct CarThreadT {
     const int pxb = car_bin_i(x), pyb = car_bin_i(y);
     if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
   }
+  static __device__ __forceinline__ bool active(const Sm& sm, int p) { return p < MAXP && (EXACT || p < sm.peds); }
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
     St s;
     s.xc = __uint_as_float(st[i]);
@@ -100,7 +103,7 @@ struct CarThreadT {
     const int cxb = car_bin_i(s.xc);
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
-      if (p < sm.peds) {
+      if (active(sm, p)) {
         s.px[p] = __uint_as_float(st[(4 + 2 * p) * cap + i]);
         s.py[p] = __uint_as_float(st[(5 + 2 * p) * cap + i]);
         gap_min(s.gap, cxb, s.px[p], s.py[p]);
@@ -119,7 +122,7 @@ struct CarThreadT {
     st[3 * cap + i] = s.g1;
 #pragma unroll
     for (int p = 0; p < MAXP; ++p)
-      if (p < sm.peds) {
+      if (active(sm, p)) {
         st[(4 + 2 * p) * cap + i] = __float_as_uint(s.px[p]);
         st[(5 + 2 * p) * cap + i] = __float_as_uint(s.py[p]);
       }
@@ -135,7 +138,7 @@ struct CarThreadT {
     f(0u, car_bin(s.xc) | (s.level << 16));
 #pragma unroll
     for (int p = 0; p < MAXP; ++p)
-      if (p < sm.peds) f((uint32_t)(1 + p), car_bin(s.px[p]) | (car_bin(s.py[p]) << 16));
+      if (active(sm, p)) f((uint32_t)(1 + p), car_bin(s.px[p]) | (car_bin(s.py[p]) << 16));
   }
   // observation word k (0: car, 1+i: pedestrian i) of a non-terminal state
   static __device__ __forceinline__ uint32_t obs_word(const St& s, int k) {
@@ -169,13 +172,13 @@ struct CarThreadT {
     s.gap = 255;
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
-      if (4 * bk >= sm.peds + 1) break;  // uniform
+      if (4 * bk >= (EXACT ? MAXP : sm.peds) + 1) break;  // uniform
       const uint4 w = bk == 0 ? w0 : philox(id, t, (uint32_t)bk, 0u, key);
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int p = 4 * bk + q - 1;  // word 4bk+q belongs to pedestrian 4bk+q-1
-        if (p >= 0 && p < MAXP && p < sm.peds) {
+        if (p >= 0 && active(sm, p)) {
           const float2 cs = sm.rot[car_noise_index(ws[q])];
           car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
           const float dx = s.px[p] - s.xc;
