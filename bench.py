@@ -568,7 +568,9 @@ def main():
     traffic = ncu_traffic(args.config)
     if kind == "car":  # the variant rule of despot.cu (launch_k2_sparse) unless forced
         q_bound = A * sum(model.node_info(lf[0])[0] for lf in leaves)
-        big, tiny = q_bound >= num_sms * 256, q_bound < num_sms * 4
+        peds = c.get("peds", 20) if args.peds is None else args.peds
+        big = q_bound >= num_sms * 256 or (peds <= 8 and q_bound >= num_sms * 4)
+        tiny = q_bound < num_sms * 4
         k2_name = {"thread": "k2_car_thread", "warp": "k2_car_warp", "group": "k2_car_group",
                    "auto": "k2_car_thread" if big else "k2_car_warp" if tiny else "k2_car_group"}[args.car_variant]
     else:

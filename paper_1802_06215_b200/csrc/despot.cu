@@ -820,7 +820,10 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   // profiles/r01/peds_sweep.jsonl); a warp per scenario for the few-item
   // batches of a tree search (latency: all pedestrians of a step in parallel)
   const bool forced = m->flags & (DESPOT_MF_UNFACTORED | DESPOT_MF_FACTORED | DESPOT_MF_GROUPED);
-  const bool big = q_bound >= (uint64_t)m->num_sms * 256, tiny = q_bound < (uint64_t)m->num_sms * 4;
+  // (with <= 8 pedestrians the thread kernel also wins the middle range:
+  // 8 roots x K = 64, 6 pedestrians: 0.107 ms vs 0.139 grouped, 0.231 warp)
+  const bool big = q_bound >= (uint64_t)m->num_sms * 256 || (dm.peds <= 8 && q_bound >= (uint64_t)m->num_sms * 4),
+             tiny = q_bound < (uint64_t)m->num_sms * 4;
   const bool grouped = (m->flags & DESPOT_MF_GROUPED) || (!forced && !big && !tiny);
   const bool unfactored = !grouped && ((m->flags & DESPOT_MF_UNFACTORED) || (!forced && big));
   if (grouped) {
