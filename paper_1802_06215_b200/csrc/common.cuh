@@ -58,6 +58,11 @@ struct DevModel {
   uint64_t t_car_fail;
   float noise_scale;
   float2 car_rot[1021];  // heading-noise rotation (c, s) by byte sum - 510 + 510 (card §3.4)
+  // dense models: the kernels' shared-memory image (the model's Sm + its
+  // tables) as M::load_sm builds it, made once at model load
+  // (k_snapshot_sm); kernels copy it in with 16-byte loads (load_sm_image)
+  const uint4* sm_snap;
+  uint32_t sm_snap_words;
 };
 
 // ---------------------------------------------------------------------------

@@ -202,6 +202,7 @@ struct despot_model {
   std::mutex mu;
   std::unordered_set<Node*> nodes;
   int k2_occ = 0;
+  void* snap = nullptr;  // device copy of the dense model's shared-memory image
 };
 
 struct despot_batch {
@@ -631,6 +632,29 @@ extern "C" int despot_model_load(const char* kind, const char* params, const des
   }
   CU(cudaMalloc(&m->dev, sizeof(DevModel)));
   CU(cudaMemcpy(m->dev, &m->host, sizeof(DevModel), cudaMemcpyHostToDevice));
+  if (m->host.slots) {  // dense models: the shared-memory image, once (load_sm_image)
+    rc = dispatch_dense(m->host, [&](auto mdl) -> int {
+      using M = decltype(mdl);
+      const size_t bytes = align16(sizeof(typename M::Sm)) + align16(m->host.sm_table_bytes);
+      const uint32_t words = (uint32_t)(bytes / 16);
+      uint4* snap = nullptr;
+      if (cudaMalloc(&snap, bytes) != cudaSuccess) return set_err(DESPOT_ENOMEM, "model image");
+      m->snap = snap;
+      kernel_occupancy((const void*)k_snapshot_sm<M>, bytes, 256);  // sets the smem attribute if > 48 KB
+      k_snapshot_sm<M><<<1, 256, bytes>>>(m->dev, snap, words);
+      if (cudaDeviceSynchronize() != cudaSuccess) return set_err(DESPOT_ECUDA, "model image kernel");
+      m->host.sm_snap = snap;
+      m->host.sm_snap_words = words;
+      if (cudaMemcpy(m->dev, &m->host, sizeof(DevModel), cudaMemcpyHostToDevice) != cudaSuccess)
+        return set_err(DESPOT_ECUDA, "model copy");
+      return DESPOT_OK;
+    });
+    if (rc) {
+      if (m->snap) cudaFree(m->snap);
+      cudaFree(m->dev);
+      return rc;
+    }
+  }
   *out = m.release();
   return DESPOT_OK;
 }
@@ -658,6 +682,7 @@ extern "C" int despot_model_free(despot_model* m) {
   }
   cudaDeviceSynchronize();
   if (m->dev) cudaFree(m->dev);
+  if (m->snap) cudaFree(m->snap);
   delete m;
   return DESPOT_OK;
 }

@@ -9,6 +9,31 @@
 namespace hd {
 
 // ---------------------------------------------------------------------------
+// The shared-memory image of a dense model (its Sm and tables).  M::load_sm
+// derives the tables from the DevModel (divisions, distance and threshold
+// look-ups: ~2/3 of an update kernel's instructions); the library runs it
+// once per model (k_snapshot_sm) and every kernel then copies the image.
+// ---------------------------------------------------------------------------
+template <class M>
+__device__ __forceinline__ void load_sm_image(typename M::Sm& sm, const DevModel& dm, int tid, int nt) {
+  if (const uint4* src = dm.sm_snap) {
+    uint4* dst = reinterpret_cast<uint4*>(hd_dyn_smem);
+    for (uint32_t i = tid; i < dm.sm_snap_words; i += nt) dst[i] = __ldg(src + i);
+  } else {
+    M::load_sm(sm, dm, tid, nt);
+  }
+}
+template <class M>
+__global__ void __launch_bounds__(256) k_snapshot_sm(const DevModel* dm, uint4* dst, uint32_t words) {
+  typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
+  M::load_sm(sm, *dm, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const uint4* s = reinterpret_cast<const uint4*>(hd_dyn_smem);
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = s[i];
+}
+
+
+// ---------------------------------------------------------------------------
 // K1: update.  One CTA per leaf: gather the parent's scenarios,
 // replay the leaf's last action at depth Delta (drawing phi_Delta), keep those
 // whose observation equals the parent's key of child `child`, and compact them
@@ -23,7 +48,7 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
   } else {
-    M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+    load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
     const uint32_t nchild = lf.p_nchild[lf.action];
     const bool valid_child = lf.child < nchild;
     const uint32_t key = valid_child ? lf.p_keys[(uint64_t)lf.action * lf.p_kcap + lf.child] : 0xFFFFFFFFu;
@@ -98,7 +123,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   uint32_t* tile_off =
       reinterpret_cast<uint32_t*>(hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes));
-  M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
   for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
   __syncthreads();
   const uint32_t total = tile_off[b.L];
@@ -255,7 +280,7 @@ __global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, con
                                                         uint32_t k0, uint32_t k1, double inv_wroot,
                                                         float* per_u, float* per_l, int64_t* acc3) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
-  M::load_sm(sm, *dmp, threadIdx.x, blockDim.x);
+  load_sm_image<M>(sm, *dmp, threadIdx.x, blockDim.x);
   __syncthreads();
   const double fx = dmp->fx;
   int64_t qW = 0, qU = 0, qL = 0;

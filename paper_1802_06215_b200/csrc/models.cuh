@@ -4,7 +4,8 @@
 //
 // Interface of a model M (used by the kernel templates in kernels.cu):
 //   M::Sm                 shared-memory copy of the hot tables
-//   M::load_sm(sm, dm)    cooperative copy (caller syncs)
+//   M::load_sm(sm, dm)    cooperative build of Sm + tables (caller syncs); the
+//                         kernels use load_sm_image (a copy of its result)
 //   M::St                 per-thread register state; load/store SoA rows
 //   M::terminal(sm, s)    terminal flag of a state
 //   M::step(...)          g(s, a, phi_t) on a non-terminal state (Eq. 9)
