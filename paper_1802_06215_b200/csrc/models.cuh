@@ -430,7 +430,7 @@ struct RockSample {
 // three rows and extracts the 3x3 neighbourhood with shifts.
 // ===========================================================================
 constexpr int kNavRowStride = 19;      // padded rows (n + 2 <= 18), odd stride
-constexpr int kNavMaxThreads = 256;    // largest block of a kernel using Nav
+constexpr int kNavMaxThreads = 512;    // largest block of a kernel using Nav (K1: one round over K = 500)
 
 template <int NW>
 struct Nav {
