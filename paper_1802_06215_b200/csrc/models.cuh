@@ -120,7 +120,6 @@ struct RockSample {
   static constexpr int kMinBlocks = HD_RS_MINB;  // 7: 72 registers, 28 warps per SM (8 / 7 / 6 measured 1.569 / 1.539 / 1.538 ms on config 2)
   static constexpr int kK1Threads = 512;  // K1 block: one round over K = 500 scenarios
   static constexpr int kMaxTable = 16384;  // n*n*m entries of the per-cell rock tables
-  static constexpr uint32_t kExitFlag = 0x8000u;  // move target flag: the robot exits (+10)
   struct Sm {
     int32_t n, m, mm, base, ncell, exitc;  // exitc = EXIT pseudo-cell = n*n; mm = max(m, 1)
     uint32_t D;
@@ -129,7 +128,9 @@ struct RockSample {
     uint32_t none_bit;       // 1 << m: __ffs(open | none_bit) - 1 = m when nothing is open
     uint32_t range_mask[2];  // policy positions of robot r (0 for the always-east policy)
     // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m, D):
-    uint32_t off_nb;    // u16 [cell][4]: target of N, S, E, W (kExitFlag | EXIT: exits east)
+    uint32_t off_act;   // u16 [cell][base]: the effect of sub-action b on a robot at the cell:
+                        // bits 0-10 the next cell (EXIT pseudo-cell included), bit 15 the +10
+                        // exit, bit 14 SAMPLE on a rock, bit 13 SENSE (not from EXIT)
     uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
     uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
     uint32_t off_pol;   // u8  [cell][m+1]: policy move toward the rock of position p (4 = on it); [m] = E
@@ -138,17 +139,18 @@ struct RockSample {
     uint32_t off_gp10;
   };
   static __host__ __device__ int gpow_len(int n, uint32_t D) { return (int)(D > (uint32_t)(2 * n) ? D : 2 * n) + 1; }
-  // table bytes (host and device agree): nb | info | thr | pol | dist | gp | gp10, with the EXIT row
+  static constexpr uint32_t kActExit = 0x8000u, kActSample = 0x4000u, kActSense = 0x2000u, kActCell = 0x7FFu;
+  // table bytes (host and device agree): act | info | thr | pol | dist | gp | gp10, with the EXIT row
   static __host__ __device__ size_t table_bytes(int n, int m, uint32_t D) {
     const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
-    return align16(8 * c) + align16(4 * c) + align16(4 * c * mm) + align16(c * (m + 1)) + align16(c * mm) +
-           align16(8 * G) + align16(8 * G);
+    return align16(2 * c * (5 + m)) + align16(4 * c) + align16(4 * c * mm) + align16(c * (m + 1)) +
+           align16(c * mm) + align16(8 * G) + align16(8 * G);
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
   }
-  static __device__ __forceinline__ uint32_t target(const Sm& sm, int c, int mv) {
-    return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_nb)[c * 4 + mv];
+  static __device__ __forceinline__ uint32_t act(const Sm& sm, int c, int sub) {
+    return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_act)[c * sm.base + sub];
   }
   static __device__ __forceinline__ uint32_t thr(const Sm& sm, int c, int j) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + j];
@@ -168,13 +170,13 @@ struct RockSample {
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc, G = gpow_len(n, dm.D);
     const uint32_t base = (uint32_t)align16(sizeof(Sm));
-    const uint32_t off_nb = base, off_info = off_nb + (uint32_t)align16(8 * (size_t)(nc + 1)),
+    const uint32_t off_act = base, off_info = off_act + (uint32_t)align16(2 * (size_t)(nc + 1) * dm.base),
                    off_thr = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
                    off_pol = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
                    off_dist = off_pol + (uint32_t)align16((size_t)(nc + 1) * (dm.m + 1)),
                    off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * mm),
                    off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
-    uint16_t* t_nb = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_nb);
+    uint16_t* t_act = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_act);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
     uint32_t* t_thr = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_thr);
     uint8_t* t_pol = hd_dyn_smem + off_pol;
@@ -182,7 +184,7 @@ struct RockSample {
     double* t_gp = reinterpret_cast<double*>(hd_dyn_smem + off_gp);
     double* t_gp10 = reinterpret_cast<double*>(hd_dyn_smem + off_gp10);
     if (tid == 0) {
-      sm.off_nb = off_nb;
+      sm.off_act = off_act;
       sm.off_info = off_info;
       sm.off_thr = off_thr;
       sm.off_pol = off_pol;
@@ -211,17 +213,20 @@ struct RockSample {
       t_dist[e] = (c < nc && j < dm.m) ? (uint8_t)(abs(c % n - dm.rx[j]) + abs(c / n - dm.ry[j])) : (uint8_t)255;
     }
     for (int c = tid; c <= nc; c += nt) {
-      if (c == exitc) {  // the pseudo-cell: every move stays, no rock
-        for (int k = 0; k < 4; ++k) t_nb[4 * c + k] = (uint16_t)exitc;
+      uint16_t* row = t_act + (size_t)c * dm.base;
+      if (c == exitc) {  // the pseudo-cell: every sub-action is a no-op, no rock
+        for (int k = 0; k < dm.base; ++k) row[k] = (uint16_t)exitc;
         t_info[c] = 0;
         continue;
       }
       const int x = c % n, y = c / n;
-      t_nb[4 * c + 0] = (uint16_t)(y > 0 ? c - n : c);                                 // N
-      t_nb[4 * c + 1] = (uint16_t)(y < n - 1 ? c + n : c);                             // S
-      t_nb[4 * c + 2] = (uint16_t)(x < n - 1 ? c + 1 : (int)(kExitFlag | exitc));      // E (exit)
-      t_nb[4 * c + 3] = (uint16_t)(x > 0 ? c - 1 : c);                                 // W
       const int8_t rock = dm.rock_at[c];
+      row[0] = (uint16_t)(y > 0 ? c - n : c);                                     // N
+      row[1] = (uint16_t)(y < n - 1 ? c + n : c);                                 // S
+      row[2] = (uint16_t)(x < n - 1 ? c + 1 : (int)(kActExit | exitc));           // E (exit)
+      row[3] = (uint16_t)(x > 0 ? c - 1 : c);                                     // W
+      row[4] = (uint16_t)(c | (rock >= 0 ? kActSample : 0u));                     // SAMPLE
+      for (int k = 5; k < dm.base; ++k) row[k] = (uint16_t)(c | kActSense);       // SENSE k - 5
       t_info[c] = (rock >= 0 ? ((uint32_t)rock | 32u) : 0u) | ((uint32_t)x << 8) | ((uint32_t)y << 16);
     }
     for (int e = tid; e < (nc + 1) * mm; e += nt) {
@@ -291,25 +296,23 @@ struct RockSample {
     for (int r = 0; r < R; ++r) {
       const int sub = b[r];
       const int c = s.cell[r];
-      // moves 0 N, 1 S, 2 E, 3 W: the table's target (itself when blocked;
-      // EXIT with the flag through the east border)
-      const uint32_t tg = target(sm, c, sub & 3);
-      const bool is_move = sub < 4;
-      // SAMPLE on the current cell
-      const uint32_t inf = info(sm, c);
-      const uint32_t jr = inf & 31u;
-      const uint32_t samp = (sub == 4) ? (inf >> 5) & 1u : 0u;
+      // the (cell, sub-action) entry: next cell (a move's target, itself
+      // when blocked or not moving, EXIT through the east border) and flags
+      const uint32_t e = act(sm, c, sub);
+      // SAMPLE on the current cell's rock
+      const uint32_t jr = info(sm, c) & 31u;
+      const uint32_t samp = (e & kActSample) ? 1u : 0u;
       const uint32_t gbit = samp & (s.good >> jr);
       // SENSE j (evaluated for every lane; masked; none from EXIT)
       const int js = max(sub - 5, 0);
       const uint32_t incorrect = u[r] > thr(sm, c, js) ? 1u : 0u;
       const uint32_t isgood = (s.good >> js) & 1u;
-      const uint32_t sense = (sub >= 5 && c != sm.exitc) ? 1u : 0u;
+      const uint32_t sense = (e & kActSense) ? 1u : 0u;
       const uint32_t zr = sense * (2u - (isgood ^ incorrect));  // GOOD (1) iff good == correct
-      reward += is_move ? 10 * (int)(tg >> 15) : 0;
+      reward += (e & kActExit) ? 10 : 0;
       reward += (int)samp * (20 * (int)gbit - 10);
       s.good &= ~(gbit << jr);
-      s.cell[r] = is_move ? (int)(tg & 0x7FFFu) : c;
+      s.cell[r] = (int)(e & kActCell);
       if (zrs) zrs[r] = zr;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
