@@ -479,6 +479,7 @@ struct Nav {
     int32_t x, y;
     uint32_t gate;
     bool term;
+    uint32_t nb;  // occupancy of the 8 neighbours of (x, y) (derived: set by load, kept by step)
     uint32_t occ[NW];
   };
   static __device__ __forceinline__ void build_grid(const Sm& sm, const St& s) {
@@ -508,6 +509,7 @@ struct Nav {
 #pragma unroll
     for (int k = 0; k < NW; ++k) s.occ[k] = st[(1 + k) * cap + i];
     build_grid(sm, s);
+    s.nb = neighbours(s.x, s.y);
     return s;
   }
   static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
@@ -539,7 +541,7 @@ struct Nav {
     const bool stay = a == 0;
     const bool fail = !stay && event(u[0], sm.t_fail);
     const int k = stay ? 0 : a - 1;  // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
-    const uint32_t occ = (neighbours(s.x, s.y) >> k) & 1u;
+    const uint32_t occ = (s.nb >> k) & 1u;  // the neighbours of the current cell (carried)
     const bool moves = !stay && !fail && !occ;
     const int nx = s.x + ((a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0);
     const int ny = s.y + ((a == 1 || a == 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0);
@@ -552,7 +554,8 @@ struct Nav {
     uint32_t flips = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) flips |= (event(u[1 + q], sm.t_flip) ? 1u : 0u) << q;
-    const uint32_t obs = neighbours(s.x, s.y) ^ flips;
+    s.nb = neighbours(s.x, s.y);  // of the new cell: the observation, and the next step's moves
+    const uint32_t obs = s.nb ^ flips;
     z = goal ? kTerminalObs : obs;
     return goal;
   }
