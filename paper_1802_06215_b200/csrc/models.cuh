@@ -289,7 +289,8 @@ struct RockSample {
   // sub-actions do not diverge.  zrs[r] returns robot r's reading (0 none,
   // 1 GOOD, 2 BAD).  Rewards are integers (exact in fp32).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
-                                                  uint32_t& z, float& rew, uint32_t* zrs = nullptr) {
+                                                  uint32_t& z, float& rew, uint32_t* zrs = nullptr,
+                                                  int* irew = nullptr) {
     int reward = 0;
     uint32_t zsum = 0;
 #pragma unroll
@@ -317,6 +318,7 @@ struct RockSample {
       zsum += zr * (r == 0 ? 1u : 3u);
     }
     rew = (float)reward;
+    if (irew) *irew = reward;  // the roll-out converts the integer straight to double (same value)
     const bool term = terminal(sm, s);
     z = term ? kTerminalObs : zsum;
     return term;
@@ -404,8 +406,9 @@ struct RockSample {
       const uint4 w = philox(id, t + 1, 0u, 0u, key);
       const uint32_t u[2] = {w.x, w.y};
       float r;
+      int ir;
       uint32_t zr[R];
-      term = step_sub(sm, s, b, u, z, r, zr);
+      term = step_sub(sm, s, b, u, z, r, zr, &ir);
       // policy memory: a GOOD reading marks the rock GOOD, a BAD one DONE; a
       // sample marks it DONE
 #pragma unroll
@@ -413,7 +416,7 @@ struct RockSample {
         gm |= tb[q] & (0u - (zr[q] & 1u));
         done |= ((zr[q] >> 1) | (uint32_t)(b[q] == 4)) ? tb[q] : 0u;
       }
-      acc += gp(sm, (int)(t - t0)) * (double)r;
+      acc += gp(sm, (int)(t - t0)) * (double)ir;
       ++t;
     }
     if (!term) acc += gp(sm, (int)(t - t0)) * sm.tail;
