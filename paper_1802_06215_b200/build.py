@@ -41,8 +41,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("nvcc failed building libdespot.so")
     if verbose:
         sys.stderr.write(res.stderr)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:  # registers / spills / smem per kernel
+        f.write("".join(l for l in res.stderr.splitlines(True) if "Compile time" not in l))
     os.replace(tmp, LIB)
     return LIB
 
