@@ -191,6 +191,19 @@ typedef struct {
   uint64_t d2h_bytes;      /*      host (leaf table, status, results; begin + end)   */
 } despot_expansion;
 
+/* Output sizes of a batch before calling it (host only, no device work):
+ * *child_capacity = an upper bound of the children C (sum over leaves of
+ * A * min(|Phi_parent|, obs_slots); sharded: (local n + 1) * world per parent,
+ * which a filtered node may exceed -- the call then fails with ECAPACITY and
+ * reports num_children), *scen_capacity = A * sum of the parents' local
+ * scenario counts (>= what DESPOT_X_RECORD_SCENARIO writes), *host_bytes =
+ * the bytes of every despot_expansion array at those sizes for `flags`
+ * (node, n_scen, weight, act_*, child_begin, the child arrays and, with
+ * RECORD, the scen_* arrays).  Any output may be NULL.  Errors: EINVAL
+ * (unknown node), ECAPACITY (the child bound does not fit in 32 bits). */
+int despot_expand_batch_bytes(despot_model* model, const despot_leaf* leaves, uint32_t L, uint32_t flags,
+                              uint32_t* child_capacity, uint64_t* scen_capacity, uint64_t* host_bytes);
+
 /* One batch: update (world-local) -> expansion + bounds + roll-outs + grouping
  * -> child ordering, CSR and outputs.  `leaves` is a host array of L <= 4096
  * descriptors.  Synchronous.  With world > 1 use the begin/exchange/end form.

@@ -758,6 +758,33 @@ extern "C" int despot_node_info(despot_model* m, despot_node h, uint32_t* n, uin
   return DESPOT_OK;
 }
 
+extern "C" int despot_expand_batch_bytes(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags,
+                                         uint32_t* child_capacity, uint64_t* scen_capacity, uint64_t* host_bytes) {
+  if (!m || (!leaves && L)) return set_err(DESPOT_EINVAL, "null argument");
+  const DevModel& dm = m->host;
+  const uint64_t W = (uint64_t)std::max(m->world, 1);
+  uint64_t C = 0, S = 0;
+  for (uint32_t l = 0; l < L; ++l) {
+    Node* p = lookup(m, leaves[l].parent);
+    if (!p) return set_err(DESPOT_EINVAL, "leaf %u: unknown node", l);
+    // a leaf's scenarios are a subset of its parent's; sharded, only the
+    // local count is known: (n + 1) * world bounds the global one for
+    // interleaved ids (a filtered node may need more: ECAPACITY says so)
+    const uint64_t g = W == 1 ? p->n : ((uint64_t)p->n + 1) * W;
+    C += (uint64_t)dm.A * (dm.slots ? std::min<uint64_t>(g, dm.slots) : g);
+    S += (uint64_t)dm.A * p->n;
+  }
+  C = std::max<uint64_t>(C, 1);
+  if (C > 0xFFFFFFFFull) return set_err(DESPOT_ECAPACITY, "child bound %llu exceeds 2^32 - 1", (unsigned long long)C);
+  const uint64_t LA = (uint64_t)L * dm.A;
+  uint64_t bytes = (uint64_t)L * (8 + 4 + 4) + LA * 3 * 4 + (LA + 1) * 4 + C * (4 * 5 + 4 * (uint64_t)dm.OW);
+  if (flags & DESPOT_X_RECORD_SCENARIO) bytes += S * (4 * (uint64_t)dm.OW + 4 * 4 + 8 + 4 * (uint64_t)dm.SW);
+  if (child_capacity) *child_capacity = (uint32_t)C;
+  if (scen_capacity) *scen_capacity = S;
+  if (host_bytes) *host_bytes = bytes;
+  return DESPOT_OK;
+}
+
 extern "C" int despot_node_read(despot_model* m, despot_node h, uint32_t* ids, float* w,
                                 uint32_t* states_soa, void* stream) {
   Node* nd = m ? lookup(m, h) : nullptr;

@@ -30,7 +30,7 @@ EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "desp
            "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
            "despot_node_release", "despot_node_release_many", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
            "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
-           "despot_search", "despot_plan", "despot_philox_ceiling"]
+           "despot_search", "despot_plan", "despot_philox_ceiling", "despot_expand_batch_bytes"]
 
 
 def _tflag(timing):
@@ -157,6 +157,8 @@ def lib():
         L.despot_batch_abort.argtypes = [vp]
         L.despot_rollout_bounds.argtypes = [vp, u64, C.POINTER(C.c_float), C.POINTER(C.c_float), vp, vp, vp]
         L.despot_stream_words.argtypes = [vp, u64, vp, u32, u32, u32, vp, vp]
+        L.despot_expand_batch_bytes.argtypes = [vp, C.POINTER(Leaf), u32, u32, C.POINTER(C.c_uint32),
+                                                C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         L.despot_philox_ceiling.argtypes = [vp, u64, u32, u32, u32, vp, C.POINTER(C.c_double),
                                             C.POINTER(C.c_uint32)]
         L.despot_search.argtypes = [C.POINTER(SearchProblem), C.POINTER(SearchConfig), C.POINTER(SearchResult),
@@ -430,6 +432,15 @@ class Model:
         res = SearchResult()
         _check(lib().despot_plan(self.h, int(root), C.byref(cfg), C.byref(res), _stream_ptr(stream)))
         return result_dict(res)
+
+    def batch_bytes(self, leaves, record=False):
+        """despot_expand_batch_bytes: (child_capacity, scen_capacity, host
+        output bytes) of a batch."""
+        c, sc, hb = C.c_uint32(), C.c_uint64(), C.c_uint64()
+        _check(lib().despot_expand_batch_bytes(self.h, self._leaves(leaves), len(leaves),
+                                               DESPOT_X_RECORD_SCENARIO if record else 0, C.byref(c),
+                                               C.byref(sc), C.byref(hb)))
+        return c.value, sc.value, hb.value
 
     def philox_ceiling(self, seed, n_threads, blocks, reps=5, stream=None):
         """K0 (despot_philox_ceiling): (ms per launch of n_threads * blocks

@@ -47,6 +47,27 @@ def test_k0_philox_ceiling_checksum_matches_oracle():
         gm.philox_ceiling(1, 0, 1)
 
 
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_expand_batch_bytes_bounds_the_outputs(cfg):
+    """despot_expand_batch_bytes: the child bound equals the binding's and
+    covers the children the call produces; the scenario bound covers the
+    per-scenario records; the byte count matches the arrays' sizes."""
+    gm, om, st, w, seed, L = setup(cfg, K=120 if cfg == 1 else 200, L=6)
+    gr = gm.belief_load(st, w, seed)
+    G0 = gm.expand([(gr, -1, 0, 0)])
+    lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(G0["child_count"], G0["child_begin"], gm.A, L)]
+    C, S, B = gm.batch_bytes(lv, record=True)
+    assert C == gm.child_capacity_bound(lv)
+    G = gm.expand(lv, record=True)
+    assert int(G["child_begin"][-1]) <= C
+    assert gm.A * int(np.sum(G["n_scen"])) <= S
+    A, OW, SW, Lc = gm.A, gm.OW, gm.SW, len(lv)
+    assert B == Lc * 16 + Lc * A * 12 + (Lc * A + 1) * 4 + C * (20 + 4 * OW) + S * (4 * OW + 24 + 4 * SW)
+    with pytest.raises(DespotError):
+        gm.batch_bytes([(123456789, 0, 0, 1)])
+    gm.close()
+
+
 # ----------------------------------------------------------------------------
 # full configs (BASELINE.json), in the launch configuration bench.py times;
 # the oracle checks a sample of the leaves (each leaf's outputs depend only on
