@@ -8,10 +8,12 @@ mkdir -p $O profiles/r01
 nvidia-smi > $O/nvidia_smi.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.txt 2>&1
-for c in 2 3 4; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_ -s 3 -c 1 -o $O/k2_config$c python bench.py --config $c --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_full_$c.log 2>&1
+for c in 1 2 3 4 5; do
+  X=""; [ $c = 5 ] && X="--K 32768"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2_ -s 3 -c 1 -o $O/k2_config$c python bench.py --config $c $X --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_full_$c.log 2>&1
   echo "rc=$?" >> $O/ncu_full_$c.log
   ncu -i $O/k2_config$c.ncu-rep --page raw --csv > $O/k2_config${c}_raw.csv 2>/dev/null && cp $O/k2_config${c}_raw.csv profiles/r01/
+  [ $c = 2 ] || rm -f $O/k2_config$c.ncu-rep   # gpurun brings back <= 64 MiB: keep config 2's report only
 done
 timeout 1800 python scripts/measure_istep.py --out $O/i_step.json > $O/i_step.log 2>&1
 cp $O/i_step.json profiles/r01/i_step.json
