@@ -15,9 +15,11 @@
  * Parity status per function (see DESIGN.md §4 for the pins):
  *   philox, thresholds, step/upper/rollout of tiger, rocksample, nav: pinned
  *   (KAT vectors, paper constants, closed forms, brute-force bounds).
- *   car step dynamics beyond the pinned invariants: "parity unpinned"
- *   (the paper defers the driving model to Bai 2015, which is not in the
- *   reference; only the invariants listed in DESIGN.md pin it).
+ *   car: step rewards (time, brake, collision, goal), speed clamp, u(s),
+ *   pi0's gap rule, step length and mean heading are pinned by closed-form
+ *   single steps (tests/test_oracle_pins.py, card §3.4); the shape of the
+ *   heading noise (tau scale) stays "parity unpinned" (the paper defers the
+ *   driving model to Bai 2015, which is not in the reference).
  */
 #include "oracle.h"
 

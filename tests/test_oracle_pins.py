@@ -509,3 +509,110 @@ def test_scenario_prefix_is_stable_across_K():
             sb, ss = slice(a * 80, a * 80 + 50), slice(a * 50, a * 50 + 50)
             for k in ("scen_obs", "scen_reward", "scen_len", "scen_hash", "scen_states", "scen_upper", "scen_lower"):
                 np.testing.assert_array_equal(big[k][sb], small[k][ss])
+
+
+# Driving, closed-form single steps of card §3.4 on one pedestrian:
+# goal and collision rewards, the speed clamp, u(s) at the goal line and at the
+# start, pi0's gap rule, and a pedestrian's step direction toward its goal.
+def _car1(xc, level, px, py, goal):
+    s = np.zeros(6, np.uint32)
+    s[0] = np.float32(xc).view(np.uint32)
+    s[1] = level
+    s[2] = goal
+    s[4] = np.float32(px).view(np.uint32)
+    s[5] = np.float32(py).view(np.uint32)
+    return s
+
+
+def _f(w):
+    return float(np.uint32(w).view(np.float32))
+
+
+CAR1 = "peds=1 D=90 gamma=0.95"
+
+
+def test_car_reaching_the_goal_line_pays_100_and_ends():
+    m = oracle.Model("car", CAR1)
+    # v = 0.5 * level 2 = 1 m/s, dt 0.25 s: 19.9 -> 20.15 >= 20; pedestrian far
+    # away at (2, -5) walking to (0, -10)
+    for sid in range(8):
+        s2, z, r, term, _ = m.step(_car1(19.9, 2, 2.0, -5.0, 0), 0, sid, 1, 3)
+        assert term and z[0] == 0xFFFFFFFF and z[1] == 0
+        assert abs(_f(s2[0]) - 20.15) < 1e-5
+        assert abs(r - (-0.1 + 100.0)) < 1e-4
+    # one step short of the line: only the time cost
+    s2, z, r, term, _ = m.step(_car1(10.0, 2, 2.0, -5.0, 0), 0, 0, 1, 3)
+    assert not term and abs(r + 0.1) < 1e-6
+    assert (z[0] & 0xFFFF) == 20 + 0 and (z[0] >> 16) == 2  # floor(2 * 10.25), level 2
+
+
+def test_car_collision_costs_speed_squared():
+    m = oracle.Model("car", CAR1)
+    # pedestrian on the car's path 0.25 m ahead of where the car lands: after
+    # both move 0.25 m they are at most 0.5 m apart (< 1 m): collision
+    for sid in range(8):
+        s2, z, r, term, _ = m.step(_car1(5.0, 2, 5.5, 0.0, 1), 0, sid, 1, 3)
+        assert term and z[0] == 0xFFFFFFFF
+        assert abs(r - (-0.1 - 1000.0 * (1.0 ** 2 + 0.5))) < 1e-2
+    # standing still (level 0, DEC clamps at 0) and braking: -0.1 - 0.1 - 1000 * 0.5
+    s2, z, r, term, _ = m.step(_car1(5.0, 0, 5.3, 0.0, 1), 2, 0, 1, 3)
+    assert term and (s2[1] & 0xFF) == 0
+    assert abs(r - (-0.2 - 500.0)) < 1e-2
+
+
+def test_car_speed_level_clamps_at_0_and_4():
+    m = oracle.Model("car", CAR1)
+    for sid in range(32):
+        s2 = m.step(_car1(0.0, 4, 2.0, -5.0, 0), 1, sid, 1, 3)[0]
+        assert (s2[1] & 0xFF) == 4 and abs(_f(s2[0]) - 0.5) < 1e-6  # v = 2 m/s
+        s2 = m.step(_car1(0.0, 0, 2.0, -5.0, 0), 2, sid, 1, 3)[0]
+        assert (s2[1] & 0xFF) == 0 and _f(s2[0]) == 0.0
+
+
+def test_car_upper_bound_goal_line_and_start():
+    m = oracle.Model("car", CAR1)
+    g = 0.95
+    assert abs(m.upper(_car1(19.5, 2, 2.0, -5.0, 0)) - 100.0) < 1e-9   # k = 1
+    assert abs(m.upper(_car1(19.9, 2, 2.0, -5.0, 0)) - 100.0) < 1e-9   # k clamped to 1
+    assert abs(m.upper(_car1(0.0, 2, 2.0, -5.0, 0)) - 100.0 * g ** 39) < 1e-9  # k = 40 half-metre bins
+    t = _car1(0.0, 2, 2.0, -5.0, 0)
+    t[1] |= 1 << 8
+    assert m.upper(t) == 0.0
+
+
+def test_car_default_policy_gap_rule():
+    m = oracle.Model("car", CAR1)
+    s = _car1(0.0, 2, 2.0, -5.0, 0)
+
+    def z(cxb, pxb, pyb):
+        return [(cxb & 0xFFFF) | (2 << 16), (pxb & 0xFFFF) | ((pyb & 0xFFFF) << 16)]
+
+    assert m.default_action(s, z(10, 14, 0), 0, 1) == 2    # gap 4 <= 8: DECELERATE
+    assert m.default_action(s, z(10, 18, -4), 0, 1) == 2   # gap 8, lowest lane bin
+    assert m.default_action(s, z(10, 22, 3), 0, 1) == 0    # gap 12 <= 16: MAINTAIN
+    assert m.default_action(s, z(10, 40, 0), 0, 1) == 1    # gap 30: ACCELERATE
+    assert m.default_action(s, z(10, 9, 0), 0, 1) == 1     # behind the car
+    assert m.default_action(s, z(10, 14, 4), 0, 1) == 1    # outside the lane (y >= 2 m)
+    assert m.default_action(s, z(10, 14, -5), 0, 1) == 1   # outside the lane (y < -2 m)
+
+
+def test_car_pedestrian_heads_to_its_goal_on_average():
+    """The heading noise is symmetric about the goal direction: over
+    many streams the mean step points at the goal, its length below 0.25 m."""
+    m = oracle.Model("car", CAR1)
+    goals = [(0.0, -10.0), (0.0, 10.0), (20.0, -10.0), (20.0, 10.0)]
+    px, py = 10.0, 0.0
+    for gi, (gx, gy) in enumerate(goals):
+        d = np.zeros(2)
+        N = 2000
+        for sid in range(N):
+            s2 = m.step(_car1(0.0, 0, px, py, gi), 0, sid, 1, 9)[0]
+            d += (_f(s2[4]) - px, _f(s2[5]) - py)
+        d /= N
+        e = np.array([gx - px, gy - py]) / math.hypot(gx - px, gy - py)
+        along, across = d @ e, d[0] * e[1] - d[1] * e[0]
+        assert 0.15 < along < 0.25, (gi, along)
+        assert abs(across) < 0.02, (gi, across)
+    # a pedestrian standing on its goal stays there
+    s2 = m.step(_car1(0.0, 0, 20.0, 10.0, 3), 0, 0, 1, 9)[0]
+    assert (_f(s2[4]), _f(s2[5])) == (20.0, 10.0)
