@@ -653,3 +653,48 @@ def test_gpu_scenario_prefix_is_stable_across_K():
         sb, ss = slice(a * 80, a * 80 + 50), slice(a * 50, a * 50 + 50)
         for k in ("scen_obs", "scen_reward", "scen_len", "scen_hash", "scen_states", "scen_upper", "scen_lower"):
             assert np.array_equal(big[k][sb], small[k][ss]), k
+
+
+def _car_edge_belief(K, peds=2):
+    """Hand-placed driving states (card §3.4): the goal line one step away,
+    a pedestrian on the car's path, speed levels 0 and 4, a pedestrian
+    standing on its goal (the d2 < 1e-6 branch), a terminal scenario."""
+    rng = np.random.Generator(np.random.PCG64(11))
+    st = np.zeros((4 + 2 * peds, K), np.uint32)
+    goals_xy = [(0.0, -10.0), (0.0, 10.0), (20.0, -10.0), (20.0, 10.0)]
+    f = lambda v: np.float32(v).view(np.uint32)
+    for k in range(K):
+        case = k % 6
+        xc = [19.9, 5.0, 0.0, 19.76, 12.0, 3.0][case]
+        level = [2, 2, 0, 4, 1, 3][case]
+        g = rng.integers(0, 4, size=peds)
+        st[0, k], st[1, k] = f(xc), level | ((1 << 8) if (case == 5 and k % 12 == 5) else 0)
+        st[2, k] = int(sum(int(g[i]) << (2 * i) for i in range(min(peds, 16))))
+        for i in range(peds):
+            if i == 0 and case == 1:
+                x, y = xc + 0.6, 0.1 * (k % 3)          # on the car's path
+            elif i == 0 and case == 2:
+                x, y = goals_xy[g[i]]                  # on its own goal
+            else:
+                x, y = 2.0 + 17.0 * rng.random(), -5.0 + 10.0 * rng.random()
+            st[4 + 2 * i, k], st[5 + 2 * i, k] = f(x), f(y)
+    return st
+
+
+@pytest.mark.parametrize("grouped", [False, True])
+def test_car_edge_states_match_oracle(grouped):
+    peds, K = 2, 47
+    gw, gt, om = _car_models(peds, 20, grouped)
+    st = _car_edge_belief(K, peds)
+    w = inputs.weights(K, K, uniform=False)
+    for gm in (gw, gt):
+        gr, orr = gm.belief_load(st, w, 77), om.belief_load(st, w, 77)
+        G0 = gm.expand([(gr, -1, 0, 0)], record=True)
+        O0 = om.expand([(orr, -1, 0, 0)], record=True)
+        compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
+        assert G0["scenario_steps"] == O0["scenario_steps"]
+        lv = [(a, c) for a in range(3) for c in range(min(4, int(G0["child_begin"][a + 1] - G0["child_begin"][a])))]
+        G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+        O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+        compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
+        assert G1["scenario_steps"] == O1["scenario_steps"]
