@@ -698,3 +698,52 @@ def test_car_edge_states_match_oracle(grouped):
         O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
         compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
         assert G1["scenario_steps"] == O1["scenario_steps"]
+
+
+# ----------------------------------------------------------------------------
+# navigation edge states (card §3.3): next to the goal, on the gate cells, in
+# the corners, fully blocked and fully free unknown maps, terminal scenarios;
+# the 13x13 map and smaller maps (other state word counts)
+# ----------------------------------------------------------------------------
+def _nav_edge_belief(K, n, wall_y, gates, goal, landmarks, seed):
+    nu = inputs.nav_unknown_count(n, wall_y, landmarks)
+    st = inputs.nav_belief(K, seed, n, wall_y, landmarks, p_occ=0.1)
+    gx, gy = goal
+    cells = [(gx, gy - 1), (gx - 1, gy), (gates[0], wall_y), (gates[1], wall_y), (0, 0), (n - 1, n - 1),
+             (n - 1, 0), (0, n - 1), (gx, gy - 2)]
+    for k in range(K):
+        x, y = cells[k % len(cells)]
+        gate = (k // len(cells)) & 1
+        st[0, k] = (y * n + x) | (gate << 8) | ((1 << 9) if k % 17 == 16 else 0)
+        if k % 5 == 3:    # every unknown cell occupied
+            for b in range(nu):
+                st[1 + b // 32, k] |= np.uint32(1 << (b % 32))
+        elif k % 5 == 4:  # every unknown cell free
+            st[1:, k] = 0
+    return st
+
+
+@pytest.mark.parametrize("n,wall_y,gates,goal,landmarks,K,D", [
+    (13, None, (3, 9), None, None, 61, 90),
+    (5, 2, (1, 3), (2, 4), [], 33, 30),
+    (9, 4, (2, 6), (4, 8), [(1, 2), (7, 6)], 40, 50),
+])
+def test_nav_edge_states_match_oracle(n, wall_y, gates, goal, landmarks, K, D):
+    params = inputs.nav_params(n, wall_y=wall_y, gates=gates, landmarks=landmarks, goal=goal, D=D)
+    wy = n // 2 if wall_y is None else wall_y
+    gl = (n // 2, n - 1) if goal is None else goal
+    lm = inputs.NAV_LANDMARKS_13 if landmarks is None else landmarks
+    gm, om = Model("nav", params), oracle.Model("nav", params)
+    st = _nav_edge_belief(K, n, wy, gates, gl, lm, K)
+    w = inputs.weights(K, K + 1, uniform=False)
+    gr, orr = gm.belief_load(st, w, 5 + K), om.belief_load(st, w, 5 + K)
+    G0 = gm.expand([(gr, -1, 0, 0)], record=True)
+    O0 = om.expand([(orr, -1, 0, 0)], record=True)
+    compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
+    assert G0["scenario_steps"] == O0["scenario_steps"]
+    lv = [(a, c) for a in range(gm.A) for c in range(min(2, int(G0["child_begin"][a + 1] - G0["child_begin"][a])))]
+    G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+    O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+    compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
+    assert G1["scenario_steps"] == O1["scenario_steps"]
+    gm.close()
