@@ -616,3 +616,29 @@ def test_car_pedestrian_heads_to_its_goal_on_average():
     # a pedestrian standing on its goal stays there
     s2 = m.step(_car1(0.0, 0, 20.0, 10.0, 3), 0, 0, 1, 9)[0]
     assert (_f(s2[4]), _f(s2[5])) == (20.0, 10.0)
+
+
+def test_mars_joint_sample_same_and_different_rocks():
+    """Two robots (reading R19): a joint action is one sub-action
+    per robot, |A| = (5 + m)^2; on the same good rock the first SAMPLE earns
+    +10 and turns it bad, the second pays -10; on two good rocks +20."""
+    rocks, _ = inputs.rocksample_layout(15, 15, 2, 7)
+    m = oracle.Model("rocksample", inputs.rocksample_params(15, 15, 2))
+    base = 5 + 15
+    samp = 4 + base * 4
+    (x0, y0), (x1, y1) = rocks[0], rocks[1]
+    allgood = (1 << 15) - 1
+    s2, z, r, term, _ = m.step(rs_state(15, allgood, [(x0, y0), (x0, y0)]), samp, 0, 1, 5)
+    assert r == 0.0 and s2[0] == allgood & ~1 and not term
+    s2, z, r, term, _ = m.step(rs_state(15, allgood, [(x0, y0), (x1, y1)]), samp, 0, 1, 5)
+    assert r == 20.0 and s2[0] == allgood & ~0b11
+    # the same rock bad: both pay -10
+    s2, z, r, term, _ = m.step(rs_state(15, allgood & ~1, [(x0, y0), (x0, y0)]), samp, 0, 1, 5)
+    assert r == -20.0
+    # robot 0 exits east (+10, P:530) while robot 1 stays: not terminal; both
+    # exit: terminal with +20
+    east = 2
+    s2, z, r, term, _ = m.step(rs_state(15, 0, [(14, 3), (5, 5)]), east + base * 0, 0, 1, 5)
+    assert r == 10.0 and not term and (int(s2[1]) & 0xFFFF) == 0xFFFF
+    s2, z, r, term, _ = m.step(rs_state(15, 0, [(14, 3), (14, 9)]), east + base * east, 0, 1, 5)
+    assert r == 20.0 and term
