@@ -747,3 +747,37 @@ def test_nav_edge_states_match_oracle(n, wall_y, gates, goal, landmarks, K, D):
     compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
     assert G1["scenario_steps"] == O1["scenario_steps"]
     gm.close()
+
+
+def test_mars_edge_states_match_oracle():
+    """MARS(15,15), 2 robots (card §3.2): robots standing on rocks (both on
+    the same rock too), on the east border, one robot exited, all rocks good
+    or all bad; a leaf's expansion plus depth-1 leaves against the oracle."""
+    n, m, R = 15, 15, 2
+    params = inputs.rocksample_params(n, m, R)
+    rocks, starts = inputs.rocksample_layout(n, m, R, 7)
+    gm, om = Model("rocksample", params), oracle.Model("rocksample", params)
+    K = 70
+    rng = np.random.default_rng(3)
+    st = np.zeros((2, K), np.uint32)
+    for k in range(K):
+        case = k % 7
+        good = [(1 << m) - 1, 0, int(rng.integers(0, 1 << m))][k % 3]
+        j0, j1 = int(rng.integers(0, m)), int(rng.integers(0, m))
+        c = {0: [rocks[j0], rocks[j0]], 1: [rocks[j0], rocks[j1]], 2: [(n - 1, 3), (n - 1, 11)],
+             3: [(-1, -1), rocks[j1]], 4: [rocks[j0], (-1, -1)], 5: [(n - 1, 0), starts[1]],
+             6: [starts[0], starts[1]]}[case]
+        st[0, k] = good
+        st[1, k] = sum((0xFFFF if xy == (-1, -1) else xy[1] * n + xy[0]) << (16 * r) for r, xy in enumerate(c))
+    w = inputs.weights(K, 9, uniform=False)
+    gr, orr = gm.belief_load(st, w, 123), om.belief_load(st, w, 123)
+    G0 = gm.expand([(gr, -1, 0, 0)], record=True)
+    O0 = om.expand([(orr, -1, 0, 0)], record=True)
+    compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
+    assert G0["scenario_steps"] == O0["scenario_steps"]
+    lv = [(a, int(G0["child_begin"][a + 1] - G0["child_begin"][a]) - 1) for a in range(0, gm.A, 23)]
+    G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
+    O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+    compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
+    assert G1["scenario_steps"] == O1["scenario_steps"]
+    gm.close()
