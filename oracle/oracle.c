@@ -801,7 +801,7 @@ int oracle_model_load(const char* kind, const char* params, oracle_model** out) 
       return fail(-1, "car: 1 <= peds <= 31");
     }
     M->p_car_fail = param_d(params, "p_fail", 0.01);
-    M->noise_scale = (float)param_d(params, "noise", 0.00133);
+    M->noise_scale = (float)param_d(params, "noise", 0.001375); /* sd of 2 atan(tau) = pi/8 (card sigma) */
     M->A = 3; M->SW = 4 + 2 * (uint32_t)M->peds; M->OW = 1 + (uint32_t)M->peds; M->slots = 0;
     M->D = (uint32_t)param_i(params, "D", 90);
     M->elements = 1 + (uint32_t)M->peds;

@@ -430,7 +430,7 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     dm.peds = (int)pi(params, "peds", 20);
     if (dm.peds < 1 || dm.peds > kCarMaxPeds) return set_err(DESPOT_EINVAL, "car: 1 <= peds <= 31");
     dm.t_car_fail = thresh(pd(params, "p_fail", 0.01));
-    dm.noise_scale = (float)pd(params, "noise", 0.00133);
+    dm.noise_scale = (float)pd(params, "noise", 0.001375);  // heading sd pi/8 (card §3.4)
     dm.A = 3; dm.SW = 4 + 2 * (uint32_t)dm.peds; dm.OW = 1 + (uint32_t)dm.peds; dm.slots = 0;
     dm.terminal_slot = 0;
     dm.D = (uint32_t)pi(params, "D", 90);
