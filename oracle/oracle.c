@@ -14,12 +14,16 @@
  *
  * Parity status per function (see DESIGN.md §4 for the pins):
  *   philox, thresholds, step/upper/rollout of tiger, rocksample, nav: pinned
- *   (KAT vectors, paper constants, closed forms, brute-force bounds).
+ *   (KAT vectors, paper constants, closed forms, brute-force bounds); the
+ *   default policies and u(s) of rocksample/MARS and nav by hand-traced
+ *   roll-outs, every-branch tables, closed forms and BFS distances
+ *   (tests/test_oracle_pins_policy.py).
  *   car: step rewards (time, brake, collision, goal), speed clamp, u(s),
  *   pi0's gap rule, step length and mean heading are pinned by closed-form
- *   single steps (tests/test_oracle_pins.py, card §3.4); the shape of the
- *   heading noise (tau scale) stays "parity unpinned" (the paper defers the
- *   driving model to Bai 2015, which is not in the reference).
+ *   single steps (tests/test_oracle_pins.py, card §3.4); the heading noise by
+ *   its statistics (mean 0, sd pi/8, reading R21).  Every function is
+ *   pinned; the driving constants themselves are PROPOSED (the paper defers
+ *   the model to Bai 2015, which is not in the reference).
  */
 #include "oracle.h"
 

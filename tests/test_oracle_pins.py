@@ -463,8 +463,9 @@ def test_terminal_start_rollout_and_all_terminal_node():
 
 
 # ----------------------------------------------------------------------------
-# Driving -- invariants; the dynamics beyond these are
-# "parity unpinned" (the paper defers the model to Bai 2015)
+# Driving -- invariants and closed-form single steps (the
+# constants are PROPOSED: the paper defers the model to Bai 2015); the
+# heading-noise statistics are pinned in test_oracle_pins_policy.py
 # ----------------------------------------------------------------------------
 def test_car_pedestrians_move_exactly_one_step_length():
     m = oracle.Model("car", inputs.car_params())
