@@ -1711,6 +1711,8 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
   if (!nd) return set_err(DESPOT_EINVAL, "unknown node");
   if (!upper_mean || !lower_mean) return set_err(DESPOT_EINVAL, "null argument");
   if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
+  // a sharded node holds only this rank's scenarios: its means are not the node's
+  if (m->world > 1) return set_err(DESPOT_EINVAL, "rollout_bounds: world > 1 (sharded node)");
   CU(cudaSetDevice(m->device));
   cudaStream_t st = (cudaStream_t)stream;
   const DevModel& dm = m->host;

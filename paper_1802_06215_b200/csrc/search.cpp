@@ -448,8 +448,10 @@ struct Search {
           nd->depth = b->depth + 1;
           next->node.store(nd);
         }
-        lk.unlock();
+        // the virtual-loss marker (Eq. 8) goes up before the lock is released,
+        // so a worker choosing under the same lock right after sees it
         next->active.fetch_add(1);
+        lk.unlock();
         path.push_back(nd);
         b = nd;
       }

@@ -98,10 +98,23 @@ def run_exchange(model, batch, ex, group=None):
         ex = model.batch_exchange(batch)
 
 
+def _torch_stream(stream, device):
+    """The torch stream object of the batch's stream (None: torch's current
+    stream, which is also what the binding hands the library)."""
+    if stream is None:
+        return torch.cuda.current_stream(device)
+    if isinstance(stream, torch.cuda.Stream):
+        return stream
+    return torch.cuda.ExternalStream(int(getattr(stream, "cuda_stream", stream)), device=device)
+
+
 def expand_sharded(model, leaves, group=None, device_outputs=False, child_capacity=None, stream=None):
     batch, ex = model.expand_begin(leaves, stream=stream)
     try:
-        run_exchange(model, batch, ex, group)
+        # the collectives run on the batch's own stream (ordered after K2 and
+        # before K3; a host backend's staging copies synchronise that stream)
+        with torch.cuda.stream(_torch_stream(stream, torch.device("cuda", model.device))):
+            run_exchange(model, batch, ex, group)
     except Exception:
         model.batch_abort(batch)
         raise

@@ -9,6 +9,7 @@ import socket
 
 import numpy as np
 import pytest
+from parity import compare_batch
 
 pytestmark = pytest.mark.gpu
 
@@ -79,8 +80,33 @@ def test_two_processes_equal_single_gpu():
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
+    orc = _oracle_results()
     for rank, res in got:
         for name in ref:
             for g, r in zip(res[name], ref[name]):
                 for k in KEYS:
                     assert np.array_equal(g[k], r[k]), (rank, name, k)
+            for g, (O, om, A) in zip(res[name], orc[name]):  # and against the oracle directly
+                compare_batch(g, O, _AOnly(A), om, [(i, i) for i in range(len(O["n_scen"]))])
+
+
+class _AOnly:
+    def __init__(self, A):
+        self.A = A
+
+
+def _oracle_results():
+    """The same batches expanded by the CPU oracle (record=True)."""
+    import oracle
+    from paper_1802_06215_b200 import inputs
+    out = {}
+    for name, kind, params, beliefs, mode in _batches():
+        om = oracle.Model(kind, params)
+        roots = [om.belief_load(s, w, sd) for s, w, sd in beliefs]
+        if mode == "roots":
+            out[name] = [(om.expand([(r, -1, 0, 0) for r in roots], record=True), om, om.A)]
+            continue
+        R = om.expand([(roots[0], -1, 0, 0)], record=True)
+        lv = inputs.select_leaves(R["child_count"], R["child_begin"], om.A, 8)
+        out[name] = [(R, om, om.A), (om.expand([(roots[0], a, c, 1) for a, c in lv], record=True), om, om.A)]
+    return out

@@ -119,6 +119,50 @@ def test_config3_nav_64_leaves():
     _full_config(3, sample=(0, 31, -1))
 
 
+def _full_mars(n, m, K=500, L=64, sample=(0, 1, -2, -1)):
+    """MARS(n, m) with two robots at BASELINE's config-2 batch shape (K = 500,
+    64 depth-1 leaves): the paper's own instance MARS(20,20) with |A| = 625
+     and MARS(11,11) with |A| = 256 -- other shared-memory
+    table sizes, range masks and occupancies than the tested (15,15)."""
+    params = inputs.rocksample_params(n, m, 2, D=20)
+    seed = 1002
+    st = inputs.rocksample_belief(n, m, 2, K, seed)
+    w = inputs.weights(K, seed)
+    gm, om = Model("rocksample", params), oracle.Model("rocksample", params)
+    assert gm.A == (5 + m) ** 2
+    gr, orr, G0, O0 = expand_root_both(gm, om, st, w, seed, record=False)
+    compare_batch(G0, O0, gm, om, [(0, 0)])
+    assert G0["scenario_steps"] == O0["scenario_steps"]
+    glv = inputs.select_leaves(G0["child_count"], G0["child_begin"], gm.A, L)
+    assert glv == inputs.select_leaves(O0["child_count"], O0["child_begin"], om.A, L)
+    G = gm.expand([(gr, a, c, 1) for a, c in glv])
+    idx = sorted({s % L for s in sample})
+    O = om.expand([(orr, glv[i][0], glv[i][1], 1) for i in idx], record=True)
+    compare_batch(G, O, gm, om, list(zip(idx, range(len(idx)))))
+    # the timed form (prepared call, pinned host outputs) equals the plain call
+    P = gm.prepare([(gr, a, c, 1) for a, c in glv], pinned=True)
+    gm.run_prepared(P)
+    for k in ("n_scen", "act_upper", "act_lower", "child_begin", "child_count", "child_first", "child_upper",
+              "child_lower"):
+        r = np.asarray(G[k]).reshape(-1)
+        assert np.array_equal(np.asarray(P["o"][k])[: len(r)], r), k
+    gm.close()
+
+
+def test_mars_20_20_paper_instance_64_leaves():
+    _full_mars(20, 20)
+
+
+def test_mars_11_11_64_leaves():
+    _full_mars(11, 11)
+
+
+def test_nav_k5000_64_leaves():
+    """Navigation at K = 5000 (the top of the paper's K sweep): 64
+    depth-1 leaves, three sampled against the oracle."""
+    _full_config(3, K=5000, sample=(0, 31, -1))
+
+
 def test_config5_sweep_k4096_256_leaves():
     mask = np.zeros(400, np.uint8)
     mask[::17] = 1
@@ -416,6 +460,10 @@ def test_fake_ranks_equal_single_gpu():
     R = g1.expand([(r1, -1, 0, 0)])
     lv = inputs.select_leaves(R["child_count"], R["child_begin"], g1.A, L)
     ref = g1.expand([(r1, a, c, 1) for a, c in lv])
+    om = oracle.Model(kind, params)
+    orr = om.belief_load(st, w, seed)
+    O0 = om.expand([(orr, -1, 0, 0)], record=True)
+    O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
     for world in (2, 3, 4, 8):
         ms = [Model(kind, params, rank=r, world=world) for r in range(world)]
         roots = [m.belief_load(st, w, seed) for m in ms]
@@ -442,6 +490,12 @@ def test_fake_ranks_equal_single_gpu():
                       "child_first", "child_weight", "child_upper", "child_lower", "child_obs"):
                 assert np.array_equal(o[k], ref[k]), (world, k)
             assert o["scenario_steps"] == ref["scenario_steps"]
+        # and against the oracle directly: every rank's merged result
+        for o in outs0:
+            compare_batch(o, O0, ms[0], om, [(0, 0)])
+        for o in outs:
+            compare_batch(o, O1, ms[0], om, [(i, i) for i in range(L)])
+            assert o["scenario_steps"] == O1["scenario_steps"]
 
 
 # ----------------------------------------------------------------------------
@@ -633,15 +687,22 @@ def test_car_sharded_equals_single_gpu():
             assert np.array_equal(o[k], ref[k]), (tag, k)
         assert o["scenario_steps"] == ref["scenario_steps"], tag
 
+    om = oracle.Model("car", params)
+    ors = [om.belief_load(s, w_, sd) for s, w_, sd in croots]
+    O0 = om.expand([(r, -1, 0, 0) for r in ors], record=True)
+    O1 = om.expand([(ors[0], a, c, 1) for a, c in lv], record=True)
     for world in (2, 3, 4):
         ms = [Model("car", params, rank=r, world=world) for r in range(world)]
         roots = [[m.belief_load(s, w_, sd) for s, w_, sd in croots] for m in ms]
         for o in _emulate_ranks(ms, [[(r, -1, 0, 0) for r in rt] for rt in roots]):
             same(o, ref0, (world, "roots"))
+            compare_batch(o, O0, ms[0], om, [(i, i) for i in range(len(croots))])  # and the oracle directly
         for o in _emulate_ranks(ms, [[(rt[0], -1, 0, 0)] for rt in roots]):
             same(o, R, (world, "root 0"))
         for o in _emulate_ranks(ms, [[(rt[0], a, c, 1) for a, c in lv] for rt in roots]):
             same(o, ref1, (world, "children"))
+            compare_batch(o, O1, ms[0], om, [(i, i) for i in range(len(lv))])
+            assert o["scenario_steps"] == O1["scenario_steps"]
 
 
 def test_gpu_scenario_prefix_is_stable_across_K():
@@ -653,6 +714,22 @@ def test_gpu_scenario_prefix_is_stable_across_K():
         sb, ss = slice(a * 80, a * 80 + 50), slice(a * 50, a * 50 + 50)
         for k in ("scen_obs", "scen_reward", "scen_len", "scen_hash", "scen_states", "scen_upper", "scen_lower"):
             assert np.array_equal(big[k][sb], small[k][ss]), k
+
+
+AGG_KEYS = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count", "child_first",
+            "child_weight", "child_upper", "child_lower", "child_obs")
+
+
+def _timed_form_equals_record(gm, leaves, Grec):
+    """The same leaves through the timed kernels (record=False: UNI_SEED round
+    keys, the dynamic tile grid, the finalize fused into K2's last CTA or the
+    grouped / wide / sparse K3 variants) give the record run's aggregates bit
+    for bit -- and so the oracle's."""
+    G = gm.expand(leaves)
+    for k in AGG_KEYS:
+        assert np.array_equal(np.asarray(G[k]), np.asarray(Grec[k])), k
+    assert G["scenario_steps"] == Grec["scenario_steps"]
+    gm.node_release_many([n for lf, n in zip(leaves, G["node"]) if lf[1] >= 0])
 
 
 def _car_edge_belief(K, peds=2):
@@ -693,11 +770,13 @@ def test_car_edge_states_match_oracle(grouped):
         O0 = om.expand([(orr, -1, 0, 0)], record=True)
         compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
         assert G0["scenario_steps"] == O0["scenario_steps"]
+        _timed_form_equals_record(gm, [(gr, -1, 0, 0)], G0)
         lv = [(a, c) for a in range(3) for c in range(min(4, int(G0["child_begin"][a + 1] - G0["child_begin"][a])))]
         G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
         O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
         compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
         assert G1["scenario_steps"] == O1["scenario_steps"]
+        _timed_form_equals_record(gm, [(gr, a, c, 1) for a, c in lv], G1)
 
 
 # ----------------------------------------------------------------------------
@@ -741,11 +820,13 @@ def test_nav_edge_states_match_oracle(n, wall_y, gates, goal, landmarks, K, D):
     O0 = om.expand([(orr, -1, 0, 0)], record=True)
     compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
     assert G0["scenario_steps"] == O0["scenario_steps"]
+    _timed_form_equals_record(gm, [(gr, -1, 0, 0)], G0)
     lv = [(a, c) for a in range(gm.A) for c in range(min(2, int(G0["child_begin"][a + 1] - G0["child_begin"][a])))]
     G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
     O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
     compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
     assert G1["scenario_steps"] == O1["scenario_steps"]
+    _timed_form_equals_record(gm, [(gr, a, c, 1) for a, c in lv], G1)
     gm.close()
 
 
@@ -775,9 +856,11 @@ def test_mars_edge_states_match_oracle():
     O0 = om.expand([(orr, -1, 0, 0)], record=True)
     compare_batch(G0, O0, gm, om, [(0, 0)], check_scen=True)
     assert G0["scenario_steps"] == O0["scenario_steps"]
+    _timed_form_equals_record(gm, [(gr, -1, 0, 0)], G0)
     lv = [(a, int(G0["child_begin"][a + 1] - G0["child_begin"][a]) - 1) for a in range(0, gm.A, 23)]
     G1 = gm.expand([(gr, a, c, 1) for a, c in lv], record=True)
     O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
     compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))], check_scen=True)
     assert G1["scenario_steps"] == O1["scenario_steps"]
+    _timed_form_equals_record(gm, [(gr, a, c, 1) for a, c in lv], G1)
     gm.close()
