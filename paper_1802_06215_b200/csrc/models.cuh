@@ -124,16 +124,24 @@ struct RockSample {
     int32_t n, m, mm, base, ncell, exitc;  // exitc = EXIT pseudo-cell = n*n; mm = max(m, 1)
     uint32_t D;
     double tail;
-    uint8_t senseb[32];      // policy position p -> SENSE sub-action 5 + rock(p); [m] = E (nothing open)
-    uint32_t none_bit;       // 1 << m: __ffs(open | none_bit) - 1 = m when nothing is open
-    uint32_t range_mask[2];  // policy positions of robot r (0 for the always-east policy)
+    // Default-policy columns: robot r walks its handled rocks in order (x, y, j)
+    // through the columns q = qstart[r] .. qstart[r] + k_r - 1, then stays on
+    // its sentinel column qstart[r] + k_r (nothing left: E).  A robot only
+    // ever marks its current target (GOOD after a GOOD reading; DONE after a
+    // BAD reading or a SAMPLE), so the card's per-rock memory is exactly a
+    // column index plus one "target known GOOD" bit per robot.
+    uint8_t senseb[40];      // column q -> SENSE sub-action 5 + rock(q); a sentinel column -> E
+    uint32_t qstart[2];      // first column of robot r
+    uint32_t polw;           // columns per cell row of the pol table (m + 2)
     // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m, D):
     uint32_t off_act;   // u16 [cell][base]: the effect of sub-action b on a robot at the cell:
                         // bits 0-10 the next cell (EXIT pseudo-cell included), bit 15 the +10
                         // exit, bit 14 SAMPLE on a rock, bit 13 SENSE (not from EXIT)
     uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
     uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
-    uint32_t off_pol;   // u8  [cell][m+1]: policy move toward the rock of position p (4 = on it); [m] = E
+    uint32_t off_pol;   // u8  [cell][m+2]: policy move toward the rock of column q (4 = on it); sentinels
+                        // E; row n*n+1 (the SENSE row) holds senseb: the sub-action of a robot whose
+                        // target is not known GOOD
     uint32_t off_dist;  // u8  [cell][mm]: |x - x_j| + |y - y_j| (255 from EXIT)
     uint32_t off_gp;    // f64 [G]: gamma^k;  off_gp10: f64 [G]: 10 gamma^k (G = max(D, 2n) + 1)
     uint32_t off_gp10;
@@ -143,7 +151,7 @@ struct RockSample {
   // table bytes (host and device agree): act | info | thr | pol | dist | gp | gp10, with the EXIT row
   static __host__ __device__ size_t table_bytes(int n, int m, uint32_t D) {
     const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
-    return align16(2 * c * (5 + m)) + align16(4 * c) + align16(4 * c * mm) + align16(c * (m + 1)) +
+    return align16((c + 1) * (m + 2)) + align16(2 * c * (5 + m)) + align16(4 * c) + align16(4 * c * mm) +
            align16(c * mm) + align16(8 * G) + align16(8 * G);
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
@@ -155,8 +163,10 @@ struct RockSample {
   static __device__ __forceinline__ uint32_t thr(const Sm& sm, int c, int j) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + j];
   }
-  static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int p) {
-    return hd_dyn_smem[sm.off_pol + c * (sm.m + 1) + p];
+  // the pol table is the first table: its offset is a compile-time constant
+  static constexpr uint32_t kOffPol = (uint32_t)align16(sizeof(Sm));
+  static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int q) {
+    return hd_dyn_smem[kOffPol + c * sm.polw + q];
   }
   static __device__ __forceinline__ const uint8_t* dist_row(const Sm& sm, int c) {
     return hd_dyn_smem + sm.off_dist + c * sm.mm;
@@ -169,11 +179,11 @@ struct RockSample {
   }
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc, G = gpow_len(n, dm.D);
-    const uint32_t base = (uint32_t)align16(sizeof(Sm));
-    const uint32_t off_act = base, off_info = off_act + (uint32_t)align16(2 * (size_t)(nc + 1) * dm.base),
+    const uint32_t polw = (uint32_t)dm.m + 2;
+    const uint32_t off_pol = kOffPol, off_act = off_pol + (uint32_t)align16((size_t)(nc + 2) * polw),
+                   off_info = off_act + (uint32_t)align16(2 * (size_t)(nc + 1) * dm.base),
                    off_thr = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
-                   off_pol = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
-                   off_dist = off_pol + (uint32_t)align16((size_t)(nc + 1) * (dm.m + 1)),
+                   off_dist = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
                    off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * mm),
                    off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
     uint16_t* t_act = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_act);
@@ -191,7 +201,7 @@ struct RockSample {
       sm.off_dist = off_dist;
       sm.off_gp = off_gp;
       sm.off_gp10 = off_gp10;
-      sm.none_bit = 1u << dm.m;
+      sm.polw = polw;
       sm.n = n;
       sm.m = dm.m;
       sm.mm = mm;
@@ -200,10 +210,22 @@ struct RockSample {
       sm.exitc = exitc;
       sm.D = dm.D;
       sm.tail = dm.tail;
-      sm.range_mask[0] = dm.range_mask[0];
-      sm.range_mask[1] = dm.range_mask[1];
+      const uint32_t k0 = (uint32_t)__popc(dm.range_mask[0]);
+      sm.qstart[0] = 0;
+      sm.qstart[1] = k0 + 1;
     }
-    if (tid < 32) sm.senseb[tid] = tid < dm.m ? (uint8_t)(5 + dm.pos_rock[tid]) : (uint8_t)2;
+    // column q -> policy position (rocks sorted by handling robot, then (x, y, j)) or a sentinel
+    const int k0 = __popc(dm.range_mask[0]), k1 = __popc(dm.range_mask[1]);
+    auto col_pos = [&](int q) -> int {
+      if (q < k0) return q;                       // robot 0's positions 0 .. k0-1
+      if (q == k0) return -1;                     // robot 0's sentinel
+      if (q - 1 < k0 + k1) return q - 1;          // robot 1's positions k0 .. k0+k1-1
+      return -1;                                  // robot 1's sentinel (and unused columns)
+    };
+    for (int q = tid; q < 40; q += nt) {
+      const int p = q < (int)polw ? col_pos(q) : -1;
+      sm.senseb[q] = p >= 0 ? (uint8_t)(5 + dm.pos_rock[p]) : (uint8_t)2;
+    }
     for (int k = tid; k < G; k += nt) {
       t_gp[k] = dm.gpow[k];
       t_gp10[k] = 10.0 * dm.gpow[k];  // the product upper() used to form per rock
@@ -238,10 +260,12 @@ struct RockSample {
       }
       t_thr[e] = t;
     }
-    for (int e = tid; e < (nc + 1) * (dm.m + 1); e += nt) {
-      const int c = e / (dm.m + 1), p = e - c * (dm.m + 1);
-      uint8_t v = 2;  // E: nothing open (p = m), or the EXIT pseudo-cell
-      if (c < nc && p < dm.m) {
+    for (int e = tid; e < (nc + 2) * (int)polw; e += nt) {
+      const int c = e / (int)polw, p = col_pos(e - c * (int)polw);
+      uint8_t v = 2;  // E: a sentinel column (nothing left), or the EXIT pseudo-cell
+      if (c == nc + 1) {
+        v = p >= 0 ? (uint8_t)(5 + dm.pos_rock[p]) : (uint8_t)2;  // the SENSE row
+      } else if (c < nc && p >= 0) {
         const int j = dm.pos_rock[p];
         const int dx = dm.rx[j] - c % n, dy = dm.ry[j] - c / n;
         // E if x < tx, W if x > tx, S if y < ty, N if y > ty, on the rock: SAMPLE
@@ -290,7 +314,7 @@ struct RockSample {
   // 1 GOOD, 2 BAD).  Rewards are integers (exact in fp32).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
                                                   uint32_t& z, float& rew, uint32_t* zrs = nullptr,
-                                                  int* irew = nullptr) {
+                                                  int* irew = nullptr, uint32_t* smps = nullptr) {
     int reward = 0;
     uint32_t zsum = 0;
 #pragma unroll
@@ -315,6 +339,7 @@ struct RockSample {
       s.good &= ~(gbit << jr);
       s.cell[r] = (int)(e & kActCell);
       if (zrs) zrs[r] = zr;
+      if (smps) smps[r] = samp;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
     rew = (float)reward;
@@ -361,39 +386,42 @@ struct RockSample {
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
 
-  // default policy (card §3.2), branch-free: memory over policy positions p
-  // (rocks sorted by handling robot, then (x, y, j)); done bit = DONE, gm bit
-  // = GOOD.  Robot r targets its first open position p: a known-GOOD rock is
-  // approached (the table's move; SAMPLE on it), an unknown one is sensed;
-  // nothing open: E.  tbit = the target's bit (0 when nothing is open).  An
-  // exited robot's sub-action is immaterial (every action is a no-op at
-  // EXIT, the table gives E there, never SAMPLE); TRACE reports E for it.
+  // default policy (card §3.2), branch-free.  Robot r's memory is its column
+  // q[r] (its current target rock, or its sentinel) and tg[r] bit 0 (the
+  // target read GOOD): a known-GOOD target is approached (the table's move;
+  // SAMPLE on it), an unknown one is sensed; at the sentinel: E.  An exited
+  // robot's sub-action is immaterial (every action is a no-op at EXIT, the
+  // table gives E there, never SAMPLE); TRACE reports E for it.
+  // One table read per robot: row = the robot's cell when its target is
+  // known GOOD, else the SENSE row.
   template <bool TRACE = false>
-  static __device__ __forceinline__ void policy(const Sm& sm, const St& s, uint32_t done, uint32_t gm,
-                                                int* b, uint32_t* tbit) {
+  static __device__ __forceinline__ void policy(const Sm& sm, const St& s, const uint32_t* q, const uint32_t* tg,
+                                                int* b, uint32_t polw, int sense_row) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const uint32_t open = ~done & sm.range_mask[r];
-      const int p = __ffs(open | sm.none_bit) - 1;  // m when nothing is open
-      const uint32_t tb = open & (0u - open);        // lowest open bit, 0 when none
-      const int mv = (int)pol(sm, s.cell[r], p);
-      const int sn = (int)sm.senseb[p];
-      b[r] = (gm & tb) ? mv : sn;
+      const int row = (tg[r] & 1u) ? s.cell[r] : sense_row;
+      b[r] = (int)hd_dyn_smem[kOffPol + (uint32_t)row * polw + q[r]];
       if (TRACE && exited(sm, s, r)) b[r] = 2;
-      tbit[r] = tb;
     }
   }
   template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
                                  const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
-    uint32_t done = 0, gm = 0;
+    uint32_t q[R], tg[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      q[r] = sm.qstart[r];
+      tg[r] = 0;
+    }
+    const double* gpk = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp);  // gamma^(t - t0)
+    const uint32_t polw = sm.polw;
+    const int sense_row = sm.exitc + 1;
     uint32_t t = t0;
     bool term = false;
     while (t < sm.D && !term) {
       int b[R];
-      uint32_t tb[R];
-      policy<TRACE>(sm, s, done, gm, b, tb);
+      policy<TRACE>(sm, s, q, tg, b, polw, sense_row);
       if (TRACE) {
         int a = 0, mul = 1;
 #pragma unroll
@@ -407,19 +435,19 @@ struct RockSample {
       const uint32_t u[2] = {w.x, w.y};
       float r;
       int ir;
-      uint32_t zr[R];
-      term = step_sub(sm, s, b, u, z, r, zr, &ir);
-      // policy memory: a GOOD reading marks the rock GOOD, a BAD one DONE; a
-      // sample marks it DONE
+      uint32_t zr[R], smp[R];
+      term = step_sub(sm, s, b, u, z, r, zr, &ir, smp);
+      // memory: a GOOD reading marks the target GOOD; a BAD reading or a
+      // SAMPLE (only ever of the target) marks it DONE: next column
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        gm |= tb[q] & (0u - (zr[q] & 1u));
-        done |= ((zr[q] >> 1) | (uint32_t)(b[q] == 4)) ? tb[q] : 0u;
+      for (int k = 0; k < R; ++k) {
+        q[k] += (zr[k] >> 1) | smp[k];
+        tg[k] = (tg[k] | zr[k]) & ~smp[k];
       }
-      acc += gp(sm, (int)(t - t0)) * (double)ir;
+      acc = __fma_rn(*gpk++, (double)ir, acc);
       ++t;
     }
-    if (!term) acc += gp(sm, (int)(t - t0)) * sm.tail;
+    if (!term) acc = __fma_rn(*gpk, sm.tail, acc);
     ret = acc;
     len = t - t0;
   }
