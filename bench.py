@@ -35,24 +35,40 @@ sys.path.insert(0, ROOT)
 
 from paper_1802_06215_b200 import inputs  # noqa: E402
 
-# thread-instructions per scenario-step of K2 (the "algorithmic" instruction
-# work of one step as implemented), from the ncu profile of round 1, see
-# DESIGN.md §7.  Used for the ALU roofline: achieved = I_step * steps / t_K2.
-# per config (ncu smsp__thread_inst_executed.sum / scenario-steps, round 1):
-# config 2/5 MARS 241, config 3 navigation 303, config 4 driving (thread per
-# scenario) 2054; config 1 RockSample(7,8) 177.
-I_STEP = {1: 177.0, 2: 223.0, 3: 303.0, 4: 2054.0, 5: 223.0}
+# Algorithmic work per scenario-step (thread-instructions), SURVEY.md §8(d)
+# "Algorithmic work per scenario-step": RockSample ~125, MARS ~175,
+# navigation ~300, driving (20 pedestrians) ~1,300.  The roofline's
+# `achieved` uses these fixed per-unit figures (not the kernel's own
+# instruction count, which would credit overhead instructions); the measured
+# count of the kernel as built is reported beside it (i_step_measured).
+I_STEP_ALGO = {1: 125.0, 2: 175.0, 3: 300.0, 4: 1300.0, 5: 175.0}
 
 
 def i_step(config):
-    """thread-instructions per scenario-step of K2 for this config: the
-    committed measurement (scripts/measure_istep.py -> profiles/r01/i_step.json)
-    if present, else the table above."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "i_step.json")) as f:
-            return float(json.load(f)[str(config)]["i_step"]), "profiles/r01/i_step.json"
-    except Exception:
-        return I_STEP[config], "bench.py I_STEP"
+    """(algorithmic thread-instructions per scenario-step, source)"""
+    return I_STEP_ALGO[config], "SURVEY.md §8(d) per-unit figure"
+
+
+def i_step_measured(config):
+    """thread-instructions per scenario-step of K2 as built (ncu
+    smsp__thread_inst_executed.sum / scenario-steps, scripts/measure_istep.py),
+    newest round first; None if never measured"""
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "i_step.json")) as f:
+                return float(json.load(f)[str(config)]["i_step"]), f"profiles/{rnd}/i_step.json"
+        except Exception:
+            continue
+    return None, None
+
+
+def _profile_file(name):
+    """newest committed profile file of that name (profiles/r02, else r01)"""
+    for rnd in ("r02", "r01"):
+        p = os.path.join(ROOT, "profiles", rnd, name)
+        if os.path.exists(p):
+            return p
+    return os.path.join(ROOT, "profiles", "r01", name)
 
 
 def ncu_traffic(config):
@@ -60,7 +76,7 @@ def ncu_traffic(config):
     per launch, from the committed `ncu --set full` raw page of this config
     (profiles/r01/k2_config<C>_raw.csv); None if there is none."""
     import csv
-    p = os.path.join(ROOT, "profiles", "r01", f"k2_config{config}_raw.csv")
+    p = _profile_file(f"k2_config{config}_raw.csv")
     try:
         rows = list(csv.reader(open(p)))
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -87,7 +103,7 @@ def ncu_k2_summary(config):
     """The per-pipe picture of the dominant kernel from the same committed
     `ncu --set full` raw page as `traffic` (SURVEY §8(d) metric list)."""
     import csv
-    p = os.path.join(ROOT, "profiles", "r01", f"k2_config{config}_raw.csv")
+    p = _profile_file(f"k2_config{config}_raw.csv")
     try:
         rows = list(csv.reader(open(p)))
         out = {}
@@ -681,7 +697,9 @@ def main():
                          if traffic else None,
                          "note": f"issue-slot peak {num_sms} SM x 4 SMSP x 32 lanes x {sm_clock} MHz "
                                  f"({peak_src} sm_max_mhz); achieved = {istep:.1f} thread-instr per "
-                                 f"scenario-step ({istep_src}, DESIGN.md §7.1) x steps / live K2 event time"},
+                                 f"scenario-step ({istep_src}, DESIGN.md §7.1) x steps / live K2 event time",
+                         "i_step_measured": {"thread_instr_per_step": i_step_measured(args.config)[0],
+                                             "source": i_step_measured(args.config)[1]}},
             "e2e": {"value": e2e_steps / (e2e_ms / 1e3), "unit": "scenario-steps/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms / e2e_n,
                     "wall_ms_per_step": 1e3 * e2e_wall / e2e_n},

@@ -135,9 +135,10 @@ struct RockSample {
     uint32_t polw;           // columns per cell row of the pol table (m + 2)
     // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m, D):
     uint32_t off_act;   // u16 [cell][base]: the effect of sub-action b on a robot at the cell:
-                        // bits 0-10 the next cell (EXIT pseudo-cell included), bit 15 the +10
-                        // exit, bit 14 SAMPLE on a rock, bit 13 SENSE (not from EXIT)
+                        // bit 0 SENSE (not from EXIT), bit 1 SAMPLE on a rock, bit 2 the +10
+                        // exit, bits 3-15 the next cell (EXIT pseudo-cell included)
     uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
+    uint32_t off_rock;  // u8  [cell]: the rock on the cell (0 if none; only read with SAMPLE's flag)
     uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
     uint32_t off_pol;   // u8  [cell][m+2]: policy move toward the rock of column q (4 = on it); sentinels
                         // E; row n*n+1 (the SENSE row) holds senseb: the sub-action of a robot whose
@@ -147,12 +148,13 @@ struct RockSample {
     uint32_t off_gp10;
   };
   static __host__ __device__ int gpow_len(int n, uint32_t D) { return (int)(D > (uint32_t)(2 * n) ? D : 2 * n) + 1; }
-  static constexpr uint32_t kActExit = 0x8000u, kActSample = 0x4000u, kActSense = 0x2000u, kActCell = 0x7FFu;
-  // table bytes (host and device agree): act | info | thr | pol | dist | gp | gp10, with the EXIT row
+  static constexpr uint32_t kActSense = 1u, kActSample = 2u, kActExit = 4u, kActShift = 3u;
+  // table bytes (host and device agree): pol | act | info | rock | thr | dist | gp | gp10, with the
+  // EXIT row (and pol's SENSE row)
   static __host__ __device__ size_t table_bytes(int n, int m, uint32_t D) {
     const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
-    return align16((c + 1) * (m + 2)) + align16(2 * c * (5 + m)) + align16(4 * c) + align16(4 * c * mm) +
-           align16(c * mm) + align16(8 * G) + align16(8 * G);
+    return align16((c + 1) * (m + 2)) + align16(2 * c * (5 + m)) + align16(4 * c) + align16(c) +
+           align16(4 * c * mm) + align16(c * mm) + align16(8 * G) + align16(8 * G);
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
@@ -160,9 +162,13 @@ struct RockSample {
   static __device__ __forceinline__ uint32_t act(const Sm& sm, int c, int sub) {
     return reinterpret_cast<const uint16_t*>(hd_dyn_smem + sm.off_act)[c * sm.base + sub];
   }
-  static __device__ __forceinline__ uint32_t thr(const Sm& sm, int c, int j) {
-    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + j];
+  // the threshold of SENSE sub-action `sub` (rock sub - 5) from cell c.  For
+  // sub < 5 the index falls on the previous row's entries or, at c = 0, on the
+  // rock table in front of the thr table: a harmless value the SENSE flag masks.
+  static __device__ __forceinline__ uint32_t thr_sub(const Sm& sm, int c, int sub) {
+    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_thr)[c * sm.mm + sub - 5];
   }
+  static __device__ __forceinline__ uint32_t rock_on(const Sm& sm, int c) { return hd_dyn_smem[sm.off_rock + c]; }
   // the pol table is the first table: its offset is a compile-time constant
   static constexpr uint32_t kOffPol = (uint32_t)align16(sizeof(Sm));
   static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int q) {
@@ -182,12 +188,14 @@ struct RockSample {
     const uint32_t polw = (uint32_t)dm.m + 2;
     const uint32_t off_pol = kOffPol, off_act = off_pol + (uint32_t)align16((size_t)(nc + 2) * polw),
                    off_info = off_act + (uint32_t)align16(2 * (size_t)(nc + 1) * dm.base),
-                   off_thr = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
+                   off_rock = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
+                   off_thr = off_rock + (uint32_t)align16((size_t)(nc + 1)),
                    off_dist = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
                    off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * mm),
                    off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
     uint16_t* t_act = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_act);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
+    uint8_t* t_rock = hd_dyn_smem + off_rock;
     uint32_t* t_thr = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_thr);
     uint8_t* t_pol = hd_dyn_smem + off_pol;
     uint8_t* t_dist = hd_dyn_smem + off_dist;
@@ -196,6 +204,7 @@ struct RockSample {
     if (tid == 0) {
       sm.off_act = off_act;
       sm.off_info = off_info;
+      sm.off_rock = off_rock;
       sm.off_thr = off_thr;
       sm.off_pol = off_pol;
       sm.off_dist = off_dist;
@@ -237,19 +246,23 @@ struct RockSample {
     for (int c = tid; c <= nc; c += nt) {
       uint16_t* row = t_act + (size_t)c * dm.base;
       if (c == exitc) {  // the pseudo-cell: every sub-action is a no-op, no rock
-        for (int k = 0; k < dm.base; ++k) row[k] = (uint16_t)exitc;
+        for (int k = 0; k < dm.base; ++k) row[k] = (uint16_t)(exitc << kActShift);
         t_info[c] = 0;
+        t_rock[c] = 0;
         continue;
       }
       const int x = c % n, y = c / n;
       const int8_t rock = dm.rock_at[c];
-      row[0] = (uint16_t)(y > 0 ? c - n : c);                                     // N
-      row[1] = (uint16_t)(y < n - 1 ? c + n : c);                                 // S
-      row[2] = (uint16_t)(x < n - 1 ? c + 1 : (int)(kActExit | exitc));           // E (exit)
-      row[3] = (uint16_t)(x > 0 ? c - 1 : c);                                     // W
-      row[4] = (uint16_t)(c | (rock >= 0 ? kActSample : 0u));                     // SAMPLE
-      for (int k = 5; k < dm.base; ++k) row[k] = (uint16_t)(c | kActSense);       // SENSE k - 5
+      const uint32_t sc = (uint32_t)c << kActShift;
+      row[0] = (uint16_t)((uint32_t)(y > 0 ? c - n : c) << kActShift);                 // N
+      row[1] = (uint16_t)((uint32_t)(y < n - 1 ? c + n : c) << kActShift);             // S
+      row[2] = (uint16_t)(x < n - 1 ? (uint32_t)(c + 1) << kActShift
+                                    : ((uint32_t)exitc << kActShift) | kActExit);      // E (exit)
+      row[3] = (uint16_t)((uint32_t)(x > 0 ? c - 1 : c) << kActShift);                 // W
+      row[4] = (uint16_t)(sc | (rock >= 0 ? kActSample : 0u));                         // SAMPLE
+      for (int k = 5; k < dm.base; ++k) row[k] = (uint16_t)(sc | kActSense);           // SENSE k - 5
       t_info[c] = (rock >= 0 ? ((uint32_t)rock | 32u) : 0u) | ((uint32_t)x << 8) | ((uint32_t)y << 16);
+      t_rock[c] = rock >= 0 ? (uint8_t)rock : (uint8_t)0;
     }
     for (int e = tid; e < (nc + 1) * mm; e += nt) {
       const int c = e / mm, j = e - c * mm;
@@ -314,36 +327,34 @@ struct RockSample {
   // 1 GOOD, 2 BAD).  Rewards are integers (exact in fp32).
   static __device__ __forceinline__ bool step_sub(const Sm& sm, St& s, const int* b, const uint32_t* u,
                                                   uint32_t& z, float& rew, uint32_t* zrs = nullptr,
-                                                  int* irew = nullptr, uint32_t* smps = nullptr) {
-    int reward = 0;
+                                                  int* k10 = nullptr, uint32_t* smps = nullptr) {
+    int k = 0;  // the step's reward / 10: exits +1, good samples +1, bad samples -1
     uint32_t zsum = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int sub = b[r];
       const int c = s.cell[r];
-      // the (cell, sub-action) entry: next cell (a move's target, itself
-      // when blocked or not moving, EXIT through the east border) and flags
+      // the (cell, sub-action) entry: flags and the next cell (a move's
+      // target, itself when blocked or not moving, EXIT through the east border)
       const uint32_t e = act(sm, c, sub);
       // SAMPLE on the current cell's rock
-      const uint32_t jr = info(sm, c) & 31u;
-      const uint32_t samp = (e & kActSample) ? 1u : 0u;
+      const uint32_t jr = rock_on(sm, c);
+      const uint32_t samp = (e >> 1) & 1u;
       const uint32_t gbit = samp & (s.good >> jr);
-      // SENSE j (evaluated for every lane; masked; none from EXIT)
-      const int js = max(sub - 5, 0);
-      const uint32_t incorrect = u[r] > thr(sm, c, js) ? 1u : 0u;
-      const uint32_t isgood = (s.good >> js) & 1u;
-      const uint32_t sense = (e & kActSense) ? 1u : 0u;
-      const uint32_t zr = sense * (2u - (isgood ^ incorrect));  // GOOD (1) iff good == correct
-      reward += (e & kActExit) ? 10 : 0;
-      reward += (int)samp * (20 * (int)gbit - 10);
+      // SENSE rock sub - 5 (evaluated for every lane; masked; none from EXIT);
+      // for sub < 5 the shift count wraps and the clamped funnel shift gives 0
+      const uint32_t incorrect = u[r] > thr_sub(sm, c, sub) ? 1u : 0u;
+      const uint32_t isgood = __funnelshift_rc(s.good, 0u, (uint32_t)sub - 5u) & 1u;
+      const uint32_t zr = (e & kActSense) ? 2u - (isgood ^ incorrect) : 0u;  // GOOD (1) iff good == correct
+      k += (int)((e >> 2) & 1u) + 2 * (int)gbit - (int)samp;
       s.good &= ~(gbit << jr);
-      s.cell[r] = (int)(e & kActCell);
+      s.cell[r] = (int)(e >> kActShift);
       if (zrs) zrs[r] = zr;
       if (smps) smps[r] = samp;
       zsum += zr * (r == 0 ? 1u : 3u);
     }
-    rew = (float)reward;
-    if (irew) *irew = reward;  // the roll-out converts the integer straight to double (same value)
+    rew = (float)(10 * k);
+    if (k10) *k10 = k;
     const bool term = terminal(sm, s);
     z = term ? kTerminalObs : zsum;
     return term;
@@ -414,7 +425,7 @@ struct RockSample {
       q[r] = sm.qstart[r];
       tg[r] = 0;
     }
-    const double* gpk = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp);  // gamma^(t - t0)
+    const double* gpk = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10);  // 10 gamma^(t - t0)
     const uint32_t polw = sm.polw;
     const int sense_row = sm.exitc + 1;
     uint32_t t = t0;
@@ -434,9 +445,9 @@ struct RockSample {
       const uint4 w = philox(id, t + 1, 0u, 0u, key);
       const uint32_t u[2] = {w.x, w.y};
       float r;
-      int ir;
+      int k10;
       uint32_t zr[R], smp[R];
-      term = step_sub(sm, s, b, u, z, r, zr, &ir, smp);
+      term = step_sub(sm, s, b, u, z, r, zr, &k10, smp);
       // memory: a GOOD reading marks the target GOOD; a BAD reading or a
       // SAMPLE (only ever of the target) marks it DONE: next column
 #pragma unroll
@@ -444,10 +455,10 @@ struct RockSample {
         q[k] += (zr[k] >> 1) | smp[k];
         tg[k] = (tg[k] | zr[k]) & ~smp[k];
       }
-      acc = __fma_rn(*gpk++, (double)ir, acc);
+      acc = __fma_rn(*gpk++, (double)k10, acc);  // + gamma^(t - t0) r, r = 10 k10
       ++t;
     }
-    if (!term) acc = __fma_rn(*gpk, sm.tail, acc);
+    if (!term) acc = __fma_rn(gp(sm, (int)(t - t0)), sm.tail, acc);
     ret = acc;
     len = t - t0;
   }

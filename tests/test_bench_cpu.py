@@ -16,7 +16,9 @@ import bench  # noqa: E402
 @pytest.mark.parametrize("config", [2, 3, 4])
 def test_roofline_inputs_from_the_committed_profiles(config):
     istep, src = bench.i_step(config)
-    assert src == "profiles/r01/i_step.json" and 100.0 < istep < 5000.0
+    assert "SURVEY" in src and istep == {2: 175.0, 3: 300.0, 4: 1300.0}[config]  # §8(d)'s per-unit figures
+    im, isrc = bench.i_step_measured(config)
+    assert isrc.startswith("profiles/") and 100.0 < im < 5000.0
     tr = bench.ncu_traffic(config)
     assert tr is not None and tr["bytes_per_launch"] > 0
     s = bench.ncu_k2_summary(config)
