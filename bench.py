@@ -501,7 +501,13 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
     c, kind, params, st, w, seed, L = workload(args.config, args.K, args.peds)
     mflags = {"auto": 0, "thread": 1, "warp": 2, "group": 4}[args.car_variant]
-    model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags)
+    comm = None
+    if world > 1 and not one_gpu_test:
+        # the library's own NCCL communicator (rank 0's unique id over the
+        # process group): every batch runs its exchange inside the call
+        from paper_1802_06215_b200.dist import init_comm
+        comm = init_comm(device=local)
+    model = Model(kind, params, device=local, rank=rank, world=world, flags=mflags, comm=comm)
     stream = torch.cuda.Stream(dev)  # a non-blocking stream of our own (not the legacy default stream)
     torch.cuda.set_stream(stream)
     if kind == "car":
@@ -530,10 +536,10 @@ def main():
     preps = {}
 
     def one_step(outputs, device_outputs, timing=True):
-        if world > 1:
+        if one_gpu_test:  # caller-driven exchange over gloo (functional test only)
             from paper_1802_06215_b200.dist import run_exchange
             b, ex = model.expand_begin(leaves, timing=timing)
-            run_exchange(model, b, ex)  # one round (dense keys) or two (sparse: + record all-gather)
+            run_exchange(model, b, ex)  # one round of in-place collectives
             o = model.expand_end(b, leaves, device_outputs=device_outputs, timing=timing, outputs=outputs)
             nodes = o["node"]
         else:
@@ -545,7 +551,9 @@ def main():
             steps, launches, nodes = model.run_prepared(prep, stream=stream)
             E = prep["E"]
             o = {"scenario_steps": steps, "launches": launches, "phase_ms": list(E.phase_ms),
-                 "num_children": E.num_children, "h2d_bytes": int(E.h2d_bytes), "d2h_bytes": int(E.d2h_bytes)}
+                 "num_children": E.num_children, "h2d_bytes": int(E.h2d_bytes), "d2h_bytes": int(E.d2h_bytes),
+                 "exchange_ms": float(E.exchange_ms), "exchange_rounds": int(E.exchange_rounds),
+                 "exchange_bytes": int(E.exchange_bytes)}
         o["new_nodes"] = [n for (lf, n) in zip(leaves, nodes) if lf[1] >= 0]  # self leaves return their own node
         return o
 
@@ -571,6 +579,8 @@ def main():
         release(o)
     k1_ph = float(np.mean([o["phase_ms"][0] for o in ph]))
     k3_ph = float(np.mean([o["phase_ms"][2] for o in ph]))
+    k4_ph = float(np.mean([o.get("exchange_ms", 0.0) for o in ph]))  # the exchange (N > 1, library-owned)
+    k4_bytes = int(ph[-1].get("exchange_bytes", 0))
     # ---- device-resident timed region 1: throughput (no library events) ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     steps_count, launches = [], 0
@@ -681,6 +691,7 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "scenario_steps_per_batch": int(total_steps / args.steps)},
             "phases_ms": {"K1_update": k1_ph, "K2_expand_rollout": k2_avg, "K3_finalize": k3_ph,
+                          "K4_exchange": k4_ph, "exchange_bytes_per_batch_per_rank": k4_bytes,
                           "K2_share_of_step": k2_share,
                           "note": "K2 from its CUDA events in timed region 2; K1/K3 from 3 untimed steps "
                                   "with every phase's events (8 events cost ~30 us of host time per call)"},

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define DESPOT_ABI_VERSION 1
+#define DESPOT_ABI_VERSION 2
 
 enum despot_status {
   DESPOT_OK = 0,
@@ -51,7 +51,8 @@ enum despot_status {
   DESPOT_ECAPACITY = -4, /* caller's child_capacity / scen_capacity too small; the
                             needed sizes are in num_children / the n_scen outputs    */
   DESPOT_ECUDA = -5,     /* CUDA error (no device, launch failure, ...)               */
-  DESPOT_ENCCL = -6,     /* reserved: collective failure reported by the caller       */
+  DESPOT_ENCCL = -6,     /* NCCL unavailable or a collective of the library's
+                            communicator failed (the model then enters ESHUTDOWN)     */
   DESPOT_ESHUTDOWN = -7, /* the model entered a failed state after a CUDA error       */
   DESPOT_EHASH = -8      /* two different sparse observation keys shared a 64-bit
                             hash inside one (leaf, action): grouping refused          */
@@ -66,12 +67,16 @@ int despot_abi_version(void);
 /* ------------------------------------------------------------------------ */
 typedef struct despot_model despot_model; /* opaque */
 typedef uint64_t despot_node;             /* opaque handle of a device node arena */
+typedef struct despot_comm despot_comm;   /* opaque: an NCCL communicator the library owns */
 
 typedef struct {
   int device;     /* CUDA device ordinal the model and its nodes live on            */
   int rank;       /* scenario shard of this process: it keeps global ids            */
   int world;      /*   with id % world == rank; world <= 1: no shard */
   uint32_t flags; /* DESPOT_MF_* below                                              */
+  despot_comm* comm; /* NULL, or a communicator of `world` ranks (despot_comm_init)
+                        whose rank is `rank`: despot_expand_batch then runs the whole
+                        sharded batch, its exchange included, in one call            */
 } despot_opts;
 
 /* Driving model kernel variant.  Default: chosen per batch -- the factored
@@ -83,6 +88,9 @@ typedef struct {
 #define DESPOT_MF_GROUPED 4u    /* a lane group per scenario: lane q owns Philox block q
                                    (the car's word and pedestrians 4q-1 .. 4q+2),
                                    32 / ceil((P+1)/4) scenarios per warp */
+#define DESPOT_MF_EXCHANGE 8u   /* with a communicator: run the exchange (pack,
+                                   collectives, unpack) even when world == 1 -- the
+                                   one-GPU test of the sharded data path */
 
 typedef struct {
   uint32_t num_actions; /* |A|                                                     */
@@ -189,6 +197,11 @@ typedef struct {
   float phase_ms[4];
   uint64_t h2d_bytes;      /* out: bytes this call copied host -> device / device -> */
   uint64_t d2h_bytes;      /*      host (leaf table, status, results; begin + end)   */
+  /* out, sharded batches run through the model's communicator: */
+  float exchange_ms;       /* K4: CUDA-event time of the exchange (collectives and the
+                              pack / unpack kernels between them; with DESPOT_X_TIMING) */
+  uint32_t exchange_rounds;/* collective rounds issued (a capacity retry adds one)   */
+  uint64_t exchange_bytes; /* bytes this rank contributed to the collectives         */
 } despot_expansion;
 
 /* Output sizes of a batch before calling it (host only, no device work):
@@ -205,34 +218,41 @@ int despot_expand_batch_bytes(despot_model* model, const despot_leaf* leaves, ui
                               uint32_t* child_capacity, uint64_t* scen_capacity, uint64_t* host_bytes);
 
 /* One batch: update (world-local) -> expansion + bounds + roll-outs + grouping
- * -> child ordering, CSR and outputs.  `leaves` is a host array of L <= 4096
- * descriptors.  Synchronous.  With world > 1 use the begin/exchange/end form.
- * Errors: EMODEL (action out of range), EINVAL (see enum), ECAPACITY, EHASH,
- * ENOMEM, ECUDA.  On error outputs are unspecified and nodes created by the
- * call are freed. */
+ * -> [exchange] -> child ordering, CSR and outputs.  `leaves` is a host array
+ * of L <= 4096 descriptors.  Synchronous.  With world > 1 the model needs a
+ * communicator (despot_opts.comm): every rank calls with identical leaves, in
+ * the same order, from one host thread per rank (SPMD), and the exchange runs
+ * inside the call on `stream` (dense keys -- an all-reduce of
+ * the slots any rank used, compacted; sparse keys -- a SUM of the per-action
+ * partials and an all-gather of the ranks' child records); without one use
+ * the begin/exchange/end form.  Errors: EMODEL (action out of range), EINVAL
+ * (see enum), ECAPACITY, EHASH, ENOMEM, ECUDA, ENCCL.  On error outputs are
+ * unspecified and nodes created by the call are freed. */
 int despot_expand_batch(despot_model* model, const despot_leaf* leaves, uint32_t L,
                         despot_expansion* out, void* stream);
 
-/* Multi-GPU scenario sharding: every rank calls with identical
- * leaves; between begin and end the caller runs the collectives each
- * exchange round names, in place, over the ranks (e.g. NCCL on `stream`):
- * SUM over `sums`, MIN over `mins`, MAX over `maxs`, and an all-gather over
- * `gather` (world blocks of gather_bytes; this rank's block, at
- * rank * gather_bytes, is filled).  While `more` is nonzero it calls
- * despot_batch_exchange again for the next round.  Dense-key models need one
- * round (SUM + MIN); sparse-key models (driving) two (SUM + MAX, then the
- * all-gather of the ranks' child records, merged by exact key in `end`).
- * `end` then produces identical outputs on every rank, equal to world == 1
- * bit for bit: the sums are exact int64 fixed-point partials, so nothing
- * depends on the reduction order.  Null pointers / zero sizes: no such
- * collective this round. */
+/* Multi-GPU scenario sharding driven by the caller, the form
+ * for a caller-supplied transport (despot_expand_batch with a communicator is
+ * the library-owned form): every rank calls with identical leaves; between
+ * begin and end the caller runs the collectives each exchange round names,
+ * in place, over the ranks (e.g. NCCL or gloo, ordered after `stream`'s
+ * work): SUM over `sums`, MIN over `mins`, and an all-gather over `gather`
+ * (world blocks of gather_bytes; this rank's block, at rank * gather_bytes,
+ * is filled).  One round for every model: dense keys SUM the exact int64
+ * partial block and MIN the first ids; sparse keys (driving) SUM the
+ * per-action partials and all-gather the ranks' child records (blocks sized
+ * on the host from the leaves alone -- no read-back), merged by exact key in
+ * `end`.  `end` then produces identical outputs on every rank, equal to
+ * world == 1 bit for bit: the sums are exact int64 fixed-point partials, so
+ * nothing depends on the reduction order.  Null pointers / zero sizes: no
+ * such collective.  `maxs` is unused since ABI 2 (NULL). */
 typedef struct despot_batch despot_batch;
 typedef struct {
   int64_t* sums;   /* device [n_sums]  all-reduce SUM (int64)  */
   uint64_t n_sums;
   int32_t* mins;   /* device [n_mins]  all-reduce MIN (int32)  */
   uint64_t n_mins;
-  int64_t* maxs;   /* device [n_maxs]  all-reduce MAX (int64)  */
+  int64_t* maxs;   /* unused (NULL): the ABI 1 MAX round is gone          */
   uint64_t n_maxs;
   void* gather;    /* device [world * gather_bytes]  all-gather (in place) */
   uint64_t gather_bytes;
@@ -249,11 +269,32 @@ int despot_batch_abort(despot_batch* batch);
 
 /* Eqs. 11-12 at the node's own depth, e.g. to initialise the root's bounds
  * (R: SURVEY §3.4): weighted means over the node's scenarios of u(s) and of a
- * default-policy roll-out from depth Delta (this rank's scenarios).  per_scen
- * arrays [n] are optional (host).  Synchronous.  Errors: EINVAL, ECUDA. */
+ * default-policy roll-out from depth Delta.  per_scen arrays [n] are optional
+ * (host; this rank's scenarios).  A sharded model (world > 1) needs its
+ * communicator: the means are then over every rank's scenarios (an all-reduce
+ * of the exact fixed-point sums; SPMD).  Synchronous.  Errors: EINVAL (sharded
+ * without a communicator), ECUDA, ENCCL. */
 int despot_rollout_bounds(despot_model* model, despot_node node, float* upper_mean,
                           float* lower_mean, float* per_scen_upper, float* per_scen_lower,
                           void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU communicator (SURVEY §8(e) "Bootstrap"): rank 0 creates the NCCL
+ * unique id, the caller broadcasts its 128 bytes to every rank over any
+ * channel (e.g. a torch.distributed process group), and every rank creates
+ * its communicator.  libnccl.so.2 is loaded at run time (the copy the process
+ * already has, else $DESPOT_NCCL_LIB, else the loader's search path); a
+ * communicator issues its collectives on the batch's stream.               */
+/* ------------------------------------------------------------------------ */
+/* id_out: 128 bytes.  Errors: ENCCL (no libnccl, or ncclGetUniqueId failed). */
+int despot_comm_unique_id(void* id_out);
+/* Collective over `world` ranks: every rank calls with the same id.
+ * Errors: EINVAL, ECUDA, ENCCL. */
+int despot_comm_init(const void* id, int rank, int world, int device, despot_comm** out);
+/* The communicator must no longer be in use by any model. */
+int despot_comm_destroy(despot_comm* comm);
+/* rank / world / NCCL version of a communicator (any output may be NULL). */
+int despot_comm_info(const despot_comm* comm, int* rank, int* world, int* nccl_version);
 
 /* ------------------------------------------------------------------------ */
 /* Host tree driver (the north star's "thin host driver

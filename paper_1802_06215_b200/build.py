@@ -10,6 +10,20 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdespot.so")
 SOURCES = ["despot.cu", "search.cpp"]
+def _nccl_include():
+    """nccl.h for the types (NCCL itself is loaded at run time, nccl_dl.h):
+    the torch-bundled NCCL's headers, else the system's."""
+    try:
+        import nvidia.nccl
+        for p in nvidia.nccl.__path__:
+            inc = os.path.join(p, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -19,6 +33,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
     "-cudart", "static", "-shared",
     "-Xptxas", "-v",
+    "-I" + _nccl_include(), "-ldl",
 ]
 
 

@@ -153,12 +153,16 @@ struct LeafDev {
 };
 
 // error bits of a batch
-enum : uint32_t { kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u };
+enum : uint32_t {
+  kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u,
+  kErrXOverflow = 16u /* the exchange's packed capacity was too small: dense fallback */
+};
 
 // status block of a batch (zeroed per batch; the host reads it back in one copy)
 enum : uint32_t {
   kStatErr = 0, kStatChildren = 1, kStatSteps = 2 /* u64: 2-3 */, kStatK1Ticket = 4, kStatK2Ticket = 5,
-  kStatK2Tile = 6 /* K2's dynamic tile counter */, kStatWords = 8 /* then n_leaf[L] */
+  kStatK2Tile = 6 /* K2's dynamic tile counter */, kStatXTotal = 7 /* slots in the exchange's union (K4) */,
+  kStatWords = 8 /* then n_leaf[L] */
 };
 
 struct BatchDev {

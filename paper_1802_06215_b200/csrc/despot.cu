@@ -27,6 +27,8 @@
 #include "models.cuh"
 #include "model_car.cuh"
 #include "kernels_sparse.cuh"
+#include "exchange.cuh"
+#include "nccl_dl.h"
 
 using namespace hd;
 
@@ -134,6 +136,8 @@ uint64_t thresh(double p) {
 // ===========================================================================
 // model, nodes, batches
 // ===========================================================================
+constexpr int kBatchEvents = 10;
+
 struct Block {
   void* ptr = nullptr;
   cudaStream_t stream = nullptr;
@@ -191,12 +195,26 @@ struct Node {
   bool expanded;
 };
 
+// An NCCL communicator owned by the library (despot_comm_init).  Collectives
+// of one communicator are enqueued under its mutex: the ranks must issue them
+// in the same order (SPMD, one host thread per rank and model).
+struct despot_comm {
+  ncclComm_t c = nullptr;
+  int rank = 0, world = 1, device = 0;
+  std::mutex mu;
+  std::atomic<bool> failed{false};
+};
+
 struct despot_model {
   DevModel host;
   DevModel* dev = nullptr;
   std::string kind;
   int device = 0, rank = 0, world = 1;
   uint32_t flags = 0;
+  despot_comm* comm = nullptr;
+  // packed-exchange capacity (K4, dense keys) in slots per (leaf, action) x 16:
+  // raised to 5/4 of the largest union seen, so a capacity retry is rare
+  std::atomic<uint32_t> xratio16{64};
   int num_sms = 148;
   std::atomic<bool> failed{false};
   std::mutex mu;
@@ -224,18 +242,22 @@ struct despot_batch {
          o_cl = 0, o_co = 0, o_so = 0;  // staging layout
   bool sparse = false;
   uint64_t n_sums = 0, n_mins = 0;
-  // scenario-sharded sparse keys (world > 1): two exchange rounds, then a merge
+  // scenario-sharded sparse keys: local grouping, one exchange round (SUM of
+  // the per-action partials, all-gather of the ranks' record blocks), merge
   bool sharded_sparse = false;
-  uint32_t xround = 0;            // exchange rounds handed out
-  int64_t* xmax = nullptr;        // device [2]: local record count, largest local child set
+  bool xlib = false;              // the exchange runs on the model's communicator (in the call)
+  uint32_t xround = 0;            // exchange rounds handed out (caller-driven form)
   void* gbuf = nullptr;           // all-gather buffer: world blocks of gblk bytes
   void* mscratch = nullptr;       // merge scratch (offsets, merged sums)
-  uint64_t gblk = 0, rmax = 0, ncmax = 0;
+  uint64_t gblk = 0, gn_max = 0;  // block bytes; the largest global scenario count of a leaf
   uint32_t hdr_pad = 0, rec_bytes = 0;
+  XDev x{};                       // packed exchange (dense keys, xlib)
+  uint32_t x_rounds = 0;          // collective rounds issued by the library
+  uint64_t x_bytes = 0;           // bytes this rank contributed to them
   bool timing = false, timing_k2 = false;  // DESPOT_X_TIMING / DESPOT_X_TIMING_K2 (K2 events only)
   uint32_t launches = 0;  // kernels launched for this batch
   uint64_t h2d = 0, d2h = 0;  // host <-> device bytes copied for this batch
-  cudaEvent_t ev[8] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end
+  cudaEvent_t ev[kBatchEvents] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end, 8/9 K4
   void mark(int i) {
     if (timing && (!timing_k2 || i == 3 || i == 4)) cudaEventRecord(ev[i], stream);
   }
@@ -570,7 +592,7 @@ class EventPool {
  public:
   bool acquire(cudaEvent_t* ev) {
     std::lock_guard<std::mutex> g(mu_);
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < kBatchEvents; ++i) {
       if (!free_.empty()) {
         ev[i] = free_.back();
         free_.pop_back();
@@ -582,7 +604,7 @@ class EventPool {
   }
   void release(cudaEvent_t* ev) {
     std::lock_guard<std::mutex> g(mu_);
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < kBatchEvents; ++i)
       if (ev[i]) free_.push_back(ev[i]);
   }
 
@@ -616,8 +638,16 @@ extern "C" int despot_model_load(const char* kind, const char* params, const des
     m->rank = opts->rank;
     m->world = opts->world < 1 ? 1 : opts->world;
     m->flags = opts->flags;
+    m->comm = opts->comm;
   }
   if (m->rank < 0 || m->rank >= m->world) return set_err(DESPOT_EINVAL, "rank outside [0, world)");
+  // initial capacity of the packed exchange, slots per (leaf, action) x 16 (a
+  // library parameter beside the model card's; tests set it low to force the
+  // capacity retry)
+  m->xratio16 = (uint32_t)std::max<long>(1, pi(params ? params : "", "xratio16", 64));
+  if (m->comm && (m->comm->world != m->world || m->comm->rank != m->rank || m->comm->device != m->device))
+    return set_err(DESPOT_EINVAL, "communicator (rank %d of %d, device %d) does not match the opts", m->comm->rank,
+                   m->comm->world, m->comm->device);
   if (m->world > (int)kMaxMergeWorld) return set_err(DESPOT_EINVAL, "world > %u", kMaxMergeWorld);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -850,7 +880,7 @@ static int launch_group_sparse(despot_model* m, despot_batch* b) {
   while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
   const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
   kernel_occupancy((const void*)k3_group_sparse, smem, 512);  // sets the smem attribute if > 48 KB
-  k3_group_sparse<<<(unsigned)((uint64_t)b->L * b->A), 512, smem, b->stream>>>(b->bd, b->io, tbits, b->xmax);
+  k3_group_sparse<<<(unsigned)((uint64_t)b->L * b->A), 512, smem, b->stream>>>(b->bd, b->io, tbits, nullptr);
   ++b->launches;
   return check_launch(m, "K3a(sparse)");
 }
@@ -921,7 +951,12 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   b->A = dm.A;
   b->S = dm.slots;
   b->sparse = dm.slots == 0;
-  b->sharded_sparse = b->sparse && m->world > 1;
+  // the exchange runs inside the call on the model's communicator (single-call
+  // form); DESPOT_MF_EXCHANGE runs it at world 1 too (the one-GPU test of the
+  // sharded data path)
+  b->xlib = bind && m->comm && (m->world > 1 || (m->flags & DESPOT_MF_EXCHANGE)) &&
+            !(flags & DESPOT_X_RECORD_SCENARIO);  // (RECORD batches are world 1: nothing to exchange)
+  b->sharded_sparse = b->sparse && (m->world > 1 || b->xlib);
   b->flags = flags;
   b->leaves.assign(leaves, leaves + L);
   b->timing = flags & (DESPOT_X_TIMING | DESPOT_X_TIMING_K2);
@@ -1028,9 +1063,9 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   b->n_sums = lay.total();
   b->n_mins = LAS;
   size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += align256(bytes);
+  auto take = [&](size_t bytes) {  // 256-byte aligned regions (vector loads need >= 16)
+    size_t o = align256(off);
+    off = o + align256(bytes);
     return o;
   };
   // status block [err u32 | total children u32 | steps u64 | K1 ticket u32 |
@@ -1047,8 +1082,17 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   off += 8 * (LA / kScanTile + 2);
   const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
                o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
-               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound),
-               o_xmax = take(b->sharded_sparse ? 16 : 0);
+               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound);
+  // packed exchange (K4, dense keys): union flags, block counts, packed sums
+  // and first ids at the model's capacity hint
+  const bool xdense = b->xlib && !b->sparse;
+  XDev& x = b->x;
+  x.las = LAS;
+  x.qn = 3 * LA + 1;
+  x.nblk = (uint32_t)((LAS + kXBlk - 1) / kXBlk);
+  x.ccap = std::min<uint64_t>(LAS, (LA * m->xratio16.load() + 15) / 16 + 256);
+  const size_t o_xflags = take(xdense ? (size_t)x.nblk * kXBlk : 0), o_xcnt = take(xdense ? 4 * (size_t)x.nblk : 0),
+               o_xcpk = take(xdense ? 8 * (4 * x.ccap + x.qn) : 0), o_xcmin = take(xdense ? 4 * x.ccap : 0);
   if (cudaMallocAsync(&b->scratch, off, st) != cudaSuccess) {
     free_batch(b.release(), true);
     return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
@@ -1077,7 +1121,32 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     b->io.keys = reinterpret_cast<uint32_t*>(s + o_keys);
     b->io.q3 = reinterpret_cast<int64_t*>(s + o_q3);
     b->io.kstride = dm.OW;
-    if (b->sharded_sparse) b->xmax = reinterpret_cast<int64_t*>(s + o_xmax);
+  }
+  if (xdense) {
+    x.flags = reinterpret_cast<uint8_t*>(s + o_xflags);
+    x.cnt = reinterpret_cast<uint32_t*>(s + o_xcnt);
+    x.cpk = reinterpret_cast<int64_t*>(s + o_xcpk);
+    x.cmin = reinterpret_cast<int32_t*>(s + o_xcmin);
+  }
+  if (b->sharded_sparse) {
+    // the record blocks of the all-gather, sized on the host from the leaves
+    // alone (identical on every rank): a leaf's local scenarios are at most
+    // ceil(K / world) of its root's K (the root shard is the largest node)
+    const uint32_t W = (uint32_t)m->world;
+    uint64_t rcap = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+      rcap += (uint64_t)dm.A * ((parent[l]->gn + W - 1) / W);
+      b->gn_max = std::max<uint64_t>(b->gn_max, parent[l]->gn);
+    }
+    b->rec_bytes = sparse_record_bytes(dm.OW);
+    b->hdr_pad = (uint32_t)(((4 * LA + b->rec_bytes - 1) / b->rec_bytes) * b->rec_bytes);
+    b->gblk = b->hdr_pad + rcap * b->rec_bytes;
+    const size_t gbytes = (size_t)W * b->gblk;
+    if (cudaMallocAsync(&b->gbuf, gbytes, st) != cudaSuccess ||
+        cudaMallocAsync(&b->mscratch, 4 * LA, st) != cudaSuccess) {
+      free_batch(b.release(), true);
+      return set_err(DESPOT_ENOMEM, "all-gather buffer (%zu bytes)", gbytes);
+    }
   }
   // all leaves are nodes themselves (e.g. roots): their sizes are known on the
   // host, so the update kernel and the prefix are skipped and the host ships
@@ -1111,7 +1180,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     }
     if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
         cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
-        (b->xmax && cudaMemsetAsync(b->xmax, 0, 16, st) != cudaSuccess) ||
+        (xdense && (size_t)x.nblk * kXBlk > LAS &&
+         cudaMemsetAsync(x.flags + LAS, 0, (size_t)x.nblk * kXBlk - LAS, st) != cudaSuccess) ||
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
     b->h2d += h2d_bytes - o_leaves;
@@ -1135,6 +1205,14 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     if (!rc && b->sharded_sparse) {  // local grouping now: its records are what the ranks exchange
       b->mark(5);
       rc = launch_group_sparse(m, b.get());
+      if (!rc) {  // this rank's records into its block of the all-gather buffer
+        PackDev pk{static_cast<unsigned char*>(b->gbuf) + (size_t)m->rank * b->gblk, b->hdr_pad, b->rec_bytes,
+                   static_cast<uint32_t*>(b->mscratch)};
+        k_pack_sparse_scan<<<1, 1024, 0, st>>>(b->bd, pk);
+        k_pack_sparse<<<(unsigned)LA, 128, 0, st>>>(b->bd, b->io, pk);
+        b->launches += 2;
+        rc = check_launch(m, "pack (sharded sparse)");
+      }
     }
   } else if (!rc) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
@@ -1161,7 +1239,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     // fused only when K2's 4 warps finish it in ~2 sweeps (else the 32-warp
     // k3_small_dense is faster than the launch it saves)
     const uint64_t G = 32 / small_group_width(b->S);
-    b->k3_fused = !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO) && m->world == 1 && b->S <= 32 &&
+    b->k3_fused = !b->sparse && !(flags & DESPOT_X_RECORD_SCENARIO) && m->world == 1 && !b->xlib && b->S <= 32 &&
                   LAd <= 4 * G * kSmallUnroll * 2;
     b->bd.fused_k3 = b->k3_fused ? 1u : 0u;
   }
@@ -1204,85 +1282,131 @@ extern "C" int despot_expand_begin(despot_model* m, const despot_leaf* leaves, u
   return begin_impl(m, leaves, L, flags, stream, nullptr, out);
 }
 
-// Exchange rounds of a sharded batch.  Dense keys: one round (SUM of the exact
-// partials, MIN of the first ids).  Sparse keys: round 0 sums the per-action
-// partials and the step count and MAXes (local record count, largest local
-// child set); round 1 hands out the all-gather buffer with this rank's
-// records packed into its block.
+// The one exchange round of a caller-driven sharded batch.  Dense keys: SUM
+// of the exact partial block, MIN of the first ids.  Sparse keys: SUM of the
+// per-action partials and the step count, all-gather of the record blocks
+// (this rank's block was packed in begin).
 extern "C" int despot_batch_exchange(despot_batch* b, despot_exchange* out) {
   if (!b || !out) return set_err(DESPOT_EINVAL, "null argument");
   memset(out, 0, sizeof *out);
   const uint64_t LA = (uint64_t)b->L * b->A;
   const SumLayout lay{LA * b->S, LA};
   out->round = b->xround;
+  if (b->xround >= 1) return set_err(DESPOT_EINVAL, "exchange: no further round (more == 0)");
   if (!b->sharded_sparse) {
-    if (b->xround >= 1) return set_err(DESPOT_EINVAL, "exchange: no further round (more == 0)");
     out->sums = b->bd.sums;
     out->n_sums = b->n_sums;
     out->mins = b->bd.mins;
     out->n_mins = b->n_mins;
-    b->xround = 1;
-    return DESPOT_OK;
-  }
-  if (b->xround == 0) {
+  } else {
     out->sums = b->bd.sums + lay.Q(0, 0);  // [L*A][3] per-action partials + the step count
     out->n_sums = 3 * LA + 1;
-    out->maxs = b->xmax;
-    out->n_maxs = 2;
-    out->more = 1;
-    b->xround = 1;
-    return DESPOT_OK;
+    out->gather = b->gbuf;
+    out->gather_bytes = b->gblk;
   }
-  if (b->xround != 1) return set_err(DESPOT_EINVAL, "exchange: no further round (more == 0)");
+  b->xround = 1;
+  return DESPOT_OK;
+}
+
+static int nccl_err(despot_model* m, despot_comm* c, ncclResult_t r, const char* what) {
+  c->failed = true;
+  m->failed = true;
+  return set_err(DESPOT_ENCCL, "%s: %s", what, nccl_api().GetErrorString ? nccl_api().GetErrorString(r) : "?");
+}
+
+// The exchange of a sharded batch on the model's communicator, enqueued on the
+// batch's stream between K2 (and the sparse local grouping) and K3 -- no host
+// round trip.  Dense keys: the packed protocol of exchange.cuh (two rounds);
+// sparse keys: one round (SUM of the per-action partials, all-gather of the
+// record blocks).
+static int lib_exchange(despot_batch* b) {
   despot_model* m = b->model;
-  CU(cudaSetDevice(m->device));
+  despot_comm* c = m->comm;
+  NcclApi& nc = nccl_api();
+  if (!nc.ok) return set_err(DESPOT_ENCCL, "%s", nc.err.c_str());
+  if (c->failed) return set_err(DESPOT_ESHUTDOWN, "communicator failed earlier");
   cudaStream_t st = b->stream;
-  // the all-reduced maxima size the blocks (identical on every rank)
-  int64_t* hx = static_cast<int64_t*>(pinned_pool().acquire(16));
-  if (!hx) return set_err(DESPOT_ENOMEM, "pinned staging");
-  b->d2h += 16;
-  const bool ok = cudaMemcpyAsync(hx, b->xmax, 16, cudaMemcpyDeviceToHost, st) == cudaSuccess &&
-                  cudaStreamSynchronize(st) == cudaSuccess;
-  b->rmax = (uint64_t)hx[0];
-  b->ncmax = (uint64_t)hx[1];
-  pinned_pool().release(hx);
-  if (!ok) return set_err(DESPOT_ECUDA, "exchange: reading the reduced maxima failed");
-  b->rec_bytes = sparse_record_bytes(m->host.OW);
-  b->hdr_pad = (uint32_t)(((4 * LA + b->rec_bytes - 1) / b->rec_bytes) * b->rec_bytes);
-  b->gblk = b->hdr_pad + b->rmax * b->rec_bytes;
-  const size_t gbytes = (size_t)m->world * b->gblk;
-  if (cudaMallocAsync(&b->gbuf, gbytes, st) != cudaSuccess || cudaMallocAsync(&b->mscratch, 4 * LA, st) != cudaSuccess)
-    return set_err(DESPOT_ENOMEM, "exchange: all-gather buffer (%zu bytes)", gbytes);
-  PackDev pk{static_cast<unsigned char*>(b->gbuf) + (size_t)m->rank * b->gblk, b->hdr_pad, b->rec_bytes,
-             static_cast<uint32_t*>(b->mscratch)};
-  k_pack_sparse_scan<<<1, 1024, 0, st>>>(b->bd, pk);
-  k_pack_sparse<<<(unsigned)LA, 128, 0, st>>>(b->bd, b->io, pk);
-  b->launches += 2;
-  if (int rc = check_launch(m, "exchange pack")) return rc;
-  out->gather = b->gbuf;
-  out->gather_bytes = b->gblk;
-  b->xround = 2;
+  const uint64_t LA = (uint64_t)b->L * b->A;
+  const SumLayout lay{LA * b->S, LA};
+  std::lock_guard<std::mutex> g(c->mu);
+  b->mark(8);
+  ncclResult_t r;
+  if (b->sharded_sparse) {
+    if ((r = nc.GroupStart()) != ncclSuccess) return nccl_err(m, c, r, "ncclGroupStart");
+    r = nc.AllReduce(b->bd.sums + lay.Q(0, 0), b->bd.sums + lay.Q(0, 0), 3 * LA + 1, ncclInt64, ncclSum, c->c, st);
+    ncclResult_t r2 = nc.AllGather(static_cast<char*>(b->gbuf) + (size_t)m->rank * b->gblk, b->gbuf, b->gblk, ncclUint8,
+                                   c->c, st);
+    ncclResult_t r3 = nc.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+      return nccl_err(m, c, r != ncclSuccess ? r : r2 != ncclSuccess ? r2 : r3, "sparse exchange");
+    b->x_rounds += 1;
+    b->x_bytes += 8 * (3 * LA + 1) + b->gblk;
+    b->xround = 1;
+  } else {
+    XDev& x = b->x;
+    const unsigned g1 = (unsigned)std::min<uint64_t>((x.las + kXThreads - 1) / kXThreads, (uint64_t)m->num_sms * 8);
+    k4_flags<<<std::max(g1, 1u), kXThreads, 0, st>>>(b->bd, x);
+    if ((r = nc.AllReduce(x.flags, x.flags, x.las, ncclUint8, ncclSum, c->c, st)) != ncclSuccess)
+      return nccl_err(m, c, r, "exchange round A (slot union)");
+    k4_count<<<x.nblk, kXThreads, 0, st>>>(x);
+    k4_pack<<<x.nblk, kXThreads, 0, st>>>(b->bd, x);
+    if ((r = nc.GroupStart()) != ncclSuccess) return nccl_err(m, c, r, "ncclGroupStart");
+    r = nc.AllReduce(x.cpk, x.cpk, 4 * x.ccap + x.qn, ncclInt64, ncclSum, c->c, st);
+    ncclResult_t r2 = nc.AllReduce(x.cmin, x.cmin, x.ccap, ncclInt32, ncclMin, c->c, st);
+    ncclResult_t r3 = nc.GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+      return nccl_err(m, c, r != ncclSuccess ? r : r2 != ncclSuccess ? r2 : r3, "exchange round B (packed sums)");
+    k4_unpack<<<x.nblk, kXThreads, 0, st>>>(b->bd, x);
+    b->launches += 4;
+    b->x_rounds += 2;
+    b->x_bytes += x.las + 8 * (4 * x.ccap + x.qn) + 4 * x.ccap;
+    b->xround = 1;
+    if (int rc = check_launch(m, "K4")) return rc;
+  }
+  b->mark(9);
+  return DESPOT_OK;
+}
+
+// Capacity fallback of the packed exchange (all ranks see the same union, so
+// all of them come here): the dense partial block, untouched by k4_unpack,
+// reduced whole.
+static int lib_exchange_dense(despot_batch* b) {
+  despot_model* m = b->model;
+  despot_comm* c = m->comm;
+  NcclApi& nc = nccl_api();
+  cudaStream_t st = b->stream;
+  std::lock_guard<std::mutex> g(c->mu);
+  ncclResult_t r = nc.GroupStart();
+  if (r != ncclSuccess) return nccl_err(m, c, r, "ncclGroupStart");
+  r = nc.AllReduce(b->bd.sums, b->bd.sums, b->n_sums, ncclInt64, ncclSum, c->c, st);
+  ncclResult_t r2 = nc.AllReduce(b->bd.mins, b->bd.mins, b->n_mins, ncclInt32, ncclMin, c->c, st);
+  ncclResult_t r3 = nc.GroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess || r3 != ncclSuccess)
+    return nccl_err(m, c, r != ncclSuccess ? r : r2 != ncclSuccess ? r2 : r3, "exchange (dense fallback)");
+  b->x_rounds += 1;
+  b->x_bytes += 8 * b->n_sums + 4 * b->n_mins;
   return DESPOT_OK;
 }
 
 // End of a sharded sparse batch: merge the gathered records into global
 // children (b->bd then points at the merged rows, b->io at the records' keys).
 static int merge_sparse(despot_model* m, despot_batch* b) {
-  if (b->xround != 2) return set_err(DESPOT_EINVAL, "sharded sparse batch: exchange rounds not completed");
+  if (b->xround != 1) return set_err(DESPOT_EINVAL, "sharded sparse batch: the exchange round was not run");
   cudaStream_t st = b->stream;
   BatchDev& bd = b->bd;
   const uint64_t LA = (uint64_t)b->L * b->A;
   const uint32_t W = (uint32_t)m->world;
-  const uint64_t nmax = std::max<uint64_t>(1, W * b->ncmax);  // items (and children) per (leaf, action)
+  // merged children per (leaf, action) <= the leaf's global scenarios <= its root's K
+  const uint64_t nmax = std::max<uint64_t>(1, b->gn_max);
   if (nmax > 4096) return set_err(DESPOT_EINVAL, "sharded sparse merge: more than 4096 children per (leaf, action)");
   const SumLayout old_lay{LA * b->S, LA};
   const uint32_t mS = (uint32_t)nmax;
   const SumLayout lay{LA * mS, LA};
   // merged rows: offsets [W][LA] | sums | mins | sp_item | nc
   size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off += align256(bytes);
+  auto take = [&](size_t bytes) {  // 256-byte aligned regions (vector loads need >= 16)
+    size_t o = align256(off);
+    off = o + align256(bytes);
     return o;
   };
   const size_t o_offs = take(4 * W * LA), o_sums = take(8 * lay.total()), o_mins = take(4 * LA * mS),
@@ -1475,61 +1599,66 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       return check_launch(m, "K2(record)");
     });
   }
-  const unsigned warps_per_cta = 4;
-  const unsigned g3 = (unsigned)((LA + warps_per_cta - 1) / warps_per_cta);
-  b->mark(5);
-  // small dense batches (few slots): rank + scan + write in one CTA (or in
-  // K2's last CTA, already done, when the batch was fused)
-  // the single-CTA finalize when its 32 warps cover the pairs in about one
-  // sweep; beyond that the multi-CTA kernels win (their launches overlap)
-  const bool small_k3 = !b->sparse && b->S <= 32 &&
-                        LA <= std::min<uint64_t>(kSmallLA, 32 * (32 / small_group_width(b->S)) * 2);
-  if (b->k3_fused) {
-  } else if (!rc && b->sharded_sparse) {
-    rc = merge_sparse(m, b);  // the ranks' records -> global children
-  } else if (!rc && b->sparse) {
-    rc = launch_group_sparse(m, b);
-  } else if (!rc && small_k3) {
-    // small batch: rank + scan + write in one CTA (one launch instead of three)
-    const size_t smem = small_finalize_smem(LA);
-    static std::once_flag once;
-    std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
-    k3_small_dense<<<1, 1024, smem, st>>>(bd);
-    ++b->launches;
-    rc = check_launch(m, "K3(small)");
-  } else if (!rc && b->S <= 16) {  // counts only: k3_write_grouped recomputes the ordinals
-    const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
-    k3_count_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
-    ++b->launches;
-    rc = check_launch(m, "K3a");
-  } else if (!rc) {
-    k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 8, st>>>(bd);
-    ++b->launches;
-    rc = check_launch(m, "K3a");
-  }
-  if (!rc && !small_k3 && !b->k3_fused) {
-    k3_scan_lookback<<<(unsigned)((LA + kScanTile - 1) / kScanTile), kScanTile, 0, st>>>(bd);
-    ++b->launches;
-    rc = check_launch(m, "K3b");
-  }
-  if (!rc && b->sparse) {
-    k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);  // (merged: keys from the gathered records)
-    ++b->launches;
-    rc = check_launch(m, "K3c(sparse)");
-  } else if (!rc && !small_k3) {
-    if (b->S > kWideS) {
-      k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
-    } else if (b->S <= 16) {
+  auto launch_k3 = [&]() -> int {
+    int rc = DESPOT_OK;
+    const unsigned warps_per_cta = 4;
+    const unsigned g3 = (unsigned)((LA + warps_per_cta - 1) / warps_per_cta);
+    b->mark(5);
+    // small dense batches (few slots): rank + scan + write in one CTA (or in
+    // K2's last CTA, already done, when the batch was fused)
+    // the single-CTA finalize when its 32 warps cover the pairs in about one
+    // sweep; beyond that the multi-CTA kernels win (their launches overlap)
+    const bool small_k3 = !b->sparse && b->S <= 32 &&
+                          LA <= std::min<uint64_t>(kSmallLA, 32 * (32 / small_group_width(b->S)) * 2);
+    if (b->k3_fused) {
+    } else if (!rc && b->sharded_sparse) {
+      rc = merge_sparse(m, b);  // the ranks' records -> global children
+    } else if (!rc && b->sparse) {
+      rc = launch_group_sparse(m, b);
+    } else if (!rc && small_k3) {
+      // small batch: rank + scan + write in one CTA (one launch instead of three)
+      const size_t smem = small_finalize_smem(LA);
+      static std::once_flag once;
+      std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
+      k3_small_dense<<<1, 1024, smem, st>>>(bd);
+      ++b->launches;
+      rc = check_launch(m, "K3(small)");
+    } else if (!rc && b->S <= 16) {  // counts only: k3_write_grouped recomputes the ordinals
       const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
-      k3_write_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
-    } else {
-      k3_write_dense<<<g3, 128, 0, st>>>(bd);
+      k3_count_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+      ++b->launches;
+      rc = check_launch(m, "K3a");
+    } else if (!rc) {
+      k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 8, st>>>(bd);
+      ++b->launches;
+      rc = check_launch(m, "K3a");
     }
-    ++b->launches;
-    rc = check_launch(m, "K3c");
-  }
+    if (!rc && !small_k3 && !b->k3_fused) {
+      k3_scan_lookback<<<(unsigned)((LA + kScanTile - 1) / kScanTile), kScanTile, 0, st>>>(bd);
+      ++b->launches;
+      rc = check_launch(m, "K3b");
+    }
+    if (!rc && b->sparse) {
+      k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);  // (merged: keys from the gathered records)
+      ++b->launches;
+      rc = check_launch(m, "K3c(sparse)");
+    } else if (!rc && !small_k3) {
+      if (b->S > kWideS) {
+        k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
+      } else if (b->S <= 16) {
+        const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
+        k3_write_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+      } else {
+        k3_write_dense<<<g3, 128, 0, st>>>(bd);
+      }
+      ++b->launches;
+      rc = check_launch(m, "K3c");
+    }
+    b->mark(6);
+    return rc;
+  };
+  if (!rc) rc = launch_k3();
   g_ht.mark("k3");
-  b->mark(6);
   // status block: err | total children | steps | ticket | pad | n_leaf[L]
   const size_t stat_bytes = 4 * kStatWords + 4 * (size_t)L;
   char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
@@ -1538,11 +1667,6 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     ~PinGuard() { pinned_pool().release(p); }
   } pin_guard{hs};
   if (!rc && !hs) rc = set_err(DESPOT_ENOMEM, "pinned staging");
-  if (!rc) {
-    b->d2h += stat_bytes;
-    if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-      rc = set_err(DESPOT_ECUDA, "status copy failed");
-  }
   // host outputs: the staging block [per-leaf | per-action | CSR | children]
   // goes to one pinned buffer; when it is small (search-sized batches) the
   // whole block travels in this first copy and no second round trip is needed
@@ -1561,34 +1685,62 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       if (p) pinned_pool().release(p);
     }
   } pin_out_guard{hp_out};
-  if (!rc && pinned_out) {
-    const struct {
-      void* dst;
-      size_t off, bytes;
-    } head[] = {{out->n_scen, o_ns, 4 * (size_t)L},  {out->weight, o_w, 4 * (size_t)L},
-                {out->act_reward, o_ar, 4 * LA},     {out->act_upper, o_au, 4 * LA},
-                {out->act_lower, o_al, 4 * LA},      {out->child_begin, o_cb, 4 * (LA + 1)}};
-    for (const auto& h : head) b->d2h += h.bytes;
-    for (const auto& h : head)
-      if (!rc && h.dst && h.bytes &&
-          cudaMemcpyAsync(h.dst, static_cast<char*>(stage) + h.off, h.bytes, cudaMemcpyDeviceToHost, st) !=
-              cudaSuccess)
+  auto copy_and_sync = [&]() -> int {
+    int rc = DESPOT_OK;
+    if (!rc) {
+      b->d2h += stat_bytes;
+      if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "status copy failed");
+    }
+    if (!rc && pinned_out) {
+      const struct {
+        void* dst;
+        size_t off, bytes;
+      } head[] = {{out->n_scen, o_ns, 4 * (size_t)L},  {out->weight, o_w, 4 * (size_t)L},
+                  {out->act_reward, o_ar, 4 * LA},     {out->act_upper, o_au, 4 * LA},
+                  {out->act_lower, o_al, 4 * LA},      {out->child_begin, o_cb, 4 * (LA + 1)}};
+      for (const auto& h : head) b->d2h += h.bytes;
+      for (const auto& h : head)
+        if (!rc && h.dst && h.bytes &&
+            cudaMemcpyAsync(h.dst, static_cast<char*>(stage) + h.off, h.bytes, cudaMemcpyDeviceToHost, st) !=
+                cudaSuccess)
+          rc = set_err(DESPOT_ECUDA, "output copy failed");
+    } else if (!rc && !dev_out) {
+      if (!hp_out) hp_out = static_cast<char*>(pinned_pool().acquire(one_copy ? body_bytes : head_bytes));
+      if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
+      else if ((b->d2h += one_copy ? body_bytes : head_bytes,
+                cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st)) !=
+               cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "output copy failed");
-  } else if (!rc && !dev_out) {
-    hp_out = static_cast<char*>(pinned_pool().acquire(one_copy ? body_bytes : head_bytes));
-    if (!hp_out) rc = set_err(DESPOT_ENOMEM, "pinned output staging");
-    else if ((b->d2h += one_copy ? body_bytes : head_bytes,
-              cudaMemcpyAsync(hp_out, stage, one_copy ? body_bytes : head_bytes, cudaMemcpyDeviceToHost, st)) !=
-             cudaSuccess)
-      rc = set_err(DESPOT_ECUDA, "output copy failed");
+    }
+    g_ht.mark("d2h_enqueued");
+    b->mark(7);  // end of the call's device work (before the host waits: no extra round trip)
+    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
+      m->failed = true;
+      rc = set_err(DESPOT_ECUDA, "batch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    g_ht.mark("synced");
+    return rc;
+  };
+  if (!rc) rc = copy_and_sync();
+  if (!rc && b->xlib && !b->sparse) {
+    // the packed exchange's capacity hint follows the largest union seen (+ 1/4)
+    uint32_t T = 0, e0 = 0;
+    memcpy(&T, hs + 4 * kStatXTotal, 4);
+    memcpy(&e0, hs, 4);
+    const uint64_t want = std::min<uint64_t>(((uint64_t)T * 20 + LA - 1) / std::max<uint64_t>(LA, 1), 16ull * b->S);
+    uint32_t cur = m->xratio16.load();
+    while (want > cur && !m->xratio16.compare_exchange_weak(cur, (uint32_t)want)) {
+    }
+    if (e0 & kErrXOverflow) {  // every rank saw the same union: the dense fallback, then K3 again
+      if (cudaMemsetAsync(bd.err, 0, 4, st) != cudaSuccess ||
+          cudaMemsetAsync(bd.scan_flags, 0, 8 * (LA / kScanTile + 2), st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "capacity retry reset failed");
+      if (!rc) rc = lib_exchange_dense(b);
+      if (!rc) rc = launch_k3();
+      if (!rc) rc = copy_and_sync();
+    }
   }
-  g_ht.mark("d2h_enqueued");
-  b->mark(7);  // end of the call's device work (before the host waits: no extra round trip)
-  if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
-    m->failed = true;
-    rc = set_err(DESPOT_ECUDA, "batch failed: %s", cudaGetErrorString(cudaGetLastError()));
-  }
-  g_ht.mark("synced");
   uint32_t err = 0, nchildren = 0;
   uint64_t steps = 0;
   if (!rc) {
@@ -1655,6 +1807,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       for (auto& p : parts)
         if (p.bytes) memcpy(p.dst, hp_out + p.off, p.bytes);
   }
+  out->exchange_ms = 0.0f;
   if (!rc && b->timing) {  // the events are complete: the stream was synchronised
     const int pairs[4][2] = {{1, 2}, {3, 4}, {5, 6}, {0, 7}};
     for (int k = 0; k < 4; ++k) {
@@ -1662,7 +1815,10 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
       if (!b->timing_k2 || k == 1) cudaEventElapsedTime(&ms, b->ev[pairs[k][0]], b->ev[pairs[k][1]]);
       out->phase_ms[k] = ms;
     }
+    if (b->xlib && !b->timing_k2) cudaEventElapsedTime(&out->exchange_ms, b->ev[8], b->ev[9]);
   }
+  out->exchange_rounds = b->x_rounds;
+  out->exchange_bytes = b->x_bytes;
   if (rc) {
     free_batch(b, true);
     return rc;
@@ -1697,11 +1853,16 @@ extern "C" int despot_expand_batch(despot_model* m, const despot_leaf* leaves, u
                                    despot_expansion* out, void* stream) {
   g_ht.start();
   if (!m || !out) return set_err(DESPOT_EINVAL, "null argument");
-  if (m->world > 1) return set_err(DESPOT_EINVAL, "world > 1: use despot_expand_begin/exchange/end");
+  if (m->world > 1 && !m->comm)
+    return set_err(DESPOT_EINVAL, "world > 1 without a communicator: use despot_expand_begin/exchange/end");
   despot_batch* b = nullptr;
   // outputs are bound before K2 so that small batches finalize in K2's last CTA
   int rc = begin_impl(m, leaves, L, out->flags, stream, out, &b);
   if (rc) return rc;
+  if (b->xlib && (rc = lib_exchange(b))) {  // K4: the exchange on the model's communicator
+    free_batch(b, true);
+    return rc;
+  }
   return despot_expand_end(b, out, stream);
 }
 
@@ -1711,8 +1872,8 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
   if (!nd) return set_err(DESPOT_EINVAL, "unknown node");
   if (!upper_mean || !lower_mean) return set_err(DESPOT_EINVAL, "null argument");
   if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
-  // a sharded node holds only this rank's scenarios: its means are not the node's
-  if (m->world > 1) return set_err(DESPOT_EINVAL, "rollout_bounds: world > 1 (sharded node)");
+  // a sharded node holds only this rank's scenarios: the means need every rank's sums
+  if (m->world > 1 && !m->comm) return set_err(DESPOT_EINVAL, "rollout_bounds: world > 1 without a communicator");
   CU(cudaSetDevice(m->device));
   cudaStream_t st = (cudaStream_t)stream;
   const DevModel& dm = m->host;
@@ -1738,6 +1899,15 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
     };
     if (dm.slots) rc = dispatch_dense(dm, launch);
     else rc = launch(CarThread{});
+  }
+  if (!rc && m->comm && (m->world > 1 || (m->flags & DESPOT_MF_EXCHANGE))) {  // every rank's exact sums (SPMD)
+    NcclApi& nc = nccl_api();
+    if (!nc.ok) rc = set_err(DESPOT_ENCCL, "%s", nc.err.c_str());
+    if (!rc) {
+      std::lock_guard<std::mutex> g(m->comm->mu);
+      const ncclResult_t r = nc.AllReduce(acc, acc, 3, ncclInt64, ncclSum, m->comm->c, st);
+      if (r != ncclSuccess) rc = nccl_err(m, m->comm, r, "rollout_bounds all-reduce");
+    }
   }
   int64_t hacc[3] = {0, 0, 0};
   if (!rc) {
@@ -1810,5 +1980,58 @@ extern "C" int despot_philox_ceiling(despot_model* m, uint64_t seed, uint32_t n_
   if (rc) return rc;
   *out_ms = (double)ms / reps;
   *out_checksum = cs;
+  return DESPOT_OK;
+}
+
+// ===========================================================================
+// communicator (SURVEY §8(e) "Bootstrap")
+// ===========================================================================
+extern "C" int despot_comm_unique_id(void* id_out) {
+  if (!id_out) return set_err(DESPOT_EINVAL, "null argument");
+  NcclApi& nc = nccl_api();
+  if (!nc.ok) return set_err(DESPOT_ENCCL, "%s", nc.err.c_str());
+  ncclUniqueId id;
+  const ncclResult_t r = nc.GetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(DESPOT_ENCCL, "ncclGetUniqueId: %s", nc.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  memcpy(id_out, &id, sizeof id);
+  return DESPOT_OK;
+}
+
+extern "C" int despot_comm_init(const void* id, int rank, int world, int device, despot_comm** out) {
+  if (!id || !out) return set_err(DESPOT_EINVAL, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return set_err(DESPOT_EINVAL, "need 0 <= rank < world");
+  NcclApi& nc = nccl_api();
+  if (!nc.ok) return set_err(DESPOT_ENCCL, "%s", nc.err.c_str());
+  CU(cudaSetDevice(device));
+  std::unique_ptr<despot_comm> c(new despot_comm());
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  const ncclResult_t r = nc.CommInitRank(&c->c, world, uid, rank);
+  if (r != ncclSuccess) return set_err(DESPOT_ENCCL, "ncclCommInitRank: %s", nc.GetErrorString(r));
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  *out = c.release();
+  return DESPOT_OK;
+}
+
+extern "C" int despot_comm_destroy(despot_comm* c) {
+  if (!c) return DESPOT_OK;
+  NcclApi& nc = nccl_api();
+  if (nc.ok && c->c) {
+    cudaSetDevice(c->device);
+    if (c->failed) nc.CommAbort(c->c);
+    else nc.CommDestroy(c->c);
+  }
+  delete c;
+  return DESPOT_OK;
+}
+
+extern "C" int despot_comm_info(const despot_comm* c, int* rank, int* world, int* nccl_version) {
+  if (!c) return set_err(DESPOT_EINVAL, "null argument");
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (nccl_version) *nccl_version = nccl_api().version;
   return DESPOT_OK;
 }

@@ -21,6 +21,7 @@ DESPOT_X_TIMING_K2 = 8
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
 DESPOT_MF_GROUPED = 4
+DESPOT_MF_EXCHANGE = 8  # run the sharded exchange path on the communicator even at world 1 (tests)
 
 STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5: "ECUDA",
           -6: "ENCCL", -7: "ESHUTDOWN", -8: "EHASH"}
@@ -30,7 +31,8 @@ EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "desp
            "despot_model_free", "despot_belief_load", "despot_node_info", "despot_node_read",
            "despot_node_release", "despot_node_release_many", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
            "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
-           "despot_search", "despot_plan", "despot_philox_ceiling", "despot_expand_batch_bytes"]
+           "despot_search", "despot_plan", "despot_philox_ceiling", "despot_expand_batch_bytes",
+           "despot_comm_unique_id", "despot_comm_init", "despot_comm_destroy", "despot_comm_info"]
 
 
 def _tflag(timing):
@@ -46,7 +48,8 @@ class DespotError(RuntimeError):
 
 
 class Opts(C.Structure):
-    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("flags", C.c_uint32)]
+    _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("flags", C.c_uint32),
+                ("comm", C.c_void_p)]
 
 
 class ModelInfo(C.Structure):
@@ -70,7 +73,8 @@ class Expansion(C.Structure):
                 ("scen_upper", C.c_void_p), ("scen_lower", C.c_void_p), ("scen_len", C.c_void_p),
                 ("scen_hash", C.c_void_p), ("scen_states", C.c_void_p),
                 ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("launches", C.c_uint32),
-                ("phase_ms", C.c_float * 4), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("phase_ms", C.c_float * 4), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("exchange_ms", C.c_float), ("exchange_rounds", C.c_uint32), ("exchange_bytes", C.c_uint64)]
 
 
 class SearchProblem(C.Structure):
@@ -164,6 +168,10 @@ def lib():
         L.despot_search.argtypes = [C.POINTER(SearchProblem), C.POINTER(SearchConfig), C.POINTER(SearchResult),
                                     vp, u32]
         L.despot_plan.argtypes = [vp, u64, C.POINTER(SearchConfig), C.POINTER(SearchResult), vp]
+        L.despot_comm_unique_id.argtypes = [vp]
+        L.despot_comm_init.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+        L.despot_comm_destroy.argtypes = [vp]
+        L.despot_comm_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
         _lib = L
     return _lib
 
@@ -185,13 +193,45 @@ def _stream_ptr(stream):
     return getattr(stream, "cuda_stream", stream)
 
 
+def comm_unique_id() -> bytes:
+    """despot_comm_unique_id: the 128-byte NCCL unique id (rank 0 creates it,
+    every rank receives it over the caller's channel)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().despot_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """A communicator owned by the library (despot_comm_init): models loaded
+    with it run sharded batches, their exchange included, in one call."""
+
+    def __init__(self, uid: bytes, rank: int, world: int, device: int = 0):
+        if len(uid) != 128:
+            raise DespotError(-1, "the unique id is 128 bytes")
+        self.h = C.c_void_p()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _check(lib().despot_comm_init(buf, int(rank), int(world), int(device), C.byref(self.h)))
+        self.rank, self.world, self.device = rank, world, device
+
+    def info(self):
+        r, w, v = C.c_int(), C.c_int(), C.c_int()
+        _check(lib().despot_comm_info(self.h, C.byref(r), C.byref(w), C.byref(v)))
+        return {"rank": r.value, "world": w.value, "nccl_version": v.value}
+
+    def close(self):
+        if self.h:
+            lib().despot_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
 class Model:
     """A loaded model (despot_model*)."""
 
     def __init__(self, kind: str, params: str = "", device: int = 0, rank: int = 0, world: int = 1,
-                 flags: int = 0):
+                 flags: int = 0, comm: "Comm | None" = None):
         self.h = C.c_void_p()
-        o = Opts(device, rank, world, flags)
+        self.comm = comm  # kept alive as long as the model
+        o = Opts(device, rank, world, flags, comm.h.value if comm is not None else None)
         _check(lib().despot_model_load(kind.encode(), params.encode(), C.byref(o), C.byref(self.h)))
         info = ModelInfo()
         _check(lib().despot_model_info_get(self.h, C.byref(info)))
@@ -320,6 +360,8 @@ class Model:
         out["phase_ms"] = [float(x) for x in E.phase_ms]
         out["launches"] = int(E.launches)
         out["h2d_bytes"], out["d2h_bytes"] = int(E.h2d_bytes), int(E.d2h_bytes)
+        out["exchange_ms"], out["exchange_rounds"] = float(E.exchange_ms), int(E.exchange_rounds)
+        out["exchange_bytes"] = int(E.exchange_bytes)
         if not device:
             for k in ("child_count", "child_first", "child_weight", "child_upper", "child_lower"):
                 out[k] = o[k][:Cn]

@@ -1,18 +1,52 @@
 """Scenario sharding across GPUs.
 
 Every rank loads the same belief with despot_opts{rank, world}; the library
-keeps the scenarios with global id % world == rank.  A batch then runs
-begin (update + expansion + roll-outs + grouping on the local shard) ->
-exchange (all-reduce SUM of the exact int64 fixed-point partials and MIN of
-the first-occurrence ids, here via torch.distributed / NCCL over NVLink; for
-the driving model's sparse keys a second round all-gathers the ranks' child
-records) -> end (merge, child order, CSR and outputs, identical on every
-rank).
+keeps the scenarios with global id % world == rank.
+
+The primary form is library-owned: `init_comm` bootstraps an NCCL
+communicator inside libdespot (rank 0's unique id broadcast over the torch
+process group), models are loaded with it, and `Model.expand` runs the whole
+sharded batch -- update, expansion, roll-outs, grouping, the exchange on the
+batch's stream (dense keys: all-reduce of the union of used slots, then of
+the packed exact int64 sums and first ids; sparse keys: SUM of the per-action
+partials and an all-gather of the ranks' child records), finalize -- in one
+call, with no Python between K2 and K3.
+
+The caller-driven form (begin -> `run_exchange` -> end) remains for a
+transport of the caller's choosing, e.g. gloo with host-staged device views
+(the CPU and two-process tests): one round of in-place collectives.
 """
 from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+
+
+def bootstrap_unique_id(group=None) -> bytes:
+    """Rank 0's 128-byte NCCL unique id on every rank (broadcast over the
+    process group; gloo or nccl)."""
+    from .despot import comm_unique_id
+    rank = dist.get_rank(group)
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    uid = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(comm_unique_id()), dtype=torch.uint8))
+    if dist.get_backend(group) == "nccl":
+        t = uid.cuda()
+        dist.broadcast(t, src=src, group=group)
+        uid = t.cpu()
+    else:
+        dist.broadcast(uid, src=src, group=group)
+    return bytes(uid.numpy().tobytes())
+
+
+def init_comm(group=None, device: int = 0):
+    """The library's communicator for this rank (SURVEY §8(e) bootstrap:
+    torch process group -> ncclGetUniqueId on rank 0 -> broadcast ->
+    ncclCommInitRank inside libdespot)."""
+    from .despot import Comm
+    uid = bootstrap_unique_id(group)
+    return Comm(uid, dist.get_rank(group), dist.get_world_size(group), device)
 
 
 def shard_ids(K: int, rank: int, world: int):
@@ -47,9 +81,9 @@ def round_views(ex, device):
 
 
 def exchange(sums: torch.Tensor, mins: torch.Tensor, group=None, maxs=None, gather=None):
-    """The collectives of one exchange round, in place: exact integer sums,
-    minima and maxima (order-independent), and the all-gather of the ranks'
-    blocks (`gather` = the whole [world * block] byte tensor; this rank's block
+    """The collectives of one exchange round, in place: exact integer sums and
+    minima (order-independent; `maxs` only for ABI-1 callers), and the
+    all-gather of the ranks' blocks (`gather` = the whole [world * block] byte tensor; this rank's block
     is already filled).  NCCL works on the device views directly; a host
     backend (gloo: the CPU tests, or device tensors staged through host
     memory) gets host copies."""
@@ -82,8 +116,7 @@ def exchange(sums: torch.Tensor, mins: torch.Tensor, group=None, maxs=None, gath
 
 
 def run_exchange(model, batch, ex, group=None):
-    """Every exchange round of a sharded batch (one for dense keys, two for
-    the driving model's sparse keys)."""
+    """The exchange round(s) of a caller-driven sharded batch (one in ABI 2)."""
     device = torch.device("cuda", model.device)
     world = dist.get_world_size(group)
     while True:
@@ -109,6 +142,8 @@ def _torch_stream(stream, device):
 
 
 def expand_sharded(model, leaves, group=None, device_outputs=False, child_capacity=None, stream=None):
+    if model.comm is not None:  # library-owned exchange: one call
+        return model.expand(leaves, device_outputs=device_outputs, child_capacity=child_capacity, stream=stream)
     batch, ex = model.expand_begin(leaves, stream=stream)
     try:
         # the collectives run on the batch's own stream (ordered after K2 and

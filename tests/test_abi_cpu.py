@@ -28,7 +28,7 @@ def test_library_builds_and_exports_every_declared_symbol():
         assert hasattr(lib, n), f"{n} declared in include/despot.h but not exported"
     assert sorted(despot.EXPORTS) == names
     lib.despot_abi_version.restype = ctypes.c_int
-    assert lib.despot_abi_version() == 1
+    assert lib.despot_abi_version() == 2
 
 
 def test_cubin_is_sm100a():
@@ -54,3 +54,11 @@ def test_bad_params_rejected_before_device_use():
     with pytest.raises(despot.DespotError) as e:
         despot.Model("rocksample", "n=7 robots=1 rocks=2:0,2:0 starts=0:3")  # two rocks on one cell
     assert e.value.code == -1
+
+
+def test_nccl_unique_id_without_a_gpu():
+    """despot_comm_unique_id resolves NCCL at run time (the torch-bundled copy
+    here) and needs no device: the bootstrap step of the multi-GPU path."""
+    import torch.distributed  # noqa: F401  (loads torch's libnccl into the process)
+    a, b = despot.comm_unique_id(), despot.comm_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b

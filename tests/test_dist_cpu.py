@@ -88,3 +88,32 @@ def test_shard_rule_partitions_ids():
         for r in range(world):
             ids = ddist.shard_ids(K, r, world)
             assert np.all(np.diff(ids) > 0) and np.all(ids % world == r)
+
+
+def _boot_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = ddist.bootstrap_unique_id()
+    q.put((rank, uid))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_communicator_bootstrap_world2_gloo():
+    """SURVEY §8(e) bootstrap of the library's NCCL communicator: rank 0's
+    ncclGetUniqueId (through libdespot, NCCL resolved at run time) reaches
+    every rank over the process group, byte for byte.  (ncclCommInitRank
+    itself needs the GPUs.)"""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_boot_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(got[0]) == 128 and got[0] == got[1] and any(got[0])
