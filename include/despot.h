@@ -231,6 +231,22 @@ int despot_expand_batch_bytes(despot_model* model, const despot_leaf* leaves, ui
 int despot_expand_batch(despot_model* model, const despot_leaf* leaves, uint32_t L,
                         despot_expansion* out, void* stream);
 
+/* Prepared batches (SURVEY §7 hard part 6: launch overhead of small, repeated
+ * batches).  despot_batch_prepare validates the leaves, allocates the batch's
+ * scratch and staging once, binds `out` (its flags, capacities and array
+ * pointers are fixed from here on) and captures the batch's device work --
+ * setup copies, K1, K2, K3 and the result copies -- into one CUDA graph.
+ * despot_batch_run then allocates the new nodes' arenas, patches the leaf
+ * table and launches the graph: every step of the batch runs again, with the
+ * host cost of one graph launch.  Each run returns new nodes exactly as
+ * despot_expand_batch does.  Single GPU, no RECORD; a run fails with EINVAL if
+ * a parent was released.  Runs of one prepared batch must not overlap. */
+typedef struct despot_prepared despot_prepared;
+int despot_batch_prepare(despot_model* model, const despot_leaf* leaves, uint32_t L, despot_expansion* out,
+                         despot_prepared** prepared_out);
+int despot_batch_run(despot_prepared* prepared, despot_expansion* out, void* stream);
+int despot_batch_prepared_free(despot_prepared* prepared);
+
 /* Multi-GPU scenario sharding driven by the caller, the form
  * for a caller-supplied transport (despot_expand_batch with a communicator is
  * the library-owned form): every rank calls with identical leaves; between

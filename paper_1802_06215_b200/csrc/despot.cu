@@ -177,6 +177,12 @@ struct HostTrace {
   }
 };
 static thread_local HostTrace g_ht;
+// set while despot_batch_prepare captures a batch's device work into a CUDA
+// graph: allocations are made outside the stream (cudaMalloc), the new
+// arenas are not allocated at all (each run allocates its own and patches
+// the leaf table), and the new nodes are templates (not registered)
+static thread_local bool g_capture = false;
+constexpr uintptr_t kTemplateBase = uintptr_t(1) << 40;  // arena base of a prepared batch's template nodes
 
 struct Node {
   despot_model* model;
@@ -236,7 +242,10 @@ struct despot_batch {
   SparseItemOut io{};
   void* pinned = nullptr;  // leaf-table staging, owned until the batch syncs
   void* stage = nullptr;   // device output staging (host outputs)
+  char* hs = nullptr;      // pinned status read-back
+  char* hp_out = nullptr;  // pinned output staging
   bool bound = false;      // outputs bound (bind_outputs)
+  bool persistent = false; // a prepared batch's (graph-captured) batch: scratch, staging, events kept
   bool k3_fused = false;   // the finalize runs in K2's last CTA
   size_t o_ns = 0, o_w = 0, o_ar = 0, o_au = 0, o_al = 0, o_cb = 0, o_cc = 0, o_cf = 0, o_cw = 0, o_cu = 0,
          o_cl = 0, o_co = 0, o_so = 0;  // staging layout
@@ -252,6 +261,9 @@ struct despot_batch {
   uint64_t gblk = 0, gn_max = 0;  // block bytes; the largest global scenario count of a leaf
   uint32_t hdr_pad = 0, rec_bytes = 0;
   XDev x{};                       // packed exchange (dense keys, xlib)
+  size_t new_bytes = 0;           // bytes of the new arenas of one run
+  size_t o_leaves = 0;            // the leaf table's offset in the scratch and the pinned staging
+  std::vector<LeafDev> ld;        // the leaf table (a prepared batch patches the new arenas' pointers)
   uint32_t x_rounds = 0;          // collective rounds issued by the library
   uint64_t x_bytes = 0;           // bytes this rank contributed to them
   bool timing = false, timing_k2 = false;  // DESPOT_X_TIMING / DESPOT_X_TIMING_K2 (K2 events only)
@@ -259,7 +271,10 @@ struct despot_batch {
   uint64_t h2d = 0, d2h = 0;  // host <-> device bytes copied for this batch
   cudaEvent_t ev[kBatchEvents] = {};  // DESPOT_X_TIMING: 0 call start, 1/2 K1, 3/4 K2, 5/6 K3, 7 end, 8/9 K4
   void mark(int i) {
-    if (timing && (!timing_k2 || i == 3 || i == 4)) cudaEventRecord(ev[i], stream);
+    // (in a prepared batch's graph capture: external event-record nodes, so
+    // every launch of the graph records them)
+    if (timing && (!timing_k2 || i == 3 || i == 4))
+      cudaEventRecordWithFlags(ev[i], stream, persistent ? cudaEventRecordExternal : cudaEventRecordDefault);
   }
 };
 
@@ -863,6 +878,11 @@ static void free_batch(despot_batch* b, bool drop_new_nodes) {
         b->leaf_node[l] = nullptr;
       }
   }
+  if (b->persistent) {  // a prepared batch: only this run's state goes
+    b->new_block.reset();
+    for (size_t l = 0; l < b->leaf_node.size(); ++l) b->leaf_node[l] = nullptr;
+    return;
+  }
   if (b->scratch) cudaFreeAsync(b->scratch, b->stream);
   if (b->stage) cudaFreeAsync(b->stage, b->stream);
   if (b->gbuf) cudaFreeAsync(b->gbuf, b->stream);
@@ -959,6 +979,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   b->sharded_sparse = b->sparse && (m->world > 1 || b->xlib);
   b->flags = flags;
   b->leaves.assign(leaves, leaves + L);
+  b->persistent = g_capture;
   b->timing = flags & (DESPOT_X_TIMING | DESPOT_X_TIMING_K2);
   b->timing_k2 = (flags & DESPOT_X_TIMING_K2) && !(flags & DESPOT_X_TIMING);
   if (b->timing) {
@@ -999,13 +1020,16 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   }
   g_ht.mark("validated");
   cudaStream_t st = b->stream;
-  if (new_bytes) {
+  b->new_bytes = new_bytes;
+  if (new_bytes && !g_capture) {
     b->new_block = std::make_shared<Block>();
     b->new_block->stream = st;
     CU(cudaMallocAsync(&b->new_block->ptr, new_bytes, st));
   }
   g_ht.mark("arena_alloc");
-  char* np = b->new_block ? static_cast<char*>(b->new_block->ptr) : nullptr;
+  // (capture: template nodes carved from a fixed fake base; every run rebases them)
+  char* np = b->new_block ? static_cast<char*>(b->new_block->ptr)
+                          : (g_capture ? reinterpret_cast<char*>(kTemplateBase) : nullptr);
   std::vector<LeafDev> ld(L);
   for (uint32_t l = 0; l < L; ++l) {
     const despot_leaf& lf = leaves[l];
@@ -1051,11 +1075,12 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     d.wroot = p->wroot;
     d.inv_wroot = 1.0 / p->wroot;
   }
-  {
+  if (!g_capture) {
     std::lock_guard<std::mutex> g(m->mu);
     for (uint32_t l = 0; l < L; ++l)
       if (b->is_new[l]) m->nodes.insert(b->leaf_node[l]);
   }
+  b->ld = ld;
   g_ht.mark("leaf_table");
   // scratch: leaves | n_leaf | tile_off | scen_off | sums | mins | rank | nc | err
   const uint64_t LA = (uint64_t)L * dm.A, LAS = LA * b->S;
@@ -1093,7 +1118,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   x.ccap = std::min<uint64_t>(LAS, (LA * m->xratio16.load() + 15) / 16 + 256);
   const size_t o_xflags = take(xdense ? (size_t)x.nblk * kXBlk : 0), o_xcnt = take(xdense ? 4 * (size_t)x.nblk : 0),
                o_xcpk = take(xdense ? 8 * (4 * x.ccap + x.qn) : 0), o_xcmin = take(xdense ? 4 * x.ccap : 0);
-  if (cudaMallocAsync(&b->scratch, off, st) != cudaSuccess) {
+  if ((g_capture ? cudaMalloc(&b->scratch, off) : cudaMallocAsync(&b->scratch, off, st)) != cudaSuccess) {
     free_batch(b.release(), true);
     return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
   }
@@ -1156,6 +1181,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   const size_t h2d_bytes = all_self ? o_stat + stat_bytes : sizeof(LeafDev) * L;
   void* hp = pinned_pool().acquire(h2d_bytes);
   b->pinned = hp;
+  b->o_leaves = o_leaves;
   int rc = DESPOT_OK;
   if (!hp) rc = set_err(DESPOT_ENOMEM, "pinned staging");
   if (!rc) {
@@ -1516,7 +1542,7 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
     bd.scen_hash = out->scen_hash;
     bd.scen_states = out->scen_states;
   } else {
-    if (cudaMallocAsync(&stage, so, st) != cudaSuccess) {
+    if ((b->persistent ? cudaMalloc(&stage, so) : cudaMallocAsync(&stage, so, st)) != cudaSuccess) {
       free_batch(b, true);
       return set_err(DESPOT_ENOMEM, "output staging (%zu bytes)", so);
     }
@@ -1570,7 +1596,11 @@ static bool outputs_pinned(const despot_expansion* out, uint32_t C) {
 
 // Completes a bound batch: [K2 for RECORD] -> K3 (unless fused into K2) ->
 // status and outputs to the host -> frees the batch.
-static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st) {
+// finish_batch modes: the whole completion (the plain call), only the device
+// work up to the copies (captured into a prepared batch's graph), or only the
+// host side after a prepared batch's graph launch
+enum FinishMode { kFinishFull = 0, kFinishEnqueue = 1, kFinishComplete = 2 };
+static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st, int mode = kFinishFull) {
   despot_model* m = b->model;
   const DevModel& dm = m->host;
   const uint32_t L = b->L;
@@ -1584,7 +1614,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
                o_cc = b->o_cc, o_cf = b->o_cf, o_cw = b->o_cw, o_cu = b->o_cu, o_cl = b->o_cl, o_co = b->o_co,
                o_so = b->o_so;
   int rc = DESPOT_OK;
-  if (record && b->sparse) {
+  if (mode == kFinishComplete) {
+  } else if (record && b->sparse) {
     rc = launch_k2_sparse(m, b, true);
   } else if (record) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
@@ -1657,20 +1688,27 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     b->mark(6);
     return rc;
   };
-  if (!rc) rc = launch_k3();
+  if (!rc && mode != kFinishComplete) rc = launch_k3();
   g_ht.mark("k3");
   // status block: err | total children | steps | ticket | pad | n_leaf[L]
   const size_t stat_bytes = 4 * kStatWords + 4 * (size_t)L;
-  char* hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
+  // (a prepared batch keeps its status and output staging: its graph copies into them)
+  if (!b->hs) b->hs = static_cast<char*>(pinned_pool().acquire(stat_bytes + 64));
+  char* hs = b->hs;
   struct PinGuard {
-    void* p;
-    ~PinGuard() { pinned_pool().release(p); }
-  } pin_guard{hs};
+    despot_batch* b;
+    ~PinGuard() {
+      if (!b->persistent) {
+        pinned_pool().release(b->hs);
+        b->hs = nullptr;
+      }
+    }
+  } pin_guard{b};
   if (!rc && !hs) rc = set_err(DESPOT_ENOMEM, "pinned staging");
   // host outputs: the staging block [per-leaf | per-action | CSR | children]
   // goes to one pinned buffer; when it is small (search-sized batches) the
   // whole block travels in this first copy and no second round trip is needed
-  char* hp_out = nullptr;
+  char*& hp_out = b->hp_out;
   const size_t head_bytes = o_cc, body_bytes = o_so;
   // page-locked caller buffers: every array is copied straight into them (no
   // staging, no host memcpy); else the head goes through the library's pinned
@@ -1680,13 +1718,17 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
   const bool pinned_out = !dev_out && !record && !small && outputs_pinned(out, C);
   const bool one_copy = small;
   struct PinRelease {
-    char*& p;
+    despot_batch* b;
     ~PinRelease() {
-      if (p) pinned_pool().release(p);
+      if (b->hp_out && !b->persistent) {
+        pinned_pool().release(b->hp_out);
+        b->hp_out = nullptr;
+      }
     }
-  } pin_out_guard{hp_out};
-  auto copy_and_sync = [&]() -> int {
+  } pin_out_guard{b};
+  auto copy_and_sync = [&](bool enqueue, bool sync) -> int {
     int rc = DESPOT_OK;
+    if (enqueue) {
     if (!rc) {
       b->d2h += stat_bytes;
       if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
@@ -1715,14 +1757,16 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
     }
     g_ht.mark("d2h_enqueued");
     b->mark(7);  // end of the call's device work (before the host waits: no extra round trip)
-    if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
+    }
+    if (sync && !rc && cudaStreamSynchronize(st) != cudaSuccess) {
       m->failed = true;
       rc = set_err(DESPOT_ECUDA, "batch failed: %s", cudaGetErrorString(cudaGetLastError()));
     }
     g_ht.mark("synced");
     return rc;
   };
-  if (!rc) rc = copy_and_sync();
+  if (!rc) rc = copy_and_sync(mode != kFinishComplete, mode != kFinishEnqueue);
+  if (mode == kFinishEnqueue) return rc;  // a prepared batch's capture ends here
   if (!rc && b->xlib && !b->sparse) {
     // the packed exchange's capacity hint follows the largest union seen (+ 1/4)
     uint32_t T = 0, e0 = 0;
@@ -1738,7 +1782,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st)
         rc = set_err(DESPOT_ECUDA, "capacity retry reset failed");
       if (!rc) rc = lib_exchange_dense(b);
       if (!rc) rc = launch_k3();
-      if (!rc) rc = copy_and_sync();
+      if (!rc) rc = copy_and_sync(true, true);
     }
   }
   uint32_t err = 0, nchildren = 0;
@@ -1864,6 +1908,157 @@ extern "C" int despot_expand_batch(despot_model* m, const despot_leaf* leaves, u
     return rc;
   }
   return despot_expand_end(b, out, stream);
+}
+
+// ===========================================================================
+// prepared batches: one CUDA graph per repeated batch (SURVEY §7 hard part 6)
+// ===========================================================================
+struct despot_prepared {
+  despot_model* m = nullptr;
+  despot_batch* b = nullptr;       // persistent: scratch, staging, events, bound outputs
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Node> tmpl;          // per leaf: the new node's template (arena at kTemplateBase)
+  std::vector<despot_leaf> leaves;
+  despot_expansion out{};          // the outputs the graph copies into
+  uint32_t launches = 0;
+  uint64_t h2d = 0, d2h = 0;
+};
+
+static void free_prepared(despot_prepared* p) {
+  if (!p) return;
+  cudaSetDevice(p->m->device);
+  if (p->exec) cudaGraphExecDestroy(p->exec);
+  if (p->graph) cudaGraphDestroy(p->graph);
+  if (despot_batch* b = p->b) {
+    cudaDeviceSynchronize();
+    if (b->scratch) cudaFree(b->scratch);
+    if (b->stage) cudaFree(b->stage);
+    if (b->pinned) pinned_pool().release(b->pinned);
+    if (b->hs) pinned_pool().release(b->hs);
+    if (b->hp_out) pinned_pool().release(b->hp_out);
+    if (b->timing) event_pool().release(b->ev);
+    delete b;
+  }
+  delete p;
+}
+
+extern "C" int despot_batch_prepare(despot_model* m, const despot_leaf* leaves, uint32_t L, despot_expansion* out,
+                                    despot_prepared** prep) {
+  if (!m || !leaves || !out || !prep) return set_err(DESPOT_EINVAL, "null argument");
+  if (m->world > 1 || (m->comm && (m->flags & DESPOT_MF_EXCHANGE)))
+    return set_err(DESPOT_EINVAL, "prepared batches are single-GPU (world == 1, no exchange)");
+  if (out->flags & DESPOT_X_RECORD_SCENARIO) return set_err(DESPOT_EINVAL, "prepared batches do not RECORD");
+  CU(cudaSetDevice(m->device));
+  std::unique_ptr<despot_prepared> p(new despot_prepared());
+  p->m = m;
+  p->leaves.assign(leaves, leaves + L);
+  cudaStream_t cs;
+  CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+    cudaStreamDestroy(cs);
+    return set_err(DESPOT_ECUDA, "cudaStreamBeginCapture failed");
+  }
+  g_capture = true;
+  despot_batch* b = nullptr;
+  int rc = begin_impl(m, leaves, L, out->flags, cs, out, &b);
+  if (!rc) rc = finish_batch(b, out, cs, kFinishEnqueue);
+  g_capture = false;
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+  cudaStreamDestroy(cs);
+  if (b) {
+    p->b = b;  // owned from here (free_prepared releases it)
+    for (uint32_t l = 0; l < L; ++l) {
+      p->tmpl.push_back(b->is_new[l] ? *b->leaf_node[l] : Node{});
+      if (b->is_new[l]) delete b->leaf_node[l];  // templates only: never registered
+      b->leaf_node[l] = nullptr;
+    }
+  }
+  p->graph = g;
+  if (!rc && (ce != cudaSuccess || !g)) rc = set_err(DESPOT_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+  if (!rc && cudaGraphInstantiate(&p->exec, g, 0) != cudaSuccess)
+    rc = set_err(DESPOT_ECUDA, "cudaGraphInstantiate failed");
+  if (rc) {
+    cudaGetLastError();
+    free_prepared(p.release());
+    return rc;
+  }
+  p->out = *out;
+  p->launches = b->launches;
+  p->h2d = b->h2d;
+  p->d2h = b->d2h;
+  *prep = p.release();
+  return DESPOT_OK;
+}
+
+extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void* stream) {
+  if (!p || !out) return set_err(DESPOT_EINVAL, "null argument");
+  despot_model* m = p->m;
+  despot_batch* b = p->b;
+  if (m->failed) return set_err(DESPOT_ESHUTDOWN, "model failed earlier");
+  if (out->flags != p->out.flags || out->child_capacity != p->out.child_capacity ||
+      out->child_count != p->out.child_count || out->n_scen != p->out.n_scen)
+    return set_err(DESPOT_EINVAL, "despot_batch_run: outputs differ from the prepared ones");
+  CU(cudaSetDevice(m->device));
+  g_ht.start();
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t L = b->L;
+  // the parents must still exist (their arenas are in the graph's leaf table)
+  for (uint32_t l = 0; l < L; ++l)
+    if (!lookup(m, p->leaves[l].parent)) return set_err(DESPOT_EINVAL, "leaf %u: parent released", l);
+  // this run's arenas, the nodes, and the leaf table the graph uploads
+  b->stream = st;
+  if (b->new_bytes) {
+    b->new_block = std::make_shared<Block>();
+    b->new_block->stream = st;
+    CU(cudaMallocAsync(&b->new_block->ptr, b->new_bytes, st));
+  }
+  const intptr_t shift = b->new_block ? static_cast<char*>(b->new_block->ptr) - reinterpret_cast<char*>(kTemplateBase) : 0;
+  auto rebase = [shift](auto* q) { return reinterpret_cast<decltype(q)>(reinterpret_cast<char*>(q) + shift); };
+  LeafDev* hl = reinterpret_cast<LeafDev*>(static_cast<char*>(b->pinned) + b->o_leaves);
+  {
+    std::lock_guard<std::mutex> g(m->mu);
+    for (uint32_t l = 0; l < L; ++l) {
+      const despot_leaf& lf = p->leaves[l];
+      if (lf.action < 0) {
+        b->leaf_node[l] = reinterpret_cast<Node*>(lf.parent);
+        b->is_new[l] = false;
+        continue;
+      }
+      Node* nd = new Node(p->tmpl[l]);
+      nd->block = b->new_block;
+      nd->ids = rebase(nd->ids);
+      nd->w = rebase(nd->w);
+      nd->states = rebase(nd->states);
+      nd->nchild = rebase(nd->nchild);
+      nd->keys = rebase(nd->keys);
+      m->nodes.insert(nd);
+      b->leaf_node[l] = nd;
+      b->is_new[l] = true;
+      LeafDev& d = hl[l];
+      d.ids = nd->ids;
+      d.w = nd->w;
+      d.states = nd->states;
+      d.keys = nd->keys;
+      d.nchild = nd->nchild;
+    }
+  }
+  b->launches = p->launches;
+  b->h2d = p->h2d;
+  b->d2h = p->d2h;
+  g_ht.mark("patched");
+  if (cudaGraphLaunch(p->exec, st) != cudaSuccess) {
+    free_batch(b, true);
+    return set_err(DESPOT_ECUDA, "cudaGraphLaunch failed");
+  }
+  g_ht.mark("graph_launched");
+  return finish_batch(b, out, st, kFinishComplete);
+}
+
+extern "C" int despot_batch_prepared_free(despot_prepared* p) {
+  free_prepared(p);
+  return DESPOT_OK;
 }
 
 extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* upper_mean, float* lower_mean,

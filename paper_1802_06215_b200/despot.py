@@ -32,7 +32,8 @@ EXPORTS = ["despot_last_error", "despot_abi_version", "despot_model_load", "desp
            "despot_node_release", "despot_node_release_many", "despot_expand_batch", "despot_expand_begin", "despot_batch_exchange",
            "despot_expand_end", "despot_batch_abort", "despot_rollout_bounds", "despot_stream_words",
            "despot_search", "despot_plan", "despot_philox_ceiling", "despot_expand_batch_bytes",
-           "despot_comm_unique_id", "despot_comm_init", "despot_comm_destroy", "despot_comm_info"]
+           "despot_comm_unique_id", "despot_comm_init", "despot_comm_destroy", "despot_comm_info",
+           "despot_batch_prepare", "despot_batch_run", "despot_batch_prepared_free"]
 
 
 def _tflag(timing):
@@ -168,6 +169,9 @@ def lib():
         L.despot_search.argtypes = [C.POINTER(SearchProblem), C.POINTER(SearchConfig), C.POINTER(SearchResult),
                                     vp, u32]
         L.despot_plan.argtypes = [vp, u64, C.POINTER(SearchConfig), C.POINTER(SearchResult), vp]
+        L.despot_batch_prepare.argtypes = [vp, C.POINTER(Leaf), u32, C.POINTER(Expansion), C.POINTER(vp)]
+        L.despot_batch_run.argtypes = [vp, C.POINTER(Expansion), vp]
+        L.despot_batch_prepared_free.argtypes = [vp]
         L.despot_comm_unique_id.argtypes = [vp]
         L.despot_comm_init.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.despot_comm_destroy.argtypes = [vp]
@@ -224,6 +228,26 @@ class Comm:
             self.h = C.c_void_p()
 
 
+class _Prepared:
+    """Owner of a despot_prepared: freed with the prepared dict, or by the
+    model's close() (whichever comes first)."""
+
+    def __init__(self, h, model):
+        self.h = h
+        model._prepared.add(self)
+
+    def free(self):
+        if self.h:
+            lib().despot_batch_prepared_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class Model:
     """A loaded model (despot_model*)."""
 
@@ -231,6 +255,8 @@ class Model:
                  flags: int = 0, comm: "Comm | None" = None):
         self.h = C.c_void_p()
         self.comm = comm  # kept alive as long as the model
+        import weakref
+        self._prepared = weakref.WeakSet()
         o = Opts(device, rank, world, flags, comm.h.value if comm is not None else None)
         _check(lib().despot_model_load(kind.encode(), params.encode(), C.byref(o), C.byref(self.h)))
         info = ModelInfo()
@@ -241,6 +267,8 @@ class Model:
         self.gamma, self.tail = info.gamma, info.tail
 
     def close(self):
+        for p in list(self._prepared):
+            p.free()
         if self.h:
             lib().despot_model_free(self.h)
             self.h = C.c_void_p()
@@ -399,23 +427,34 @@ class Model:
         return self._finish(o, E, L, nodes, record, device_outputs)
 
     # ---- prepared calls (repeated batches: no per-call marshalling) ----
-    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False, pinned=False):
-        """Build the ctypes leaf table, output arrays and expansion struct of a
-        batch once; `run_prepared` then costs one foreign call.  pinned: host
-        outputs in page-locked memory (copied into directly)."""
+    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False, pinned=False, graph=True):
+        """A repeated batch: the leaf table, output arrays and expansion struct
+        built once, and (graph=True, single GPU) despot_batch_prepare's CUDA
+        graph of the batch's device work; `run_prepared` then costs one
+        foreign call (despot_batch_run: new arenas, leaf-table patch, one
+        graph launch).  pinned: host outputs in page-locked memory (copied
+        into directly)."""
         L = len(leaves)
         C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
         o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs, pinned=pinned)
         nodes = (C.c_uint64 * L)()
         E.node = C.addressof(nodes)
         E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | _tflag(timing)
-        return {"lv": self._leaves(leaves), "L": L, "E": E, "o": o, "nodes": nodes, "ref": C.byref(E),
-                "leaves": list(leaves)}
+        prep = {"lv": self._leaves(leaves), "L": L, "E": E, "o": o, "nodes": nodes, "ref": C.byref(E),
+                "leaves": list(leaves), "graph": None}
+        if graph and self.world == 1 and self.comm is None:
+            g = C.c_void_p()
+            _check(lib().despot_batch_prepare(self.h, prep["lv"], L, prep["ref"], C.byref(g)))
+            prep["graph"] = _Prepared(g, self)
+        return prep
 
     def run_prepared(self, prep, stream=None):
-        """despot_expand_batch on a prepared batch; returns (scenario_steps,
-        launches, node handles); outputs are in prep["o"], prep["E"]."""
-        _check(lib().despot_expand_batch(self.h, prep["lv"], prep["L"], prep["ref"], _stream_ptr(stream)))
+        """One run of a prepared batch; returns (scenario_steps, launches,
+        node handles); outputs are in prep["o"], prep["E"]."""
+        if prep["graph"] is not None:
+            _check(lib().despot_batch_run(prep["graph"].h, prep["ref"], _stream_ptr(stream)))
+        else:
+            _check(lib().despot_expand_batch(self.h, prep["lv"], prep["L"], prep["ref"], _stream_ptr(stream)))
         E = prep["E"]
         return E.scenario_steps, E.launches, prep["nodes"]
 

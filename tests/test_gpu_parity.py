@@ -864,3 +864,66 @@ def test_mars_edge_states_match_oracle():
     assert G1["scenario_steps"] == O1["scenario_steps"]
     _timed_form_equals_record(gm, [(gr, a, c, 1) for a, c in lv], G1)
     gm.close()
+
+
+def test_prepared_graph_runs_equal_plain_calls():
+    """despot_batch_prepare / despot_batch_run (one CUDA graph per repeated
+    batch): every run equals the plain call bit for bit, returns new nodes
+    (distinct handles, usable as parents of the next batch), for dense and
+    sparse keys, roots and depth-1 leaves, host and device outputs; a run whose
+    parent was released fails cleanly."""
+    import torch
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+            "child_first", "child_weight", "child_upper", "child_lower", "child_obs")
+    for cfg, K, L in ((1, 100, 1), (2, 150, 12), (3, 120, 6)):
+        gm, om, st, w, seed, _ = setup(cfg, K=K, L=L)
+        gr = gm.belief_load(st, w, seed)
+        R = gm.expand([(gr, -1, 0, 0)])
+        lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)]
+        for leaves in ([(gr, -1, 0, 0)], lv):
+            ref = gm.expand(leaves)
+            for dev in (False, True):
+                P = gm.prepare(leaves, device_outputs=dev, pinned=not dev)
+                assert P["graph"] is not None
+                seen = set()
+                for run in range(3):
+                    steps, launches, nodes = gm.run_prepared(P)
+                    torch.cuda.synchronize()
+                    assert steps == ref["scenario_steps"]
+                    for k in keys:
+                        r = np.asarray(ref[k]).reshape(-1)
+                        got = P["o"][k]
+                        got = got.cpu().numpy() if dev else np.asarray(got)
+                        got = got.reshape(-1)[: len(r)]
+                        assert np.array_equal(got.view(r.dtype) if got.dtype != r.dtype else got, r), (cfg, k, run)
+                    new = [int(n) for lf, n in zip(leaves, nodes) if lf[1] >= 0]
+                    assert not (set(new) & seen)
+                    seen |= set(new)
+                    if new and run == 2:  # a prepared run's node is a parent like any other
+                        G2 = gm.expand([(new[0], 0, 0, 2)])
+                        assert G2["n_scen"][0] > 0
+        gm.close()
+    # sparse keys (driving roots)
+    params = inputs.car_params(6, D=30)
+    cm = Model("car", params)
+    cl = [(cm.belief_load(s, w_, sd), -1, 0, 0) for s, w_, sd in inputs.car_roots(4, 60, peds=6)]
+    ref = cm.expand(cl)
+    P = cm.prepare(cl, pinned=True)
+    for run in range(2):
+        cm.run_prepared(P)
+        for k in keys:
+            r = np.asarray(ref[k]).reshape(-1)
+            assert np.array_equal(np.asarray(P["o"][k]).reshape(-1)[: len(r)], r), k
+    # a released parent
+    gm, om, st, w, seed, _ = setup(2, K=60, L=2)
+    gr = gm.belief_load(st, w, seed)
+    R = gm.expand([(gr, -1, 0, 0)])
+    lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, 2)]
+    G1 = gm.expand(lv)
+    leaves2 = [(G1["node"][0], 3, 0, 2)]
+    P = gm.prepare(leaves2)
+    gm.run_prepared(P)
+    gm.node_release(G1["node"][0])
+    with pytest.raises(DespotError):
+        gm.run_prepared(P)
+    gm.close()
