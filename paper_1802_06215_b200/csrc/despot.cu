@@ -422,6 +422,9 @@ int build_model(const char* kind, const std::string& params, DevModel& dm) {
     pxy(params, "landmarks", lx, ly);
     dm.t_fail = thresh(pd(params, "p_fail", 0.03));
     dm.t_flip = thresh(pd(params, "p_flip", 0.03));
+    // the device compares 32-bit words with 32-bit thresholds (R14: T < 2^32)
+    if (dm.t_fail >= (1ull << 32) || dm.t_flip >= (1ull << 32))
+      return set_err(DESPOT_EINVAL, "nav: p_fail and p_flip must be < 1");
     if (dm.n < 3 || dm.n > kNavMaxN || dm.wall_y <= 0 || dm.wall_y >= dm.n - 1)
       return set_err(DESPOT_EINVAL, "nav: need 3 <= n <= 16 and 0 < wall_y < n-1");
     // cell classes: rows 0 and n-1 known free, wall row obstacles except the

@@ -488,13 +488,23 @@ struct Nav {
     int32_t n, wall_y, goal_x, goal_y;
     int32_t gate_x[2];
     int32_t n_unknown;
-    uint64_t t_fail, t_flip;
+    uint32_t t_fail, t_flip;  // T(p) < 2^32 (checked at load): an event is u < T
     uint32_t D;
     double tail;
+    double rew_d[4];          // step rewards by outcome code (stay, move / failed move, crash, goal), as
+    float rew_f[4];           //   the card's fp32 constants and their doubles
     double gpow[kGpowN];
     uint32_t known_rows[kNavMaxN + 2];  // padded rows of the border + known obstacles (gates open)
     uint16_t unk_pos[kNavMaxN * kNavMaxN];  // unknown index -> (x+1) | (y+1) << 8
+    uint8_t nb_lut[512];      // 3x3 window bits (row above | row | row below, 3 bits each) -> the
+                              //   neighbour occupancy bits N, NE, E, SE, S, SW, W, NW
+    uint8_t pol_lut[64];      // pi0: (E, SE, S, SW, W readings) | (t odd) << 5 -> action
   };
+  // per-action displacement, 2 bits each (d + 1), actions 0 STAY, 1..8 = N, NE, E, SE, S, SW, W, NW
+  static constexpr uint32_t kDX = (1u << 0) | (1u << 2) | (2u << 4) | (2u << 6) | (2u << 8) | (1u << 10) | (0u << 12) |
+                                  (0u << 14) | (0u << 16);
+  static constexpr uint32_t kDY = (1u << 0) | (0u << 2) | (0u << 4) | (1u << 6) | (2u << 8) | (2u << 10) | (2u << 12) |
+                                  (1u << 14) | (0u << 16);
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     if (tid == 0) {
       sm.n = dm.n;
@@ -504,10 +514,31 @@ struct Nav {
       sm.gate_x[0] = dm.gate_x[0];
       sm.gate_x[1] = dm.gate_x[1];
       sm.n_unknown = dm.nav_unknown;
-      sm.t_fail = dm.t_fail;
-      sm.t_flip = dm.t_flip;
+      sm.t_fail = (uint32_t)dm.t_fail;
+      sm.t_flip = (uint32_t)dm.t_flip;
       sm.D = dm.D;
       sm.tail = dm.tail;
+      // stay -0.2, failed move -0.1, crash -1 in place, move -0.1, goal +20
+      const float rf[4] = {-0.2f, -0.1f, -1.0f, 20.0f};
+      for (int k = 0; k < 4; ++k) {
+        sm.rew_f[k] = rf[k];
+        sm.rew_d[k] = (double)rf[k];
+      }
+    }
+    for (int i = tid; i < 512; i += nt) {
+      const uint32_t up = i & 7u, mid = (i >> 3) & 7u, dn = (i >> 6) & 7u;
+      sm.nb_lut[i] = (uint8_t)(((up >> 1) & 1u) | ((up >> 1) & 2u) | (mid & 4u) | ((dn & 4u) << 1) |
+                               ((dn & 2u) << 3) | ((dn & 1u) << 5) | ((mid & 1u) << 6) | ((up & 1u) << 7));
+    }
+    for (int i = tid; i < 64; i += nt) {
+      // bits of i: 0 E, 1 SE, 2 S, 3 SW, 4 W read occupied; bit 5: t odd
+      const bool odd = (i >> 5) & 1;
+      const int cand[5] = {5, 4, 6, odd ? 7 : 3, odd ? 3 : 7};  // S, SE, SW, then E/W by parity
+      const int bitof[9] = {-1, -1, -1, 0, 1, 2, 3, 4, -1};       // action -> bit of i
+      int a = 0;
+      for (int k = 4; k >= 0; --k)
+        if (!((i >> bitof[cand[k]]) & 1)) a = cand[k];
+      sm.pol_lut[i] = (uint8_t)a;
     }
     copy_words(sm.gpow, dm.gpow, sizeof(sm.gpow), tid, nt);
     copy_words(sm.known_rows, dm.nav_known_rows, sizeof(sm.known_rows), tid, nt);
@@ -551,7 +582,7 @@ struct Nav {
 #pragma unroll
     for (int k = 0; k < NW; ++k) s.occ[k] = st[(1 + k) * cap + i];
     build_grid(sm, s);
-    s.nb = neighbours(s.x, s.y);
+    s.nb = neighbours(sm, s.x, s.y);
     return s;
   }
   static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
@@ -564,42 +595,54 @@ struct Nav {
   static constexpr uint32_t kTerminalObs = 0x100u;
 
   // occupancy of the 8 neighbours of (x, y), bit k = direction k+1
-  // (N, NE, E, SE, S, SW, W, NW); off-grid counts as occupied
-  static __device__ __forceinline__ uint32_t neighbours(int x, int y) {
+  // (N, NE, E, SE, S, SW, W, NW); off-grid counts as occupied: the 3x3 window
+  // of the padded grid through a 512-entry table
+  static __device__ __forceinline__ uint32_t neighbours(const Sm& sm, int x, int y) {
     const uint32_t* g = grid();
-    const uint32_t up = g[y] >> x, mid = g[y + 1] >> x, dn = g[y + 2] >> x;
-    return ((up >> 1) & 1u) | ((up >> 1) & 2u) | ((mid & 4u)) | ((dn & 4u) << 1) | ((dn & 2u) << 3) |
-           ((dn & 1u) << 5) | ((mid & 1u) << 6) | ((up & 1u) << 7);
+    const uint32_t up = (g[y] >> x) & 7u, mid = (g[y + 1] >> x) & 7u, dn = (g[y + 2] >> x) & 7u;
+    return sm.nb_lut[up | (mid << 3) | (dn << 6)];
   }
-  // g(s, a, phi_t), branch-free so that roll-out lanes choosing different
-  // actions do not diverge
+  // the nine random words of a step (R13): u[0] move failure, u[1..8] the
+  // reading flips N .. NW -- blocks 0 and 1 whole, word 0 of block 2
+  struct Words {
+    uint4 b0, b1;
+    uint32_t w8;
+  };
+  template <class KeyT>
+  static __device__ __forceinline__ Words words(uint32_t id, uint32_t t, const KeyT& key) {
+    return Words{philox(id, t, 0u, 0u, key), philox(id, t, 1u, 0u, key), philox(id, t, 2u, 0u, key).x};
+  }
+  // g(s, a, phi_t) on the step's words, branch-free (integer selects) so that
+  // roll-out lanes choosing different actions do not diverge; rcode = the
+  // outcome (0 stay, 1 move or failed move, 2 crash, 3 goal), whose reward is
+  // the card's constant
+  static __device__ __forceinline__ bool step_words(const Sm& sm, St& s, int a, const Words& u, uint32_t t_fail,
+                                                    uint32_t t_flip, uint32_t& z, int& rcode) {
+    const uint32_t go = a != 0 ? 1u : 0u;                        // not STAY
+    const uint32_t fail = go & (u.b0.x < t_fail ? 1u : 0u);      // the attempt fails (0.03)
+    const uint32_t occ = ((s.nb << 1) >> a) & 1u;                 // the target cell (carried neighbourhood)
+    const uint32_t mv = go & ~fail & ~occ & 1u;
+    const int dx = (int)((kDX >> (2 * a)) & 3u) - 1, dy = (int)((kDY >> (2 * a)) & 3u) - 1;
+    s.x += (int)mv * dx;
+    s.y += (int)mv * dy;
+    const uint32_t goal = mv & (s.x == sm.goal_x ? 1u : 0u) & (s.y == sm.goal_y ? 1u : 0u);
+    rcode = (int)(go * (1u + (occ & ~fail) + 2u * goal));
+    s.term = goal != 0;
+    const uint32_t flips = (u.b0.y < t_flip ? 1u : 0u) | (u.b0.z < t_flip ? 2u : 0u) | (u.b0.w < t_flip ? 4u : 0u) |
+                           (u.b1.x < t_flip ? 8u : 0u) | (u.b1.y < t_flip ? 16u : 0u) |
+                           (u.b1.z < t_flip ? 32u : 0u) | (u.b1.w < t_flip ? 64u : 0u) |
+                           (u.w8 < t_flip ? 128u : 0u);
+    s.nb = neighbours(sm, s.x, s.y);  // of the new cell: the observation, and the next step's moves
+    z = goal ? kTerminalObs : (s.nb ^ flips);
+    return goal != 0;
+  }
   template <class KeyT>
   static __device__ __forceinline__ bool step(const Sm& sm, St& s, int a, uint32_t id, uint32_t t,
                                               const KeyT& key, uint32_t& z, float& r) {
-    const uint4 u0 = philox(id, t, 0u, 0u, key);
-    const uint4 u1 = philox(id, t, 1u, 0u, key);
-    const uint4 u2 = philox(id, t, 2u, 0u, key);
-    const uint32_t u[9] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w, u2.x};
-    const bool stay = a == 0;
-    const bool fail = !stay && event(u[0], sm.t_fail);
-    const int k = stay ? 0 : a - 1;  // direction a: 1 N, 2 NE, 3 E, 4 SE, 5 S, 6 SW, 7 W, 8 NW
-    const uint32_t occ = (s.nb >> k) & 1u;  // the neighbours of the current cell (carried)
-    const bool moves = !stay && !fail && !occ;
-    const int nx = s.x + ((a >= 2 && a <= 4) ? 1 : (a >= 6) ? -1 : 0);
-    const int ny = s.y + ((a == 1 || a == 2 || a == 8) ? -1 : (a >= 4 && a <= 6) ? 1 : 0);
-    s.x = moves ? nx : s.x;
-    s.y = moves ? ny : s.y;
-    const bool goal = moves && s.x == sm.goal_x && s.y == sm.goal_y;
-    // stay -0.2, failed move -0.1, crash -1 in place, move -0.1, goal +20
-    r = stay ? -0.2f : fail ? -0.1f : occ ? -1.0f : goal ? 20.0f : -0.1f;
-    s.term = goal;
-    uint32_t flips = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) flips |= (event(u[1 + q], sm.t_flip) ? 1u : 0u) << q;
-    s.nb = neighbours(s.x, s.y);  // of the new cell: the observation, and the next step's moves
-    const uint32_t obs = s.nb ^ flips;
-    z = goal ? kTerminalObs : obs;
-    return goal;
+    int rc;
+    const bool term = step_words(sm, s, a, words(id, t, key), sm.t_fail, sm.t_flip, z, rc);
+    r = sm.rew_f[rc];
+    return term;
   }
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
     const int gx = sm.gate_x[s.gate];
@@ -611,20 +654,10 @@ struct Nav {
     return 20.0 * sm.gpow[d - 1];
   }
   static __device__ __forceinline__ uint32_t initial_obs(const Sm&, const St&) { return 0u; }
-  // pi0: first of [S, SE, SW, t even ? E : W, t even ? W : E] read FREE
-  // (branch-free: the candidates are selected in reverse priority order, so
-  // roll-out lanes reading different observations do not diverge)
-  static __device__ __forceinline__ int policy(uint32_t z, uint32_t t) {
-    const uint32_t fr = ~z;
-    const bool even = (t & 1u) == 0u;
-    const int e1 = even ? 3 : 7, e2 = even ? 7 : 3;
-    int a = 0;
-    a = ((fr >> (e2 - 1)) & 1u) ? e2 : a;
-    a = ((fr >> (e1 - 1)) & 1u) ? e1 : a;
-    a = ((fr >> 5) & 1u) ? 6 : a;
-    a = ((fr >> 3) & 1u) ? 4 : a;
-    a = ((fr >> 4) & 1u) ? 5 : a;
-    return a;
+  // pi0: first of [S, SE, SW, t even ? E : W, t even ? W : E] read FREE,
+  // else STAY -- one table read (the E..W readings are bits 2..6 of z)
+  static __device__ __forceinline__ int policy(const Sm& sm, uint32_t z, uint32_t t) {
+    return sm.pol_lut[((z >> 2) & 31u) | ((t & 1u) << 5)];
   }
   template <bool TRACE, class KeyT>
   static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
@@ -632,15 +665,23 @@ struct Nav {
     double acc = 0.0;
     uint32_t t = t0;
     bool term = false;
-    while (t < sm.D && !term) {
-      const int a = policy(z, t);
+    const uint32_t t_fail = sm.t_fail, t_flip = sm.t_flip, D = sm.D;
+    const double* gp = sm.gpow - t0;  // gamma^(t - t0)
+    // the stream words do not depend on the state: each step draws the next
+    // step's words while its own state chain runs (instruction-level
+    // parallelism for the latency-bound long roll-outs)
+    Words u = words(id, t + 1, key);
+    while (t < D && !term) {
+      const int a = policy(sm, z, t);
       if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
-      float r;
-      term = step(sm, s, a, id, t + 1, key, z, r);
-      acc += sm.gpow[t - t0] * (double)r;
+      const Words cur = u;
+      u = words(id, t + 2, key);
+      int rc;
+      term = step_words(sm, s, a, cur, t_fail, t_flip, z, rc);
+      acc = __fma_rn(gp[t], sm.rew_d[rc], acc);
       ++t;
     }
-    if (!term) acc += sm.gpow[t - t0] * sm.tail;
+    if (!term) acc = __fma_rn(gp[t], sm.tail, acc);
     ret = acc;
     len = t - t0;
   }
