@@ -461,7 +461,7 @@ def main():
                     help="also time the oracle in one process per host core")
     ap.add_argument("--no-all-cores-baseline", dest="all_cores_baseline", action="store_false")
     ap.add_argument("--peds", type=int, default=None, help="pedestrians of the driving config (NEXT-3 study)")
-    ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread", "group"],
+    ap.add_argument("--car-variant", default="auto", choices=["auto", "warp", "thread", "group", "pair"],
                     help="driving kernel: factored warp per scenario, thread per scenario, or per-batch choice")
     ap.add_argument("--plan", action="store_true",
                     help="tree size per planning time: despot_plan vs the serial oracle-backed driver (NEXT-1/2)")
@@ -500,7 +500,7 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=dev)
     c, kind, params, st, w, seed, L = workload(args.config, args.K, args.peds)
-    mflags = {"auto": 0, "thread": 1, "warp": 2, "group": 4}[args.car_variant]
+    mflags = {"auto": 0, "thread": 1, "warp": 2, "group": 4, "pair": 16}[args.car_variant]
     comm = None
     if world > 1 and not one_gpu_test:
         # the library's own NCCL communicator (rank 0's unique id over the
@@ -663,7 +663,7 @@ def main():
         peds = c.get("peds", 20) if args.peds is None else args.peds
         big = q_bound >= num_sms * 256 or (peds <= 8 and q_bound >= num_sms * 4)
         tiny = q_bound < num_sms * 4
-        k2_name = {"thread": "k2_car_thread", "warp": "k2_car_warp", "group": "k2_car_group",
+        k2_name = {"thread": "k2_car_thread", "warp": "k2_car_warp", "group": "k2_car_group", "pair": "k2_car_group<B>",
                    "auto": "k2_car_thread" if big else "k2_car_warp" if tiny else "k2_car_group"}[args.car_variant]
     else:
         k2_name = "k2_expand_dense"

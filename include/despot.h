@@ -88,6 +88,9 @@ typedef struct {
 #define DESPOT_MF_GROUPED 4u    /* a lane group per scenario: lane q owns Philox block q
                                    (the car's word and pedestrians 4q-1 .. 4q+2),
                                    32 / ceil((P+1)/4) scenarios per warp */
+#define DESPOT_MF_PAIRED 16u    /* a lane pair per scenario: each lane owns half of a
+                                   step's Philox blocks (20 pedestrians: 3 blocks,
+                                   11 / 9 pedestrians), 16 scenarios per warp */
 #define DESPOT_MF_EXCHANGE 8u   /* with a communicator: run the exchange (pack,
                                    collectives, unpack) even when world == 1 -- the
                                    one-GPU test of the sharded data path */

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <type_traits>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -924,14 +925,28 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
   // in between (its packed lane groups beat both others at 8 roots x K = 64,
   // profiles/r01/peds_sweep.jsonl); a warp per scenario for the few-item
   // batches of a tree search (latency: all pedestrians of a step in parallel)
-  const bool forced = m->flags & (DESPOT_MF_UNFACTORED | DESPOT_MF_FACTORED | DESPOT_MF_GROUPED);
+  const bool forced = m->flags & (DESPOT_MF_UNFACTORED | DESPOT_MF_FACTORED | DESPOT_MF_GROUPED | DESPOT_MF_PAIRED);
   // (with <= 8 pedestrians the thread kernel also wins the middle range:
   // 8 roots x K = 64, 6 pedestrians: 0.107 ms vs 0.139 grouped, 0.231 warp)
   const bool big = q_bound >= (uint64_t)m->num_sms * 256 || (dm.peds <= 8 && q_bound >= (uint64_t)m->num_sms * 4),
              tiny = q_bound < (uint64_t)m->num_sms * 4;
   const bool grouped = (m->flags & DESPOT_MF_GROUPED) || (!forced && !big && !tiny);
   const bool unfactored = !grouped && ((m->flags & DESPOT_MF_UNFACTORED) || (!forced && big));
-  if (grouped) {
+  const bool paired = m->flags & DESPOT_MF_PAIRED;
+  if (paired) {  // a lane pair per scenario: lane q owns ceil(blocks / 2) Philox blocks
+    const uint32_t NB = ((uint32_t)dm.peds + 4) / 4, Bp = (NB + 1) / 2;
+    const uint64_t G = (NB + Bp - 1) / Bp, gpw = 32 / G;
+    const uint64_t warps = (q_bound + gpw - 1) / gpw;
+    auto pick = [&](auto bc) {
+      constexpr int BB = decltype(bc)::value;
+      return record ? k2_car_group<true, BB> : k2_car_group<false, BB>;
+    };
+    auto kern = Bp <= 1 ? pick(std::integral_constant<int, 1>{}) : Bp == 2 ? pick(std::integral_constant<int, 2>{})
+                : Bp == 3 ? pick(std::integral_constant<int, 3>{}) : pick(std::integral_constant<int, 4>{});
+    const int occ = kernel_occupancy((const void*)kern, 0, 128);
+    const uint64_t g = std::min<uint64_t>((warps + 3) / 4, (uint64_t)m->num_sms * occ);
+    kern<<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+  } else if (grouped) {
     const uint64_t G = ((uint64_t)dm.peds + 4) / 4, gpw = 32 / G;
     const uint64_t warps = (q_bound + gpw - 1) / gpw;
     auto kern = record ? k2_car_group<true> : k2_car_group<false>;

@@ -121,11 +121,14 @@ struct SparseItemOut {
 // ---------------------------------------------------------------------------
 // K2t: thread per (leaf, action, scenario)
 // ---------------------------------------------------------------------------
+#ifndef HD_CART_MINB
+#define HD_CART_MINB 3  // CTAs of 128 per SM (4: 128 registers with spills, measured slower)
+#endif
 template <class M, bool RECORD>
 // 3 CTAs of 128 per SM: 168 registers, no spills (without the bound ptxas
 // may take 181, which leaves 2 CTAs: 0.96 -> 1.25 ms on config 4; 4 CTAs
 // spill: 1.06 ms)
-__global__ void __launch_bounds__(128, 3) k2_car_thread(BatchDev b, SparseItemOut io) {
+__global__ void __launch_bounds__(128, HD_CART_MINB) k2_car_thread(BatchDev b, SparseItemOut io) {
   __shared__ typename M::Sm sm;
   M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -354,19 +357,24 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
 // policy's gap a minimum over the group.  32 / G scenarios per warp (five
 // for 20 pedestrians).  Bit-identical to K2t (same operation sequence per
 // element).  The group loops run warp-uniformly (shuffles need every lane).
+// B > 1: lane q owns B consecutive blocks (words 4Bq .. 4B(q+1)-1), so a group
+// has ceil(blocks / B) lanes -- e.g. B = 3 for 20 pedestrians: a lane pair
+// per scenario, sixteen scenarios per warp (DESPOT_MF_PAIRED).
 // ---------------------------------------------------------------------------
 #ifndef HD_CARG_MINB
 #define HD_CARG_MINB 6  // 80 registers: the best of 1, 5, 6, 8 CTAs per SM (config 4)
 #endif
-template <bool RECORD>
-__global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, SparseItemOut io) {
+template <bool RECORD, int B = 1>
+__global__ void __launch_bounds__(128, B == 1 ? HD_CARG_MINB : 4) k2_car_group(BatchDev b, SparseItemOut io) {
+  constexpr int W = 4 * B;  // words (elements) per lane
   __shared__ typename CarThreadT<1>::Sm sm;  // scalar parameters + gamma table + rotations
   CarThreadT<1>::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
   __syncthreads();
   const DevModel& dm = *b.model;
   const uint32_t OW = dm.OW, SW = dm.SW;
   const int P = sm.peds;
-  const uint32_t G = (uint32_t)(P + 1 + 3) / 4, GPW = 32 / G;  // lanes per scenario, scenarios per warp
+  const uint32_t NB = (uint32_t)(P + 1 + 3) / 4;                 // Philox blocks per step
+  const uint32_t G = (NB + B - 1) / B, GPW = 32 / G;             // lanes per scenario, scenarios per warp
   const uint32_t lane = threadIdx.x & 31, gw = lane / G, q = lane - gw * G;
   const bool in_group = gw < GPW;                 // the last 32 mod G lanes idle
   const uint32_t g0 = gw * G;                     // first lane of the group
@@ -396,16 +404,22 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
     float xc = 0.0f;
     uint32_t level = 0;
     bool term = true;
-    float px[4] = {0.0f, 0.0f, 0.0f, 0.0f}, py[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    uint32_t goal[4] = {0u, 0u, 0u, 0u};
+    float px[W], py[W];
+    uint32_t goal[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      px[k] = 0.0f;
+      py[k] = 0.0f;
+      goal[k] = 0u;
+    }
     if (valid) {
       xc = __uint_as_float(lf.states[i]);
       const uint32_t w1 = lf.states[cap + i];
       level = w1 & 0xFFu;
       term = (w1 >> 8) & 1u;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int p = (int)(4 * q) + k - 1;
+      for (int k = 0; k < W; ++k) {
+        const int p = (int)(W * q) + k - 1;
         if (p >= 0 && p < P) {
           px[k] = __uint_as_float(lf.states[(4 + 2 * p) * cap + i]);
           py[k] = __uint_as_float(lf.states[(5 + 2 * p) * cap + i]);
@@ -416,10 +430,18 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
     // one factored step g(s, a, phi_tt) of this lane's group (active: the
     // group still steps; inactive groups run the shuffles only)
     auto step = [&](bool active, int a, uint32_t tt, float& r) {
-      const uint4 wv = philox4x32_10(id, tt, q, 0u, lf.seed_lo, lf.seed_hi);  // words 4q .. 4q+3
-      const uint32_t ws[4] = {wv.x, wv.y, wv.z, wv.w};
+      uint32_t ws[W];  // words Wq .. Wq+W-1 (blocks Bq .. Bq+B-1)
+#pragma unroll
+      for (int bb = 0; bb < B; ++bb) {
+        uint4 wv = make_uint4(0u, 0u, 0u, 0u);
+        if (B == 1 || B * q + bb < NB) wv = philox4x32_10(id, tt, B * q + (uint32_t)bb, 0u, lf.seed_lo, lf.seed_hi);
+        ws[4 * bb] = wv.x;
+        ws[4 * bb + 1] = wv.y;
+        ws[4 * bb + 2] = wv.z;
+        ws[4 * bb + 3] = wv.w;
+      }
       // 1. the car: lane 0's word 0 decides the failure
-      const int fail0 = event(wv.x, sm.t_fail) ? 1 : 0;
+      const int fail0 = event(ws[0], sm.t_fail) ? 1 : 0;
       const bool fail = __shfl_sync(0xffffffffu, fail0, in_group ? g0 : lane) != 0;
       if (active && !fail) {
         if (a == 1 && level < 4u) level += 1u;
@@ -430,8 +452,8 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
       // 2. pedestrians, 3. collision
       bool hit = false;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int p = (int)(4 * q) + k - 1;
+      for (int k = 0; k < W; ++k) {
+        const int p = (int)(W * q) + k - 1;
         if (active && p >= 0 && p < P) {
           const float2 cs = sm.rot[car_noise_index(ws[k])];
           car_ped_move(px[k], py[k], goal[k], cs.x, cs.y);
@@ -449,11 +471,11 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
     step(live0, (int)a0, lf.depth + 1, r0);
     if (!live0) r0 = 0.0f;
     if (live0 && q == 0) ++steps_acc;
-    // the child's key: this lane's words 4q .. 4q+3 (word 0: the car)
+    // the child's key: this lane's words Wq .. Wq+W-1 (word 0: the car)
     uint64_t hk = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t w = 4 * q + (uint32_t)k;
+    for (int k = 0; k < W; ++k) {
+      const uint32_t w = W * q + (uint32_t)k;
       if (valid && w < OW) {
         const int p = (int)w - 1;
         uint32_t zw;
@@ -481,8 +503,8 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
         dst[3] = lf.states[3 * cap + i];
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int p = (int)(4 * q) + k - 1;
+      for (int k = 0; k < W; ++k) {
+        const int p = (int)(W * q) + k - 1;
         if (p >= 0 && p < P) {
           dst[4 + 2 * p] = __float_as_uint(px[k]);
           dst[5 + 2 * p] = __float_as_uint(py[k]);
@@ -508,8 +530,8 @@ __global__ void __launch_bounds__(128, HD_CARG_MINB) k2_car_group(BatchDev b, Sp
       const int cxb = car_bin_i(xc);
       int gap = 255;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int p = (int)(4 * q) + k - 1;
+      for (int k = 0; k < W; ++k) {
+        const int p = (int)(W * q) + k - 1;
         if (p >= 0 && p < P) {
           const int pxb = car_bin_i(px[k]), pyb = car_bin_i(py[k]);
           if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;

@@ -21,6 +21,7 @@ DESPOT_X_TIMING_K2 = 8
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
 DESPOT_MF_GROUPED = 4
+DESPOT_MF_PAIRED = 16  # a lane pair per scenario (driving)
 DESPOT_MF_EXCHANGE = 8  # run the sharded exchange path on the communicator even at world 1 (tests)
 
 STATUS = {0: "OK", -1: "EINVAL", -2: "EMODEL", -3: "ENOMEM", -4: "ECAPACITY", -5: "ECUDA",

@@ -927,3 +927,29 @@ def test_prepared_graph_runs_equal_plain_calls():
     with pytest.raises(DespotError):
         gm.run_prepared(P)
     gm.close()
+
+
+@pytest.mark.parametrize("peds,K,D", [(20, 48, 40), (6, 40, 30), (31, 20, 20), (12, 33, 30), (3, 37, 25)])
+def test_car_paired_lanes_equal_thread_kernel_and_oracle(peds, K, D):
+    """DESPOT_MF_PAIRED (a lane pair per scenario, each lane owning half of a
+    step's Philox blocks) is bit-identical to the thread-per-scenario kernel
+    (roots and depth-1 leaves, per-scenario records) and matches the oracle."""
+    from paper_1802_06215_b200.despot import DESPOT_MF_PAIRED
+    params = inputs.car_params(peds, D=D)
+    gp, gt, om = Model("car", params, flags=DESPOT_MF_PAIRED), Model("car", params, flags=1), oracle.Model("car", params)
+    st = inputs.car_belief(K, 9 + K, peds)
+    st[0] = np.float32(12.0).view(np.uint32)
+    w = inputs.weights(K, K, uniform=False)
+    rp, rt, ro = gp.belief_load(st, w, 31), gt.belief_load(st, w, 31), om.belief_load(st, w, 31)
+    for rec in (True, False):
+        P0 = gp.expand([(rp, -1, 0, 0)], record=rec)
+        T0 = gt.expand([(rt, -1, 0, 0)], record=rec)
+        for k in AGG_KEYS + (("scen_obs", "scen_reward", "scen_states", "scen_len", "scen_hash", "scen_upper",
+                              "scen_lower") if rec else ()):
+            assert np.array_equal(np.asarray(P0[k]), np.asarray(T0[k])), (rec, k)
+    O0 = om.expand([(ro, -1, 0, 0)], record=True)
+    compare_batch(P0, O0, gp, om, [(0, 0)])
+    lv = [(a, c) for a in range(3) for c in range(min(3, int(P0["child_begin"][a + 1] - P0["child_begin"][a])))]
+    P1 = gp.expand([(rp, a, c, 1) for a, c in lv], record=True)
+    O1 = om.expand([(ro, a, c, 1) for a, c in lv], record=True)
+    compare_batch(P1, O1, gp, om, [(i, i) for i in range(len(lv))], check_scen=True)
