@@ -44,6 +44,26 @@ def _deps():
     return files
 
 
+CHECKED = os.path.join(HERE, "libdespot_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The self-check build (-DHD_CHECKS: device checks of index and protocol
+    invariants; common.cuh), loaded by the self-check tests through DESPOT_LIB."""
+    if not force and os.path.exists(CHECKED) and all(os.path.getmtime(CHECKED) >= os.path.getmtime(f) for f in _deps()):
+        return CHECKED
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    tmp = CHECKED + f".tmp{os.getpid()}"
+    cmd = [nvcc, *[f for f in NVCC_FLAGS if f not in ("-Xptxas", "-v")], "-DHD_CHECKS", "-o", tmp,
+           *[os.path.join(CSRC, s) for s in SOURCES]]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libdespot_checked.so")
+    os.replace(tmp, CHECKED)
+    return CHECKED
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(f) for f in _deps()):
         return LIB

@@ -155,8 +155,24 @@ struct LeafDev {
 // error bits of a batch
 enum : uint32_t {
   kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u,
-  kErrXOverflow = 16u /* the exchange's packed capacity was too small: dense fallback */
+  kErrXOverflow = 16u /* the exchange's packed capacity was too small: dense fallback */,
+  kErrCheck = 32u     /* a device self-check failed (HD_CHECKS builds only) */
 };
+
+// Device self-checks of index and protocol invariants (the self-check build,
+// -DHD_CHECKS, libdespot_checked.so; compute-sanitizer is not available on the
+// GPU pool): a violated invariant sets kErrCheck in the batch's error word and
+// the call fails.  Compiled out of the product build.
+#ifdef HD_CHECKS
+#define HD_CHECK(errp, cond)              \
+  do {                                    \
+    if (!(cond)) atomicOr((errp), kErrCheck); \
+  } while (0)
+#else
+#define HD_CHECK(errp, cond) \
+  do {                       \
+  } while (0)
+#endif
 
 // status block of a batch (zeroed per batch; the host reads it back in one copy)
 enum : uint32_t {

@@ -1251,7 +1251,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       rc = launch_group_sparse(m, b.get());
       if (!rc) {  // this rank's records into its block of the all-gather buffer
         PackDev pk{static_cast<unsigned char*>(b->gbuf) + (size_t)m->rank * b->gblk, b->hdr_pad, b->rec_bytes,
-                   static_cast<uint32_t*>(b->mscratch)};
+                   static_cast<uint32_t*>(b->mscratch), b->gblk};
         k_pack_sparse_scan<<<1, 1024, 0, st>>>(b->bd, pk);
         k_pack_sparse<<<(unsigned)LA, 128, 0, st>>>(b->bd, b->io, pk);
         b->launches += 2;
@@ -1812,7 +1812,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
     out->num_children = nchildren;
     out->scenario_steps = steps;
     out->launches = b->launches;
-    if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
+    if (err & kErrCheck) rc = set_err(DESPOT_ECUDA, "a device self-check failed (HD_CHECKS build)");
+    else if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
     else if (err & kErrHash) rc = set_err(DESPOT_EHASH, "64-bit observation-hash collision");
     else if (err & kErrChildCap)
       rc = set_err(DESPOT_ECAPACITY, "child_capacity %u < %u children", C, nchildren);

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kXThreads) k4_pack(BatchDev b, XDev x) {
   const uint64_t i0 = (uint64_t)blockIdx.x * kXBlk + (uint64_t)threadIdx.x * kXPer;
   for (uint32_t bits = p.bits; bits; bits &= bits - 1u, ++o) {
     const uint64_t i = i0 + (uint64_t)(__ffs(bits) - 1);
+    HD_CHECK(b.err, o < x.ccap && i < x.las);
     int64_t* q = x.cpk + 4 * o;
     q[0] = b.sums[lay.W(i)];
     q[1] = b.sums[lay.U(i)];

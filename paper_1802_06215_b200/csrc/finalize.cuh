@@ -103,6 +103,7 @@ __device__ __forceinline__ void rank_one(const BatchDev& b, uint64_t la, uint32_
     cnt += __popc(bal);
   }
   __syncwarp();
+  HD_CHECK(b.err, cnt <= S);
   for (uint32_t i = lane; i < cnt; i += 32) {
     const int32_t f = s_first[i];
     uint32_t r = 0;
@@ -135,6 +136,7 @@ __global__ void __launch_bounds__(kScanTile) k3_scan_lookback(BatchDev b) {
   if (threadIdx.x == 0) tile_sh = (uint32_t)atomicAdd(&b.scan_flags[0], 1ull);
   __syncthreads();
   const uint32_t tile = tile_sh;
+  HD_CHECK(b.err, (uint64_t)tile * kScanTile < LA + kScanTile);  // one ticket per CTA
   const uint64_t i = (uint64_t)tile * kScanTile + threadIdx.x;
   const uint32_t v = i < LA ? b.nc[i] : 0u;
   uint64_t tot;
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(kScanTile) k3_scan_lookback(BatchDev b) {
     } else {
       atomicExch(&st[tile], kAgg | tot);
       for (int p = (int)tile - 1;;) {
+        HD_CHECK(b.err, p >= 0);  // tile 0 always publishes an inclusive prefix
         const unsigned long long f = atomicAdd(&st[p], 0ull);  // device-scope read
         if (!(f >> 62)) continue;                               // predecessor not published yet
         excl += f & kVal;
@@ -189,6 +192,7 @@ __device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32
     nt += N;
     const uint32_t rk = b.rank[base + s];
     const uint32_t c = cb + rk;
+    HD_CHECK(b.err, rk < nc && rk < S);
     if (c < b.child_capacity) {
       const double Wd = (double)W;
       b.child_count[c] = (uint32_t)N;

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
       for (int w = 0; w < wid; ++w) off += warp_cnt[w];
       off += __popc(ballot & ((1u << lane) - 1u));
       if (keep) {
+        HD_CHECK(b.err, off < lf.cap);
         lf.ids[off] = id;
         lf.w[off] = lf.p_w[i];
         M::store(sm, s, lf.states, lf.cap, off);
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     const uint32_t a = local / chunks;
     const uint32_t i = (local - a * chunks) * 32 + lane;
     const bool valid = i < n;
+    HD_CHECK(b.err, a < b.A && leaf < b.L && (!valid || i < lf.cap));
     uint32_t z = 0xFFFFFFFFu, id = 0;
     int64_t qW = 0, qU = 0, qL = 0, qR = 0, qUq = 0, qLq = 0;
     auto item = [&](const auto& key) {
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
         const int64_t gW = group_sum64(gmask, qW), gU = group_sum64(gmask, qU), gL = group_sum64(gmask, qL);
         if ((int)lane == leader) {
           const uint64_t slot = la * b.S + zk;
+          HD_CHECK(b.err, zk < b.S && la < (uint64_t)b.L * b.A);
           atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)gW);
           atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)gU);
           atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)gL);

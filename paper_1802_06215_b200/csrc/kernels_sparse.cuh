@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
     for (int w = 0; w < wid; ++w) off += warp_cnt[w];
     off += __popc(ballot & ((1u << lane) - 1u));
     if (keep) {
+      HD_CHECK(b.err, off < lf.cap);
       lf.ids[off] = id;
       lf.w[off] = lf.p_w[i];
       M::store(sm, s, lf.states, lf.cap, off);
@@ -753,6 +754,7 @@ struct PackDev {
   unsigned char* blk;  // this rank's block
   uint32_t hdr_pad, rec_bytes;
   uint32_t* loc_off;   // [L*A] record offset of each (leaf, action)
+  uint64_t blk_bytes;  // the block's size (self-checks)
 };
 // header + record offsets (one CTA)
 __global__ void __launch_bounds__(1024) k_pack_sparse_scan(BatchDev b, PackDev p) {
@@ -779,6 +781,7 @@ __global__ void __launch_bounds__(128) k_pack_sparse(BatchDev b, SparseItemOut i
   const uint32_t nc = b.nc[la];
   for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
     unsigned char* r = p.blk + p.hdr_pad + (uint64_t)(p.loc_off[la] + c) * p.rec_bytes;
+    HD_CHECK(b.err, p.hdr_pad + (uint64_t)(p.loc_off[la] + c + 1) * p.rec_bytes <= p.blk_bytes);
     const uint32_t it = b.sp_item[base + c];
     int64_t* q = reinterpret_cast<int64_t*>(r + kRecN);
     *reinterpret_cast<uint64_t*>(r) = io.hash[it];
@@ -850,7 +853,10 @@ __global__ void __launch_bounds__(512) k3_merge_sparse(BatchDev b, MergeDev g, u
     while (rs[r + 1] <= i) ++r;
     return (r * g.blk + g.hdr_pad) / g.rec_bytes + g.offs[r * LA + la] + (i - rs[r]);
   };
-  auto rec = [&](uint64_t gi) { return g.gbuf + gi * g.rec_bytes; };
+  auto rec = [&](uint64_t gi) {
+    HD_CHECK(b.err, (gi + 1) * g.rec_bytes <= g.world * g.blk);
+    return g.gbuf + gi * g.rec_bytes;
+  };
   auto slot_of = [&](unsigned long long h) {
     uint32_t s = (uint32_t)(h ^ (h >> 32)) & tmask;
     while (tkey[s] != h) s = (s + 1u) & tmask;

@@ -393,6 +393,7 @@ class Model:
         out["exchange_bytes"] = int(E.exchange_bytes)
         if not device:
             for k in ("child_count", "child_first", "child_weight", "child_upper", "child_lower"):
+                out["_full_" + k] = o[k]  # the whole capacity (self-check runs: nothing written past Cn)
                 out[k] = o[k][:Cn]
             out["child_obs"] = o["child_obs"][: Cn * self.OW].reshape(Cn, self.OW)
             if record:
