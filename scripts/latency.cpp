@@ -43,9 +43,11 @@ int main(int argc, char** argv) {
   despot_leaf leaf{root, -1, 0, 0, 0};
   const uint32_t C = A * 4;
   // host outputs (pinned) and device outputs; mode 2 = device outputs
-  // through the two-phase form (begin/end: separate K3, no fusion)
-  for (int mode = 0; mode < 3; ++mode) {
-    const int dev = mode > 0;
+  // through the two-phase form (begin/end: separate K3, no fusion); modes 3, 4
+  // = a prepared batch (despot_batch_prepare: one CUDA graph per run) with
+  // host / device outputs
+  for (int mode = 0; mode < 5; ++mode) {
+    const int dev = mode == 1 || mode == 2 || mode == 4;
     despot_expansion out;
     memset(&out, 0, sizeof out);
     despot_node node;
@@ -74,7 +76,10 @@ int main(int argc, char** argv) {
     out.child_upper = (float*)take(4 * C);
     out.child_lower = (float*)take(4 * C);
     out.child_obs = (uint32_t*)take(4 * C);
+    despot_prepared* prep = nullptr;
+    if (mode >= 3) OK(despot_batch_prepare(m, &leaf, 1, &out, &prep));
     auto call = [&]() -> int {
+      if (mode >= 3) return despot_batch_run(prep, &out, s);
       if (mode < 2) return despot_expand_batch(m, &leaf, 1, &out, s);
       despot_batch* b = nullptr;
       if (int rc = despot_expand_begin(m, &leaf, 1, out.flags, s, &b)) return rc;
@@ -85,11 +90,15 @@ int main(int argc, char** argv) {
     const auto t0 = std::chrono::steady_clock::now();
     for (int i = 0; i < N; ++i) OK(call());
     const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count() / N;
-    out.flags |= DESPOT_X_TIMING;
-    OK(call());
+    if (mode < 3) {
+      out.flags |= DESPOT_X_TIMING;
+      OK(call());
+    }
+    const char* name[] = {"host", "device", "device-two-phase", "host-prepared-graph", "device-prepared-graph"};
     printf("{\"outputs\": \"%s\", \"us_per_call\": %.2f, \"launches\": %u, \"scenario_steps\": %llu, \"phases_ms\": [%.4f, %.4f, %.4f, %.4f]}\n",
-           mode == 2 ? "device-two-phase" : dev ? "device" : "host", us, out.launches, (unsigned long long)out.scenario_steps, out.phase_ms[0], out.phase_ms[1],
+           name[mode], us, out.launches, (unsigned long long)out.scenario_steps, out.phase_ms[0], out.phase_ms[1],
            out.phase_ms[2], out.phase_ms[3]);
+    if (prep) despot_batch_prepared_free(prep);
     if (dev) cudaFree(buf);
     else cudaFreeHost(buf);
   }
