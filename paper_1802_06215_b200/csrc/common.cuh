@@ -5,6 +5,7 @@
 // Nothing here is shared with oracle/: the CUDA path is an independent
 // implementation of the model cards in DESIGN.md §3.
 #pragma once
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -124,6 +125,56 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
     c3 = lo0;
   }
   return make_uint4(c0, c1, c2, c3);
+}
+
+// NB consecutive blocks of one stream address, ctr = (c0, c1, j, 0) for
+// j = 0 .. NB-1 (words 4j .. 4j+3 of scenario c0 at depth c1), computed round
+// by round side by side: the blocks' independent multiply/xor chains
+// interleave in the instruction stream (in-order issue gets NB-fold
+// instruction-level parallelism instead of NB serial chains)
+template <int NB, class KeyT>
+__device__ __forceinline__ void philox_blocks(uint32_t id, uint32_t t, const KeyT& key, uint4* out) {
+  uint32_t c0[NB], c1[NB], c2[NB], c3[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    c0[j] = id;
+    c1[j] = t;
+    c2[j] = (uint32_t)j;
+    c3[j] = 0u;
+  }
+  uint32_t k0, k1;
+  if constexpr (std::is_same<KeyT, SeedKey>::value) {
+    k0 = key.k0;
+    k1 = key.k1;
+  }
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t rk0, rk1;
+    if constexpr (std::is_same<KeyT, SeedKey>::value) {
+      if (r) {
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+      }
+      rk0 = k0;
+      rk1 = k1;
+    } else {
+      rk0 = key.k0[r];
+      rk1 = key.k1[r];
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const uint32_t lo0 = 0xD2511F53u * c0[j], hi0 = __umulhi(0xD2511F53u, c0[j]);
+      const uint32_t lo1 = 0xCD9E8D57u * c2[j], hi1 = __umulhi(0xCD9E8D57u, c2[j]);
+      const uint32_t n0 = hi1 ^ c1[j] ^ rk0;
+      const uint32_t n2 = hi0 ^ c3[j] ^ rk1;
+      c0[j] = n0;
+      c1[j] = lo1;
+      c2[j] = n2;
+      c3[j] = lo0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) out[j] = make_uint4(c0[j], c1[j], c2[j], c3[j]);
 }
 
 // event of probability p: (uint64)u < T(p), T(p) = floor(p 2^32) (R14)

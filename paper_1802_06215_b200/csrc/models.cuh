@@ -610,7 +610,9 @@ struct Nav {
   };
   template <class KeyT>
   static __device__ __forceinline__ Words words(uint32_t id, uint32_t t, const KeyT& key) {
-    return Words{philox(id, t, 0u, 0u, key), philox(id, t, 1u, 0u, key), philox(id, t, 2u, 0u, key).x};
+    uint4 b[3];
+    philox_blocks<3>(id, t, key, b);  // the three blocks' rounds interleaved
+    return Words{b[0], b[1], b[2].x};
   }
   // g(s, a, phi_t) on the step's words, branch-free (integer selects) so that
   // roll-out lanes choosing different actions do not diverge; rcode = the
