@@ -13,7 +13,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for K in (500, 64):
     for peds in (6, 12, 20):
-        for variant in ("warp", "group", "thread"):
+        for variant in ("warp", "group", "pair", "thread"):
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "4", "--peds", str(peds), "--K", str(K),
                    "--car-variant", variant, "--steps", "10", "--warmup", "3", "--no-cpu-baseline"]
             out = subprocess.run(cmd, capture_output=True, text=True)
