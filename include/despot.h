@@ -77,6 +77,15 @@ typedef struct {
   despot_comm* comm; /* NULL, or a communicator of `world` ranks (despot_comm_init)
                         whose rank is `rank`: despot_expand_batch then runs the whole
                         sharded batch, its exchange included, in one call            */
+  /* Device allocator hooks (both or neither; e.g. torch's caching allocator):
+   * node arenas, batch scratch and staging come from dev_alloc(bytes, stream,
+   * alloc_ctx) and go back through dev_free(ptr, stream, alloc_ctx), ordered on
+   * the call's stream (a prepared batch's persistent scratch excepted).  NULL:
+   * cudaMallocAsync / cudaFreeAsync.  dev_alloc returns NULL on failure
+   * (ENOMEM).  The hooks must stay valid until despot_model_free returns.   */
+  void* (*dev_alloc)(size_t bytes, void* stream, void* ctx);
+  void (*dev_free)(void* ptr, void* stream, void* ctx);
+  void* alloc_ctx;
 } despot_opts;
 
 /* Driving model kernel variant.  Default: chosen per batch -- the factored
@@ -159,6 +168,15 @@ typedef struct {
 #define DESPOT_X_TIMING_K2 8u       /* only phase_ms[1] (K2), two events: the cheap
                                        form for timing loops (8 events cost ~30 us
                                        of host time per call)                     */
+#define DESPOT_X_INDEX_LISTS 16u    /* the paper's update form ("the leaf ...
+                                       only contains a set of indexes"): leaf l with
+                                       action >= 0 takes the parent positions
+                                       index[index_begin[l] .. index_begin[l+1]-1]
+                                       (ascending) instead of replay + filter; the
+                                       update still replays the action on them and
+                                       fails with EINVAL if a position's observation
+                                       is not the leaf's key (validation mode; single
+                                       call, world == 1)                               */
 
 /* Caller-owned outputs.  Sizes: L leaves, A = |A|, C = child_capacity,
  * S = scen_capacity.  Children of (l, a) are child_begin[l*A+a] ..
@@ -205,6 +223,14 @@ typedef struct {
                               pack / unpack kernels between them; with DESPOT_X_TIMING) */
   uint32_t exchange_rounds;/* collective rounds issued (a capacity retry adds one)   */
   uint64_t exchange_bytes; /* bytes this rank contributed to the collectives         */
+  /* with DESPOT_X_RECORD_SCENARIO: [S] each scenario's child ordinal under its
+   * (leaf, action) -- the per-scenario observations' children the paper returns
+   * to the host, from which host index lists are built               */
+  uint32_t* scen_child;
+  /* in, with DESPOT_X_INDEX_LISTS (host arrays): [L+1] offsets, and the parent
+   * positions of every leaf (positions in the parent's ascending-id list)     */
+  const uint32_t* index_begin;
+  const uint32_t* index;
 } despot_expansion;
 
 /* Output sizes of a batch before calling it (host only, no device work):

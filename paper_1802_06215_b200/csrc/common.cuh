@@ -201,13 +201,16 @@ struct LeafDev {
   uint32_t child, depth;
   uint32_t seed_lo, seed_hi;
   double inv_wroot, wroot;
+  const uint32_t* idx;       // DESPOT_X_INDEX_LISTS: the parent positions of the leaf (else null)
+  uint32_t idx_n;
 };
 
 // error bits of a batch
 enum : uint32_t {
   kErrEmptyLeaf = 1u, kErrChildCap = 2u, kErrHash = 4u, kErrScenCap = 8u,
   kErrXOverflow = 16u /* the exchange's packed capacity was too small: dense fallback */,
-  kErrCheck = 32u     /* a device self-check failed (HD_CHECKS builds only) */
+  kErrCheck = 32u     /* a device self-check failed (HD_CHECKS builds only) */,
+  kErrIndexList = 64u /* a host index list names a scenario whose replay is not the leaf's key */
 };
 
 // Device self-checks of index and protocol invariants (the self-check build,
@@ -262,6 +265,7 @@ struct BatchDev {
   uint32_t* scen_len;
   uint64_t* scen_hash;
   uint32_t* scen_states;
+  uint32_t* scen_child;
   // sparse-key scratch
   uint64_t* sp_hash;         // [L*A*S] per-slot key hash (0 = empty)
   uint32_t* sp_item;         // [L*A*S] scenario position holding the slot's key

@@ -139,11 +139,14 @@ uint64_t thresh(double p) {
 // ===========================================================================
 constexpr int kBatchEvents = 10;
 
+struct despot_model;
+static void dev_free(const despot_model* m, void* p, cudaStream_t st);
 struct Block {
   void* ptr = nullptr;
   cudaStream_t stream = nullptr;
+  const despot_model* model = nullptr;  // its allocator (despot_opts hooks or stream-ordered)
   ~Block() {
-    if (ptr) cudaFreeAsync(ptr, stream);
+    if (ptr) dev_free(model, ptr, stream);
   }
 };
 
@@ -219,6 +222,11 @@ struct despot_model {
   int device = 0, rank = 0, world = 1;
   uint32_t flags = 0;
   despot_comm* comm = nullptr;
+  // device allocator hooks (despot_opts; e.g. torch's caching allocator), else
+  // cudaMallocAsync / cudaFreeAsync on the call's stream
+  void* (*alloc_fn)(size_t, void*, void*) = nullptr;
+  void (*free_fn)(void*, void*, void*) = nullptr;
+  void* alloc_ctx = nullptr;
   // packed-exchange capacity (K4, dense keys) in slots per (leaf, action) x 16:
   // raised to 5/4 of the largest union seen, so a capacity retry is rare
   std::atomic<uint32_t> xratio16{64};
@@ -229,6 +237,21 @@ struct despot_model {
   int k2_occ = 0;
   void* snap = nullptr;  // device copy of the dense model's shared-memory image
 };
+
+static void* dev_alloc(const despot_model* m, size_t bytes, cudaStream_t st) {
+  if (m && m->alloc_fn) return m->alloc_fn(bytes ? bytes : 1, st, m->alloc_ctx);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes ? bytes : 1, st) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+static void dev_free(const despot_model* m, void* p, cudaStream_t st) {
+  if (!p) return;
+  if (m && m->free_fn) m->free_fn(p, st, m->alloc_ctx);
+  else cudaFreeAsync(p, st);
+}
 
 struct despot_batch {
   despot_model* model;
@@ -658,6 +681,11 @@ extern "C" int despot_model_load(const char* kind, const char* params, const des
     m->world = opts->world < 1 ? 1 : opts->world;
     m->flags = opts->flags;
     m->comm = opts->comm;
+    if ((opts->dev_alloc == nullptr) != (opts->dev_free == nullptr))
+      return set_err(DESPOT_EINVAL, "dev_alloc and dev_free come together");
+    m->alloc_fn = opts->dev_alloc;
+    m->free_fn = opts->dev_free;
+    m->alloc_ctx = opts->alloc_ctx;
   }
   if (m->rank < 0 || m->rank >= m->world) return set_err(DESPOT_EINVAL, "rank outside [0, world)");
   // initial capacity of the packed exchange, slots per (leaf, action) x 16 (a
@@ -764,8 +792,9 @@ extern "C" int despot_belief_load(despot_model* m, const uint32_t* states_soa, c
   cudaStream_t st = (cudaStream_t)stream;
   auto blk = std::make_shared<Block>();
   blk->stream = st;
+  blk->model = m;
   const uint32_t kcap = (m->world > 1 && !dm.slots) ? std::max<uint32_t>(K, 1) : key_cap(dm, cap);
-  CU(cudaMallocAsync(&blk->ptr, node_bytes(dm, cap, kcap), st));
+  if (!(blk->ptr = dev_alloc(m, node_bytes(dm, cap, kcap), st))) return set_err(DESPOT_ENOMEM, "belief arena");
   Node* nd = new Node();
   nd->model = m;
   nd->block = blk;
@@ -887,10 +916,10 @@ static void free_batch(despot_batch* b, bool drop_new_nodes) {
     for (size_t l = 0; l < b->leaf_node.size(); ++l) b->leaf_node[l] = nullptr;
     return;
   }
-  if (b->scratch) cudaFreeAsync(b->scratch, b->stream);
-  if (b->stage) cudaFreeAsync(b->stage, b->stream);
-  if (b->gbuf) cudaFreeAsync(b->gbuf, b->stream);
-  if (b->mscratch) cudaFreeAsync(b->mscratch, b->stream);
+  dev_free(b->model, b->scratch, b->stream);
+  dev_free(b->model, b->stage, b->stream);
+  dev_free(b->model, b->gbuf, b->stream);
+  dev_free(b->model, b->mscratch, b->stream);
   if (b->pinned) {
     cudaStreamSynchronize(b->stream);  // the H2D from it must have completed
     pinned_pool().release(b->pinned);
@@ -1025,6 +1054,27 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     }
     parent[l] = p;
   }
+  // DESPOT_X_INDEX_LISTS (the paper's update form): host lists of
+  // parent positions replace the replay + filter (validated here and, per
+  // scenario, against the replay in K1)
+  const bool ilist = flags & DESPOT_X_INDEX_LISTS;
+  uint64_t idx_total = 0;
+  if (ilist) {
+    if (!bind || !bind->index_begin || !bind->index || m->world > 1)
+      return set_err(DESPOT_EINVAL, "index lists need the single-call form, index_begin / index and world == 1");
+    if (bind->index_begin[0] != 0) return set_err(DESPOT_EINVAL, "index_begin[0] must be 0");
+    for (uint32_t l = 0; l < L; ++l) {
+      const uint32_t b0 = bind->index_begin[l], b1 = bind->index_begin[l + 1];
+      if (b1 < b0) return set_err(DESPOT_EINVAL, "leaf %u: index_begin decreases", l);
+      if (leaves[l].action < 0 && b1 != b0) return set_err(DESPOT_EINVAL, "leaf %u: an index list on a self leaf", l);
+      if (leaves[l].action >= 0 && b1 == b0) return set_err(DESPOT_EINVAL, "leaf %u: empty index list", l);
+      for (uint32_t k = b0; k < b1; ++k)
+        if (bind->index[k] >= parent[l]->n || (k > b0 && bind->index[k] <= bind->index[k - 1]))
+          return set_err(DESPOT_EINVAL, "leaf %u: index list not ascending within the parent's %u scenarios", l,
+                         parent[l]->n);
+    }
+    idx_total = bind->index_begin[L];
+  }
   uint64_t q_bound = 0;  // sparse: per-item scratch bound sum_l A cap_l
   if (b->sparse) {
     uint32_t smax = 1;
@@ -1042,7 +1092,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   if (new_bytes && !g_capture) {
     b->new_block = std::make_shared<Block>();
     b->new_block->stream = st;
-    CU(cudaMallocAsync(&b->new_block->ptr, new_bytes, st));
+    b->new_block->model = m;
+    if (!(b->new_block->ptr = dev_alloc(m, new_bytes, st))) return set_err(DESPOT_ENOMEM, "new arenas");
   }
   g_ht.mark("arena_alloc");
   // (capture: template nodes carved from a fixed fake base; every run rebases them)
@@ -1125,7 +1176,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   off += 8 * (LA / kScanTile + 2);
   const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
                o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
-               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound);
+               o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound),
+               o_idx = take(4 * idx_total);
   // packed exchange (K4, dense keys): union flags, block counts, packed sums
   // and first ids at the model's capacity hint
   const bool xdense = b->xlib && !b->sparse;
@@ -1136,7 +1188,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   x.ccap = std::min<uint64_t>(LAS, (LA * m->xratio16.load() + 15) / 16 + 256);
   const size_t o_xflags = take(xdense ? (size_t)x.nblk * kXBlk : 0), o_xcnt = take(xdense ? 4 * (size_t)x.nblk : 0),
                o_xcpk = take(xdense ? 8 * (4 * x.ccap + x.qn) : 0), o_xcmin = take(xdense ? 4 * x.ccap : 0);
-  if ((g_capture ? cudaMalloc(&b->scratch, off) : cudaMallocAsync(&b->scratch, off, st)) != cudaSuccess) {
+  if (g_capture ? cudaMalloc(&b->scratch, off) != cudaSuccess : !(b->scratch = dev_alloc(m, off, st))) {
     free_batch(b.release(), true);
     return set_err(DESPOT_ENOMEM, "batch scratch (%zu bytes)", off);
   }
@@ -1185,8 +1237,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     b->hdr_pad = (uint32_t)(((4 * LA + b->rec_bytes - 1) / b->rec_bytes) * b->rec_bytes);
     b->gblk = b->hdr_pad + rcap * b->rec_bytes;
     const size_t gbytes = (size_t)W * b->gblk;
-    if (cudaMallocAsync(&b->gbuf, gbytes, st) != cudaSuccess ||
-        cudaMallocAsync(&b->mscratch, 4 * LA, st) != cudaSuccess) {
+    if (!(b->gbuf = dev_alloc(m, gbytes, st)) || !(b->mscratch = dev_alloc(m, 4 * LA, st))) {
       free_batch(b.release(), true);
       return set_err(DESPOT_ENOMEM, "all-gather buffer (%zu bytes)", gbytes);
     }
@@ -1197,8 +1248,13 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   bool all_self = true;
   for (uint32_t l = 0; l < L; ++l) all_self = all_self && leaves[l].action < 0;
   const size_t h2d_bytes = all_self ? o_stat + stat_bytes : sizeof(LeafDev) * L;
-  void* hp = pinned_pool().acquire(h2d_bytes);
+  void* hp = pinned_pool().acquire(std::max<size_t>(h2d_bytes, ilist ? o_idx + 4 * idx_total : 0));
   b->pinned = hp;
+  if (ilist)
+    for (uint32_t l = 0; l < L; ++l) {
+      ld[l].idx = leaves[l].action >= 0 ? reinterpret_cast<const uint32_t*>(s + o_idx) + bind->index_begin[l] : nullptr;
+      ld[l].idx_n = bind->index_begin[l + 1] - bind->index_begin[l];
+    }
   b->o_leaves = o_leaves;
   int rc = DESPOT_OK;
   if (!hp) rc = set_err(DESPOT_ENOMEM, "pinned staging");
@@ -1229,6 +1285,12 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
     b->h2d += h2d_bytes - o_leaves;
+    if (!rc && ilist && idx_total) {
+      memcpy(h + o_idx, bind->index, 4 * idx_total);
+      if (cudaMemcpyAsync(s + o_idx, h + o_idx, 4 * idx_total, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "index list copy failed");
+      b->h2d += 4 * idx_total;
+    }
   }
   g_ht.mark("setup_copies");
   // RECORD needs the per-scenario offsets: K1 and K2pre first, then outputs
@@ -1456,8 +1518,8 @@ static int merge_sparse(despot_model* m, despot_batch* b) {
   const size_t o_offs = take(4 * W * LA), o_sums = take(8 * lay.total()), o_mins = take(4 * LA * mS),
                o_item = take(4 * LA * mS), o_nc = take(4 * LA);
   void* ms = nullptr;
-  if (cudaMallocAsync(&ms, off, st) != cudaSuccess) return set_err(DESPOT_ENOMEM, "merge scratch (%zu bytes)", off);
-  cudaFreeAsync(b->mscratch, st);  // the pack offsets are no longer needed
+  if (!(ms = dev_alloc(m, off, st))) return set_err(DESPOT_ENOMEM, "merge scratch (%zu bytes)", off);
+  dev_free(m, b->mscratch, st);  // the pack offsets are no longer needed
   b->mscratch = ms;
   char* s = static_cast<char*>(ms);
   int64_t* nsums = reinterpret_cast<int64_t*>(s + o_sums);
@@ -1530,7 +1592,7 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
   auto& o_ns = b->o_ns; auto& o_w = b->o_w; auto& o_ar = b->o_ar; auto& o_au = b->o_au; auto& o_al = b->o_al;
   auto& o_cb = b->o_cb; auto& o_cc = b->o_cc; auto& o_cf = b->o_cf; auto& o_cw = b->o_cw; auto& o_cu = b->o_cu;
   auto& o_cl = b->o_cl; auto& o_co = b->o_co; auto& o_so = b->o_so;
-  size_t o_sr, o_su, o_sl, o_sn, o_sh, o_ss;
+  size_t o_sr, o_su, o_sl, o_sn, o_sh, o_ss, o_sc;
   o_ns = take(4 * L), o_w = take(4 * L), o_ar = take(4 * LA), o_au = take(4 * LA),
   o_al = take(4 * LA), o_cb = take(4 * (LA + 1)), o_cc = take(4 * (size_t)C),
   o_cf = take(4 * (size_t)C), o_cw = take(4 * (size_t)C), o_cu = take(4 * (size_t)C),
@@ -1538,7 +1600,8 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
   o_so = take(record ? 4 * S * dm.OW : 0), o_sr = take(record ? 4 * S : 0),
   o_su = take(record ? 4 * S : 0), o_sl = take(record ? 4 * S : 0),
   o_sn = take(record ? 4 * S : 0), o_sh = take(record ? 8 * S : 0),
-  o_ss = take(record && out->scen_states ? 4 * S * dm.SW : 0);
+  o_ss = take(record && out->scen_states ? 4 * S * dm.SW : 0),
+  o_sc = take(record && out->scen_child ? 4 * S : 0);
   if (dev_out) {
     bd.n_scen = out->n_scen;
     bd.weight = out->weight;
@@ -1559,8 +1622,9 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
     bd.scen_len = out->scen_len;
     bd.scen_hash = out->scen_hash;
     bd.scen_states = out->scen_states;
+    bd.scen_child = record ? out->scen_child : nullptr;
   } else {
-    if ((b->persistent ? cudaMalloc(&stage, so) : cudaMallocAsync(&stage, so, st)) != cudaSuccess) {
+    if (b->persistent ? cudaMalloc(&stage, so) != cudaSuccess : !(stage = dev_alloc(b->model, so, st))) {
       free_batch(b, true);
       return set_err(DESPOT_ENOMEM, "output staging (%zu bytes)", so);
     }
@@ -1584,6 +1648,7 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
     bd.scen_len = reinterpret_cast<uint32_t*>(p + o_sn);
     bd.scen_hash = reinterpret_cast<uint64_t*>(p + o_sh);
     bd.scen_states = (record && out->scen_states) ? reinterpret_cast<uint32_t*>(p + o_ss) : nullptr;
+    bd.scen_child = (record && out->scen_child) ? reinterpret_cast<uint32_t*>(p + o_sc) : nullptr;
   }
   b->bound = true;
   return DESPOT_OK;
@@ -1703,6 +1768,11 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
       ++b->launches;
       rc = check_launch(m, "K3c");
     }
+    if (!rc && record && bd.scen_child) {  // each scenario's child ordinal
+      k3_scen_child<<<(unsigned)m->num_sms * 4, 256, 0, st>>>(bd, b->sparse ? 0u : 1u);
+      ++b->launches;
+      rc = check_launch(m, "scen_child");
+    }
     b->mark(6);
     return rc;
   };
@@ -1813,6 +1883,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
     out->scenario_steps = steps;
     out->launches = b->launches;
     if (err & kErrCheck) rc = set_err(DESPOT_ECUDA, "a device self-check failed (HD_CHECKS build)");
+    else if (err & kErrIndexList)
+      rc = set_err(DESPOT_EINVAL, "an index list names a scenario whose replayed observation is not the leaf's key");
     else if (err & kErrEmptyLeaf) rc = set_err(DESPOT_EINVAL, "a leaf has an empty scenario set (unknown child ordinal)");
     else if (err & kErrHash) rc = set_err(DESPOT_EHASH, "64-bit observation-hash collision");
     else if (err & kErrChildCap)
@@ -1859,6 +1931,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
         {record ? out->scen_len : nullptr, bd.scen_len, 4 * Su},
         {record ? out->scen_hash : nullptr, bd.scen_hash, 8 * Su},
         {record ? out->scen_states : nullptr, bd.scen_states, 4 * Su * dm.SW},
+        {record ? out->scen_child : nullptr, bd.scen_child, 4 * Su},
     };
     for (auto& c : cps)
       if (!rc && c.dst && c.src && c.bytes &&
@@ -1967,7 +2040,8 @@ extern "C" int despot_batch_prepare(despot_model* m, const despot_leaf* leaves, 
   if (!m || !leaves || !out || !prep) return set_err(DESPOT_EINVAL, "null argument");
   if (m->world > 1 || (m->comm && (m->flags & DESPOT_MF_EXCHANGE)))
     return set_err(DESPOT_EINVAL, "prepared batches are single-GPU (world == 1, no exchange)");
-  if (out->flags & DESPOT_X_RECORD_SCENARIO) return set_err(DESPOT_EINVAL, "prepared batches do not RECORD");
+  if (out->flags & (DESPOT_X_RECORD_SCENARIO | DESPOT_X_INDEX_LISTS))
+    return set_err(DESPOT_EINVAL, "prepared batches do not RECORD or take index lists");
   CU(cudaSetDevice(m->device));
   std::unique_ptr<despot_prepared> p(new despot_prepared());
   p->m = m;
@@ -2031,7 +2105,8 @@ extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void*
   if (b->new_bytes) {
     b->new_block = std::make_shared<Block>();
     b->new_block->stream = st;
-    CU(cudaMallocAsync(&b->new_block->ptr, b->new_bytes, st));
+    b->new_block->model = m;
+    if (!(b->new_block->ptr = dev_alloc(m, b->new_bytes, st))) return set_err(DESPOT_ENOMEM, "new arenas");
   }
   const intptr_t shift = b->new_block ? static_cast<char*>(b->new_block->ptr) - reinterpret_cast<char*>(kTemplateBase) : 0;
   auto rebase = [shift](auto* q) { return reinterpret_cast<decltype(q)>(reinterpret_cast<char*>(q) + shift); };
@@ -2094,7 +2169,7 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
   const uint32_t n = nd->n;
   void* scratch = nullptr;
   const size_t bytes = 256 + 8 * (size_t)(n ? n : 1);
-  CU(cudaMallocAsync(&scratch, bytes, st));
+  if (!(scratch = dev_alloc(m, bytes, st))) return set_err(DESPOT_ENOMEM, "rollout_bounds scratch");
   int64_t* acc = static_cast<int64_t*>(scratch);
   float* du = reinterpret_cast<float*>(static_cast<char*>(scratch) + 256);
   float* dl = du + (n ? n : 1);
@@ -2131,7 +2206,7 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
         cudaStreamSynchronize(st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "rollout_bounds copy failed");
   }
-  cudaFreeAsync(scratch, st);
+  dev_free(m, scratch, st);
   if (rc) return rc;
   *upper_mean = hacc[0] ? (float)((double)hacc[1] / (double)hacc[0]) : 0.0f;
   *lower_mean = hacc[0] ? (float)((double)hacc[2] / (double)hacc[0]) : 0.0f;

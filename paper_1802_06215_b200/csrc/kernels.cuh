@@ -56,12 +56,16 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     uint32_t steps = 0;
-    for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
-      const uint32_t i = base + threadIdx.x;
+    // the parent's scenarios (replay + filter), or the host's index list
+    // (gather + replay, the replay checked against the leaf's key)
+    const uint32_t cnt = lf.idx ? lf.idx_n : lf.p_n;
+    for (uint32_t base = 0; base < cnt; base += blockDim.x) {
+      const uint32_t j = base + threadIdx.x;
+      const uint32_t i = lf.idx ? (j < cnt ? lf.idx[j] : 0u) : j;
       bool keep = false;
       typename M::St s;
       uint32_t id = 0;
-      if (i < lf.p_n && valid_child) {
+      if (j < cnt && valid_child) {
         s = M::load(sm, lf.p_states, lf.p_cap, i);
         id = lf.p_ids[i];
         uint32_t z;
@@ -73,6 +77,10 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
           ++steps;
         }
         keep = z == key;
+        if (lf.idx && !keep) {
+          atomicOr(b.err, kErrIndexList);
+          keep = true;
+        }
       }
       const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
       if (lane == 0) warp_cnt[wid] = __popc(ballot);

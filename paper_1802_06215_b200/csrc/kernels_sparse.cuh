@@ -51,12 +51,15 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t steps = 0;
-  for (uint32_t base = 0; base < lf.p_n; base += blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
+  // the parent's scenarios (replay + filter), or the host's index list
+  const uint32_t cnt = lf.idx ? lf.idx_n : lf.p_n;
+  for (uint32_t base = 0; base < cnt; base += blockDim.x) {
+    const uint32_t j = base + threadIdx.x;
+    const uint32_t i = lf.idx ? (j < cnt ? lf.idx[j] : 0u) : j;
     bool keep = false;
     typename M::St s;
     uint32_t id = 0;
-    if (i < lf.p_n && valid_child) {
+    if (j < cnt && valid_child) {
       s = M::load(sm, lf.p_states, lf.p_cap, i);
       id = lf.p_ids[i];
       bool term = M::terminal(sm, s);
@@ -71,6 +74,10 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
       } else {
         keep = true;
         M::for_obs_words(sm, s, [&](uint32_t k, uint32_t zk) { keep = keep && zk == key[k]; });
+      }
+      if (lf.idx && !keep) {
+        atomicOr(b.err, kErrIndexList);
+        keep = true;
       }
     }
     const uint32_t ballot = __ballot_sync(0xffffffffu, keep);
@@ -923,6 +930,46 @@ __global__ void __launch_bounds__(512) k3_merge_sparse(BatchDev b, MergeDev g, u
     }
   }
   if (threadIdx.x == 0) b.nc[la] = nr;
+}
+
+// ---------------------------------------------------------------------------
+// RECORD: each scenario's child ordinal under its (leaf, action) (the
+// per-scenario observations' children of P:434), after the finalize.  Dense
+// keys: the number of the (leaf, action)'s used slots with a smaller first id
+// than the record's slot; sparse keys: the child whose key equals the record's.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k3_scen_child(BatchDev b, uint32_t dense) {
+  const uint64_t Q = b.scen_off[b.L];
+  const uint32_t OW = b.model->OW;
+  const uint64_t LA = (uint64_t)b.L * b.A;
+  const SumLayout lay{LA * b.S, LA};
+  for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < Q && q < b.scen_capacity;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t leaf = find_leaf(b.scen_off, b.L, q);
+    const uint32_t n = b.n_leaf[leaf];
+    const uint32_t a = (uint32_t)((q - b.scen_off[leaf]) / n);
+    const uint64_t la = (uint64_t)leaf * b.A + a;
+    uint32_t c = 0xFFFFFFFFu;
+    if (dense) {
+      const uint64_t base = la * b.S;
+      const uint32_t z = b.scen_obs[q];
+      const int32_t f = b.mins[base + z];
+      uint32_t r = 0;
+      for (uint32_t s = 0; s < b.S; ++s) r += (b.sums[lay.N(base + s)] != 0 && b.mins[base + s] < f) ? 1u : 0u;
+      c = r;
+    } else {
+      const uint32_t cb = b.child_begin[la], ce = b.child_begin[la + 1];
+      for (uint32_t k = cb; k < ce && k < b.child_capacity; ++k) {
+        bool eq = true;
+        for (uint32_t w = 0; w < OW && eq; ++w) eq = b.child_obs[(uint64_t)k * OW + w] == b.scen_obs[q * OW + w];
+        if (eq) {
+          c = k - cb;
+          break;
+        }
+      }
+    }
+    b.scen_child[q] = c;
+  }
 }
 
 }  // namespace hd

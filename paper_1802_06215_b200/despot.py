@@ -18,6 +18,7 @@ DESPOT_X_DEVICE_OUTPUTS = 1
 DESPOT_X_RECORD_SCENARIO = 2
 DESPOT_X_TIMING = 4
 DESPOT_X_TIMING_K2 = 8
+DESPOT_X_INDEX_LISTS = 16
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
 DESPOT_MF_GROUPED = 4
@@ -49,9 +50,32 @@ class DespotError(RuntimeError):
         self.code = code
 
 
+DEV_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+DEV_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
 class Opts(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("flags", C.c_uint32),
-                ("comm", C.c_void_p)]
+                ("comm", C.c_void_p), ("dev_alloc", DEV_ALLOC_FN), ("dev_free", DEV_FREE_FN),
+                ("alloc_ctx", C.c_void_p)]
+
+
+def torch_allocator(device: int):
+    """despot_opts allocator hooks backed by torch's caching allocator (node
+    arenas and batch scratch then share torch's pool): (alloc, free) ctypes
+    callbacks, to be kept alive as long as the model."""
+    import torch
+
+    def alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+        except Exception:  # ENOMEM for the library
+            return None
+
+    def free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    return DEV_ALLOC_FN(alloc), DEV_FREE_FN(free)
 
 
 class ModelInfo(C.Structure):
@@ -76,7 +100,8 @@ class Expansion(C.Structure):
                 ("scen_hash", C.c_void_p), ("scen_states", C.c_void_p),
                 ("scenario_steps", C.c_uint64), ("num_children", C.c_uint32), ("launches", C.c_uint32),
                 ("phase_ms", C.c_float * 4), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("exchange_ms", C.c_float), ("exchange_rounds", C.c_uint32), ("exchange_bytes", C.c_uint64)]
+                ("exchange_ms", C.c_float), ("exchange_rounds", C.c_uint32), ("exchange_bytes", C.c_uint64),
+                ("scen_child", C.c_void_p), ("index_begin", C.c_void_p), ("index", C.c_void_p)]
 
 
 class SearchProblem(C.Structure):
@@ -253,12 +278,16 @@ class Model:
     """A loaded model (despot_model*)."""
 
     def __init__(self, kind: str, params: str = "", device: int = 0, rank: int = 0, world: int = 1,
-                 flags: int = 0, comm: "Comm | None" = None):
+                 flags: int = 0, comm: "Comm | None" = None, allocator: "str | None" = None):
+        """allocator: None (the library's stream-ordered cudaMallocAsync) or
+        "torch" (torch's caching allocator through despot_opts' hooks)."""
         self.h = C.c_void_p()
         self.comm = comm  # kept alive as long as the model
         import weakref
         self._prepared = weakref.WeakSet()
-        o = Opts(device, rank, world, flags, comm.h.value if comm is not None else None)
+        self._hooks = torch_allocator(device) if allocator == "torch" else (DEV_ALLOC_FN(), DEV_FREE_FN())
+        o = Opts(device, rank, world, flags, comm.h.value if comm is not None else None, self._hooks[0],
+                 self._hooks[1], None)
         _check(lib().despot_model_load(kind.encode(), params.encode(), C.byref(o), C.byref(self.h)))
         info = ModelInfo()
         _check(lib().despot_model_info_get(self.h, C.byref(info)))
@@ -369,7 +398,7 @@ class Model:
         if record:
             o.update(scen_obs=z(S_cap * OW, u32), scen_reward=z(S_cap, f32), scen_upper=z(S_cap, f32),
                      scen_lower=z(S_cap, f32), scen_len=z(S_cap, u32), scen_hash=z(S_cap, i64),
-                     scen_states=z(S_cap * SW, u32))
+                     scen_states=z(S_cap * SW, u32), scen_child=z(S_cap, u32))
         E = Expansion()
         for k, v in o.items():
             setattr(E, k, ptr(v))
@@ -398,16 +427,18 @@ class Model:
             out["child_obs"] = o["child_obs"][: Cn * self.OW].reshape(Cn, self.OW)
             if record:
                 S = int(o["n_scen"].astype(np.int64).sum()) * A
-                for k in ("scen_reward", "scen_upper", "scen_lower", "scen_len", "scen_hash"):
+                for k in ("scen_reward", "scen_upper", "scen_lower", "scen_len", "scen_hash", "scen_child"):
                     out[k] = o[k][:S]
                 out["scen_obs"] = o["scen_obs"][: S * self.OW].reshape(S, self.OW)
                 out["scen_states"] = o["scen_states"][: S * self.SW].reshape(S, self.SW)
         return out
 
     def expand(self, leaves, record=False, device_outputs=False, child_capacity=None, scen_capacity=None,
-               stream=None, timing=False, outputs=None):
+               stream=None, timing=False, outputs=None, index_lists=None):
         """leaves: list of (node, action, child, depth).  Returns a dict of
-        arrays (numpy, or torch CUDA tensors with device_outputs=True)."""
+        arrays (numpy, or torch CUDA tensors with device_outputs=True).
+        index_lists: per leaf, the parent positions it holds (the paper's
+        update form, DESPOT_X_INDEX_LISTS; [] for self leaves)."""
         L = len(leaves)
         lv = self._leaves(leaves)
         C_cap = child_capacity
@@ -425,7 +456,17 @@ class Model:
         E.node = C.addressof(nodes)
         E.flags = ((DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | (DESPOT_X_RECORD_SCENARIO if record else 0)
                    | _tflag(timing))
+        keep_idx = None
+        if index_lists is not None:
+            begin = np.zeros(L + 1, np.uint32)
+            begin[1:] = np.cumsum([len(x) for x in index_lists])
+            idx = np.ascontiguousarray(np.concatenate([np.asarray(x, np.uint32) for x in index_lists])
+                                       if int(begin[-1]) else np.zeros(1, np.uint32), dtype=np.uint32)
+            keep_idx = (begin, idx)
+            E.flags |= DESPOT_X_INDEX_LISTS
+            E.index_begin, E.index = begin.ctypes.data, idx.ctypes.data
         _check(lib().despot_expand_batch(self.h, lv, L, C.byref(E), _stream_ptr(stream)))
+        del keep_idx
         return self._finish(o, E, L, nodes, record, device_outputs)
 
     # ---- prepared calls (repeated batches: no per-call marshalling) ----

@@ -94,6 +94,9 @@ def compare_batch(G, O, gm: Model, om: oracle.Model, pairs, check_scen=False):
             assert np.array_equal(G["scen_len"][gs], O["scen_len"][os_]), "roll-out lengths"
             assert np.array_equal(G["scen_hash"][gs].view(np.uint64), O["scen_hash"][os_]), "roll-out action hashes"
             assert np.array_equal(G["scen_states"][gs], O["scen_states"][os_]), "states after the step"
+            if "scen_child" in G:  # each scenario's child ordinal
+                assert np.array_equal(np.asarray(G["scen_child"][gs], np.int64),
+                                      np.asarray(O["scen_child"][os_], np.int64)), "per-scenario child ordinals"
             # per-scenario returns: fp32 of the fp64 value
             lam = O["scen_lower"][os_]
             close(G["scen_lower"][gs], lam, np.abs(lam) + 1e-6, "per-scenario roll-out return")

@@ -953,3 +953,69 @@ def test_car_paired_lanes_equal_thread_kernel_and_oracle(peds, K, D):
     P1 = gp.expand([(rp, a, c, 1) for a, c in lv], record=True)
     O1 = om.expand([(ro, a, c, 1) for a, c in lv], record=True)
     compare_batch(P1, O1, gp, om, [(i, i) for i in range(len(lv))], check_scen=True)
+
+
+@pytest.mark.parametrize("cfg,K,L", [(2, 120, 10), (3, 90, 8), (1, 100, 6)])
+def test_host_index_lists_equal_replay_filter(cfg, K, L):
+    """The paper's update form: the host receives every
+    scenario's child ordinal (RECORD's scen_child, equal to the oracle's) and
+    builds each leaf's index list of parent positions; expanding the leaves
+    from those lists (DESPOT_X_INDEX_LISTS: gather + replay) gives the nodes
+    and outputs of the replay + filter form bit for bit.  A list naming a
+    scenario of another child is refused (EINVAL)."""
+    gm, om, st, w, seed, _ = setup(cfg, K=K, L=L)
+    gr, orr, G0, O0 = expand_root_both(gm, om, st, w, seed, record=True)
+    n = int(G0["n_scen"][0])
+    assert np.array_equal(np.asarray(G0["scen_child"], np.int64), np.asarray(O0["scen_child"], np.int64))
+    lv = inputs.select_leaves(G0["child_count"], G0["child_begin"], gm.A, L)
+    lists = [np.nonzero(np.asarray(G0["scen_child"][a * n:(a + 1) * n]) == c)[0] for a, c in lv]
+    ref = gm.expand([(gr, a, c, 1) for a, c in lv])
+    got = gm.expand([(gr, a, c, 1) for a, c in lv], index_lists=lists)
+    for k in AGG_KEYS:
+        assert np.array_equal(np.asarray(got[k]), np.asarray(ref[k])), k
+    # the update replays only the listed scenarios (replay + filter replays every parent scenario)
+    assert 0 < got["scenario_steps"] <= ref["scenario_steps"]
+    for i in range(L):
+        a_, b_ = gm.node_read(got["node"][i]), gm.node_read(ref["node"][i])
+        assert np.array_equal(a_["ids"], b_["ids"]) and np.array_equal(a_["states"], b_["states"])
+    # a list holding a scenario of another child of the same action
+    a, c = lv[0]
+    other = np.nonzero(np.asarray(G0["scen_child"][a * n:(a + 1) * n]) != c)[0]
+    if len(other):
+        bad = sorted(set(lists[0].tolist()) | {int(other[0])})
+        with pytest.raises(DespotError) as e:
+            gm.expand([(gr, a, c, 1)], index_lists=[bad])
+        assert e.value.code == -1
+    with pytest.raises(DespotError):
+        gm.expand([(gr, a, c, 1)], index_lists=[[n + 5]])  # outside the parent
+    gm.close()
+
+
+def test_torch_allocator_hooks():
+    """despot_opts' allocator hooks with torch's caching allocator: the same
+    results as the library's own stream-ordered allocations (roots, depth-1
+    leaves, a prepared graph batch); the node arenas live in torch's pool and
+    go back to it when released."""
+    import torch
+    kind, params, st, w, seed, L = inputs.config_inputs(2, K=150, L=8)
+    plain, hooked = Model(kind, params), Model(kind, params, allocator="torch")
+    before = torch.cuda.memory_allocated()
+    rp, rh = plain.belief_load(st, w, seed), hooked.belief_load(st, w, seed)
+    assert torch.cuda.memory_allocated() > before  # the hooked root arena came from torch
+    P0, H0 = plain.expand([(rp, -1, 0, 0)]), hooked.expand([(rh, -1, 0, 0)])
+    lv = inputs.select_leaves(P0["child_count"], P0["child_begin"], plain.A, L)
+    P1 = plain.expand([(rp, a, c, 1) for a, c in lv])
+    H1 = hooked.expand([(rh, a, c, 1) for a, c in lv])
+    for k in AGG_KEYS:
+        assert np.array_equal(np.asarray(P1[k]), np.asarray(H1[k])), k
+    mid = torch.cuda.memory_allocated()
+    hooked.node_release_many(H1["node"])
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() < mid  # released arenas went back to torch's pool
+    prep = hooked.prepare([(rh, a, c, 1) for a, c in lv])
+    hooked.run_prepared(prep)
+    for k in AGG_KEYS:
+        r = np.asarray(P1[k]).reshape(-1)
+        assert np.array_equal(np.asarray(prep["o"][k]).reshape(-1)[: len(r)], r), k
+    hooked.close()
+    plain.close()
