@@ -112,6 +112,22 @@ struct Tiger {
 // This moves the step's work from the ALU pipe (the kernel's limiter) to the
 // load/store pipe, and the pseudo-cell removes the per-robot "exited" selects.
 // ===========================================================================
+// roll-out pipe balance (ALU vs FMA-heavy), A/B-measured
+#ifndef HD_RS_ONE
+#define HD_RS_ONE 0
+#endif
+#ifndef HD_RS_SENSE_LOP
+#define HD_RS_SENSE_LOP 1
+#endif
+#ifndef HD_RS_ROWSEL
+#define HD_RS_ROWSEL 1
+#endif
+#ifndef HD_RS_CELL_SHF
+#define HD_RS_CELL_SHF 0
+#endif
+#ifndef HD_RS_EX_SHF
+#define HD_RS_EX_SHF 0
+#endif
 template <int R>
 struct RockSample {
 #ifndef HD_RS_MINB
@@ -133,12 +149,14 @@ struct RockSample {
     uint8_t senseb[40];      // column q -> SENSE sub-action 5 + rock(q); a sentinel column -> E
     uint32_t qstart[2];      // first column of robot r
     uint32_t polw;           // columns per cell row of the pol table (m + 2)
+    uint32_t one;            // 1, opaque to the compiler: address sums in the roll-out become IMADs
+                             // (FMA pipe) instead of IADD3s on the ALU pipe, the loop's limiter
     // byte offsets in hd_dyn_smem of the variable-size tables (sized by n, m, D):
     uint32_t off_act;   // u16 [cell][base]: the effect of sub-action b on a robot at the cell:
                         // bit 0 SENSE (not from EXIT), bit 1 SAMPLE on a rock, bit 2 the +10
                         // exit, bits 3-15 the next cell (EXIT pseudo-cell included)
     uint32_t off_info;  // u32 [cell]: bits 0-4 rock on the cell, bit 5 has a rock; 8-15 x; 16-23 y
-    uint32_t off_rock;  // u8  [cell]: the rock on the cell (0 if none; only read with SAMPLE's flag)
+    uint32_t off_rock;  // u8  [cell]: 5 + the rock on the cell (0 if none; only read with SAMPLE's flag)
     uint32_t off_thr;   // u32 [cell][mm]: sensing rock j from the cell is correct iff u <= thr
     uint32_t off_pol;   // u8  [cell][m+2]: policy move toward the rock of column q (4 = on it); sentinels
                         // E; row n*n+1 (the SENSE row) holds senseb: the sub-action of a robot whose
@@ -211,6 +229,7 @@ struct RockSample {
       sm.off_gp = off_gp;
       sm.off_gp10 = off_gp10;
       sm.polw = polw;
+      sm.one = 1u;
       sm.n = n;
       sm.m = dm.m;
       sm.mm = mm;
@@ -262,7 +281,7 @@ struct RockSample {
       row[4] = (uint16_t)(sc | (rock >= 0 ? kActSample : 0u));                         // SAMPLE
       for (int k = 5; k < dm.base; ++k) row[k] = (uint16_t)(sc | kActSense);           // SENSE k - 5
       t_info[c] = (rock >= 0 ? ((uint32_t)rock | 32u) : 0u) | ((uint32_t)x << 8) | ((uint32_t)y << 16);
-      t_rock[c] = rock >= 0 ? (uint8_t)rock : (uint8_t)0;
+      t_rock[c] = rock >= 0 ? (uint8_t)(rock + 5) : (uint8_t)0;  // the rock's bit in good << 5
     }
     for (int e = tid; e < (nc + 1) * mm; e += nt) {
       const int c = e / mm, j = e - c * mm;
@@ -338,7 +357,7 @@ struct RockSample {
       // target, itself when blocked or not moving, EXIT through the east border)
       const uint32_t e = act(sm, c, sub);
       // SAMPLE on the current cell's rock
-      const uint32_t jr = rock_on(sm, c);
+      const uint32_t jr = rock_on(sm, c) - 5u;  // (a cell without a rock: wraps, masked by SAMPLE's flag)
       const uint32_t samp = (e >> 1) & 1u;
       const uint32_t gbit = samp & (s.good >> jr);
       // SENSE rock sub - 5 (evaluated for every lane; masked; none from EXIT);
@@ -416,8 +435,8 @@ struct RockSample {
     }
   }
   template <bool TRACE, class KeyT>
-  static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
-                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
+  static __device__ void rollout_generic(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
+                                         const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
     double acc = 0.0;
     uint32_t q[R], tg[R];
 #pragma unroll
@@ -459,6 +478,125 @@ struct RockSample {
       ++t;
     }
     if (!term) acc = __fma_rn(gp(sm, (int)(t - t0)), sm.tail, acc);
+    ret = acc;
+    len = t - t0;
+  }
+
+  // shared-memory loads at explicit 32-bit shared-space addresses (the
+  // roll-out computes its table addresses itself, with IMADs)
+  static __device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  static __device__ __forceinline__ uint32_t lds16(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  static __device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+  }
+  // Eq. 12's roll-out, the ALU-lean form (m <= 27; else rollout_generic, the
+  // same card): the roll-out is bound by the ALU pipe, so its bit work is
+  // reorganised --
+  //   * the good-rock mask is kept as g5 = good << 5, so SENSE sub-action
+  //     5 + j and the rock table's 5 + j index it directly;
+  //   * every table address is computed with IMADs (an opaque 1 for the unit
+  //     strides) on shared-space addresses;
+  //   * the flags of an action entry come out through multiply-high
+  //     extractions (FMA pipe), the next cell by one;
+  //   * the policy row is selected arithmetically (tg in {0, 1});
+  //   * the memory update needs no reading code: GOOD = SENSE & x,
+  //     BAD = SENSE & ~x with x = (good == correct);
+  //   * terminal = no robot left (a live count).
+  // It computes exactly the card's step and policy (bit-identical outputs).
+  template <bool TRACE, class KeyT>
+  static __device__ void rollout(const Sm& sm, St s, uint32_t z, uint32_t id, uint32_t t0,
+                                 const KeyT& key, double& ret, uint32_t& len, uint64_t& h) {
+    if (sm.m > 27) {  // (uniform) the shifted mask would not fit
+      rollout_generic<TRACE>(sm, s, z, id, t0, key, ret, len, h);
+      return;
+    }
+    const uint32_t one = sm.one, polw = sm.polw, base = sm.base, mm = sm.mm;
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(hd_dyn_smem);
+    const uint32_t a_act = sb + sm.off_act, a_thr = sb + sm.off_thr - 20u, a_rock = sb + sm.off_rock;
+    const int sense_row = sm.exitc + 1;
+    uint32_t g5 = s.good << 5;
+    uint32_t qa[R], tg[R];  // qa: shared address of the robot's column in pol row 0
+    int live = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      qa[r] = sb + kOffPol + sm.qstart[r];
+      tg[r] = 0;
+      live += exited(sm, s, r) ? 0 : 1;
+    }
+    const double* gpk = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10);  // 10 gamma^(t - t0)
+    double acc = 0.0;
+    uint32_t t = t0;
+    while (t < sm.D && live > 0) {
+      const uint4 w = philox(id, t + 1, 0u, 0u, key);
+      const uint32_t u[2] = {w.x, w.y};
+      int k = 0;  // the step's reward / 10
+      int a = 0, mul = 1;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int c = s.cell[r];
+        // pi0: row = the cell when the target is known GOOD, else the SENSE row
+#if HD_RS_ROWSEL
+        const int row = tg[r] ? c : sense_row;
+#else
+        const int row = sense_row + (int)tg[r] * (c - sense_row);
+#endif
+        const uint32_t b = lds8((uint32_t)row * polw + qa[r]);
+        if (TRACE) {
+          a += (exited(sm, s, r) ? 2 : (int)b) * mul;
+          mul *= (int)base;
+        }
+        const uint32_t e = lds16((uint32_t)c * (2u * base) + (b * 2u + a_act));
+        const uint32_t thr = lds32((uint32_t)c * (4u * mm) + (b * 4u + a_thr));  // SENSE rock b - 5
+#if HD_RS_ONE
+        const uint32_t jr5 = lds8((uint32_t)c * one + a_rock);                 // 5 + the rock on the cell
+#else
+        const uint32_t jr5 = lds8((uint32_t)c + a_rock);                       // 5 + the rock on the cell
+#endif
+#if HD_RS_SENSE_LOP
+        const uint32_t sense = e & 1u;
+#else
+        const uint32_t sense = __umulhi(e << 31, 2u);
+#endif
+        const uint32_t samp = __umulhi(e << 30, 2u);
+#if HD_RS_EX_SHF
+        const uint32_t ex = (e >> 2) & 1u;
+#else
+        const uint32_t ex = __umulhi(e << 29, 2u);
+#endif
+        const uint32_t incorrect = u[r] > thr ? 1u : 0u;
+        const uint32_t x = ((g5 >> b) ^ incorrect) & 1u;  // 1: the reading says GOOD
+        const uint32_t gbit = (g5 >> jr5) & samp;         // SAMPLE of a good rock
+        g5 &= ~(gbit << jr5);                              // it turns bad
+        k += (int)ex + 2 * (int)gbit - (int)samp;
+        live -= (int)ex;
+#if HD_RS_CELL_SHF
+        s.cell[r] = (int)(e >> 3);                         // the next cell
+#else
+        s.cell[r] = (int)__umulhi(e, 1u << 29);           // e >> 3: the next cell
+#endif
+        // memory: GOOD -> target GOOD; BAD or SAMPLE -> target DONE (next column)
+#if HD_RS_ONE
+        qa[r] += ((sense & ~x) | samp) * one;
+#else
+        qa[r] += (sense & ~x) | samp;
+#endif
+        tg[r] = (tg[r] | (sense & x)) & ~samp;
+      }
+      if (TRACE) h = (h ^ (uint64_t)(uint32_t)a) * kFnvPrime;
+      acc = __fma_rn(*gpk++, (double)k, acc);  // + gamma^(t - t0) r, r = 10 k
+      ++t;
+    }
+    if (live > 0) acc = __fma_rn(gp(sm, (int)(t - t0)), sm.tail, acc);
     ret = acc;
     len = t - t0;
   }
