@@ -132,7 +132,9 @@ int despot_model_free(despot_model* model);
  * states_soa [state_words][K] u32 (host), weights [K] f32 > 0 (host), global
  * scenario id = position, stream_seed = the Philox key sigma of phi_t (R13).
  * With world > 1 only ids with id % world == rank are kept on this device.
- * The root has depth 0.  Errors: EINVAL (K == 0, weight <= 0), ENOMEM, ECUDA. */
+ * The root has depth 0.  Errors: EINVAL (K == 0, weight <= 0; driving: a car
+ * or pedestrian coordinate not finite or beyond |4096| m, outside the model's
+ * int16 observation bins, R21), ENOMEM, ECUDA. */
 int despot_belief_load(despot_model* model, const uint32_t* states_soa, const float* weights,
                        uint32_t K, uint64_t stream_seed, void* stream, despot_node* root_out);
 /* n = scenarios of the node on this device (after the call that created it

@@ -776,6 +776,15 @@ extern "C" int despot_belief_load(despot_model* m, const uint32_t* states_soa, c
     if (!(weights[i] > 0.0f) || !std::isfinite(weights[i])) return set_err(DESPOT_EINVAL, "weights must be finite and > 0");
     wroot += (double)weights[i];
   }
+  if (dm.kind == kCar) {  // positions finite with |v| <= 4096: the bins floor(2v) stay int16 (R21)
+    for (uint32_t i = 0; i < K; ++i)
+      for (uint32_t k = 0; k < 4 + 2 * (uint32_t)dm.peds; ++k) {
+        if (k == 1 || k == 2 || k == 3) continue;
+        float v;
+        memcpy(&v, &states_soa[(size_t)k * K + i], 4);
+        if (!(std::fabs(v) <= 4096.0f)) return set_err(DESPOT_EINVAL, "car: coordinates must be finite, |v| <= 4096");
+      }
+  }
   // this rank's shard: global ids with id % world == rank
   std::vector<uint32_t> ids;
   for (uint32_t i = (uint32_t)m->rank; i < K; i += (uint32_t)m->world) ids.push_back(i);

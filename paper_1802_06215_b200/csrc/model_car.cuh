@@ -85,10 +85,21 @@ struct CarThreadT {
     int gap;
     float px[MAXP], py[MAXP];
   };
-  // the default policy's view of pedestrian (x, y) from car bin cxb (card §3.4)
-  static __device__ __forceinline__ void gap_min(int& gap, int cxb, float x, float y) {
-    const int pxb = car_bin_i(x), pyb = car_bin_i(y);
-    if (pxb >= cxb && pyb >= -4 && pyb <= 3 && pxb - cxb < gap) gap = pxb - cxb;
+  // The default policy's view of pedestrian (x, y) from car bin cxb (card
+  // §3.4): the nearest pedestrian ahead in the lane, min over {x_bin - cxb :
+  // x_bin >= cxb, -4 <= y_bin <= 3} capped at 255, the bins floor(2v).  Kept
+  // in float compares, without a conversion per pedestrian: y_bin in -4..3
+  // <=> -2 <= y < 2, x_bin >= cxb <=> x >= cxb / 2 (both exact), and the
+  // minimum bin is the bin of the minimum x (floor is monotone); gap_end
+  // converts once.  Equal to the bins' form for |coordinates| < 2^14, which
+  // belief_load guarantees for the driving model (reading R21).
+  static __device__ __forceinline__ void gap_min(float& mx, float hcx, float x, float y) {
+    if (y >= -2.0f && y < 2.0f && x >= hcx) mx = fminf(mx, x);
+  }
+  static __device__ __forceinline__ int gap_end(float mx, int cxb) {
+    if (!(mx < 3.0e38f)) return 255;
+    const int g = car_bin_i(mx) - cxb;
+    return g < 255 ? g : 255;
   }
   static __device__ __forceinline__ bool active(const Sm& sm, int p) { return p < MAXP && (EXACT || p < sm.peds); }
   static __device__ __forceinline__ St load(const Sm& sm, const uint32_t* st, uint32_t cap, uint32_t i) {
@@ -99,19 +110,21 @@ struct CarThreadT {
     s.term = (w1 >> 8) & 1u;
     s.g0 = st[2 * cap + i];
     s.g1 = st[3 * cap + i];
-    s.gap = 255;
     const int cxb = car_bin_i(s.xc);
+    const float hcx = 0.5f * (float)cxb;
+    float mx = 3.4e38f;
 #pragma unroll
     for (int p = 0; p < MAXP; ++p) {
       if (active(sm, p)) {
         s.px[p] = __uint_as_float(st[(4 + 2 * p) * cap + i]);
         s.py[p] = __uint_as_float(st[(5 + 2 * p) * cap + i]);
-        gap_min(s.gap, cxb, s.px[p], s.py[p]);
+        gap_min(mx, hcx, s.px[p], s.py[p]);
       } else {
         s.px[p] = 0.0f;
         s.py[p] = 0.0f;
       }
     }
+    s.gap = gap_end(mx, cxb);
     return s;
   }
   static __device__ __forceinline__ void store(const Sm& sm, const St& s, uint32_t* st, uint32_t cap,
@@ -169,7 +182,8 @@ struct CarThreadT {
     s.xc = s.xc + v * 0.25f;
     bool coll = false;
     const int cxb = car_bin_i(s.xc);
-    s.gap = 255;
+    const float hcx = 0.5f * (float)cxb;
+    float mx = 3.4e38f;
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
       if (4 * bk >= (EXACT ? MAXP : sm.peds) + 1) break;  // uniform
@@ -183,10 +197,11 @@ struct CarThreadT {
           car_ped_move(s.px[p], s.py[p], goal(s, p), cs.x, cs.y);
           const float dx = s.px[p] - s.xc;
           coll = coll || (dx * dx + s.py[p] * s.py[p] < 1.0f);
-          gap_min(s.gap, cxb, s.px[p], s.py[p]);
+          gap_min(mx, hcx, s.px[p], s.py[p]);
         }
       }
     }
+    s.gap = gap_end(mx, cxb);
     const bool g = s.xc >= 20.0f;
     r = car_reward(a, coll, g, v);
     s.term = coll || g;

@@ -735,7 +735,9 @@ def _timed_form_equals_record(gm, leaves, Grec):
 def _car_edge_belief(K, peds=2):
     """Hand-placed driving states (card §3.4): the goal line one step away,
     a pedestrian on the car's path, speed levels 0 and 4, a pedestrian
-    standing on its goal (the d2 < 1e-6 branch), a terminal scenario."""
+    standing on its goal (the d2 < 1e-6 branch), a terminal scenario, a
+    pedestrian on or next to the edges of pi0's lane test (y = +-2, x on a
+    car bin boundary)."""
     rng = np.random.Generator(np.random.PCG64(11))
     st = np.zeros((4 + 2 * peds, K), np.uint32)
     goals_xy = [(0.0, -10.0), (0.0, 10.0), (20.0, -10.0), (20.0, 10.0)]
@@ -752,10 +754,30 @@ def _car_edge_belief(K, peds=2):
                 x, y = xc + 0.6, 0.1 * (k % 3)          # on the car's path
             elif i == 0 and case == 2:
                 x, y = goals_xy[g[i]]                  # on its own goal
+            elif i == 1 and case in (3, 4):            # near pi0's lane edges, ahead of the car
+                x = xc + 0.5 * rng.integers(-1, 16) + (0.0 if k % 4 else 0.01 * rng.random())
+                y = float(rng.choice([-2.0, 2.0])) + float(rng.choice([0.0, 0.02, -0.02, 0.13, -0.13]))
             else:
                 x, y = 2.0 + 17.0 * rng.random(), -5.0 + 10.0 * rng.random()
             st[4 + 2 * i, k], st[5 + 2 * i, k] = f(x), f(y)
     return st
+
+
+def test_car_coordinates_beyond_the_bins_rejected():
+    """belief_load refuses driving coordinates outside +-4096 m or not finite
+    (the int16 observation bins, reading R21); 4096 itself is accepted"""
+    gm = Model("car", inputs.car_params(2, D=20), flags=1)
+    K = 4
+    w = inputs.weights(K, 5)
+    for word, bad in ((0, 4097.0), (4, -5000.0), (7, np.inf), (5, np.nan)):
+        st = _car_edge_belief(K, 2)
+        st[word, 1] = np.float32(bad).view(np.uint32)
+        with pytest.raises(DespotError):
+            gm.belief_load(st, w, 3)
+    st = _car_edge_belief(K, 2)
+    st[4, 2] = np.float32(4096.0).view(np.uint32)
+    gm.node_release(gm.belief_load(st, w, 3))
+    gm.close()
 
 
 @pytest.mark.parametrize("grouped", [False, True])
