@@ -535,7 +535,7 @@ def main():
 
     preps = {}
 
-    def one_step(outputs, device_outputs, timing=True):
+    def one_step(outputs, device_outputs, timing=True, ev_end=None):
         if one_gpu_test:  # caller-driven exchange over gloo (functional test only)
             from paper_1802_06215_b200.dist import run_exchange
             b, ex = model.expand_begin(leaves, timing=timing)
@@ -549,6 +549,8 @@ def main():
                                            pinned=not device_outputs)  # e2e: page-locked host results
             prep = preps[key]
             steps, launches, nodes = model.run_prepared(prep, stream=stream)
+            if ev_end is not None:  # the call has returned (synchronous): the step ends here
+                ev_end.record(stream)
             E = prep["E"]
             o = {"scenario_steps": steps, "launches": launches, "phase_ms": list(E.phase_ms),
                  "num_children": E.num_children, "h2d_bytes": int(E.h2d_bytes), "d2h_bytes": int(E.d2h_bytes),
@@ -589,8 +591,9 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        o = one_step(dev_out, True, timing=False)
-        ev[i][1].record(stream)
+        o = one_step(dev_out, True, timing=False, ev_end=ev[i][1])
+        if one_gpu_test:
+            ev[i][1].record(stream)
         release(o)  # host bookkeeping of the bench (the arenas a search would keep), outside the events
         steps_count.append(o["scenario_steps"])
         launches += o["launches"]

@@ -28,6 +28,16 @@ enum Kind : int32_t { kTiger = 1, kRockSample = 2, kNav = 3, kCar = 4 };
 // struct at offset 0, then the model's variable-size tables
 // (DevModel::sm_table_bytes, aligned to 16), then the kernel's own data.
 extern __shared__ __align__(16) unsigned char hd_dyn_smem[];
+
+// Programmatic dependent launch (the batch's kernel chain K1 -> K2 -> K3 is
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization): a kernel
+// lets its successor's CTAs launch as soon as all of its own CTAs have started
+// (pdl_trigger), and the successor waits for the predecessor's completion and
+// memory (pdl_wait) before it touches anything but the model's constants, so
+// launch latency and the successor's prologue (the model's shared-memory
+// image) overlap the predecessor.  Both are no-ops on a plain launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct DevModel {

@@ -582,6 +582,29 @@ int kernel_occupancy(const void* kern, size_t smem, int block) {
   return occ;
 }
 
+// The batch's K2 and K3 kernels can be launched with programmatic stream
+// serialization (common.cuh, pdl_wait / pdl_trigger): DESPOT_PDL = bit mask,
+// 1 = K2 after K1, 2 = the K3 kernels (default 0: measured no faster).
+static int pdl_mask() {
+  static const int mk = getenv("DESPOT_PDL") ? atoi(getenv("DESPOT_PDL")) : 0;
+  return mk;
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(int role, void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = (pdl_mask() & role) ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // errors: check_launch
+}
+
 int check_launch(despot_model* m, const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -942,7 +965,7 @@ static int launch_group_sparse(despot_model* m, despot_batch* b) {
   while ((1u << tbits) < 2 * b->S) ++tbits;  // hash table >= 2 n slots
   const size_t smem = 12 * ((size_t)1 << tbits) + 4 * (size_t)b->S;
   kernel_occupancy((const void*)k3_group_sparse, smem, 512);  // sets the smem attribute if > 48 KB
-  k3_group_sparse<<<(unsigned)((uint64_t)b->L * b->A), 512, smem, b->stream>>>(b->bd, b->io, tbits, nullptr);
+  launch_pdl(2, k3_group_sparse, (unsigned)((uint64_t)b->L * b->A), 512, smem, b->stream, b->bd, b->io, tbits, nullptr);
   ++b->launches;
   return check_launch(m, "K3a(sparse)");
 }
@@ -983,26 +1006,26 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
                 : Bp == 3 ? pick(std::integral_constant<int, 3>{}) : pick(std::integral_constant<int, 4>{});
     const int occ = kernel_occupancy((const void*)kern, 0, 128);
     const uint64_t g = std::min<uint64_t>((warps + 3) / 4, (uint64_t)m->num_sms * occ);
-    kern<<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+    launch_pdl(1, kern, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
   } else if (grouped) {
     const uint64_t G = ((uint64_t)dm.peds + 4) / 4, gpw = 32 / G;
     const uint64_t warps = (q_bound + gpw - 1) / gpw;
     auto kern = record ? k2_car_group<true> : k2_car_group<false>;
     const int occ = kernel_occupancy((const void*)kern, 0, 128);
     const uint64_t g = std::min<uint64_t>((warps + 3) / 4, (uint64_t)m->num_sms * occ);
-    kern<<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+    launch_pdl(1, kern, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
   } else if (unfactored) {
     dispatch_car(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       const uint64_t g = std::min<uint64_t>((q_bound + 127) / 128, (uint64_t)m->num_sms * 16);
-      if (record) k2_car_thread<M, true><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
-      else k2_car_thread<M, false><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+      if (record) launch_pdl(1, k2_car_thread<M, true>, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
+      else launch_pdl(1, k2_car_thread<M, false>, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
       return 0;
     });
   } else {
     const uint64_t g = std::min<uint64_t>((q_bound + 3) / 4, (uint64_t)m->num_sms * 16);
-    if (record) k2_car_warp<true><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
-    else k2_car_warp<false><<<(unsigned)std::max<uint64_t>(g, 1), 128, 0, st>>>(b->bd, b->io);
+    if (record) launch_pdl(1, k2_car_warp<true>, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
+    else launch_pdl(1, k2_car_warp<false>, (unsigned)std::max<uint64_t>(g, 1), 128, 0, st, b->bd, b->io);
   }
   b->mark(4);
   ++b->launches;
@@ -1011,6 +1034,16 @@ static int launch_k2_sparse(despot_model* m, despot_batch* b, bool record) {
 
 static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st);
 
+// K3 for many slots as the single fused kernel (dense keys, S > 32, the
+// compacted slot arrays within its shared-memory limit)
+static bool wide_fused(uint32_t S, bool sparse) {
+  return !sparse && S > kWideS && wide_fused_smem(S) <= kWideFusedMaxSmem;
+}
+// look-back words: the tile counter + one per tile (a tile of kScanTile
+// (leaf, action) pairs, or one pair in the fused wide kernel) + 1
+static uint64_t scan_words(uint64_t LA, uint32_t S, bool sparse) {
+  return (wide_fused(S, sparse) ? LA : LA / kScanTile) + 2;
+}
 static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, uint32_t flags, void* stream,
                       despot_expansion* bind, despot_batch** out) {
   if (!m || !leaves || !out) return set_err(DESPOT_EINVAL, "null argument");
@@ -1182,7 +1215,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   // K3b's look-back flags (tile counter + one word per 1024 (leaf, action)
   // pairs), zeroed by the same memset as the status block and the sums
   const size_t o_scan = off;
-  off += 8 * (LA / kScanTile + 2);
+  off += 8 * scan_words(LA, b->S, b->sparse);
   const size_t o_sums = take(8 * b->n_sums), o_mins = take(4 * b->n_mins), o_rank = take(4 * LAS),
                o_nc = take(4 * LA), o_item = take(b->sparse ? 4 * LAS : 0),
                o_hash = take(8 * q_bound), o_keys = take(4 * q_bound * dm.OW), o_q3 = take(24 * q_bound),
@@ -1377,7 +1410,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       if (grid > maxg) grid = maxg;
       if (grid < 1) grid = 1;
       b->mark(3);
-      kern<<<(unsigned)grid, 128, smem, st>>>(bd, round_keys(ld[0].seed_lo, ld[0].seed_hi));
+      launch_pdl(1, kern, (unsigned)grid, 128, smem, st, bd, round_keys(ld[0].seed_lo, ld[0].seed_hi));
       ++b->launches;
       b->mark(4);
       return check_launch(m, "K2");
@@ -1734,6 +1767,15 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
     const bool small_k3 = !b->sparse && b->S <= 32 &&
                           LA <= std::min<uint64_t>(kSmallLA, 32 * (32 / small_group_width(b->S)) * 2);
     if (b->k3_fused) {
+    } else if (!rc && wide_fused(b->S, b->sparse)) {
+      // many slots: rank + look-back scan + write in one kernel, a CTA per (leaf, action)
+      static std::once_flag once;
+      std::call_once(once, [] {
+        cudaFuncSetAttribute(k3_wide_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideFusedMaxSmem);
+      });
+      launch_pdl(2, k3_wide_fused, (unsigned)LA, kWideFusedThreads, wide_fused_smem(b->S), st, bd);
+      ++b->launches;
+      rc = check_launch(m, "K3(wide)");
     } else if (!rc && b->sharded_sparse) {
       rc = merge_sparse(m, b);  // the ranks' records -> global children
     } else if (!rc && b->sparse) {
@@ -1743,42 +1785,43 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
       const size_t smem = small_finalize_smem(LA);
       static std::once_flag once;
       std::call_once(once, [] { cudaFuncSetAttribute(k3_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 << 10); });
-      k3_small_dense<<<1, 1024, smem, st>>>(bd);
+      launch_pdl(2, k3_small_dense, 1, 1024, smem, st, bd);
       ++b->launches;
       rc = check_launch(m, "K3(small)");
     } else if (!rc && b->S <= 16) {  // counts only: k3_write_grouped recomputes the ordinals
       const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
-      k3_count_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+      launch_pdl(2, k3_count_grouped, (unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st, bd);
       ++b->launches;
       rc = check_launch(m, "K3a");
     } else if (!rc) {
-      k3_rank_dense<<<g3, 128, warps_per_cta * b->S * 8, st>>>(bd);
+      launch_pdl(2, k3_rank_dense, g3, 128, warps_per_cta * b->S * 8, st, bd);
       ++b->launches;
       rc = check_launch(m, "K3a");
     }
-    if (!rc && !small_k3 && !b->k3_fused) {
-      k3_scan_lookback<<<(unsigned)((LA + kScanTile - 1) / kScanTile), kScanTile, 0, st>>>(bd);
+    const bool wide1 = wide_fused(b->S, b->sparse);
+    if (!rc && !small_k3 && !b->k3_fused && !wide1) {
+      launch_pdl(2, k3_scan_lookback, (unsigned)((LA + kScanTile - 1) / kScanTile), kScanTile, 0, st, bd);
       ++b->launches;
       rc = check_launch(m, "K3b");
     }
     if (!rc && b->sparse) {
-      k3_write_sparse<<<(unsigned)LA, 256, 0, st>>>(bd, b->io);  // (merged: keys from the gathered records)
+      launch_pdl(2, k3_write_sparse, (unsigned)LA, 256, 0, st, bd, b->io);  // (merged: keys from the gathered records)
       ++b->launches;
       rc = check_launch(m, "K3c(sparse)");
-    } else if (!rc && !small_k3) {
+    } else if (!rc && !small_k3 && !wide1) {
       if (b->S > kWideS) {
-        k3_write_wide<<<(unsigned)LA, 256, 0, st>>>(bd);
+        launch_pdl(2, k3_write_wide, (unsigned)LA, 256, 0, st, bd);
       } else if (b->S <= 16) {
         const uint64_t pairs_per_cta = 4 * (32 / small_group_width(b->S));
-        k3_write_grouped<<<(unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st>>>(bd);
+        launch_pdl(2, k3_write_grouped, (unsigned)((LA + pairs_per_cta - 1) / pairs_per_cta), 128, 0, st, bd);
       } else {
-        k3_write_dense<<<g3, 128, 0, st>>>(bd);
+        launch_pdl(2, k3_write_dense, g3, 128, 0, st, bd);
       }
       ++b->launches;
       rc = check_launch(m, "K3c");
     }
     if (!rc && record && bd.scen_child) {  // each scenario's child ordinal
-      k3_scen_child<<<(unsigned)m->num_sms * 4, 256, 0, st>>>(bd, b->sparse ? 0u : 1u);
+      launch_pdl(2, k3_scen_child, (unsigned)m->num_sms * 4, 256, 0, st, bd, b->sparse ? 0u : 1u);
       ++b->launches;
       rc = check_launch(m, "scen_child");
     }
@@ -1875,7 +1918,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
     }
     if (e0 & kErrXOverflow) {  // every rank saw the same union: the dense fallback, then K3 again
       if (cudaMemsetAsync(bd.err, 0, 4, st) != cudaSuccess ||
-          cudaMemsetAsync(bd.scan_flags, 0, 8 * (LA / kScanTile + 2), st) != cudaSuccess)
+          cudaMemsetAsync(bd.scan_flags, 0, 8 * scan_words(LA, b->S, b->sparse), st) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "capacity retry reset failed");
       if (!rc) rc = lib_exchange_dense(b);
       if (!rc) rc = launch_k3();
@@ -2119,7 +2162,25 @@ extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void*
   }
   const intptr_t shift = b->new_block ? static_cast<char*>(b->new_block->ptr) - reinterpret_cast<char*>(kTemplateBase) : 0;
   auto rebase = [shift](auto* q) { return reinterpret_cast<decltype(q)>(reinterpret_cast<char*>(q) + shift); };
+  // the leaf table's arena pointers first (the graph uploads it), the node
+  // bookkeeping after the launch, while the GPU runs
   LeafDev* hl = reinterpret_cast<LeafDev*>(static_cast<char*>(b->pinned) + b->o_leaves);
+  for (uint32_t l = 0; l < L; ++l) {
+    if (p->leaves[l].action < 0) continue;
+    const Node& t = p->tmpl[l];
+    LeafDev& d = hl[l];
+    d.ids = rebase(t.ids);
+    d.w = rebase(t.w);
+    d.states = rebase(t.states);
+    d.keys = rebase(t.keys);
+    d.nchild = rebase(t.nchild);
+  }
+  b->launches = p->launches;
+  b->h2d = p->h2d;
+  b->d2h = p->d2h;
+  g_ht.mark("patched");
+  const bool launched = cudaGraphLaunch(p->exec, st) == cudaSuccess;
+  g_ht.mark("graph_launched");
   {
     std::lock_guard<std::mutex> g(m->mu);
     for (uint32_t l = 0; l < L; ++l) {
@@ -2139,23 +2200,12 @@ extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void*
       m->nodes.insert(nd);
       b->leaf_node[l] = nd;
       b->is_new[l] = true;
-      LeafDev& d = hl[l];
-      d.ids = nd->ids;
-      d.w = nd->w;
-      d.states = nd->states;
-      d.keys = nd->keys;
-      d.nchild = nd->nchild;
     }
   }
-  b->launches = p->launches;
-  b->h2d = p->h2d;
-  b->d2h = p->d2h;
-  g_ht.mark("patched");
-  if (cudaGraphLaunch(p->exec, st) != cudaSuccess) {
+  if (!launched) {
     free_batch(b, true);
     return set_err(DESPOT_ECUDA, "cudaGraphLaunch failed");
   }
-  g_ht.mark("graph_launched");
   return finish_batch(b, out, st, kFinishComplete);
 }
 

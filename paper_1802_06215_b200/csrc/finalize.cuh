@@ -114,6 +114,8 @@ __device__ __forceinline__ void rank_one(const BatchDev& b, uint64_t la, uint32_
   __syncwarp();
 }
 __global__ void __launch_bounds__(128) k3_rank_dense(BatchDev b) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char k3_smem[];
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
@@ -131,6 +133,8 @@ __global__ void __launch_bounds__(kScanTile) k3_scan_lookback(BatchDev b) {
   __shared__ uint64_t wsum[32];
   __shared__ uint32_t tile_sh;
   __shared__ uint64_t excl_sh;
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kVal = (1ull << 62) - 1;
   const uint64_t LA = (uint64_t)b.L * b.A;
   if (threadIdx.x == 0) tile_sh = (uint32_t)atomicAdd(&b.scan_flags[0], 1ull);
@@ -220,6 +224,8 @@ __device__ __forceinline__ void write_one(const BatchDev& b, uint64_t la, uint32
   }
 }
 __global__ void __launch_bounds__(128) k3_write_dense(BatchDev b) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t la = (uint64_t)blockIdx.x * (blockDim.x >> 5) + wid;
   if (la >= (uint64_t)b.L * b.A) return;
@@ -237,6 +243,8 @@ __host__ __device__ inline uint32_t small_group_width(uint32_t S) {
 // (leaf, action) -- k3_write_grouped recomputes the ordinals -- a lane per
 // slot, 32/S' pairs per warp
 __global__ void __launch_bounds__(128) k3_count_grouped(BatchDev b) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t lane = threadIdx.x & 31, S = b.S, LA = b.L * b.A;
   const uint32_t Sp = small_group_width(S);
   const uint32_t j = lane & (Sp - 1), gshift = lane & ~(Sp - 1);
@@ -254,6 +262,8 @@ __global__ void __launch_bounds__(128) k3_count_grouped(BatchDev b) {
 // of two), the child ordinals recomputed in registers from the first ids
 // (the rank array is not read), every load of a pair issued at once
 __global__ void __launch_bounds__(128) k3_write_grouped(BatchDev b) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t lane = threadIdx.x & 31, S = b.S, A = b.A;
   const uint32_t LA = b.L * A;
   const uint32_t Sp = small_group_width(S), G = 32 / Sp;
@@ -322,6 +332,8 @@ __global__ void __launch_bounds__(128) k3_write_grouped(BatchDev b) {
 constexpr uint32_t kWideS = 32;
 __global__ void __launch_bounds__(256) k3_write_wide(BatchDev b) {
   __shared__ int64_t s_wt[8], s_nt[8];
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t S = b.S, A = b.A;
   const uint64_t LA = (uint64_t)b.L * A, la = blockIdx.x;
   const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
@@ -374,6 +386,149 @@ __global__ void __launch_bounds__(256) k3_write_wide(BatchDev b) {
     }
   }
 }
+
+// K3 for many observation slots (S > 32: navigation's 257) in ONE kernel:
+// rank, scan and write of (leaf, action) la per CTA, the CTAs in ticket order
+// (la = ticket, so every predecessor a CTA looks back on is already running)
+// and the child_begin prefix by decoupled look-back over one (flag, value)
+// word per la.  Replaces k3_rank_dense + k3_scan_lookback + k3_write_wide and
+// their global rank / count round trips.  Dynamic shared memory: 12 S bytes
+// (the compacted non-empty slots' first ids, slot numbers and ranks).
+constexpr uint32_t kWideFusedThreads = 256;
+__global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
+  extern __shared__ __align__(16) unsigned char k3w_smem[];
+  __shared__ uint32_t s_wcnt[kWideFusedThreads / 32], s_ticket, s_cnt;
+  __shared__ int64_t s_wt[kWideFusedThreads / 32], s_nt[kWideFusedThreads / 32];
+  constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kVal = (1ull << 62) - 1;
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
+  const uint32_t S = b.S, A = b.A, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr uint32_t NW = kWideFusedThreads / 32;
+  const uint64_t LA = (uint64_t)b.L * A;
+  int32_t* s_first = reinterpret_cast<int32_t*>(k3w_smem);
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(s_first + S);
+  uint32_t* s_rank = s_slot + S;
+  if (threadIdx.x == 0) s_ticket = (uint32_t)atomicAdd(&b.scan_flags[0], 1ull);
+  __syncthreads();
+  const uint64_t la = s_ticket;
+  HD_CHECK(b.err, la < LA);
+  const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
+  const SumLayout lay{LA * S, LA};
+  const uint64_t base = la * S;
+  // 1. the non-empty slots, compacted in slot order
+  uint32_t cnt = 0;
+  for (uint32_t s0 = 0; s0 < S; s0 += kWideFusedThreads) {
+    const uint32_t s = s0 + threadIdx.x;
+    const bool ne = s < S && __ldcg(&b.sums[lay.N(base + s)]) != 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, ne);
+    if (lane == 0) s_wcnt[wid] = __popc(bal);
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (uint32_t w = 0; w < NW; ++w) {
+      before += w < wid ? s_wcnt[w] : 0u;
+      tot += s_wcnt[w];
+    }
+    if (ne) {
+      const uint32_t pos = cnt + before + __popc(bal & ((1u << lane) - 1u));
+      s_first[pos] = __ldcg(&b.mins[base + s]);
+      s_slot[pos] = s;
+    }
+    cnt += tot;
+    __syncthreads();
+  }
+  HD_CHECK(b.err, cnt <= S);
+  unsigned long long* st = b.scan_flags + 1;
+  if (threadIdx.x == 0) atomicExch(&st[la], (la == 0 ? kIncl : kAgg) | cnt);  // publish early
+  // 2. look-back (warp 0, a window of 32 predecessors per L2 round trip)
+  // while the other warps rank
+  if (wid == 0) {
+    uint64_t excl = 0;
+    if (la > 0) {
+      int64_t p = (int64_t)la - 1;  // window [p - 31, p], lane j reads p - j
+      for (;;) {
+        const int64_t q = p - (int64_t)lane;
+        const unsigned long long f = q >= 0 ? atomicAdd(&st[q], 0ull) : (kIncl | 0ull);
+        // the nearest inclusive prefix in the window
+        const uint32_t incl = __ballot_sync(0xffffffffu, (f >> 62) == 2);
+        const uint32_t upto = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
+        if (__any_sync(0xffffffffu, lane <= upto && !(f >> 62))) continue;  // a predecessor not published yet
+        excl += __reduce_add_sync(0xffffffffu, lane <= upto ? (uint32_t)(f & kVal) : 0u);
+        if (incl) break;
+        p -= 32;
+      }
+      if (lane == 0) atomicExch(&st[la], kIncl | (excl + cnt));
+    }
+    if (lane == 0) s_cnt = (uint32_t)excl;
+  } else {
+    for (uint32_t i = threadIdx.x - 32; i < cnt; i += kWideFusedThreads - 32) {
+      const int32_t f = s_first[i];
+      uint32_t r = 0;
+      for (uint32_t q = 0; q < cnt; ++q) r += s_first[q] < f;
+      s_rank[i] = r;  // first occurrence (R8)
+    }
+  }
+  __syncthreads();
+  // 3. outputs: Eq. 11/12 child bounds, one-level Eq. 4, the child-key table
+  const LeafDev& lf = b.leaves[leaf];
+  const DevModel& dm = *b.model;
+  const uint32_t cb = s_cnt;  // the exclusive prefix of the child counts
+  int64_t wt = 0, nt = 0;
+  for (uint32_t i = threadIdx.x; i < cnt; i += kWideFusedThreads) {
+    const uint32_t s = s_slot[i], rk = s_rank[i];
+    HD_CHECK(b.err, rk < cnt);
+    const int64_t N = __ldcg(&b.sums[lay.N(base + s)]);
+    const int64_t W = __ldcg(&b.sums[lay.W(base + s)]);
+    wt += W;
+    nt += N;
+    const uint32_t c = cb + rk;
+    if (c < b.child_capacity) {
+      const double Wd = (double)W;
+      b.child_count[c] = (uint32_t)N;
+      b.child_first[c] = (uint32_t)s_first[i];
+      b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
+      b.child_upper[c] = (float)((double)__ldcg(&b.sums[lay.U(base + s)]) / Wd);
+      b.child_lower[c] = (float)((double)__ldcg(&b.sums[lay.Lm(base + s)]) / Wd);
+      b.child_obs[c] = s;
+    }
+    if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = s;  // key table for later updates
+  }
+  wt = warp_sum64(wt);
+  nt = warp_sum64(nt);
+  if (lane == 0) {
+    s_wt[wid] = wt;
+    s_nt[wid] = nt;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t w = 1; w < NW; ++w) {
+      wt += s_wt[w];
+      nt += s_nt[w];
+    }
+    b.child_begin[la] = cb;
+    lf.nchild[a] = cnt;
+    const double Wd = (double)wt;
+    b.act_reward[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 0)]) / Wd);
+    b.act_upper[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 1)]) / Wd);
+    b.act_lower[la] = (float)((double)__ldcg(&b.sums[lay.Q(la, 2)]) / Wd);
+    if (a == 0) {
+      b.n_scen[leaf] = (uint32_t)nt;
+      b.weight[leaf] = (float)(Wd * dm.inv_fx * lf.wroot);
+      if (nt == 0) atomicOr(b.err, kErrEmptyLeaf);
+    }
+    if (la + 1 == LA) {  // the last pair: totals
+      const uint64_t total = (uint64_t)cb + cnt;
+      b.child_begin[LA] = (uint32_t)total;
+      if (total > b.child_capacity) atomicOr(b.err, kErrChildCap);
+      b.status[1] = (uint32_t)total;
+      const uint64_t steps = (uint64_t)__ldcg(&b.sums[lay.steps()]);
+      b.status[2] = (uint32_t)steps;
+      b.status[3] = (uint32_t)(steps >> 32);
+    }
+  }
+}
+__host__ __device__ inline size_t wide_fused_smem(uint32_t S) { return 12 * (size_t)S; }
+constexpr size_t kWideFusedMaxSmem = 96 << 10;
 
 // K3 for small batches (L*A <= kSmallLA, S <= 32): rank, scan and write in
 // one CTA -- a kernel of its own, or the tail of K2's last CTA.  The path is
@@ -508,6 +663,8 @@ __device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char*
 // out of line for K2's tail: its registers do not constrain K2's main loop
 __device__ __noinline__ void small_finalize_tail(const BatchDev& b, unsigned char* smem) { small_finalize(b, smem); }
 __global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char k3s_smem[];
   small_finalize(b, k3s_smem);
 }

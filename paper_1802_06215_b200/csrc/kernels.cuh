@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   __shared__ uint32_t warp_cnt[16];
   __shared__ uint32_t s_base;
+  pdl_trigger();  // K2 may launch (it waits for this grid before reading)
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
@@ -133,6 +134,8 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   uint32_t* tile_off =
       reinterpret_cast<uint32_t*>(hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes));
   load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
+  pdl_wait();  // K1 complete: tile_off, the leaf arenas
+  pdl_trigger();
   for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
   __syncthreads();
   const uint32_t total = tile_off[b.L];

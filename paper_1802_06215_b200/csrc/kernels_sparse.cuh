@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
   __shared__ typename M::Sm sm;
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_base;
+  pdl_trigger();  // K2 may launch (it waits for this grid before reading)
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
@@ -139,6 +140,8 @@ template <class M, bool RECORD>
 __global__ void __launch_bounds__(128, HD_CART_MINB) k2_car_thread(BatchDev b, SparseItemOut io) {
   __shared__ typename M::Sm sm;
   M::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   __syncthreads();
   const DevModel& dm = *b.model;
   const uint32_t OW = dm.OW, SW = dm.SW;
@@ -211,6 +214,8 @@ template <bool RECORD>
 __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io) {
   __shared__ typename CarThreadT<1>::Sm sm;  // scalar parameters + gamma table
   CarThreadT<1>::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   __syncthreads();
   const DevModel& dm = *b.model;
   const uint32_t OW = dm.OW, SW = dm.SW;
@@ -377,6 +382,8 @@ __global__ void __launch_bounds__(128, B == 1 ? HD_CARG_MINB : 4) k2_car_group(B
   constexpr int W = 4 * B;  // words (elements) per lane
   __shared__ typename CarThreadT<1>::Sm sm;  // scalar parameters + gamma table + rotations
   CarThreadT<1>::load_sm(sm, *b.model, threadIdx.x, blockDim.x);
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   __syncthreads();
   const DevModel& dm = *b.model;
   const uint32_t OW = dm.OW, SW = dm.SW;
@@ -598,6 +605,8 @@ __global__ void __launch_bounds__(128, B == 1 ? HD_CARG_MINB : 4) k2_car_group(B
 __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut io, uint32_t tbits,
                                                        int64_t* xmax) {
   extern __shared__ __align__(16) unsigned char gs_smem[];
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t tsize = 1u << tbits, tmask = tsize - 1u;
   unsigned long long* tkey = reinterpret_cast<unsigned long long*>(gs_smem);  // [tsize]
   uint32_t* titem = reinterpret_cast<uint32_t*>(tkey + tsize);              // [tsize]
@@ -686,6 +695,8 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
 // (children are already in first-occurrence order)
 __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut io) {
   __shared__ int64_t s_wt[8], s_nt[8];
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint32_t A = b.A;
   const uint64_t LA = (uint64_t)b.L * A;
   const uint64_t la = blockIdx.x;
@@ -939,6 +950,8 @@ __global__ void __launch_bounds__(512) k3_merge_sparse(BatchDev b, MergeDev g, u
 // than the record's slot; sparse keys: the child whose key equals the record's.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k3_scen_child(BatchDev b, uint32_t dense) {
+  pdl_wait();  // the predecessor complete
+  pdl_trigger();
   const uint64_t Q = b.scen_off[b.L];
   const uint32_t OW = b.model->OW;
   const uint64_t LA = (uint64_t)b.L * b.A;
