@@ -545,8 +545,11 @@ def main():
         else:
             key = (device_outputs, timing)
             if key not in preps:
+                # device outputs (inputs resident in HBM): DESPOT_X_RESIDENT where the batch
+                # qualifies (self leaves, fused finalize: the graph is K2 alone); e2e:
+                # page-locked host results and the per-step leaf-table copy
                 preps[key] = model.prepare(leaves, device_outputs=device_outputs, child_capacity=cap, timing=timing,
-                                           pinned=not device_outputs)  # e2e: page-locked host results
+                                           pinned=not device_outputs, resident=device_outputs)
             prep = preps[key]
             steps, launches, nodes = model.run_prepared(prep, stream=stream)
             if ev_end is not None:  # the call has returned (synchronous): the step ends here

@@ -271,6 +271,14 @@ struct despot_batch {
   bool bound = false;      // outputs bound (bind_outputs)
   bool persistent = false; // a prepared batch's (graph-captured) batch: scratch, staging, events kept
   bool k3_fused = false;   // the finalize runs in K2's last CTA
+  // resident prepared batch (all leaves are nodes themselves, fused finalize):
+  // the graph holds K2 alone; the scratch's zero state and the leaf table are
+  // set up once (resident_init) and restored by K2's last CTA, the status
+  // arrives in mapped host memory (hmapped); dirty: re-initialise before the
+  // next run (after an error)
+  bool resident = false, dirty = false;
+  uint32_t* hmapped = nullptr;
+  size_t r_stat = 0, r_zero = 0, r_h2d = 0;  // status offset, bytes zeroed from it, leaf-table bytes
   size_t o_ns = 0, o_w = 0, o_ar = 0, o_au = 0, o_al = 0, o_cb = 0, o_cc = 0, o_cf = 0, o_cw = 0, o_cu = 0,
          o_cl = 0, o_co = 0, o_so = 0;  // staging layout
   bool sparse = false;
@@ -1290,6 +1298,14 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   bool all_self = true;
   for (uint32_t l = 0; l < L; ++l) all_self = all_self && leaves[l].action < 0;
   const size_t h2d_bytes = all_self ? o_stat + stat_bytes : sizeof(LeafDev) * L;
+  // a prepared batch of self leaves that will fuse its finalize: resident
+  // (the same rule as k3_fused below, with the outputs bound)
+  {
+    const uint64_t G = 32 / small_group_width(b->S);
+    b->resident = g_capture && all_self && bind && !ilist && !b->sparse && !xdense && m->world == 1 &&
+                  !(flags & DESPOT_X_RECORD_SCENARIO) && b->S <= 32 &&
+                  (uint64_t)L * dm.A <= 4 * G * kSmallUnroll * 2 && (bind->flags & DESPOT_X_RESIDENT);
+  }
   void* hp = pinned_pool().acquire(std::max<size_t>(h2d_bytes, ilist ? o_idx + 4 * idx_total : 0));
   b->pinned = hp;
   if (ilist)
@@ -1320,13 +1336,25 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       tile[L] = (uint32_t)tacc;
       scen[L] = sacc;
     }
-    if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
+    b->r_stat = o_stat;
+    b->r_zero = (o_sums - o_stat) + 8 * b->n_sums;
+    b->r_h2d = h2d_bytes - o_leaves;
+    if (b->resident) {  // set up once, outside the graph (resident_init)
+      if (cudaHostAlloc(reinterpret_cast<void**>(&b->hmapped), stat_bytes, cudaHostAllocMapped) != cudaSuccess) {
+        b->hmapped = nullptr;
+        rc = set_err(DESPOT_ENOMEM, "mapped status block");
+      }
+      uint32_t* dptr = nullptr;
+      if (!rc && cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), b->hmapped, 0) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "mapped status block: device pointer");
+      bd.hstat = dptr;
+    } else if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
         cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
         (xdense && (size_t)x.nblk * kXBlk > LAS &&
          cudaMemsetAsync(x.flags + LAS, 0, (size_t)x.nblk * kXBlk - LAS, st) != cudaSuccess) ||
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
-    b->h2d += h2d_bytes - o_leaves;
+    if (!b->resident) b->h2d += h2d_bytes - o_leaves;
     if (!rc && ilist && idx_total) {
       memcpy(h + o_idx, bind->index, 4 * idx_total);
       if (cudaMemcpyAsync(s + o_idx, h + o_idx, 4 * idx_total, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -1869,7 +1897,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
   auto copy_and_sync = [&](bool enqueue, bool sync) -> int {
     int rc = DESPOT_OK;
     if (enqueue) {
-    if (!rc) {
+    if (!rc && !b->resident) {  // (resident: K2's last CTA writes it to mapped memory)
       b->d2h += stat_bytes;
       if (cudaMemcpyAsync(hs, bd.status, stat_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "status copy failed");
@@ -1907,6 +1935,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
   };
   if (!rc) rc = copy_and_sync(mode != kFinishComplete, mode != kFinishEnqueue);
   if (mode == kFinishEnqueue) return rc;  // a prepared batch's capture ends here
+  if (b->resident) hs = reinterpret_cast<char*>(b->hmapped);  // published by K2's last CTA
   if (!rc && b->xlib && !b->sparse) {
     // the packed exchange's capacity hint follows the largest union seen (+ 1/4)
     uint32_t T = 0, e0 = 0;
@@ -1943,6 +1972,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
       rc = set_err(DESPOT_ECAPACITY, "child_capacity %u < %u children", C, nchildren);
     else if (err & kErrScenCap) rc = set_err(DESPOT_ECAPACITY, "scen_capacity too small");
   }
+  if (b->resident && (rc || err)) b->dirty = true;  // the device state is not known to be restored
   if (!rc && !dev_out) {
     const uint64_t Cu = nchildren;
     uint64_t Su = 0;
@@ -2069,6 +2099,19 @@ struct despot_prepared {
   uint64_t h2d = 0, d2h = 0;
 };
 
+// a resident batch's starting state: zero status header, n_leaf and the
+// prefixes from the host, zero sums, 0x7F first ids, the leaf table
+static int resident_init(despot_batch* b, cudaStream_t st) {
+  char* s = static_cast<char*>(b->scratch);
+  const char* h = static_cast<const char*>(b->pinned);
+  if (cudaMemsetAsync(s + b->r_stat, 0, b->r_zero, st) != cudaSuccess ||
+      cudaMemsetAsync(b->bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
+      cudaMemcpyAsync(s + b->o_leaves, h + b->o_leaves, b->r_h2d, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return set_err(DESPOT_ECUDA, "resident batch set-up failed");
+  b->dirty = false;
+  return DESPOT_OK;
+}
+
 static void free_prepared(despot_prepared* p) {
   if (!p) return;
   cudaSetDevice(p->m->device);
@@ -2081,6 +2124,7 @@ static void free_prepared(despot_prepared* p) {
     if (b->pinned) pinned_pool().release(b->pinned);
     if (b->hs) pinned_pool().release(b->hs);
     if (b->hp_out) pinned_pool().release(b->hp_out);
+    if (b->hmapped) cudaFreeHost(b->hmapped);
     if (b->timing) event_pool().release(b->ev);
     delete b;
   }
@@ -2121,9 +2165,33 @@ extern "C" int despot_batch_prepare(despot_model* m, const despot_leaf* leaves, 
     }
   }
   p->graph = g;
+  if (g && getenv("DESPOT_HOST_TRACE")) {  // the captured nodes, by type
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    fprintf(stderr, "[despot prepared graph] %zu nodes:", nn);
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      cudaGraphNodeGetType(nd, &t);
+      const char* nm = "";
+      cudaKernelNodeParams kp;
+      if (t == cudaGraphNodeTypeKernel && cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess)
+        cudaFuncGetName(&nm, kp.func);
+      fprintf(stderr, " %d%s%.40s", (int)t, *nm ? ":" : "", nm);
+    }
+    fprintf(stderr, "\n");
+  }
   if (!rc && (ce != cudaSuccess || !g)) rc = set_err(DESPOT_ECUDA, "graph capture failed: %s", cudaGetErrorString(ce));
   if (!rc && cudaGraphInstantiate(&p->exec, g, 0) != cudaSuccess)
     rc = set_err(DESPOT_ECUDA, "cudaGraphInstantiate failed");
+  if (!rc && b->resident) {
+    cudaStream_t is;
+    CU(cudaStreamCreateWithFlags(&is, cudaStreamNonBlocking));
+    rc = resident_init(b, is);
+    if (!rc && cudaStreamSynchronize(is) != cudaSuccess) rc = set_err(DESPOT_ECUDA, "resident batch set-up failed");
+    cudaStreamDestroy(is);
+  }
   if (rc) {
     cudaGetLastError();
     free_prepared(p.release());
@@ -2178,6 +2246,10 @@ extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void*
   b->launches = p->launches;
   b->h2d = p->h2d;
   b->d2h = p->d2h;
+  if (b->resident && b->dirty) {
+    if (int rc = resident_init(b, st)) return rc;
+    b->h2d += b->r_h2d;
+  }
   g_ht.mark("patched");
   const bool launched = cudaGraphLaunch(p->exec, st) == cudaSuccess;
   g_ht.mark("graph_launched");

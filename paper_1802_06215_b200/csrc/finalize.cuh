@@ -662,6 +662,25 @@ __device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char*
 }
 // out of line for K2's tail: its registers do not constrain K2's main loop
 __device__ __noinline__ void small_finalize_tail(const BatchDev& b, unsigned char* smem) { small_finalize(b, smem); }
+// A resident prepared batch (a graph of one kernel): after
+// the fused finalize the last CTA publishes the status block to mapped host
+// memory (the host reads it after the stream synchronises: no D2H copy) and
+// puts the scratch back into the state the next run starts from (zero sums,
+// 0x7F7F7F7F first ids, zero status header; n_leaf and the prefixes are the
+// batch's constants), so the graph needs no memset nodes.  Every other CTA
+// has finished (it took its ticket after its last tile).
+__device__ __noinline__ void resident_epilogue(const BatchDev& b) {
+  __syncthreads();  // this CTA's finalize is complete
+  const uint32_t nst = kStatWords + b.L;
+  for (uint32_t i = threadIdx.x; i < nst; i += blockDim.x) b.hstat[i] = __ldcg(&b.status[i]);
+  __threadfence_system();
+  __syncthreads();
+  const SumLayout lay{(uint64_t)b.L * b.A * b.S, (uint64_t)b.L * b.A};
+  const uint64_t ns = lay.total(), nm = lay.las;
+  for (uint64_t i = threadIdx.x; i < ns; i += blockDim.x) b.sums[i] = 0;
+  for (uint64_t i = threadIdx.x; i < nm; i += blockDim.x) b.mins[i] = 0x7F7F7F7F;
+  if (threadIdx.x < kStatWords) b.status[threadIdx.x] = 0u;
+}
 __global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
   pdl_wait();  // the predecessor complete
   pdl_trigger();

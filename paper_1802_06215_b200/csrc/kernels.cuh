@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     if (k2_last) {
       __threadfence();
       small_finalize_tail(b, reinterpret_cast<unsigned char*>(tile_off) + align16(4 * ((size_t)b.L + 1)));
+      if (b.hstat) resident_epilogue(b);
     }
   }
 }

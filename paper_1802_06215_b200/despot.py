@@ -19,6 +19,7 @@ DESPOT_X_RECORD_SCENARIO = 2
 DESPOT_X_TIMING = 4
 DESPOT_X_TIMING_K2 = 8
 DESPOT_X_INDEX_LISTS = 16
+DESPOT_X_RESIDENT = 32
 DESPOT_MF_UNFACTORED = 1
 DESPOT_MF_FACTORED = 2
 DESPOT_MF_GROUPED = 4
@@ -470,19 +471,22 @@ class Model:
         return self._finish(o, E, L, nodes, record, device_outputs)
 
     # ---- prepared calls (repeated batches: no per-call marshalling) ----
-    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False, pinned=False, graph=True):
+    def prepare(self, leaves, device_outputs=False, child_capacity=None, timing=False, pinned=False, graph=True,
+                resident=False):
         """A repeated batch: the leaf table, output arrays and expansion struct
         built once, and (graph=True, single GPU) despot_batch_prepare's CUDA
         graph of the batch's device work; `run_prepared` then costs one
         foreign call (despot_batch_run: new arenas, leaf-table patch, one
         graph launch).  pinned: host outputs in page-locked memory (copied
-        into directly)."""
+        into directly).  resident: DESPOT_X_RESIDENT (self leaves, small
+        batch: the graph is K2 alone)."""
         L = len(leaves)
         C_cap = child_capacity if child_capacity is not None else self.child_capacity_bound(leaves)
         o, E = self._alloc_outputs(L, C_cap, 0, False, device_outputs, pinned=pinned)
         nodes = (C.c_uint64 * L)()
         E.node = C.addressof(nodes)
-        E.flags = (DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | _tflag(timing)
+        E.flags = ((DESPOT_X_DEVICE_OUTPUTS if device_outputs else 0) | _tflag(timing) |
+                   (DESPOT_X_RESIDENT if resident else 0))
         prep = {"lv": self._leaves(leaves), "L": L, "E": E, "o": o, "nodes": nodes, "ref": C.byref(E),
                 "leaves": list(leaves), "graph": None}
         if graph and self.world == 1 and self.comm is None:

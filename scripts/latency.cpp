@@ -45,9 +45,10 @@ int main(int argc, char** argv) {
   // host outputs (pinned) and device outputs; mode 2 = device outputs
   // through the two-phase form (begin/end: separate K3, no fusion); modes 3, 4
   // = a prepared batch (despot_batch_prepare: one CUDA graph per run) with
-  // host / device outputs
-  for (int mode = 0; mode < 5; ++mode) {
-    const int dev = mode == 1 || mode == 2 || mode == 4;
+  // host / device outputs; mode 5 = a resident prepared batch
+  // (DESPOT_X_RESIDENT: the graph is K2 alone), device outputs
+  for (int mode = 0; mode < 6; ++mode) {
+    const int dev = mode == 1 || mode == 2 || mode == 4 || mode == 5;
     despot_expansion out;
     memset(&out, 0, sizeof out);
     despot_node node;
@@ -61,7 +62,7 @@ int main(int argc, char** argv) {
       p += (n + 15) & ~size_t(15);
       return q;
     };
-    out.flags = dev ? DESPOT_X_DEVICE_OUTPUTS : 0;
+    out.flags = (dev ? DESPOT_X_DEVICE_OUTPUTS : 0) | (mode == 5 ? DESPOT_X_RESIDENT : 0);
     out.node = &node;
     out.n_scen = (uint32_t*)take(4);
     out.weight = (float*)take(4);
@@ -94,7 +95,8 @@ int main(int argc, char** argv) {
       out.flags |= DESPOT_X_TIMING;
       OK(call());
     }
-    const char* name[] = {"host", "device", "device-two-phase", "host-prepared-graph", "device-prepared-graph"};
+    const char* name[] = {"host", "device", "device-two-phase", "host-prepared-graph", "device-prepared-graph",
+                          "device-resident-graph"};
     printf("{\"outputs\": \"%s\", \"us_per_call\": %.2f, \"launches\": %u, \"scenario_steps\": %llu, \"phases_ms\": [%.4f, %.4f, %.4f, %.4f]}\n",
            name[mode], us, out.launches, (unsigned long long)out.scenario_steps, out.phase_ms[0], out.phase_ms[1],
            out.phase_ms[2], out.phase_ms[3]);

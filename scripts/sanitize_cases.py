@@ -18,7 +18,7 @@ shows as a nonzero word).  Cases:
             k1_update_sparse on the merged children
   exchange  the library-owned exchange at world 1 (DESPOT_MF_EXCHANGE): k4_* packing, its
             capacity retry, the sparse record round
-  graph     a prepared batch (CUDA graph) run three times
+  graph     a prepared batch (CUDA graph) and a resident one (DESPOT_X_RESIDENT), each run three times
 
 Usage: python scripts/sanitize_cases.py [--stress N] [CASE ...]   (no case: all)
 """
@@ -143,15 +143,17 @@ def graph():
     r = g.belief_load(st, w, seed)
     R = g.expand([(r, -1, 0, 0)])
     lv = [(r, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], g.A, L)]
-    P = g.prepare(lv)
     outs = []
-    for _ in range(3):
-        g.run_prepared(P)
-        o = {k: np.array(v, copy=True) for k, v in P["o"].items() if not k.startswith("_")}
-        o.update({"_full_" + k: o[k] for k in ("child_count", "child_first", "child_weight", "child_upper",
-                                               "child_lower")})
-        o["num_children"] = int(P["E"].num_children)
-        outs.append(o)
+    # a prepared batch of depth-1 leaves, and a resident one (self leaves: the
+    # graph is K2 alone, its last CTA restores the scratch)
+    for P in (g.prepare(lv), g.prepare([(r, -1, 0, 0)], resident=True)):
+        for _ in range(3):
+            g.run_prepared(P)
+            o = {k: np.array(v, copy=True) for k, v in P["o"].items() if not k.startswith("_")}
+            o.update({"_full_" + k: o[k] for k in ("child_count", "child_first", "child_weight", "child_upper",
+                                                   "child_lower")})
+            o["num_children"] = int(P["E"].num_children)
+            outs.append(o)
     return outs
 
 

@@ -904,8 +904,8 @@ def test_prepared_graph_runs_equal_plain_calls():
         lv = [(gr, a, c, 1) for a, c in inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)]
         for leaves in ([(gr, -1, 0, 0)], lv):
             ref = gm.expand(leaves)
-            for dev in (False, True):
-                P = gm.prepare(leaves, device_outputs=dev, pinned=not dev)
+            for dev, res in ((False, False), (True, False), (True, True), (False, True)):
+                P = gm.prepare(leaves, device_outputs=dev, pinned=not dev, resident=res)
                 assert P["graph"] is not None
                 seen = set()
                 for run in range(3):
@@ -949,6 +949,55 @@ def test_prepared_graph_runs_equal_plain_calls():
     with pytest.raises(DespotError):
         gm.run_prepared(P)
     gm.close()
+
+
+def test_resident_prepared_batches():
+    """DESPOT_X_RESIDENT (self leaves, fused finalize: the graph is K2 alone,
+    the scratch restored by K2's last CTA, the status in mapped host memory):
+    many runs equal the plain call and the oracle -- several roots of two
+    beliefs, Tiger with terminal scenarios, RockSample(7,8) -- and after a
+    failed run (child capacity too small) the next prepared run of the model
+    is still exact; a failed resident batch sets up again and fails the same
+    way (no state left over from the failed run)."""
+    import torch
+    keys = ("n_scen", "weight", "act_reward", "act_upper", "act_lower", "child_begin", "child_count",
+            "child_first", "child_weight", "child_upper", "child_lower", "child_obs")
+
+    def check(gm, om, leaves, oleaves, runs=6):
+        ref = gm.expand(leaves)
+        O = om.expand(oleaves, record=True)
+        compare_batch(ref, O, gm, om, [(i, i) for i in range(len(leaves))])
+        for dev in (True, False):
+            P = gm.prepare(leaves, device_outputs=dev, pinned=not dev, resident=True)
+            for run in range(runs):
+                steps, _, _ = gm.run_prepared(P)
+                torch.cuda.synchronize()
+                assert steps == ref["scenario_steps"], run
+                assert int(P["E"].num_children) == ref["num_children"]
+                for k in keys:
+                    r = np.asarray(ref[k]).reshape(-1)
+                    got = P["o"][k]
+                    got = (got.cpu().numpy() if dev else np.asarray(got)).reshape(-1)[: len(r)]
+                    assert np.array_equal(got.view(r.dtype) if got.dtype != r.dtype else got, r), (k, run, dev)
+
+    gm, om, st, w, seed, _ = setup(1, K=100)
+    roots = [(gm.belief_load(st, w, seed), -1, 0, 0), (gm.belief_load(st[:, :37], w[:37], seed + 5), -1, 0, 0)]
+    oroots = [(om.belief_load(st, w, seed), -1, 0, 0), (om.belief_load(st[:, :37], w[:37], seed + 5), -1, 0, 0)]
+    check(gm, om, roots[:1], oroots[:1])
+    check(gm, om, roots, oroots)
+    # a failing resident batch: too small a child capacity, twice (set up again), then a good one
+    bad = gm.prepare(roots[:1], device_outputs=True, resident=True, child_capacity=1)
+    for _ in range(2):
+        with pytest.raises(DespotError):
+            gm.run_prepared(bad)
+    check(gm, om, roots[:1], oroots[:1], runs=2)
+    gm.close()
+    tm = Model("tiger", inputs.tiger_params(D=12))
+    to = oracle.Model("tiger", inputs.tiger_params(D=12))
+    tst = np.array([[0, 1, 2, 3, 1, 0, 3, 2, 1]], np.uint32)  # 2, 3 = terminal
+    tw = inputs.weights(9, 5, uniform=False)
+    check(tm, to, [(tm.belief_load(tst, tw, 77), -1, 0, 0)], [(to.belief_load(tst, tw, 77), -1, 0, 0)])
+    tm.close()
 
 
 @pytest.mark.parametrize("peds,K,D", [(20, 48, 40), (6, 40, 30), (31, 20, 20), (12, 33, 30), (3, 37, 25)])
