@@ -312,6 +312,17 @@ __device__ __forceinline__ int64_t group_sum64(uint32_t mask, int64_t v) {
   return (int64_t)((uint64_t)s0 + ((uint64_t)s1 << 27) + ((uint64_t)(int64_t)s2 << 54));
 }
 __device__ __forceinline__ int64_t warp_sum64(int64_t v) { return group_sum64(0xffffffffu, v); }
+
+// Fire-and-forget reductions into the batch's global sums (relaxed, device
+// scope: what atomicAdd / atomicMin without a used result are).  Through the
+// global state space explicitly: on a generic pointer the compiler adds a
+// shared-window test and a fallback path around every atomic.
+__device__ __forceinline__ void red_add(int64_t* p, int64_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_min(int32_t* p, int32_t v) {
+  asm volatile("red.relaxed.gpu.global.min.s32 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t warp_sum32(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
 
 // exact fixed-point quantisation of a normalised weighted value

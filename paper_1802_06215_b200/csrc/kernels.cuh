@@ -239,9 +239,9 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     const uint64_t la = (uint64_t)leaf * b.A + a;
     const int64_t sR = warp_sum64(qR), sUq = warp_sum64(qUq), sLq = warp_sum64(qLq);
     if (lane == 0) {
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)sR);
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)sUq);
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)sLq);
+      red_add(&b.sums[lay.Q(la, 0)], sR);
+      red_add(&b.sums[lay.Q(la, 1)], sUq);
+      red_add(&b.sums[lay.Q(la, 2)], sLq);
     }
     // ---- grouping by observation (Eq. 10) ------------------------------
     uint32_t pending = __ballot_sync(0xffffffffu, valid);
@@ -256,17 +256,17 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
         if ((int)lane == leader) {
           const uint64_t slot = la * b.S + zk;
           HD_CHECK(b.err, zk < b.S && la < (uint64_t)b.L * b.A);
-          atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)gW);
-          atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)gU);
-          atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)gL);
-          atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], (unsigned long long)__popc(gmask));
-          atomicMin(&b.mins[slot], (int32_t)id);  // leader = lowest position = smallest id
+          red_add(&b.sums[lay.W(slot)], gW);
+          red_add(&b.sums[lay.U(slot)], gU);
+          red_add(&b.sums[lay.Lm(slot)], gL);
+          red_add(&b.sums[lay.N(slot)], (int64_t)__popc(gmask));
+          red_min(&b.mins[slot], (int32_t)id);  // leader = lowest position = smallest id
         }
       }
     }
   }
   const uint32_t ws = warp_sum32(steps_acc);
-  if (lane == 0 && ws) atomicAdd((unsigned long long*)&b.sums[lay.steps()], (unsigned long long)ws);
+  if (lane == 0 && ws) red_add(&b.sums[lay.steps()], (int64_t)ws);
   if (b.fused_k3) {
     // small batch: the last CTA to finish ranks, scans and writes the
     // children (K3) -- one launch per expansion instead of two

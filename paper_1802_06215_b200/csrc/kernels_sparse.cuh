@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(128, HD_CART_MINB) k2_car_thread(BatchDev b, S
     io.q3[3 * t + 1] = fxq(wn * u, fx);
     io.q3[3 * t + 2] = fxq(wn * lam, fx);
     const uint64_t la = (uint64_t)leaf * b.A + a;
-    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r, fx));
-    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r + gamma * u), fx));
-    atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r + gamma * lam), fx));
+    red_add(&b.sums[lay.Q(la, 0)], fxq(wn * (double)r, fx));
+    red_add(&b.sums[lay.Q(la, 1)], fxq(wn * ((double)r + gamma * u), fx));
+    red_add(&b.sums[lay.Q(la, 2)], fxq(wn * ((double)r + gamma * lam), fx));
     if (RECORD) {
       b.scen_reward[t] = r;
       b.scen_upper[t] = (float)u;
@@ -343,9 +343,9 @@ __global__ void __launch_bounds__(128) k2_car_warp(BatchDev b, SparseItemOut io)
       io.q3[3 * t + 1] = fxq(wn * u, fx);
       io.q3[3 * t + 2] = fxq(wn * lam, fx);
       const uint64_t la = (uint64_t)leaf * b.A + a0;
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r0, fx));
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r0 + gamma * u), fx));
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r0 + gamma * lam), fx));
+      red_add(&b.sums[lay.Q(la, 0)], fxq(wn * (double)r0, fx));
+      red_add(&b.sums[lay.Q(la, 1)], fxq(wn * ((double)r0 + gamma * u), fx));
+      red_add(&b.sums[lay.Q(la, 2)], fxq(wn * ((double)r0 + gamma * lam), fx));
       if (RECORD) {
         b.scen_reward[t] = r0;
         b.scen_upper[t] = (float)u;
@@ -576,9 +576,9 @@ __global__ void __launch_bounds__(128, B == 1 ? HD_CARG_MINB : 4) k2_car_group(B
       io.q3[3 * t + 1] = fxq(wn * u, fx);
       io.q3[3 * t + 2] = fxq(wn * lam, fx);
       const uint64_t la = (uint64_t)leaf * b.A + a0;
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 0)], (unsigned long long)fxq(wn * (double)r0, fx));
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 1)], (unsigned long long)fxq(wn * ((double)r0 + gamma * u), fx));
-      atomicAdd((unsigned long long*)&b.sums[lay.Q(la, 2)], (unsigned long long)fxq(wn * ((double)r0 + gamma * lam), fx));
+      red_add(&b.sums[lay.Q(la, 0)], fxq(wn * (double)r0, fx));
+      red_add(&b.sums[lay.Q(la, 1)], fxq(wn * ((double)r0 + gamma * u), fx));
+      red_add(&b.sums[lay.Q(la, 2)], fxq(wn * ((double)r0 + gamma * lam), fx));
       if (RECORD) {
         b.scen_reward[t] = r0;
         b.scen_upper[t] = (float)u;

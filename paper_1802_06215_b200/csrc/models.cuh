@@ -139,6 +139,8 @@ struct RockSample {
   struct Sm {
     int32_t n, m, mm, base, ncell, exitc;  // exitc = EXIT pseudo-cell = n*n; mm = max(m, 1)
     uint32_t D;
+    uint32_t md;          // the dist table's row stride: mm rounded up to 4 (word loads of 4 rocks)
+    uint32_t base_magic;  // ceil(2^32 / base): a / base = umulhi(a, magic) for a < 2^16
     double tail;
     // Default-policy columns: robot r walks its handled rocks in order (x, y, j)
     // through the columns q = qstart[r] .. qstart[r] + k_r - 1, then stays on
@@ -161,8 +163,10 @@ struct RockSample {
     uint32_t off_pol;   // u8  [cell][m+2]: policy move toward the rock of column q (4 = on it); sentinels
                         // E; row n*n+1 (the SENSE row) holds senseb: the sub-action of a robot whose
                         // target is not known GOOD
-    uint32_t off_dist;  // u8  [cell][mm]: |x - x_j| + |y - y_j| (255 from EXIT)
-    uint32_t off_gp;    // f64 [G]: gamma^k;  off_gp10: f64 [G]: 10 gamma^k (G = max(D, 2n) + 1)
+    uint32_t off_dist;  // u8  [cell][md]: |x - x_j| + |y - y_j| (255 from EXIT and past m)
+    uint32_t off_gp;    // f64 [G]: gamma^k;  off_gp10: f64 [G + 1]: 10 gamma^k (k < G = max(D, 2n) + 1),
+                        // then 0.0 (index G: a bad rock's term in upper())
+    uint32_t gzero4;    // G in every byte (the index of gp10's 0.0)
     uint32_t off_gp10;
   };
   static __host__ __device__ int gpow_len(int n, uint32_t D) { return (int)(D > (uint32_t)(2 * n) ? D : 2 * n) + 1; }
@@ -171,8 +175,9 @@ struct RockSample {
   // EXIT row (and pol's SENSE row)
   static __host__ __device__ size_t table_bytes(int n, int m, uint32_t D) {
     const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
+    const size_t md = (mm + 3) & ~size_t(3);
     return align16((c + 1) * (m + 2)) + align16(2 * c * (5 + m)) + align16(4 * c) + align16(c) +
-           align16(4 * c * mm) + align16(c * mm) + align16(8 * G) + align16(8 * G);
+           align16(4 * c * mm) + align16(c * md) + align16(8 * G) + align16(8 * (G + 1));
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
@@ -192,8 +197,8 @@ struct RockSample {
   static __device__ __forceinline__ uint32_t pol(const Sm& sm, int c, int q) {
     return hd_dyn_smem[kOffPol + c * sm.polw + q];
   }
-  static __device__ __forceinline__ const uint8_t* dist_row(const Sm& sm, int c) {
-    return hd_dyn_smem + sm.off_dist + c * sm.mm;
+  static __device__ __forceinline__ const uint32_t* dist_row(const Sm& sm, int c) {
+    return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_dist + c * sm.md);
   }
   static __device__ __forceinline__ double gp(const Sm& sm, int k) {
     return reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp)[k];
@@ -203,13 +208,14 @@ struct RockSample {
   }
   static __device__ void load_sm(Sm& sm, const DevModel& dm, int tid, int nt) {
     const int n = dm.n, mm = dm.m > 0 ? dm.m : 1, nc = n * n, exitc = nc, G = gpow_len(n, dm.D);
+    const int md = (mm + 3) & ~3;
     const uint32_t polw = (uint32_t)dm.m + 2;
     const uint32_t off_pol = kOffPol, off_act = off_pol + (uint32_t)align16((size_t)(nc + 2) * polw),
                    off_info = off_act + (uint32_t)align16(2 * (size_t)(nc + 1) * dm.base),
                    off_rock = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
                    off_thr = off_rock + (uint32_t)align16((size_t)(nc + 1)),
                    off_dist = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
-                   off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * mm),
+                   off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * md),
                    off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
     uint16_t* t_act = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_act);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
@@ -234,6 +240,9 @@ struct RockSample {
       sm.m = dm.m;
       sm.mm = mm;
       sm.base = dm.base;
+      sm.md = (uint32_t)md;
+      sm.gzero4 = (uint32_t)G * 0x01010101u;  // G <= 251
+      sm.base_magic = (uint32_t)((0x100000000ull + (uint64_t)dm.base - 1) / (uint64_t)dm.base);
       sm.ncell = nc;
       sm.exitc = exitc;
       sm.D = dm.D;
@@ -254,12 +263,11 @@ struct RockSample {
       const int p = q < (int)polw ? col_pos(q) : -1;
       sm.senseb[q] = p >= 0 ? (uint8_t)(5 + dm.pos_rock[p]) : (uint8_t)2;
     }
-    for (int k = tid; k < G; k += nt) {
-      t_gp[k] = dm.gpow[k];
-      t_gp10[k] = 10.0 * dm.gpow[k];  // the product upper() used to form per rock
-    }
-    for (int e = tid; e < (nc + 1) * mm; e += nt) {
-      const int c = e / mm, j = e - c * mm;
+    for (int k = tid; k < G; k += nt) t_gp[k] = dm.gpow[k];
+    for (int k = tid; k <= G; k += nt)
+      t_gp10[k] = k < G ? 10.0 * dm.gpow[k] : 0.0;  // the product upper() used to form per rock
+    for (int e = tid; e < (nc + 1) * md; e += nt) {
+      const int c = e / md, j = e - c * md;
       t_dist[e] = (c < nc && j < dm.m) ? (uint8_t)(abs(c % n - dm.rx[j]) + abs(c / n - dm.ry[j])) : (uint8_t)255;
     }
     for (int c = tid; c <= nc; c += nt) {
@@ -384,9 +392,10 @@ struct RockSample {
     int b[R];
     int rest = a;
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      b[q] = rest % sm.base;
-      rest /= sm.base;
+    for (int q = 0; q < R; ++q) {  // a < 2^16 (checked at load): exact with the magic
+      const int qt = (int)__umulhi((uint32_t)rest, sm.base_magic);
+      b[q] = rest - qt * sm.base;
+      rest = qt;
     }
     const uint4 w = philox(id, t, 0u, 0u, key);
     const uint32_t u[2] = {w.x, w.y};
@@ -397,17 +406,26 @@ struct RockSample {
   // the premultiplied table; an exited robot's row is 255, never the min
   // while some robot is active -- upper() is only asked of non-terminal states)
   static __device__ __forceinline__ double upper(const Sm& sm, const St& s) {
-    const uint8_t* dr[R];
+    // four rocks per word: the robots' byte distances, their byte-wise
+    // minimum, a bad rock's byte replaced by G (the table's 0.0 after
+    // 10 gamma^(G-1), so it adds +0.0 exactly as a skipped term would); the
+    // terms are added in rock order j = 0, 1, ... (padding rocks past m have
+    // no good bit: +0.0 too)
+    const uint32_t* dr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) dr[r] = dist_row(sm, s.cell[r]);
     const double* g10 = reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10);
     double u = 0.0;
-    for (int j = 0; j < sm.m; ++j) {  // uniform trip count, branch-free; bad rocks add +0.0
-      uint32_t dmin = dr[0][j];
+    const int nw = (sm.m + 3) >> 2;
+    for (int k = 0; k < nw; ++k) {  // uniform trip count, branch-free
+      uint32_t mn = dr[0][k];
 #pragma unroll
-      for (int r = 1; r < R; ++r) dmin = min(dmin, (uint32_t)dr[r][j]);
-      const double v = g10[dmin];
-      u += ((s.good >> j) & 1u) ? v : 0.0;
+      for (int r = 1; r < R; ++r) mn = __vminu4(mn, dr[r][k]);
+      const uint32_t g4 = (s.good >> (4 * k)) & 0xFu;
+      const uint32_t gm = ((g4 * 0x00204081u) & 0x01010101u) * 0xFFu;  // 0xFF in the byte of each GOOD rock
+      const uint32_t idx = (mn & gm) | (sm.gzero4 & ~gm);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u += g10[__byte_perm(idx, 0u, 0x4440u + (uint32_t)q)];
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
