@@ -1397,7 +1397,10 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       if (!all_self) {
         const size_t smem1 = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
         kernel_occupancy((const void*)k1_update<M>, smem1, M::kK1Threads);  // sets the smem attribute if > 48 KB
-        k1_update<M><<<L, M::kK1Threads, smem1, st>>>(bd);  // + prefix in its last CTA
+        // the tile prefix: K2 forms it (no per-scenario records: nothing else
+        // reads the prefixes), else K1's last CTA
+        bd.k2_prefix = (flags & DESPOT_X_RECORD_SCENARIO) ? 0u : 1u;
+        k1_update<M><<<L, M::kK1Threads, smem1, st>>>(bd);  // + prefix in its last CTA unless k2_prefix
         ++b->launches;
       }
       b->mark(2);

@@ -109,7 +109,9 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
                 (unsigned long long)ws);
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = s_base;  // may be 0 on a shard
   }
-  last_cta_prefix(b);  // K2pre folded in: the last CTA scans the leaf sizes
+  // K2pre folded in: the last CTA scans the leaf sizes -- unless K2 forms the
+  // tile prefix itself (no serial tail on K1)
+  if (!b.k2_prefix) last_cta_prefix(b);
 }
 
 // ---------------------------------------------------------------------------
@@ -136,7 +138,25 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
   pdl_wait();  // K1 complete: tile_off, the leaf arenas
   pdl_trigger();
-  for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
+  if (b.k2_prefix) {  // tile_off[l] = sum_{l' < l} A ceil(n_l' / 32), every CTA for itself
+    __shared__ uint64_t wsum[32];
+    const uint32_t per = (b.L + blockDim.x - 1) / blockDim.x, l0 = threadIdx.x * per;
+    auto tiles_of = [&](uint32_t l) { return (uint64_t)b.A * ((__ldcg(&b.n_leaf[l]) + 31u) >> 5); };
+    uint64_t tiles = 0;
+    for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) tiles += tiles_of(l);
+    uint64_t ttot;
+    uint64_t tb = block_excl_scan(tiles, wsum, ttot);
+    for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
+      tile_off[l] = (uint32_t)tb;
+      tb += tiles_of(l);
+    }
+    if (threadIdx.x == 0) {
+      tile_off[b.L] = (uint32_t)ttot;
+      if (ttot >= 0xFFFFFFFFull && blockIdx.x == 0) atomicOr(b.err, kErrChildCap);
+    }
+  } else {
+    for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
+  }
   __syncthreads();
   const uint32_t total = tile_off[b.L];
   const uint32_t lane = threadIdx.x & 31;
