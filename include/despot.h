@@ -170,16 +170,21 @@ typedef struct {
 #define DESPOT_X_TIMING_K2 8u       /* only phase_ms[1] (K2), two events: the cheap
                                        form for timing loops (8 events cost ~30 us
                                        of host time per call)                     */
-#define DESPOT_X_RESIDENT 32u       /* despot_batch_prepare only, leaves that are all
-                                       nodes themselves (action == -1, e.g. roots)
-                                       and a batch small enough to finalize in K2:
-                                       the leaf table and the scratch's zero state
-                                       are set up once at prepare, K2's last CTA
-                                       restores that state and publishes the status
-                                       to mapped host memory, so the graph is K2
-                                       alone (no memset, H2D or status D2H per run;
-                                       a run after an error sets up again).  Ignored
-                                       when the batch does not qualify.            */
+#define DESPOT_X_RESIDENT 32u       /* despot_batch_prepare only (single GPU, no
+                                       RECORD), for a batch that finalizes in K2 (few
+                                       slots, small L*A) or in the one-kernel wide
+                                       finalize (> 32 slots): the scratch's zero
+                                       state is set up once at prepare and restored
+                                       by the kernels at the end of every run (K2's
+                                       last CTA, or each wide-finalize CTA for its
+                                       (leaf, action) and the last one for the
+                                       counters), which also publishes the status to
+                                       mapped host memory: no memset or status D2H
+                                       per run.  When every leaf is a node itself
+                                       (roots) the leaf table is uploaded once too
+                                       and the graph is K2 alone.  A run after an
+                                       error sets up again.  Ignored when the batch
+                                       does not qualify.                           */
 #define DESPOT_X_INDEX_LISTS 16u    /* the paper's update form ("the leaf ...
                                        only contains a set of indexes"): leaf l with
                                        action >= 0 takes the parent positions

@@ -242,7 +242,8 @@ enum : uint32_t {
 enum : uint32_t {
   kStatErr = 0, kStatChildren = 1, kStatSteps = 2 /* u64: 2-3 */, kStatK1Ticket = 4, kStatK2Ticket = 5,
   kStatK2Tile = 6 /* K2's dynamic tile counter */, kStatXTotal = 7 /* slots in the exchange's union (K4) */,
-  kStatWords = 8 /* then n_leaf[L] */
+  kStatK3Done = 8 /* resident batches: K3 CTAs finished (the last one publishes and restores) */,
+  kStatWords = 9 /* then n_leaf[L] */
 };
 
 struct BatchDev {

@@ -276,7 +276,7 @@ struct despot_batch {
   // set up once (resident_init) and restored by K2's last CTA, the status
   // arrives in mapped host memory (hmapped); dirty: re-initialise before the
   // next run (after an error)
-  bool resident = false, dirty = false;
+  bool resident = false, resident_table = false, dirty = false;
   uint32_t* hmapped = nullptr;
   size_t r_stat = 0, r_zero = 0, r_h2d = 0;  // status offset, bytes zeroed from it, leaf-table bytes
   size_t o_ns = 0, o_w = 0, o_ar = 0, o_au = 0, o_al = 0, o_cb = 0, o_cc = 0, o_cf = 0, o_cw = 0, o_cu = 0,
@@ -1302,9 +1302,14 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   // (the same rule as k3_fused below, with the outputs bound)
   {
     const uint64_t G = 32 / small_group_width(b->S);
-    b->resident = g_capture && all_self && bind && !ilist && !b->sparse && !xdense && m->world == 1 &&
-                  !(flags & DESPOT_X_RECORD_SCENARIO) && b->S <= 32 &&
-                  (uint64_t)L * dm.A <= 4 * G * kSmallUnroll * 2 && (bind->flags & DESPOT_X_RESIDENT);
+    // the zero state is restored by K2's last CTA (finalize fused into K2) or
+    // by the wide finalize's CTAs (many slots); the leaf table is uploaded
+    // once only when every leaf is a node itself (no new arenas per run)
+    const bool fusable = b->S <= 32 && (uint64_t)L * dm.A <= 4 * G * kSmallUnroll * 2;
+    b->resident = g_capture && bind && !ilist && !b->sparse && !xdense && m->world == 1 &&
+                  !(flags & DESPOT_X_RECORD_SCENARIO) && (fusable || wide_fused(b->S, false)) &&
+                  (bind->flags & DESPOT_X_RESIDENT);
+    b->resident_table = b->resident && all_self;
   }
   void* hp = pinned_pool().acquire(std::max<size_t>(h2d_bytes, ilist ? o_idx + 4 * idx_total : 0));
   b->pinned = hp;
@@ -1348,13 +1353,16 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       if (!rc && cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), b->hmapped, 0) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "mapped status block: device pointer");
       bd.hstat = dptr;
+      if (!rc && !b->resident_table &&
+          cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
     } else if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
         cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
         (xdense && (size_t)x.nblk * kXBlk > LAS &&
          cudaMemsetAsync(x.flags + LAS, 0, (size_t)x.nblk * kXBlk - LAS, st) != cudaSuccess) ||
         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
-    if (!b->resident) b->h2d += h2d_bytes - o_leaves;
+    if (!b->resident_table) b->h2d += h2d_bytes - o_leaves;
     if (!rc && ilist && idx_total) {
       memcpy(h + o_idx, bind->index, 4 * idx_total);
       if (cudaMemcpyAsync(s + o_idx, h + o_idx, 4 * idx_total, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -1938,7 +1946,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
   };
   if (!rc) rc = copy_and_sync(mode != kFinishComplete, mode != kFinishEnqueue);
   if (mode == kFinishEnqueue) return rc;  // a prepared batch's capture ends here
-  if (b->resident) hs = reinterpret_cast<char*>(b->hmapped);  // published by K2's last CTA
+  if (b->resident) hs = reinterpret_cast<char*>(b->hmapped);  // published by K2's / K3's last CTA
   if (!rc && b->xlib && !b->sparse) {
     // the packed exchange's capacity hint follows the largest union seen (+ 1/4)
     uint32_t T = 0, e0 = 0;
@@ -2109,7 +2117,8 @@ static int resident_init(despot_batch* b, cudaStream_t st) {
   const char* h = static_cast<const char*>(b->pinned);
   if (cudaMemsetAsync(s + b->r_stat, 0, b->r_zero, st) != cudaSuccess ||
       cudaMemsetAsync(b->bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
-      cudaMemcpyAsync(s + b->o_leaves, h + b->o_leaves, b->r_h2d, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      (b->resident_table &&
+       cudaMemcpyAsync(s + b->o_leaves, h + b->o_leaves, b->r_h2d, cudaMemcpyHostToDevice, st) != cudaSuccess))
     return set_err(DESPOT_ECUDA, "resident batch set-up failed");
   b->dirty = false;
   return DESPOT_OK;
@@ -2251,7 +2260,7 @@ extern "C" int despot_batch_run(despot_prepared* p, despot_expansion* out, void*
   b->d2h = p->d2h;
   if (b->resident && b->dirty) {
     if (int rc = resident_init(b, st)) return rc;
-    b->h2d += b->r_h2d;
+    if (b->resident_table) b->h2d += b->r_h2d;
   }
   g_ht.mark("patched");
   const bool launched = cudaGraphLaunch(p->exec, st) == cudaSuccess;

@@ -526,6 +526,34 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
       b.status[3] = (uint32_t)(steps >> 32);
     }
   }
+  if (b.hstat) {  // resident prepared batch: restore the zero state for the next run
+    __syncthreads();  // this pair's sums are read
+    for (uint32_t s = threadIdx.x; s < S; s += kWideFusedThreads) {
+      b.sums[lay.W(base + s)] = 0;
+      b.sums[lay.U(base + s)] = 0;
+      b.sums[lay.Lm(base + s)] = 0;
+      b.sums[lay.N(base + s)] = 0;
+      b.mins[base + s] = 0x7F7F7F7F;
+    }
+    if (threadIdx.x < 3) b.sums[lay.Q(la, threadIdx.x)] = 0;
+    __shared__ bool s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&b.status[kStatK3Done], 1u) == LA - 1;
+    }
+    __syncthreads();
+    if (s_last) {  // every pair is done: publish the status, reset the counters
+      __threadfence();
+      const uint32_t nst = kStatWords + b.L;
+      for (uint32_t i = threadIdx.x; i < nst; i += kWideFusedThreads) b.hstat[i] = __ldcg(&b.status[i]);
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x < kStatWords) b.status[threadIdx.x] = 0u;
+      if (threadIdx.x == 0) b.sums[lay.steps()] = 0;
+      for (uint64_t i = threadIdx.x; i < LA + 2; i += kWideFusedThreads) b.scan_flags[i] = 0ull;
+    }
+  }
 }
 __host__ __device__ inline size_t wide_fused_smem(uint32_t S) { return 12 * (size_t)S; }
 constexpr size_t kWideFusedMaxSmem = 96 << 10;

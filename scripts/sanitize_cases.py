@@ -18,7 +18,8 @@ shows as a nonzero word).  Cases:
             k1_update_sparse on the merged children
   exchange  the library-owned exchange at world 1 (DESPOT_MF_EXCHANGE): k4_* packing, its
             capacity retry, the sparse record round
-  graph     a prepared batch (CUDA graph) and a resident one (DESPOT_X_RESIDENT), each run three times
+  graph     a prepared batch (CUDA graph) and resident ones (DESPOT_X_RESIDENT: a root, and
+            navigation's depth-1 leaves with the wide finalize restoring the scratch), three runs each
 
 Usage: python scripts/sanitize_cases.py [--stress N] [CASE ...]   (no case: all)
 """
@@ -146,9 +147,15 @@ def graph():
     outs = []
     # a prepared batch of depth-1 leaves, and a resident one (self leaves: the
     # graph is K2 alone, its last CTA restores the scratch)
-    for P in (g.prepare(lv), g.prepare([(r, -1, 0, 0)], resident=True)):
+    kn, pn, stn, wn, sdn, Ln = inputs.config_inputs(3, K=150, L=8)
+    gn = Model(kn, pn)
+    rn = gn.belief_load(stn, wn, sdn)
+    Rn = gn.expand([(rn, -1, 0, 0)])
+    lvn = [(rn, a, c, 1) for a, c in inputs.select_leaves(Rn["child_count"], Rn["child_begin"], gn.A, Ln)]
+    for g_, P in ((g, g.prepare(lv)), (g, g.prepare([(r, -1, 0, 0)], resident=True)),
+                  (gn, gn.prepare(lvn, resident=True))):
         for _ in range(3):
-            g.run_prepared(P)
+            g_.run_prepared(P)
             o = {k: np.array(v, copy=True) for k, v in P["o"].items() if not k.startswith("_")}
             o.update({"_full_" + k: o[k] for k in ("child_count", "child_first", "child_weight", "child_upper",
                                                    "child_lower")})

@@ -952,10 +952,12 @@ def test_prepared_graph_runs_equal_plain_calls():
 
 
 def test_resident_prepared_batches():
-    """DESPOT_X_RESIDENT (self leaves, fused finalize: the graph is K2 alone,
-    the scratch restored by K2's last CTA, the status in mapped host memory):
-    many runs equal the plain call and the oracle -- several roots of two
-    beliefs, Tiger with terminal scenarios, RockSample(7,8) -- and after a
+    """DESPOT_X_RESIDENT (the scratch restored by K2's last CTA -- fused
+    finalize -- or by the wide finalize's CTAs, the status in mapped host
+    memory; self leaves: the graph is K2 alone): many runs equal the plain
+    call and the oracle -- several roots of two beliefs, Tiger with terminal
+    scenarios, RockSample(7,8), depth-1 leaves of RockSample and navigation --
+    and after a
     failed run (child capacity too small) the next prepared run of the model
     is still exact; a failed resident batch sets up again and fails the same
     way (no state left over from the failed run)."""
@@ -992,6 +994,17 @@ def test_resident_prepared_batches():
             gm.run_prepared(bad)
     check(gm, om, roots[:1], oroots[:1], runs=2)
     gm.close()
+    # depth-1 leaves (new arenas every run): the fused finalize (RockSample,
+    # a few leaves) and navigation's wide finalize, whose CTAs restore their
+    # own slots and whose last CTA publishes the status
+    for cfg, K, L in ((1, 100, 5), (3, 120, 6), (3, 300, 24)):
+        gm, om, st, w, seed, _ = setup(cfg, K=K, L=L)
+        gr, orr = gm.belief_load(st, w, seed), om.belief_load(st, w, seed)
+        R = gm.expand([(gr, -1, 0, 0)])
+        om.expand([(orr, -1, 0, 0)])
+        lv = inputs.select_leaves(R["child_count"], R["child_begin"], gm.A, L)
+        check(gm, om, [(gr, a, c, 1) for a, c in lv], [(orr, a, c, 1) for a, c in lv], runs=4)
+        gm.close()
     tm = Model("tiger", inputs.tiger_params(D=12))
     to = oracle.Model("tiger", inputs.tiger_params(D=12))
     tst = np.array([[0, 1, 2, 3, 1, 0, 3, 2, 1]], np.uint32)  # 2, 3 = terminal
