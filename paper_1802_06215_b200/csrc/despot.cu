@@ -1403,7 +1403,8 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       using M = decltype(mdl);
       b->mark(1);
       if (!all_self) {
-        const size_t smem1 = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
+        const size_t smem1 = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
+                             (size_t)M::kScratchPerThread * M::kK1Threads;
         kernel_occupancy((const void*)k1_update<M>, smem1, M::kK1Threads);  // sets the smem attribute if > 48 KB
         // the tile prefix: K2 forms it (no per-scenario records: nothing else
         // reads the prefixes), else K1's last CTA
@@ -1435,9 +1436,11 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     // K2 now (the exchange block is complete after it)
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
+      // Sm | tables | tile_off | max(the fused finalize's region, the per-thread scratch)
       const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
                           align16(4 * ((size_t)L + 1)) +
-                          (b->k3_fused ? small_finalize_smem((uint64_t)L * dm.A) : 0);
+                          std::max<size_t>(b->k3_fused ? small_finalize_smem((uint64_t)L * dm.A) : 0,
+                                           (size_t)M::kScratchPerThread * 128);
       bool uni = true;
       for (uint32_t l = 1; l < L; ++l) uni = uni && ld[l].seed_lo == ld[0].seed_lo && ld[l].seed_hi == ld[0].seed_hi;
       auto kern = uni ? k2_expand_dense<M, false, true> : k2_expand_dense<M, false, false>;
@@ -1784,7 +1787,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
   } else if (record) {
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) + 4 * ((size_t)L + 1);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
+                          align16(4 * ((size_t)L + 1)) + (size_t)M::kScratchPerThread * 128;
       auto kern = k2_expand_dense<M, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       b->mark(3);
@@ -2321,7 +2325,8 @@ extern "C" int despot_rollout_bounds(despot_model* m, despot_node h, float* uppe
   if (!rc) {
     auto launch = [&](auto mdl) -> int {
       using M = decltype(mdl);
-      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes);
+      const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
+                          (size_t)M::kScratchPerThread * 128;
       auto kern = k_rollout_bounds<M>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>((n + 127) / 128, m->num_sms * 8));

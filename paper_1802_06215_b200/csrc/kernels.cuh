@@ -50,6 +50,8 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
   } else {
     load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0)  // the per-thread scratch after the model's tables (synced below)
+      M::bind_scratch((uint32_t)(align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes)));
     const uint32_t nchild = lf.p_nchild[lf.action];
     const bool valid_child = lf.child < nchild;
     const uint32_t key = valid_child ? lf.p_keys[(uint64_t)lf.action * lf.p_kcap + lf.child] : 0xFFFFFFFFu;
@@ -136,6 +138,9 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
   uint32_t* tile_off =
       reinterpret_cast<uint32_t*>(hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes));
   load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
+  // the per-thread scratch shares the fused finalize's region (used after the tiles)
+  if (threadIdx.x == 0) M::bind_scratch((uint32_t)(reinterpret_cast<unsigned char*>(tile_off) - hd_dyn_smem) +
+                                        (uint32_t)align16(4 * ((size_t)b.L + 1)));
   pdl_wait();  // K1 complete: tile_off, the leaf arenas
   pdl_trigger();
   if (b.k2_prefix) {  // tile_off[l] = sum_{l' < l} A ceil(n_l' / 32), every CTA for itself
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(128) k_rollout_bounds(const DevModel* dmp, con
                                                         float* per_u, float* per_l, int64_t* acc3) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   load_sm_image<M>(sm, *dmp, threadIdx.x, blockDim.x);
+  if (threadIdx.x == 0) M::bind_scratch((uint32_t)(align16(sizeof(typename M::Sm)) + align16(dmp->sm_table_bytes)));
   __syncthreads();
   const double fx = dmp->fx;
   int64_t qW = 0, qU = 0, qL = 0;

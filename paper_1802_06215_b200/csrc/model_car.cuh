@@ -53,6 +53,8 @@ __device__ __forceinline__ int car_policy_from_gap(int gap) { return gap <= 8 ? 
 template <int MAXP, bool EXACT = false>
 struct CarThreadT {
   static constexpr int kMaxP = MAXP;
+  static constexpr uint32_t kScratchPerThread = 0;  // no per-thread shared scratch
+  static __device__ __forceinline__ void bind_scratch(uint32_t) {}
   struct Sm {
     int32_t peds;
     uint64_t t_fail;

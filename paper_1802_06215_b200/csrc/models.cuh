@@ -26,6 +26,8 @@ __device__ __forceinline__ void copy_words(void* dst, const void* src, int bytes
 // Tiger: state bit0 side, bit1 terminal; 0 LISTEN, 1 OPEN-LEFT, 2 OPEN-RIGHT
 // ===========================================================================
 struct Tiger {
+  static constexpr uint32_t kScratchPerThread = 0;  // no per-thread shared scratch
+  static __device__ __forceinline__ void bind_scratch(uint32_t) {}
   static constexpr int kK1Threads = 512;  // K1 block: one round over K = 500 scenarios
   static constexpr int kMinBlocks = 8;  // K2 occupancy target (CTAs of 128 per SM)
   struct Sm {
@@ -130,6 +132,8 @@ struct Tiger {
 #endif
 template <int R>
 struct RockSample {
+  static constexpr uint32_t kScratchPerThread = 0;  // no per-thread shared scratch
+  static __device__ __forceinline__ void bind_scratch(uint32_t) {}
 #ifndef HD_RS_MINB
 #define HD_RS_MINB 7
 #endif
@@ -700,9 +704,18 @@ struct Nav {
     copy_words(sm.known_rows, dm.nav_known_rows, sizeof(sm.known_rows), tid, nt);
     copy_words(sm.unk_pos, dm.nav_unk_pos, sizeof(sm.unk_pos), tid, nt);
   }
+  // Per-thread scratch in the kernel's dynamic shared memory (each kernel
+  // places it after its own data and binds the offset before first use): the
+  // scenario's padded occupancy rows, sized by the launching block, not by the
+  // largest block of any kernel.
+  static constexpr uint32_t kScratchPerThread = 4 * kNavRowStride;
+  static __device__ __forceinline__ uint32_t& rows_off() {
+    __shared__ uint32_t off;
+    return off;
+  }
+  static __device__ __forceinline__ void bind_scratch(uint32_t off) { rows_off() = off; }  // one thread; caller syncs
   static __device__ __forceinline__ uint32_t* grid() {
-    __shared__ uint32_t rows[kNavMaxThreads * kNavRowStride];
-    return rows + threadIdx.x * kNavRowStride;
+    return reinterpret_cast<uint32_t*>(hd_dyn_smem + rows_off()) + threadIdx.x * kNavRowStride;
   }
   struct St {
     int32_t x, y;
