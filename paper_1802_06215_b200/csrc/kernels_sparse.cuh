@@ -709,24 +709,38 @@ __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut
   const uint32_t cb = b.child_begin[la];
   const uint32_t nc = b.nc[la];
   int64_t wt = 0, nt = 0;
-  for (uint32_t c = threadIdx.x; c < nc; c += blockDim.x) {
-    const int64_t N = b.sums[lay.N(base + c)];
-    const int64_t W = b.sums[lay.W(base + c)];
-    wt += W;
-    nt += N;
-    const uint32_t oc = cb + c;
-    const uint32_t* key = io.keys + (uint64_t)b.sp_item[base + c] * io.kstride;
-    if (oc < b.child_capacity) {
-      const double Wd = (double)W;
-      b.child_count[oc] = (uint32_t)N;
-      b.child_first[oc] = (uint32_t)b.mins[base + c];
-      b.child_weight[oc] = (float)(Wd * dm.inv_fx * lf.wroot);
-      b.child_upper[oc] = (float)((double)b.sums[lay.U(base + c)] / Wd);
-      b.child_lower[oc] = (float)((double)b.sums[lay.Lm(base + c)] / Wd);
-      for (uint32_t k = 0; k < OW; ++k) b.child_obs[(uint64_t)oc * OW + k] = key[k];
+  const uint32_t lane = threadIdx.x & 31, nwc = blockDim.x >> 5;
+  // a warp per 32 children: the scalar outputs a lane per child, then the
+  // children's keys (OW <= 32 words each) copied a child at a time, a lane
+  // per word, so that the key reads and both key writes are contiguous
+  for (uint32_t c0 = (threadIdx.x >> 5) * 32; c0 < nc; c0 += nwc * 32) {
+    const uint32_t c = c0 + lane;
+    uint32_t item = 0;
+    if (c < nc) {
+      const int64_t N = b.sums[lay.N(base + c)];
+      const int64_t W = b.sums[lay.W(base + c)];
+      wt += W;
+      nt += N;
+      item = b.sp_item[base + c];
+      const uint32_t oc = cb + c;
+      if (oc < b.child_capacity) {
+        const double Wd = (double)W;
+        b.child_count[oc] = (uint32_t)N;
+        b.child_first[oc] = (uint32_t)b.mins[base + c];
+        b.child_weight[oc] = (float)(Wd * dm.inv_fx * lf.wroot);
+        b.child_upper[oc] = (float)((double)b.sums[lay.U(base + c)] / Wd);
+        b.child_lower[oc] = (float)((double)b.sums[lay.Lm(base + c)] / Wd);
+      }
     }
-    if (c < lf.kcap)
-      for (uint32_t k = 0; k < OW; ++k) lf.keys[((uint64_t)a * lf.kcap + c) * OW + k] = key[k];
+    const uint32_t cn = nc - c0 < 32 ? nc - c0 : 32;
+    for (uint32_t j = 0; j < cn; ++j) {
+      const uint32_t cj = c0 + j, it = __shfl_sync(0xffffffffu, item, j);
+      if (lane < OW) {
+        const uint32_t v = io.keys[(uint64_t)it * io.kstride + lane];
+        if (cb + cj < b.child_capacity) b.child_obs[(uint64_t)(cb + cj) * OW + lane] = v;
+        if (cj < lf.kcap) lf.keys[((uint64_t)a * lf.kcap + cj) * OW + lane] = v;
+      }
+    }
   }
   wt = warp_sum64(wt);
   nt = warp_sum64(nt);
