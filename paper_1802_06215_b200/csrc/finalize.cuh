@@ -568,8 +568,7 @@ constexpr size_t kWideFusedMaxSmem = 96 << 10;
 constexpr uint32_t kSmallLA = 4096;
 constexpr uint32_t kSmallUnroll = 4;
 __host__ __device__ inline size_t small_finalize_smem(uint64_t LA) { return align16(4 * (LA + 1)); }
-__device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char* smem) {
-  __shared__ uint64_t wsum[32];
+__device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char* smem, uint64_t* wsum) {
   const uint32_t wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const uint32_t S = b.S, A = b.A, LA = b.L * b.A;
   const uint32_t Sp = small_group_width(S), G = 32 / Sp;
@@ -689,7 +688,10 @@ __device__ __forceinline__ void small_finalize(const BatchDev& b, unsigned char*
   }
 }
 // out of line for K2's tail: its registers do not constrain K2's main loop
-__device__ __noinline__ void small_finalize_tail(const BatchDev& b, unsigned char* smem) { small_finalize(b, smem); }
+// (wsum: the caller's 32-word scan scratch, shared with its other scans)
+__device__ __noinline__ void small_finalize_tail(const BatchDev& b, unsigned char* smem, uint64_t* wsum) {
+  small_finalize(b, smem, wsum);
+}
 // A resident prepared batch (a graph of one kernel): after
 // the fused finalize the last CTA publishes the status block to mapped host
 // memory (the host reads it after the stream synchronises: no D2H copy) and
@@ -713,7 +715,8 @@ __global__ void __launch_bounds__(1024) k3_small_dense(BatchDev b) {
   pdl_wait();  // the predecessor complete
   pdl_trigger();
   extern __shared__ __align__(16) unsigned char k3s_smem[];
-  small_finalize(b, k3s_smem);
+  __shared__ uint64_t wsum[32];
+  small_finalize(b, k3s_smem, wsum);
 }
 
 __global__ void k_stream_words(uint32_t k0, uint32_t k1, const uint32_t* ids, uint32_t n, uint32_t t,

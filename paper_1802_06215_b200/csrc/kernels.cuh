@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
                                         (uint32_t)align16(4 * ((size_t)b.L + 1)));
   pdl_wait();  // K1 complete: tile_off, the leaf arenas
   pdl_trigger();
+  __shared__ uint64_t wsum[32];  // block scans: the tile prefix, the fused finalize
   if (b.k2_prefix) {  // tile_off[l] = sum_{l' < l} A ceil(n_l' / 32), every CTA for itself
-    __shared__ uint64_t wsum[32];
     const uint32_t per = (b.L + blockDim.x - 1) / blockDim.x, l0 = threadIdx.x * per;
     auto tiles_of = [&](uint32_t l) { return (uint64_t)b.A * ((__ldcg(&b.n_leaf[l]) + 31u) >> 5); };
     uint64_t tiles = 0;
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     __syncthreads();
     if (k2_last) {
       __threadfence();
-      small_finalize_tail(b, reinterpret_cast<unsigned char*>(tile_off) + align16(4 * ((size_t)b.L + 1)));
+      small_finalize_tail(b, reinterpret_cast<unsigned char*>(tile_off) + align16(4 * ((size_t)b.L + 1)), wsum);
       if (b.hstat) resident_epilogue(b);
     }
   }

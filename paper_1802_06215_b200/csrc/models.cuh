@@ -168,10 +168,10 @@ struct RockSample {
                         // E; row n*n+1 (the SENSE row) holds senseb: the sub-action of a robot whose
                         // target is not known GOOD
     uint32_t off_dist;  // u8  [cell][md]: |x - x_j| + |y - y_j| (255 from EXIT and past m)
-    uint32_t off_gp;    // f64 [G]: gamma^k;  off_gp10: f64 [G + 1]: 10 gamma^k (k < G = max(D, 2n) + 1),
-                        // then 0.0 (index G: a bad rock's term in upper())
+    const double* gpow_g;  // gamma^k in the model's global memory (once per roll-out: the tail term)
+    uint32_t off_gp10;  // f64 [G + 1]: 10 gamma^k (k < G = max(D, 2n) + 1), then 0.0 (index G: a bad
+                        // rock's term in upper())
     uint32_t gzero4;    // G in every byte (the index of gp10's 0.0)
-    uint32_t off_gp10;
   };
   static __host__ __device__ int gpow_len(int n, uint32_t D) { return (int)(D > (uint32_t)(2 * n) ? D : 2 * n) + 1; }
   static constexpr uint32_t kActSense = 1u, kActSample = 2u, kActExit = 4u, kActShift = 3u;
@@ -181,7 +181,7 @@ struct RockSample {
     const size_t c = (size_t)n * n + 1, mm = m > 0 ? (size_t)m : 1, G = (size_t)gpow_len(n, D);
     const size_t md = (mm + 3) & ~size_t(3);
     return align16((c + 1) * (m + 2)) + align16(2 * c * (5 + m)) + align16(4 * c) + align16(c) +
-           align16(4 * c * mm) + align16(c * md) + align16(8 * G) + align16(8 * (G + 1));
+           align16(4 * c * mm) + align16(c * md) + align16(8 * (G + 1));
   }
   static __device__ __forceinline__ uint32_t info(const Sm& sm, int c) {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_info)[c];
@@ -205,7 +205,7 @@ struct RockSample {
     return reinterpret_cast<const uint32_t*>(hd_dyn_smem + sm.off_dist + c * sm.md);
   }
   static __device__ __forceinline__ double gp(const Sm& sm, int k) {
-    return reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp)[k];
+    return sm.gpow_g[k];
   }
   static __device__ __forceinline__ double gp10(const Sm& sm, int k) {
     return reinterpret_cast<const double*>(hd_dyn_smem + sm.off_gp10)[k];
@@ -219,15 +219,13 @@ struct RockSample {
                    off_rock = off_info + (uint32_t)align16(4 * (size_t)(nc + 1)),
                    off_thr = off_rock + (uint32_t)align16((size_t)(nc + 1)),
                    off_dist = off_thr + (uint32_t)align16(4 * (size_t)(nc + 1) * mm),
-                   off_gp = off_dist + (uint32_t)align16((size_t)(nc + 1) * md),
-                   off_gp10 = off_gp + (uint32_t)align16(8 * (size_t)G);
+                   off_gp10 = off_dist + (uint32_t)align16((size_t)(nc + 1) * md);
     uint16_t* t_act = reinterpret_cast<uint16_t*>(hd_dyn_smem + off_act);
     uint32_t* t_info = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_info);
     uint8_t* t_rock = hd_dyn_smem + off_rock;
     uint32_t* t_thr = reinterpret_cast<uint32_t*>(hd_dyn_smem + off_thr);
     uint8_t* t_pol = hd_dyn_smem + off_pol;
     uint8_t* t_dist = hd_dyn_smem + off_dist;
-    double* t_gp = reinterpret_cast<double*>(hd_dyn_smem + off_gp);
     double* t_gp10 = reinterpret_cast<double*>(hd_dyn_smem + off_gp10);
     if (tid == 0) {
       sm.off_act = off_act;
@@ -236,7 +234,7 @@ struct RockSample {
       sm.off_thr = off_thr;
       sm.off_pol = off_pol;
       sm.off_dist = off_dist;
-      sm.off_gp = off_gp;
+      sm.gpow_g = dm.gpow;
       sm.off_gp10 = off_gp10;
       sm.polw = polw;
       sm.one = 1u;
@@ -267,7 +265,6 @@ struct RockSample {
       const int p = q < (int)polw ? col_pos(q) : -1;
       sm.senseb[q] = p >= 0 ? (uint8_t)(5 + dm.pos_rock[p]) : (uint8_t)2;
     }
-    for (int k = tid; k < G; k += nt) t_gp[k] = dm.gpow[k];
     for (int k = tid; k <= G; k += nt)
       t_gp10[k] = k < G ? 10.0 * dm.gpow[k] : 0.0;  // the product upper() used to form per rock
     for (int e = tid; e < (nc + 1) * md; e += nt) {
