@@ -1045,7 +1045,7 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
 // K3 for many slots as the single fused kernel (dense keys, S > 32, the
 // compacted slot arrays within its shared-memory limit)
 static bool wide_fused(uint32_t S, bool sparse) {
-  return !sparse && S > kWideS && wide_fused_smem(S) <= kWideFusedMaxSmem;
+  return !sparse && S > kWideS && S <= kWideFusedMaxS && wide_fused_smem(S) <= kWideFusedMaxSmem;
 }
 // look-back words: the tile counter + one per tile (a tile of kScanTile
 // (leaf, action) pairs, or one pair in the fused wide kernel) + 1
@@ -1814,9 +1814,13 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
       // many slots: rank + look-back scan + write in one kernel, a CTA per (leaf, action)
       static std::once_flag once;
       std::call_once(once, [] {
-        cudaFuncSetAttribute(k3_wide_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideFusedMaxSmem);
+        for (auto k : {k3_wide_fused<1>, k3_wide_fused<2>, k3_wide_fused<4>})
+          cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideFusedMaxSmem);
       });
-      launch_pdl(2, k3_wide_fused, (unsigned)LA, kWideFusedThreads, wide_fused_smem(b->S), st, bd);
+      auto kern = b->S <= kWideFusedThreads       ? k3_wide_fused<1>
+                  : b->S <= 2 * kWideFusedThreads ? k3_wide_fused<2>
+                                                  : k3_wide_fused<4>;
+      launch_pdl(2, kern, (unsigned)LA, kWideFusedThreads, wide_fused_smem(b->S), st, bd);
       ++b->launches;
       rc = check_launch(m, "K3(wide)");
     } else if (!rc && b->sharded_sparse) {

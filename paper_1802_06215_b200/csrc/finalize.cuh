@@ -392,9 +392,12 @@ __global__ void __launch_bounds__(256) k3_write_wide(BatchDev b) {
 // (la = ticket, so every predecessor a CTA looks back on is already running)
 // and the child_begin prefix by decoupled look-back over one (flag, value)
 // word per la.  Replaces k3_rank_dense + k3_scan_lookback + k3_write_wide and
-// their global rank / count round trips.  Dynamic shared memory: 12 S bytes
-// (the compacted non-empty slots' first ids, slot numbers and ranks).
+// their global rank / count round trips.  Each thread holds its (up to P)
+// slots' sums and first id in registers from one round of loads and writes
+// their outputs itself.  Dynamic shared memory: 8 S bytes (the compacted
+// non-empty slots' first ids and ranks).
 constexpr uint32_t kWideFusedThreads = 256;
+template <int P>  // ceil(S / 256) slots per thread (S <= 1024)
 __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
   extern __shared__ __align__(16) unsigned char k3w_smem[];
   __shared__ uint32_t s_wcnt[kWideFusedThreads / 32], s_ticket, s_cnt;
@@ -406,8 +409,7 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
   constexpr uint32_t NW = kWideFusedThreads / 32;
   const uint64_t LA = (uint64_t)b.L * A;
   int32_t* s_first = reinterpret_cast<int32_t*>(k3w_smem);
-  uint32_t* s_slot = reinterpret_cast<uint32_t*>(s_first + S);
-  uint32_t* s_rank = s_slot + S;
+  uint32_t* s_rank = reinterpret_cast<uint32_t*>(s_first + S);
   if (threadIdx.x == 0) s_ticket = (uint32_t)atomicAdd(&b.scan_flags[0], 1ull);
   __syncthreads();
   const uint64_t la = s_ticket;
@@ -415,11 +417,25 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
   const uint32_t leaf = (uint32_t)(la / A), a = (uint32_t)(la - (uint64_t)leaf * A);
   const SumLayout lay{LA * S, LA};
   const uint64_t base = la * S;
-  // 1. the non-empty slots, compacted in slot order
+  // 1. each thread's slots s = p * 256 + tid, every sum and first id loaded at
+  // once (one round trip), then the non-empty ones compacted in slot order
+  int64_t N[P], W[P], U[P], Lm[P];
+  int32_t mn[P];
+  int32_t pos[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint32_t s = p * kWideFusedThreads + threadIdx.x;
+    const bool in = s < S;
+    N[p] = in ? __ldcg(&b.sums[lay.N(base + s)]) : 0;
+    W[p] = in ? __ldcg(&b.sums[lay.W(base + s)]) : 0;
+    U[p] = in ? __ldcg(&b.sums[lay.U(base + s)]) : 0;
+    Lm[p] = in ? __ldcg(&b.sums[lay.Lm(base + s)]) : 0;
+    mn[p] = in ? __ldcg(&b.mins[base + s]) : 0;
+  }
   uint32_t cnt = 0;
-  for (uint32_t s0 = 0; s0 < S; s0 += kWideFusedThreads) {
-    const uint32_t s = s0 + threadIdx.x;
-    const bool ne = s < S && __ldcg(&b.sums[lay.N(base + s)]) != 0;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const bool ne = N[p] != 0;
     const uint32_t bal = __ballot_sync(0xffffffffu, ne);
     if (lane == 0) s_wcnt[wid] = __popc(bal);
     __syncthreads();
@@ -429,10 +445,10 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
       before += w < wid ? s_wcnt[w] : 0u;
       tot += s_wcnt[w];
     }
+    pos[p] = -1;
     if (ne) {
-      const uint32_t pos = cnt + before + __popc(bal & ((1u << lane) - 1u));
-      s_first[pos] = __ldcg(&b.mins[base + s]);
-      s_slot[pos] = s;
+      pos[p] = (int32_t)(cnt + before + __popc(bal & ((1u << lane) - 1u)));
+      s_first[pos[p]] = mn[p];
     }
     cnt += tot;
     __syncthreads();
@@ -469,26 +485,27 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
     }
   }
   __syncthreads();
-  // 3. outputs: Eq. 11/12 child bounds, one-level Eq. 4, the child-key table
+  // 3. outputs, by each slot's owner from its registers: Eq. 11/12 child
+  // bounds, one-level Eq. 4, the child-key table
   const LeafDev& lf = b.leaves[leaf];
   const DevModel& dm = *b.model;
   const uint32_t cb = s_cnt;  // the exclusive prefix of the child counts
   int64_t wt = 0, nt = 0;
-  for (uint32_t i = threadIdx.x; i < cnt; i += kWideFusedThreads) {
-    const uint32_t s = s_slot[i], rk = s_rank[i];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    if (pos[p] < 0) continue;
+    const uint32_t s = p * kWideFusedThreads + threadIdx.x, rk = s_rank[pos[p]];
     HD_CHECK(b.err, rk < cnt);
-    const int64_t N = __ldcg(&b.sums[lay.N(base + s)]);
-    const int64_t W = __ldcg(&b.sums[lay.W(base + s)]);
-    wt += W;
-    nt += N;
+    wt += W[p];
+    nt += N[p];
     const uint32_t c = cb + rk;
     if (c < b.child_capacity) {
-      const double Wd = (double)W;
-      b.child_count[c] = (uint32_t)N;
-      b.child_first[c] = (uint32_t)s_first[i];
+      const double Wd = (double)W[p];
+      b.child_count[c] = (uint32_t)N[p];
+      b.child_first[c] = (uint32_t)mn[p];
       b.child_weight[c] = (float)(Wd * dm.inv_fx * lf.wroot);
-      b.child_upper[c] = (float)((double)__ldcg(&b.sums[lay.U(base + s)]) / Wd);
-      b.child_lower[c] = (float)((double)__ldcg(&b.sums[lay.Lm(base + s)]) / Wd);
+      b.child_upper[c] = (float)((double)U[p] / Wd);
+      b.child_lower[c] = (float)((double)Lm[p] / Wd);
       b.child_obs[c] = s;
     }
     if (rk < lf.kcap) lf.keys[(uint64_t)a * lf.kcap + rk] = s;  // key table for later updates
@@ -555,7 +572,8 @@ __global__ void __launch_bounds__(kWideFusedThreads) k3_wide_fused(BatchDev b) {
     }
   }
 }
-__host__ __device__ inline size_t wide_fused_smem(uint32_t S) { return 12 * (size_t)S; }
+__host__ __device__ inline size_t wide_fused_smem(uint32_t S) { return 8 * (size_t)S; }
+constexpr uint32_t kWideFusedMaxS = 4 * kWideFusedThreads;  // P <= 4 register-held slots per thread
 constexpr size_t kWideFusedMaxSmem = 96 << 10;
 
 // K3 for small batches (L*A <= kSmallLA, S <= 32): rank, scan and write in
