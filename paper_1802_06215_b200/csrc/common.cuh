@@ -249,6 +249,8 @@ enum : uint32_t {
 struct BatchDev {
   const DevModel* model;
   const LeafDev* leaves;
+  const LeafDev* leaves_src;  // the leaf table in page-locked host memory: K1's CTA l copies entry l
+                              // into `leaves` first (no H2D copy of the table; null: already there)
   uint32_t L, A, S;          // S = dense slots per (leaf, action) (or per-leaf cap for sparse)
   uint32_t* n_leaf;          // [L] local scenarios per leaf (K1)
   uint32_t* tile_off;        // [L+1] K2 warp tiles prefix
@@ -286,6 +288,19 @@ struct BatchDev {
   uint32_t* sp_item;         // [L*A*S] scenario position holding the slot's key
   uint32_t* sp_keys;         // [L*A*S*OW] per-item observation keys (position-indexed)
 };
+
+// K1's prologue: this CTA's leaf descriptor from the host-side table (read
+// over the bus once, kept in the device table for K2 and K3)
+__device__ __forceinline__ void fetch_leaf(const BatchDev& b) {
+  if (!b.leaves_src) return;
+  constexpr uint32_t kWords = sizeof(LeafDev) / 4;
+  static_assert(sizeof(LeafDev) % 4 == 0, "LeafDev is copied in words");
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(b.leaves_src + blockIdx.x);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(const_cast<LeafDev*>(b.leaves) + blockIdx.x);
+  for (uint32_t k = threadIdx.x; k < kWords; k += blockDim.x) dst[k] = src[k];
+  __syncthreads();
+}
+
 
 // layout of the SUM block: W, U, LAMBDA, N per slot; R, Uq, Lq per action; steps
 struct SumLayout {

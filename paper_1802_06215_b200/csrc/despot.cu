@@ -1344,6 +1344,18 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
     b->r_stat = o_stat;
     b->r_zero = (o_sums - o_stat) + 8 * b->n_sums;
     b->r_h2d = h2d_bytes - o_leaves;
+    // when K1 runs, its CTAs read their leaf descriptors straight from the
+    // page-locked staging (fetch_leaf): no copy of the table
+    bool table_copy = true;
+    if (!all_self) {
+      LeafDev* dsrc = nullptr;
+      if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dsrc), h + o_leaves, 0) == cudaSuccess) {
+        bd.leaves_src = dsrc;
+        table_copy = false;
+      } else {
+        cudaGetLastError();
+      }
+    }
     if (b->resident) {  // set up once, outside the graph (resident_init)
       if (cudaHostAlloc(reinterpret_cast<void**>(&b->hmapped), stat_bytes, cudaHostAllocMapped) != cudaSuccess) {
         b->hmapped = nullptr;
@@ -1353,14 +1365,15 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       if (!rc && cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), b->hmapped, 0) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "mapped status block: device pointer");
       bd.hstat = dptr;
-      if (!rc && !b->resident_table &&
+      if (!rc && !b->resident_table && table_copy &&
           cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
         rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
     } else if (cudaMemsetAsync(s + o_stat, 0, (o_sums - o_stat) + 8 * b->n_sums, st) != cudaSuccess ||
         cudaMemsetAsync(bd.mins, 0x7F, 4 * b->n_mins, st) != cudaSuccess ||
         (xdense && (size_t)x.nblk * kXBlk > LAS &&
          cudaMemsetAsync(x.flags + LAS, 0, (size_t)x.nblk * kXBlk - LAS, st) != cudaSuccess) ||
-        cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        (table_copy &&
+         cudaMemcpyAsync(s + o_leaves, h + o_leaves, h2d_bytes - o_leaves, cudaMemcpyHostToDevice, st) != cudaSuccess))
       rc = set_err(DESPOT_ECUDA, "batch setup copies failed");
     if (!b->resident_table) b->h2d += h2d_bytes - o_leaves;
     if (!rc && ilist && idx_total) {

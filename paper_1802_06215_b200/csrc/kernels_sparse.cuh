@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(256) k1_update_sparse(BatchDev b) {
   __shared__ uint32_t warp_cnt[8];
   __shared__ uint32_t s_base;
   pdl_trigger();  // K2 may launch (it waits for this grid before reading)
+  fetch_leaf(b);
   const LeafDev& lf = b.leaves[blockIdx.x];
   if (lf.action < 0) {
     if (threadIdx.x == 0) b.n_leaf[blockIdx.x] = lf.p_n;
