@@ -1456,7 +1456,12 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
                                            (size_t)M::kScratchPerThread * 128);
       bool uni = true;
       for (uint32_t l = 1; l < L; ++l) uni = uni && ld[l].seed_lo == ld[0].seed_lo && ld[l].seed_hi == ld[0].seed_hi;
-      auto kern = uni ? k2_expand_dense<M, false, true> : k2_expand_dense<M, false, false>;
+      // per-lane reductions unless some (leaf, action) spans many tiles (kernels.cuh)
+      uint32_t max_chunks = 0;
+      for (uint32_t l = 0; l < L; ++l) max_chunks = std::max<uint32_t>(max_chunks, (parent[l]->cap + 31) / 32);
+      const bool lane_red = HD_K2_LANE_RED && max_chunks <= kLaneRedChunks;
+      auto kern = uni ? (lane_red ? k2_expand_dense<M, false, true, true> : k2_expand_dense<M, false, true, false>)
+                      : (lane_red ? k2_expand_dense<M, false, false, true> : k2_expand_dense<M, false, false, false>);
       const int occ = kernel_occupancy((const void*)kern, smem, 128);
       uint64_t tiles_bound = 0;
       for (uint32_t l = 0; l < L; ++l) tiles_bound += (uint64_t)dm.A * ((parent[l]->cap + 31) / 32);

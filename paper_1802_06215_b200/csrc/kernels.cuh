@@ -129,14 +129,15 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
 // Philox key is a kernel parameter (uniform registers; the key schedule costs
 // no per-lane instructions).
 #ifndef HD_K2_LANE_RED
-#define HD_K2_LANE_RED 1  // 0: the warp groups its lanes by observation before reducing
+#define HD_K2_LANE_RED 1  // 0: the warp always groups its lanes by observation before reducing
 #endif
+constexpr uint32_t kLaneRedChunks = 16;  // per-lane reductions up to this many tiles per (leaf, action)
 __device__ __forceinline__ uint32_t next_tile(const BatchDev& b, uint32_t nwarps, uint32_t lane) {
   uint32_t t = 0;
   if (lane == 0) t = nwarps + atomicAdd(&b.status[kStatK2Tile], 1u);
   return __shfl_sync(0xffffffffu, t, 0);
 }
-template <class M, bool RECORD, bool UNI_SEED = false>
+template <class M, bool RECORD, bool UNI_SEED = false, bool LANE_RED = false>
 __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, const RoundKeys rk) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
   uint32_t* tile_off =
@@ -275,26 +276,30 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
       red_add(&b.sums[lay.Q(la, 2)], sLq);
     }
     // ---- grouping by observation (Eq. 10) ------------------------------
-#if HD_K2_LANE_RED
-    // Every lane reduces its exact terms straight into its (leaf, action,
-    // observation) slot: the L2's atomic units do the grouping.  The warp's
-    // own grouping (the loop below: the distinct observations, a REDUX sum of
-    // each group's 64-bit terms in three parts, one leader's reductions) cost
-    // ~95 instructions per group, ~3 groups per tile; the reductions it saved
-    // cost less than that (config 2 K2 1.148 -> 1.078 ms, config 3 63.5 ->
-    // 59.9 us).  Sums are exact int64 and order-independent either way.
-    if (valid) {
-      const uint64_t slot = la * b.S + z;
-      red_add(&b.sums[lay.W(slot)], qW);
-      red_add(&b.sums[lay.U(slot)], qU);
-      red_add(&b.sums[lay.Lm(slot)], qL);
-      red_add(&b.sums[lay.N(slot)], (int64_t)1);
-      red_min(&b.mins[slot], (int32_t)id);
-    }
+    // Few tiles per (leaf, action): every lane reduces its exact terms
+    // straight into its (leaf, action, observation) slot and the L2's atomic
+    // units do the grouping -- the warp's own grouping (the loop below: the
+    // distinct observations, a REDUX sum of each group's 64-bit terms in
+    // three parts, one leader's reductions) costs ~95 instructions per group,
+    // ~3 groups per tile (config 2 K2 1.148 -> 1.078 ms, config 3 63.5 ->
+    // 59.9 us).  Many tiles per (leaf, action) (large beliefs, config 5): the
+    // warps working at any moment share a few slots, and same-address
+    // reductions from every lane serialise in the L2 (config 5 224 -> 509 ms),
+    // so the warp groups first (LANE_RED: chosen per batch on the host from
+    // the parents' sizes).  Exact int64 sums: the same result either way.
     uint32_t pending = 0;
-#else
-    uint32_t pending = __ballot_sync(0xffffffffu, valid);
-#endif
+    if constexpr (LANE_RED) {
+      if (valid) {
+        const uint64_t slot = la * b.S + z;
+        red_add(&b.sums[lay.W(slot)], qW);
+        red_add(&b.sums[lay.U(slot)], qU);
+        red_add(&b.sums[lay.Lm(slot)], qL);
+        red_add(&b.sums[lay.N(slot)], (int64_t)1);
+        red_min(&b.mins[slot], (int32_t)id);
+      }
+    } else {
+      pending = __ballot_sync(0xffffffffu, valid);
+    }
     while (pending) {
       const int leader = __ffs(pending) - 1;
       const uint32_t zk = __shfl_sync(0xffffffffu, z, leader);

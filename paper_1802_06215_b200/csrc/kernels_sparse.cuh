@@ -673,10 +673,10 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
     const uint32_t rep = titem[s];
     const uint32_t c = ord[rep];
     const uint64_t slot = base + c;
-    atomicAdd((unsigned long long*)&b.sums[lay.W(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 0]);
-    atomicAdd((unsigned long long*)&b.sums[lay.U(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 1]);
-    atomicAdd((unsigned long long*)&b.sums[lay.Lm(slot)], (unsigned long long)io.q3[3 * (q0 + i) + 2]);
-    atomicAdd((unsigned long long*)&b.sums[lay.N(slot)], 1ull);
+    red_add(&b.sums[lay.W(slot)], io.q3[3 * (q0 + i) + 0]);
+    red_add(&b.sums[lay.U(slot)], io.q3[3 * (q0 + i) + 1]);
+    red_add(&b.sums[lay.Lm(slot)], io.q3[3 * (q0 + i) + 2]);
+    red_add(&b.sums[lay.N(slot)], (int64_t)1);
     if (rep == i) {
       b.mins[slot] = (int32_t)b.leaves[leaf].ids[i];
       b.rank[slot] = c;
@@ -734,12 +734,20 @@ __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut
       }
     }
     const uint32_t cn = nc - c0 < 32 ? nc - c0 : 32;
-    for (uint32_t j = 0; j < cn; ++j) {
-      const uint32_t cj = c0 + j, it = __shfl_sync(0xffffffffu, item, j);
-      if (lane < OW) {
-        const uint32_t v = io.keys[(uint64_t)it * io.kstride + lane];
-        if (cb + cj < b.child_capacity) b.child_obs[(uint64_t)(cb + cj) * OW + lane] = v;
-        if (cj < lf.kcap) lf.keys[((uint64_t)a * lf.kcap + cj) * OW + lane] = v;
+    for (uint32_t j0 = 0; j0 < cn; j0 += 8) {  // eight children's loads in flight, then their stores
+      uint32_t v[8];
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        const uint32_t j = j0 + u, it = __shfl_sync(0xffffffffu, item, j & 31u);
+        v[u] = (j < cn && lane < OW) ? __ldcg(&io.keys[(uint64_t)it * io.kstride + lane]) : 0u;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < 8; ++u) {
+        const uint32_t cj = c0 + j0 + u;
+        if (j0 + u < cn && lane < OW) {
+          if (cb + cj < b.child_capacity) b.child_obs[(uint64_t)(cb + cj) * OW + lane] = v[u];
+          if (cj < lf.kcap) lf.keys[((uint64_t)a * lf.kcap + cj) * OW + lane] = v[u];
+        }
       }
     }
   }
