@@ -262,6 +262,8 @@ struct BatchDev {
   unsigned long long* scan_flags;  // K3b look-back: [0] tile counter, [1 + t] tile t's (flag, prefix)
   uint32_t* status;          // [kStatWords header (kStat*), n_leaf[L]]
   uint32_t fused_k3;         // 1: K2's last CTA runs the small finalize
+  uint32_t tile_off_global;  // 1: K2 searches tile_off in global memory (many leaves: the shared
+                             // copy would cost a CTA per SM), not a shared copy
   uint32_t k2_prefix;        // 1: K2 forms the tile prefix from n_leaf itself (K1 skips its
                              // last-CTA prefix: dense keys, no per-scenario records)
   uint32_t* hstat;           // resident prepared batch (else null): K2's last CTA publishes the

@@ -1044,6 +1044,7 @@ static int bind_outputs(despot_batch* b, despot_expansion* out, cudaStream_t st)
 
 // K3 for many slots as the single fused kernel (dense keys, S > 32, the
 // compacted slot arrays within its shared-memory limit)
+constexpr uint32_t kTileOffSharedMaxL = 64;  // K2 keeps a shared copy of tile_off up to this many leaves
 static bool wide_fused(uint32_t S, bool sparse) {
   return !sparse && S > kWideS && S <= kWideFusedMaxS && wide_fused_smem(S) <= kWideFusedMaxSmem;
 }
@@ -1421,7 +1422,11 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
         kernel_occupancy((const void*)k1_update<M>, smem1, M::kK1Threads);  // sets the smem attribute if > 48 KB
         // the tile prefix: K2 forms it (no per-scenario records: nothing else
         // reads the prefixes), else K1's last CTA
-        bd.k2_prefix = (flags & DESPOT_X_RECORD_SCENARIO) ? 0u : 1u;
+        // many leaves: K2 searches the tile prefix in global memory (K1's last
+        // CTA forms it) -- a shared copy of 4 (L + 1) bytes per CTA would cost
+        // MARS its seventh CTA per SM at L = 256
+        bd.tile_off_global = L > kTileOffSharedMaxL ? 1u : 0u;
+        bd.k2_prefix = ((flags & DESPOT_X_RECORD_SCENARIO) || bd.tile_off_global) ? 0u : 1u;
         k1_update<M><<<L, M::kK1Threads, smem1, st>>>(bd);  // + prefix in its last CTA unless k2_prefix
         ++b->launches;
       }
@@ -1451,7 +1456,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       using M = decltype(mdl);
       // Sm | tables | tile_off | max(the fused finalize's region, the per-thread scratch)
       const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
-                          align16(4 * ((size_t)L + 1)) +
+                          (bd.tile_off_global ? 0 : align16(4 * ((size_t)L + 1))) +
                           std::max<size_t>(b->k3_fused ? small_finalize_smem((uint64_t)L * dm.A) : 0,
                                            (size_t)M::kScratchPerThread * 128);
       bool uni = true;
@@ -1806,7 +1811,8 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
     rc = dispatch_dense(dm, [&](auto mdl) -> int {
       using M = decltype(mdl);
       const size_t smem = align16(sizeof(typename M::Sm)) + align16(dm.sm_table_bytes) +
-                          align16(4 * ((size_t)L + 1)) + (size_t)M::kScratchPerThread * 128;
+                          (bd.tile_off_global ? 0 : align16(4 * ((size_t)L + 1))) +
+                          (size_t)M::kScratchPerThread * 128;
       auto kern = k2_expand_dense<M, true>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       b->mark(3);

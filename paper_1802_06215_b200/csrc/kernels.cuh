@@ -140,16 +140,20 @@ __device__ __forceinline__ uint32_t next_tile(const BatchDev& b, uint32_t nwarps
 template <class M, bool RECORD, bool UNI_SEED = false, bool LANE_RED = false>
 __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b, const RoundKeys rk) {
   typename M::Sm& sm = *reinterpret_cast<typename M::Sm*>(hd_dyn_smem);
-  uint32_t* tile_off =
-      reinterpret_cast<uint32_t*>(hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes));
+  // dynamic shared memory: Sm | tables | tile_off (unless searched in global
+  // memory) | the per-thread scratch / the fused finalize's region
+  unsigned char* region = hd_dyn_smem + align16(sizeof(typename M::Sm)) + align16(b.model->sm_table_bytes);
+  const uint32_t toff_bytes = b.tile_off_global ? 0u : (uint32_t)align16(4 * ((size_t)b.L + 1));
+  uint32_t* tile_off_s = reinterpret_cast<uint32_t*>(region);
+  const uint32_t* tile_off = b.tile_off_global ? b.tile_off : tile_off_s;
   load_sm_image<M>(sm, *b.model, threadIdx.x, blockDim.x);
   // the per-thread scratch shares the fused finalize's region (used after the tiles)
-  if (threadIdx.x == 0) M::bind_scratch((uint32_t)(reinterpret_cast<unsigned char*>(tile_off) - hd_dyn_smem) +
-                                        (uint32_t)align16(4 * ((size_t)b.L + 1)));
+  if (threadIdx.x == 0) M::bind_scratch((uint32_t)(region - hd_dyn_smem) + toff_bytes);
   pdl_wait();  // K1 complete: tile_off, the leaf arenas
   pdl_trigger();
   __shared__ uint64_t wsum[32];  // block scans: the tile prefix, the fused finalize
-  if (b.k2_prefix) {  // tile_off[l] = sum_{l' < l} A ceil(n_l' / 32), every CTA for itself
+  if (b.tile_off_global) {
+  } else if (b.k2_prefix) {  // tile_off[l] = sum_{l' < l} A ceil(n_l' / 32), every CTA for itself
     const uint32_t per = (b.L + blockDim.x - 1) / blockDim.x, l0 = threadIdx.x * per;
     auto tiles_of = [&](uint32_t l) { return (uint64_t)b.A * ((__ldcg(&b.n_leaf[l]) + 31u) >> 5); };
     uint64_t tiles = 0;
@@ -157,15 +161,15 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     uint64_t ttot;
     uint64_t tb = block_excl_scan(tiles, wsum, ttot);
     for (uint32_t l = l0; l < l0 + per && l < b.L; ++l) {
-      tile_off[l] = (uint32_t)tb;
+      tile_off_s[l] = (uint32_t)tb;
       tb += tiles_of(l);
     }
     if (threadIdx.x == 0) {
-      tile_off[b.L] = (uint32_t)ttot;
+      tile_off_s[b.L] = (uint32_t)ttot;
       if (ttot >= 0xFFFFFFFFull && blockIdx.x == 0) atomicOr(b.err, kErrChildCap);
     }
   } else {
-    for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off[l] = b.tile_off[l];
+    for (uint32_t l = threadIdx.x; l <= b.L; l += blockDim.x) tile_off_s[l] = b.tile_off[l];
   }
   __syncthreads();
   const uint32_t total = tile_off[b.L];
@@ -334,7 +338,7 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     __syncthreads();
     if (k2_last) {
       __threadfence();
-      small_finalize_tail(b, reinterpret_cast<unsigned char*>(tile_off) + align16(4 * ((size_t)b.L + 1)), wsum);
+      small_finalize_tail(b, region + toff_bytes, wsum);
       if (b.hstat) resident_epilogue(b);
     }
   }
