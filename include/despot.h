@@ -197,7 +197,10 @@ typedef struct {
 
 /* Caller-owned outputs.  Sizes: L leaves, A = |A|, C = child_capacity,
  * S = scen_capacity.  Children of (l, a) are child_begin[l*A+a] ..
- * child_begin[l*A+a+1]-1, in first-occurrence order (R8). */
+ * child_begin[l*A+a+1]-1, in first-occurrence order (R8).  Host outputs that
+ * are all page-locked (cudaHostAlloc / cudaHostRegister) are written in place
+ * by the kernels (dense keys, <= 4 MB at capacity) or copied into directly;
+ * either way they are valid when the call returns. */
 typedef struct {
   uint32_t flags;
   despot_node* node;     /* [L] host: new node holding leaf l's scenarios (for
@@ -233,8 +236,10 @@ typedef struct {
    * grouping (K2), [2] child order / CSR / outputs (K3a-c), [3] whole call
    * from the first enqueued operation to the last (device time, ms)          */
   float phase_ms[4];
-  uint64_t h2d_bytes;      /* out: bytes this call copied host -> device / device -> */
-  uint64_t d2h_bytes;      /*      host (leaf table, status, results; begin + end)   */
+  uint64_t h2d_bytes;      /* out: bytes this call moved host -> device / device ->  */
+  uint64_t d2h_bytes;      /*      host (leaf table -- copied, or read by K1 from the
+                              page-locked staging --, status, results -- copied, or
+                              written in place --; begin + end)                      */
   /* out, sharded batches run through the model's communicator: */
   float exchange_ms;       /* K4: CUDA-event time of the exchange (collectives and the
                               pack / unpack kernels between them; with DESPOT_X_TIMING) */
