@@ -1921,7 +1921,7 @@ static int finish_batch(despot_batch* b, despot_expansion* out, cudaStream_t st,
       rc = check_launch(m, "K3b");
     }
     if (!rc && b->sparse) {
-      launch_pdl(2, k3_write_sparse, (unsigned)LA, 256, 0, st, bd, b->io);  // (merged: keys from the gathered records)
+      launch_pdl(2, k3_write_sparse, (unsigned)LA, kWriteSparseThreads, 0, st, bd, b->io);  // (merged: keys from the gathered records)
       ++b->launches;
       rc = check_launch(m, "K3c(sparse)");
     } else if (!rc && !small_k3 && !wide1) {

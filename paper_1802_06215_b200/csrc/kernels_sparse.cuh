@@ -694,8 +694,9 @@ __global__ void __launch_bounds__(512) k3_group_sparse(BatchDev b, SparseItemOut
 
 // K3c for sparse keys: one CTA per (leaf, action), one thread per child
 // (children are already in first-occurrence order)
-__global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut io) {
-  __shared__ int64_t s_wt[8], s_nt[8];
+constexpr uint32_t kWriteSparseThreads = 512;  // a warp per 32 children: one round for ~500 children
+__global__ void __launch_bounds__(kWriteSparseThreads) k3_write_sparse(BatchDev b, SparseItemOut io) {
+  __shared__ int64_t s_wt[kWriteSparseThreads / 32], s_nt[kWriteSparseThreads / 32];
   pdl_wait();  // the predecessor complete
   pdl_trigger();
   const uint32_t A = b.A;
@@ -734,15 +735,15 @@ __global__ void __launch_bounds__(256) k3_write_sparse(BatchDev b, SparseItemOut
       }
     }
     const uint32_t cn = nc - c0 < 32 ? nc - c0 : 32;
-    for (uint32_t j0 = 0; j0 < cn; j0 += 8) {  // eight children's loads in flight, then their stores
-      uint32_t v[8];
+    for (uint32_t j0 = 0; j0 < cn; j0 += 16) {  // sixteen children's loads in flight, then their stores
+      uint32_t v[16];
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) {
+      for (uint32_t u = 0; u < 16; ++u) {
         const uint32_t j = j0 + u, it = __shfl_sync(0xffffffffu, item, j & 31u);
         v[u] = (j < cn && lane < OW) ? __ldcg(&io.keys[(uint64_t)it * io.kstride + lane]) : 0u;
       }
 #pragma unroll
-      for (uint32_t u = 0; u < 8; ++u) {
+      for (uint32_t u = 0; u < 16; ++u) {
         const uint32_t cj = c0 + j0 + u;
         if (j0 + u < cn && lane < OW) {
           if (cb + cj < b.child_capacity) b.child_obs[(uint64_t)(cb + cj) * OW + lane] = v[u];
