@@ -252,6 +252,7 @@ struct BatchDev {
   const LeafDev* leaves_src;  // the leaf table in page-locked host memory: K1's CTA l copies entry l
                               // into `leaves` first (no H2D copy of the table; null: already there)
   uint32_t L, A, S;          // S = dense slots per (leaf, action) (or per-leaf cap for sparse)
+  unsigned long long a_magic;  // floor((2^64 - 1) / A) + 1: x / A = umul64hi(x, a_magic) for x < 2^32
   uint32_t* n_leaf;          // [L] local scenarios per leaf (K1)
   uint32_t* tile_off;        // [L+1] K2 warp tiles prefix
   uint64_t* scen_off;        // [L+1] per-scenario record prefix (A * n)

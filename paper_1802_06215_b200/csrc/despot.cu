@@ -1256,6 +1256,7 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
   bd.leaves = reinterpret_cast<LeafDev*>(s + o_leaves);
   bd.L = L;
   bd.A = dm.A;
+  bd.a_magic = dm.A > 1 ? ~0ull / dm.A + 1 : 0;
   bd.S = b->S;
   bd.status = reinterpret_cast<uint32_t*>(s + o_stat);
   bd.err = bd.status;

@@ -205,8 +205,12 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     const uint32_t n = b.n_leaf[leaf];
     const uint32_t chunks = (n + 31) >> 5;
     const uint32_t local = t - tile_off[leaf];
-    const uint32_t a = local / chunks;
-    const uint32_t i = (local - a * chunks) * 32 + lane;
+    // chunk-major within the leaf (local = chunk * A + a: consecutive tiles
+    // share their 32 scenarios' states), the division by A as a 64-bit
+    // multiply-high (exact for 32-bit dividends)
+    const uint32_t chunk = b.A > 1 ? (uint32_t)__umul64hi((unsigned long long)local, b.a_magic) : local;
+    const uint32_t a = local - chunk * b.A;
+    const uint32_t i = chunk * 32 + lane;
     const bool valid = i < n;
     HD_CHECK(b.err, a < b.A && leaf < b.L && (!valid || i < lf.cap));
     uint32_t z = 0xFFFFFFFFu, id = 0;
