@@ -1471,7 +1471,10 @@ static int begin_impl(despot_model* m, const despot_leaf* leaves, uint32_t L, ui
       // per-lane reductions unless some (leaf, action) spans many tiles (kernels.cuh)
       uint32_t max_chunks = 0;
       for (uint32_t l = 0; l < L; ++l) max_chunks = std::max<uint32_t>(max_chunks, (parent[l]->cap + 31) / 32);
-      const bool lane_red = HD_K2_LANE_RED && max_chunks <= kLaneRedChunks;
+      // (with chunk-major tiles the warps in flight spread over all A x S
+      // slots of a leaf: enough of them keep per-lane reductions cheap at any
+      // belief size -- config 5 208 -> 198 ms)
+      const bool lane_red = HD_K2_LANE_RED && (max_chunks <= kLaneRedChunks || (uint64_t)dm.A * b->S >= 1024);
       auto kern = uni ? (lane_red ? k2_expand_dense<M, false, true, true> : k2_expand_dense<M, false, true, false>)
                       : (lane_red ? k2_expand_dense<M, false, false, true> : k2_expand_dense<M, false, false, false>);
       const int occ = kernel_occupancy((const void*)kern, smem, 128);

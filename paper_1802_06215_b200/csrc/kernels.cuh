@@ -131,7 +131,10 @@ __global__ void __launch_bounds__(512) k1_update(BatchDev b) {
 #ifndef HD_K2_LANE_RED
 #define HD_K2_LANE_RED 1  // 0: the warp always groups its lanes by observation before reducing
 #endif
-constexpr uint32_t kLaneRedChunks = 16;  // per-lane reductions up to this many tiles per (leaf, action)
+#ifndef HD_K2_LANE_RED_CHUNKS
+#define HD_K2_LANE_RED_CHUNKS 16
+#endif
+constexpr uint32_t kLaneRedChunks = HD_K2_LANE_RED_CHUNKS;  // per-lane reductions up to this many tiles per (leaf, action)
 __device__ __forceinline__ uint32_t next_tile(const BatchDev& b, uint32_t nwarps, uint32_t lane) {
   uint32_t t = 0;
   if (lane == 0) t = nwarps + atomicAdd(&b.status[kStatK2Tile], 1u);
@@ -292,9 +295,11 @@ __global__ void __launch_bounds__(128, M::kMinBlocks) k2_expand_dense(BatchDev b
     // ~3 groups per tile (config 2 K2 1.148 -> 1.078 ms, config 3 63.5 ->
     // 59.9 us).  Many tiles per (leaf, action) (large beliefs, config 5): the
     // warps working at any moment share a few slots, and same-address
-    // reductions from every lane serialise in the L2 (config 5 224 -> 509 ms),
-    // so the warp groups first (LANE_RED: chosen per batch on the host from
-    // the parents' sizes).  Exact int64 sums: the same result either way.
+    // reductions from every lane serialise in the L2 (config 5 224 -> 509 ms
+    // with action-major tiles), so the warp groups first -- unless the leaf
+    // has many slots (A x S >= 1024: chunk-major tiles keep the warps in
+    // flight on different slots; LANE_RED is chosen per batch on the host).
+    // Exact int64 sums: the same result either way.
     uint32_t pending = 0;
     if constexpr (LANE_RED) {
       if (valid) {
