@@ -111,6 +111,24 @@ def test_config1_rocksample_root():
     assert G["scenario_steps"] == O["scenario_steps"]
 
 
+def test_large_belief_few_slots_uses_warp_groups():
+    """K2's warp-level observation groups (the LANE_RED = false form: many
+    tiles per (leaf, action) and few slots per leaf, A * S < 1024): a
+    RockSample(7,8) root with K = 2048 (64 tiles per action, 13 x 4 slots),
+    its depth-1 children, and the record form, against the oracle; the timed
+    and record kernels agree bit for bit."""
+    gm, om, st, w, seed, L = setup(1, K=2048, uniform=False)
+    gr, orr, G, O = expand_root_both(gm, om, st, w, seed, record=True)
+    compare_batch(G, O, gm, om, [(0, 0)], check_scen=True)
+    assert G["scenario_steps"] == O["scenario_steps"]
+    _timed_form_equals_record(gm, [(gr, -1, 0, 0)], G)
+    lv = inputs.select_leaves(G["child_count"], G["child_begin"], gm.A, 6)
+    G1 = gm.expand([(gr, a, c, 1) for a, c in lv])
+    O1 = om.expand([(orr, a, c, 1) for a, c in lv], record=True)
+    compare_batch(G1, O1, gm, om, [(i, i) for i in range(len(lv))])
+    gm.close()
+
+
 def test_config2_mars_64_leaves():
     _full_config(2)
 
